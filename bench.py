@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark: random-forest fit trees/s (+ predict rows/s) on B200 vs the host CPU reference.
+
+Workload (BASELINE.json configs[3], "C4"): synthetic AIWC table 1,000,036 rows x 64
+predictors (synthesize(6757 kernels, 37 devices) + make_dataset), mtry 8, min.node.size 5,
+1000 trees per GPU (weak scaling: rank r grows trees [1000r, 1000(r+1)) of the
+1000*N-tree forest keyed by derive_seed(1, "forest")), OOB statistics included (a fit
+step is `fit()` exactly as forest.hpp:480 defines it: grow + compute_oob).
+Secondary (reported in "predict"): configs[4] "C5", a 1000-tree forest on the C1 table
+(m=6, mns=5) scoring 100M device-selection query rows.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One JSON line on rank 0.  Timing: CUDA events, barrier + synchronize around the K timed
+steps, max over ranks.  Inputs (512 MB column store + ranks) exceed the 126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C4_KERNELS, C4_DEVICES, C4_MTRY, C4_MNS = 6757, 37, 8, 5
+C5_TREES, C5_MTRY, C5_MNS = 1000, 6, 5
+METRIC = "RF fit trees/s + predict rows/s at 1/2/4/8 B200 (% HBM roofline) vs host CPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,utilization.gpu,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        util = [int(s[2]) if s[2].isdigit() else 0 for s in self.samples]
+        loaded = [s for s, u in zip(self.samples, util) if u > 0] or self.samples
+        sm = sorted(int(s[0]) for s in loaded if s[0].isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in loaded for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None,
+                "sm_max_mhz": int(self.samples[0][1]) if self.samples[0][1].isdigit() else None,
+                "reasons": reasons, "samples": len(loaded)}
+
+
+# ----------------------------------------------------------------------------------------
+# CPU arms (reference compiled from /root/reference by oracle/Makefile -> oracle/_ref)
+# ----------------------------------------------------------------------------------------
+def cpu_worker(args) -> dict:
+    """Times the reference's own fit (forest.hpp:480) on a bounded tree sample of C4.
+    Runs in a subprocess: the reference's multi-threaded fit reads freed memory
+    (oracle/REFERENCE_DEFECT.md), so a crash must not take the bench down."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Ref, RefData
+
+    L = Ref.lib()
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    d = RefData(C4_KERNELS, C4_DEVICES)
+    t1 = time.perf_counter()
+    prep = d.prepared()
+    t2 = time.perf_counter()
+    seed = Ref.derive_seed(1, "forest")
+    sample = args.cpu_trees or max(8, min(cores, 64))
+    rates = []
+    import ctypes as C
+
+    for step in range(max(1, args.cpu_steps)):
+        nodes = C.c_uint64()
+        s = time.perf_counter()
+        Ref.check(L.ref_grow_range(prep, 1000, C4_MTRY, C4_MNS, seed, 0, sample, cores,
+                                   C.byref(nodes)))
+        rates.append(sample / (time.perf_counter() - s))
+    return {"value": float(np.median(rates)), "unit": "trees/s", "cores": cores,
+            "kind": "reference", "rates": rates,
+            "sample": f"C4 trees [0,{sample}) of the 1000-tree m=8 mns=5 forest, "
+                      f"TreeGrower::grow via parallel_for_with_state (forest.hpp:500-505), "
+                      f"jobs={cores}; synth+join {t1 - t0:.1f}s and PreparedDataset "
+                      f"{t2 - t1:.1f}s excluded (reported separately)",
+            "prepare_s": t2 - t1, "synth_s": t1 - t0}
+
+
+def run_cpu_subprocess(trees: int, steps: int, timeout: int = 900) -> dict:
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-worker", "--cpu-trees", str(trees),
+           "--cpu-steps", str(steps)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+        for line in r.stdout.splitlines()[::-1]:
+            if line.startswith("{"):
+                return json.loads(line)
+        return {"value": None, "error": (r.stderr or r.stdout)[-400:], "kind": "reference"}
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "error": str(e), "kind": "reference"}
+
+
+# ----------------------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--trees-per-gpu", type=int, default=1000)
+    ap.add_argument("--predict-rows", type=int, default=100_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--skip-predict", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-worker", action="store_true")
+    ap.add_argument("--cpu-trees", type=int, default=0)
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    args = ap.parse_args()
+
+    if args.cpu_worker:
+        print(json.dumps(cpu_worker(args)))
+        return
+
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = max(1, args.steps)
+        res = run_cpu_subprocess(args.cpu_trees, steps)
+        v = res.get("value")
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "trees/s",
+                "n_gpus": world, "steps": steps, "warmup": args.warmup,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C4 fit: synthetic AIWC 1,000,036 x 64, mtry 8, "
+                                       "min.node.size 5, seed derive_seed(1,'forest')",
+                           "parallelism": "host threads"},
+                "cpu_baseline": {k: res.get(k) for k in ("value", "unit", "cores", "kind",
+                                                         "sample")},
+                "e2e": {"value": v, "unit": "trees/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        if v is None:
+            line["error"] = res.get("error")
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1811_00156_b200 as pkg
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    # CPU baseline in the background on rank 0 (bounded sample, own subprocess)
+    cpu_res = {}
+    cpu_thread = None
+    if rank == 0 and not args.skip_cpu:
+        def _cpu():
+            cpu_res.update(run_cpu_subprocess(args.cpu_trees, 1))
+        cpu_thread = threading.Thread(target=_cpu, daemon=True)
+
+    # ---------------- C4 fit ----------------
+    t_setup = time.perf_counter()
+    table = pkg.Table(C4_KERNELS, C4_DEVICES)
+    prep = pkg.PreparedDataset.from_table(table, device=local)
+    setup_s = time.perf_counter() - t_setup
+    if cpu_thread:
+        cpu_thread.start()  # after our host-side setup so the two do not share cores
+    per = args.trees_per_gpu
+    total_trees = per * world
+    seed = pkg.derive_seed(1, "forest")
+    params = pkg.ForestParams(total_trees, C4_MTRY, C4_MNS, seed)
+    tb, te = rank * per, (rank + 1) * per
+
+    def chained_oob(forest):
+        """Exact tree-ordered OOB over ranks: rank r continues rank r-1's per-row sums."""
+        n = table.n
+        rs = np.zeros(n)
+        rc = np.zeros(n, np.uint32)
+        if rank > 0:
+            buf = torch.empty(n * 12 // 4, dtype=torch.int32, device="cuda")
+            dist.recv(buf, src=rank - 1)
+            raw = buf.cpu().numpy().view(np.uint8)
+            rs = raw[: 8 * n].view(np.float64).copy()
+            rc = raw[8 * n:].view(np.uint32).copy()
+        pkg.oob_accumulate(forest, prep, rs, rc)
+        if rank < world - 1:
+            raw = np.concatenate([rs.view(np.uint8), rc.view(np.uint8)])
+            dist.send(torch.from_numpy(raw.view(np.int32).copy()).cuda(), dst=rank + 1)
+            return None
+        return pkg.oob_finalize(table.y, rs, rc)
+
+    def fit_step():
+        if world == 1:
+            f = pkg.fit(prep, params)
+            return f, f.oob
+        f = pkg.fit(prep, params, tb, te, compute_oob_stats=False)
+        return f, chained_oob(f)
+
+    for _ in range(args.warmup):
+        f, _ = fit_step()
+        del f
+    barrier()
+    launches0 = pkg.launch_count()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    grow_ms, split_rows, grow_launch = 0.0, 0, 0
+    oob = None
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            f, o = fit_step()
+            prof = f.profile()
+            grow_ms += prof["grow_ms"]
+            split_rows += prof["split_rows"]
+            grow_launch += prof["grow_launches"]
+            oob = o if o is not None else oob
+            nodes_last = f.total_nodes
+            del f
+        ev1.record(stream)
+        barrier()
+    launches = pkg.launch_count() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = total_trees * args.steps / (ms / 1e3)
+    # roofline of the grow kernel: SURVEY 8d algorithmic bytes
+    #   B_tree = 4n + sum_split_nodes rows(N) * (24*mtry + 16)
+    n = table.n
+    alg_bytes = args.steps * per * 4 * n + split_rows * (24 * C4_MTRY + 16)
+    achieved = alg_bytes / (grow_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+
+    # ---------------- e2e through the C-ABI with host buffers ----------------
+    e2e_times, h2d, d2h = [], 0, 0
+    barrier()
+    for _ in range(max(1, args.e2e_steps)):
+        s = time.perf_counter()
+        p2 = pkg.PreparedDataset(table.col, table.y, table.n, table.p, device=local)
+        if world == 1:
+            f2 = pkg.fit(p2, params)
+            _ = f2.oob
+        else:
+            f2 = pkg.fit(p2, params, tb, te, compute_oob_stats=False)
+        arrs = f2.export()
+        ib = f2.inbag()
+        e2e_times.append(time.perf_counter() - s)
+        h2d = table.col.nbytes + table.y.nbytes
+        d2h = sum(a.nbytes for a in arrs) + ib.nbytes
+        del f2, p2, arrs, ib
+    e2e_s = max_over_ranks(float(np.median(e2e_times)))
+    e2e_value = total_trees / e2e_s
+
+    del prep
+    torch.cuda.empty_cache()
+
+    # ---------------- C5 predict ----------------
+    predict = None
+    if not args.skip_predict:
+        predict = bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
+
+    if cpu_thread:
+        cpu_thread.join(timeout=1200)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference synthesize()+make_dataset() restated bit-exactly; "
+                "random forest trained from scratch each step)",
+        "config": {"workload": "C4 fit: synthetic AIWC 1,000,036 x 64 (6757 kernels x 4 "
+                               "sizes x 37 devices), mtry 8, min.node.size 5, "
+                               f"{per} trees/GPU, OOB included",
+                   "trees_total": total_trees, "rows": table.n, "predictors": table.p,
+                   "parallelism": f"tree-seed shards x{world}, chained OOB",
+                   "l2": "inputs (512 MB f64 column store + 128 MB ranks) exceed L2"},
+        "oob_error_pct": None if oob is None else oob.error_pct,
+        "nodes_per_tree": nodes_last / per,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "grow_kernel",
+                     "algorithmic_bytes_per_launch": alg_bytes / max(1, grow_launch),
+                     "kernel_ms_per_launch": grow_ms / max(1, grow_launch),
+                     "kernel_share_of_step": grow_ms / max(1e-9, ms)},
+        "e2e": {"value": e2e_value, "unit": "trees/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "path": "aiwc_ctx_create(host col,y)+aiwc_fit+export(nodes,inbag)"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "setup_s": setup_s,
+        "cpu_baseline": ({k: cpu_res.get(k) for k in ("value", "unit", "cores", "kind", "sample")}
+                         if cpu_res else None),
+        "predict": predict,
+    }
+    if cpu_res.get("error"):
+        line["cpu_baseline_error"] = cpu_res["error"]
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak):
+    """C5: 1000-tree forest on the C1 table; 100M queries per GPU resident in HBM."""
+    t = pkg.Table()
+    prep = pkg.PreparedDataset.from_table(t, device=local)
+    seed = pkg.derive_seed(1, "forest")
+    forest = pkg.fit(prep, pkg.ForestParams(C5_TREES, C5_MTRY, C5_MNS, seed))
+    rows = torch.from_numpy(t.predictor_rows()).cuda()
+    q = args.predict_rows
+    qbuf = torch.empty((q, t.p), dtype=torch.float64, device="cuda")
+    out = torch.empty(q, dtype=torch.float64, device="cuda")
+    pkg.make_queries(rows.data_ptr(), t.n, t.p, q, 7, local, qbuf.data_ptr())
+    for _ in range(max(1, args.warmup)):
+        forest.predict_device(qbuf.data_ptr(), q, t.p, out.data_ptr())
+    barrier()
+    steps = max(1, args.steps)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(steps):
+        forest.predict_device(qbuf.data_ptr(), q, t.p, out.data_ptr())
+    ev1.record()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1)) / steps
+    rate = q * world / (ms / 1e3)
+    alg = q * (8 * t.p + 8)
+    # e2e: host rows through aiwc_predict (H2D + kernel + D2H), bounded host buffer
+    qe = min(q, 10_000_000)
+    host = qbuf[:qe].cpu().numpy()
+    s = time.perf_counter()
+    _ = forest.predict_response(host)
+    e2e = qe / (time.perf_counter() - s)
+    del qbuf, out
+    torch.cuda.empty_cache()
+    return {"workload": "C5: 1000-tree C1 forest (m=6, mns=5), 100M device-selection queries "
+                        "(row q = C1 row Rng(derive_seed(7,'query',q)).bounded(2220))",
+            "rows_per_s": rate, "unit": "rows/s", "ms_per_pass": ms, "rows": q * world,
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / peak,
+                         "note": "B_row = 8p+8 = 344 B; node visits (~12K/row) bind on-chip"},
+            "e2e": {"value": e2e, "unit": "rows/s", "rows": qe,
+                    "h2d_bytes": qe * t.p * 8, "d2h_bytes": qe * 8}}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,779 @@
+// C-ABI entry points of libaiwc_cuda.so (declared in include/aiwc_cuda.h).
+//
+// Host driver around the sm_100a kernels: PreparedDataset upload (presort + ranks),
+// fit (grow_kernel launch over persistent per-tree CTAs, pool compaction, OOB),
+// forest export/import, OOB, predict and hold-one-kernel-out evaluate.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "aiwc_cuda.h"
+#include "forest_kernels.cuh"
+#include "grow.cuh"
+#include "host_common.hpp"
+
+namespace aiwc_b200 {
+
+namespace {
+thread_local std::string g_last_error;
+}
+std::atomic<uint64_t> g_launches{0};  // kernels launched by this library (bench evidence)
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+#define CK(expr)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (expr);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      throw Status(AIWC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t c) { alloc(c); }
+  void alloc(size_t c) {
+    release();
+    if (c) CK(cudaMalloc(&p, c * sizeof(T)));
+    count = c;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count) {
+    o.p = nullptr;
+    o.count = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p;
+    count = o.count;
+    o.p = nullptr;
+    o.count = 0;
+    return *this;
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      throw Status(AIWC_ECUDA, "no CUDA device available (libaiwc_cuda has no CPU fallback)");
+    if (dev < 0 || dev >= count)
+      throw Status(AIWC_EARG, "device index " + std::to_string(dev) + " out of range");
+    cudaGetDevice(&prev);
+    CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  Stream() { CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+}  // namespace aiwc_b200
+
+using namespace aiwc_b200;
+
+// ---------------------------------------------------------------------------------
+// PreparedDataset on the device
+// ---------------------------------------------------------------------------------
+struct aiwc_ctx {
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t p = 0;
+  uint32_t rank_bytes = 2;
+  std::vector<double> y;  // host copy (OOB finalize runs the reference's row-order sums)
+  DevBuf<double> col, dy, vals;
+  DevBuf<uint32_t> order;
+  DevBuf<uint8_t> rank;
+  DevBuf<uint64_t> vals_off;
+  // grow scratch, reused across fits on this dataset (serialised by `mu`)
+  std::mutex mu;
+  DevBuf<char> scratch;
+  DevBuf<char> gbits;
+
+  DevData view() const {
+    return DevData{n, p, rank_bytes, col.p, dy.p, order.p, rank.p, vals.p, vals_off.p};
+  }
+};
+
+namespace {
+
+// per-column argsort by (value asc, row asc) (forest.hpp:148-159) + dense ranks +
+// distinct values; host threads over columns
+void presort(const double* col, uint64_t n, uint32_t p, std::vector<uint32_t>& order,
+             std::vector<uint32_t>& rank, std::vector<double>& vals,
+             std::vector<uint64_t>& vals_off) {
+  order.resize(size_t{p} * n);
+  rank.resize(size_t{p} * n);
+  std::vector<std::vector<double>> distinct(p);
+  const unsigned hw = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
+  std::atomic<uint32_t> next{0};
+  auto work = [&] {
+    for (;;) {
+      const uint32_t c = next.fetch_add(1);
+      if (c >= p) return;
+      const double* v = col + size_t{c} * n;
+      uint32_t* o = order.data() + size_t{c} * n;
+      std::iota(o, o + n, 0u);
+      std::sort(o, o + n, [&](uint32_t a, uint32_t b) {
+        if (v[a] != v[b]) return v[a] < v[b];
+        return a < b;
+      });
+      uint32_t* rk = rank.data() + size_t{c} * n;
+      auto& dv = distinct[c];
+      for (uint64_t k = 0; k < n; ++k) {
+        const double x = v[o[k]];
+        if (k == 0 || x != dv.back()) dv.push_back(x);
+        rk[o[k]] = static_cast<uint32_t>(dv.size() - 1);
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (unsigned i = 0; i < std::min<unsigned>(hw, p); ++i) th.emplace_back(work);
+  for (auto& t : th) t.join();
+  vals_off.assign(p + 1, 0);
+  for (uint32_t c = 0; c < p; ++c) vals_off[c + 1] = vals_off[c] + distinct[c].size();
+  vals.resize(vals_off[p]);
+  for (uint32_t c = 0; c < p; ++c)
+    std::copy(distinct[c].begin(), distinct[c].end(), vals.begin() + vals_off[c]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+// Forest
+// ---------------------------------------------------------------------------------
+struct aiwc_forest {
+  int device = 0;
+  uint64_t n = 0;  // training rows (inbag / oob arrays)
+  uint32_t trees = 0, tree_begin = 0;
+  uint32_t num_trees = 0, mtry = 0, mns = 0;
+  uint64_t seed = 0;
+  std::vector<uint64_t> off;  // trees+1, tree order
+  DevBuf<int32_t> feature, left;
+  DevBuf<double> thr, value;
+  DevBuf<PredNode> packed;
+  DevBuf<uint64_t> d_off;
+  DevBuf<uint32_t> inbag;  // trees x n (may be empty)
+  DevBuf<double> oobval;   // trees x n NaN = in bag (may be empty)
+  bool has_oob = false;
+  aiwc_oob_stats oob{};
+  // measurement: grow-kernel device time (CUDA events on its stream), whole fit time,
+  // sum over split nodes of their rows (the algorithmic-bytes unit)
+  double grow_ms = 0, fit_ms = 0;
+  uint64_t split_rows = 0;
+  uint32_t grow_launches = 0;
+};
+
+extern "C" {
+
+const char* aiwc_last_error(void) { return g_last_error.c_str(); }
+
+const char* aiwc_version(void) { return "aiwc-b200 1 sm_100a"; }
+
+int aiwc_device_count(int* out) {
+  return guard([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+    cudaGetLastError();
+    if (out) *out = c;
+  });
+}
+
+uint64_t aiwc_derive_seed(uint64_t seed, const char* tag, uint64_t index) {
+  return host_derive_seed(seed, tag, index);
+}
+
+int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, int device,
+                    aiwc_ctx** out) {
+  return guard([&] {
+    if (!col || !y || !out) throw Status(AIWC_EARG, "NULL argument");
+    if (n < 2) throw Status(AIWC_EEXEC, "dataset must have at least 2 rows");
+    if (p < 1 || p > 1024) throw Status(AIWC_EARG, "predictor count must be in [1, 1024]");
+    if (n >= (uint64_t{1} << 31)) throw Status(AIWC_EARG, "too many rows (max 2^31-1)");
+    for (uint64_t i = 0; i < n * p; ++i)
+      if (!std::isfinite(col[i])) throw Status(AIWC_EEXEC, "non-finite predictor value");
+    for (uint64_t i = 0; i < n; ++i)
+      if (!std::isfinite(y[i])) throw Status(AIWC_EEXEC, "non-finite response value");
+    DeviceGuard dg(device);
+    auto ctx = std::make_unique<aiwc_ctx>();
+    ctx->device = device;
+    ctx->n = n;
+    ctx->p = p;
+    ctx->y.assign(y, y + n);
+    std::vector<uint32_t> order, rank;
+    std::vector<double> vals;
+    std::vector<uint64_t> voff;
+    presort(col, n, p, order, rank, vals, voff);
+    uint64_t maxk = 0;
+    for (uint32_t c = 0; c < p; ++c) maxk = std::max(maxk, voff[c + 1] - voff[c]);
+    ctx->rank_bytes = maxk <= 65536 ? 2 : 4;
+    ctx->col.alloc(size_t{p} * n);
+    ctx->dy.alloc(n);
+    ctx->order.alloc(size_t{p} * n);
+    ctx->rank.alloc(size_t{p} * n * ctx->rank_bytes);
+    ctx->vals.alloc(vals.size());
+    ctx->vals_off.alloc(voff.size());
+    CK(cudaMemcpy(ctx->col.p, col, size_t{p} * n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->dy.p, y, n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+    if (ctx->rank_bytes == 2) {
+      std::vector<uint16_t> r16(rank.begin(), rank.end());
+      CK(cudaMemcpy(ctx->rank.p, r16.data(), r16.size() * 2, cudaMemcpyHostToDevice));
+    } else {
+      CK(cudaMemcpy(ctx->rank.p, rank.data(), rank.size() * 4, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(ctx->vals.p, vals.data(), vals.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->vals_off.p, voff.data(), voff.size() * 8, cudaMemcpyHostToDevice));
+    *out = ctx.release();
+  });
+}
+
+int aiwc_ctx_free(aiwc_ctx* ctx) {
+  if (!ctx) return AIWC_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(ctx->device);
+  delete ctx;
+  cudaSetDevice(prev);
+  return AIWC_OK;
+}
+
+int aiwc_ctx_info(const aiwc_ctx* ctx, uint64_t* n, uint32_t* p, int* device) {
+  return guard([&] {
+    if (!ctx) throw Status(AIWC_EARG, "ctx is NULL");
+    if (n) *n = ctx->n;
+    if (p) *p = ctx->p;
+    if (device) *device = ctx->device;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Per-row tree-ordered sums -> OobStats with the reference's row-order loops
+// (forest.hpp:396-453); host side so the reduction order is literally the same.
+aiwc_oob_stats finalize_oob(const double* y, uint64_t n, const double* sum,
+                            const uint32_t* count) {
+  aiwc_oob_stats st{};
+  double mean = 0;
+  for (uint64_t i = 0; i < n; ++i) mean += y[i];
+  mean /= static_cast<double>(n);
+  double var = 0;
+  bool constant = true;
+  for (uint64_t i = 0; i < n; ++i) {
+    var += (y[i] - mean) * (y[i] - mean);
+    if (y[i] != y[0]) constant = false;
+  }
+  var /= static_cast<double>(n);
+  st.response_variance = var;
+  if (constant) {
+    st.degenerate = 1;
+    return st;
+  }
+  double mse = 0;
+  uint64_t ev = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (!count[i]) continue;
+    const double pred = sum[i] / static_cast<double>(count[i]);
+    mse += (pred - y[i]) * (pred - y[i]);
+    ++ev;
+  }
+  if (ev == 0) throw Status(AIWC_EEXEC, "no out-of-bag rows: every row was in every bag");
+  mse /= static_cast<double>(ev);
+  st.mse = mse;
+  st.rows_evaluated = ev;
+  st.error_pct = 100.0 * mse / var;
+  st.r_squared = 1.0 - mse / var;
+  return st;
+}
+
+void oob_accumulate_device(aiwc_forest* f, double* row_sum, uint32_t* row_count,
+                           cudaStream_t s) {
+  const uint64_t n = f->n;
+  DevBuf<double> ds(n);
+  DevBuf<uint32_t> dc(n);
+  CK(cudaMemcpyAsync(ds.p, row_sum, n * 8, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc.p, row_count, n * 4, cudaMemcpyHostToDevice, s));
+  oob_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f->oobval.p, f->trees,
+                                                                            n, ds.p, dc.p);
+  CK(cudaGetLastError());
+  g_launches += 1;
+  CK(cudaMemcpyAsync(row_sum, ds.p, n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(row_count, dc.p, n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+}
+
+int pick_threads(uint64_t n) { return n >= 65536 ? 512 : 256; }
+
+}  // namespace
+
+extern "C" {
+
+int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
+             uint64_t seed, uint32_t tree_begin, uint32_t tree_end, int compute_oob,
+             aiwc_forest** out) {
+  return guard([&] {
+    if (!ctx || !out) throw Status(AIWC_EARG, "NULL argument");
+    // parameter checks of forest.hpp:482-490
+    if (ctx->n < 2) throw Status(AIWC_EEXEC, "dataset must have at least 2 rows");
+    if (num_trees < 1) throw Status(AIWC_EEXEC, "num_trees must be >= 1");
+    if (min_node_size < 1) throw Status(AIWC_EEXEC, "min_node_size must be >= 1");
+    if (mtry < 1 || mtry > ctx->p)
+      throw Status(AIWC_EEXEC, "mtry must be in [1, " + std::to_string(ctx->p) + "], got " +
+                                   std::to_string(mtry));
+    if (tree_begin >= tree_end || tree_end > num_trees)
+      throw Status(AIWC_EARG, "bad tree range");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    const uint64_t n = ctx->n;
+    const uint32_t p = ctx->p;
+    const uint32_t T = tree_end - tree_begin;
+    const int nt = pick_threads(n);
+
+    int dev = ctx->device, sms = 0, max_optin = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t nwords = (n + 31) / 32, nblk = (n + 63) / 64;
+    const size_t bits_smem = (((nwords + 1) & ~size_t{1}) + nblk + 2) * 4;
+    const bool smem_bits = bits_smem + 4096 <= static_cast<size_t>(max_optin);
+    const size_t dyn = smem_bits ? bits_smem : 0;
+    SlotLayout L = make_layout(n, p, mtry, min_node_size, !smem_bits);
+
+    GrowArgs a{};
+    a.d = ctx->view();
+    a.mtry = mtry;
+    a.mns = min_node_size;
+    a.seed = seed;
+    a.tag_tree = host_fnv1a64("tree", 4);
+    a.tree_begin = tree_begin;
+    a.tree_end = tree_end;
+    a.L = L;
+    a.bits_in_smem = smem_bits ? 1 : 0;
+
+    int per_sm = 0;
+    CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
+    if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    // outputs first: in-bag draws, OOB leaf values, node pool
+    auto f = std::make_unique<aiwc_forest>();
+    f->device = dev;
+    f->n = n;
+    f->trees = T;
+    f->tree_begin = tree_begin;
+    f->num_trees = num_trees;
+    f->mtry = mtry;
+    f->mns = min_node_size;
+    f->seed = seed;
+    f->inbag.alloc(size_t{T} * n);
+    f->oobval.alloc(size_t{T} * n);
+    CK(cudaMemsetAsync(f->oobval.p, 0xff, size_t{T} * n * 8, st.s));
+    a.inbag = f->inbag.p;
+    a.oobval = f->oobval.p;
+
+    uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
+    int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t pool_bytes = cap * 28;
+    const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
+    slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
+    if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
+    const size_t need = size_t(slots) * L.bytes;
+    if (ctx->scratch.count < need) ctx->scratch.alloc(need);
+    a.scratch = ctx->scratch.p;
+
+    DevBuf<uint32_t> queue(1), tree_cnt(T);
+    DevBuf<int> err(1);
+    DevBuf<uint64_t> tree_off(T);
+    a.queue = queue.p;
+    a.tree_off = tree_off.p;
+    a.tree_cnt = tree_cnt.p;
+    a.err = err.p;
+    DevBuf<int32_t> pf, pl;
+    DevBuf<double> pt, pv;
+    DevBuf<uint32_t> pr;
+    DevBuf<unsigned long long> used(1), split_rows(1);
+    a.split_rows = split_rows.p;
+    std::vector<uint32_t> cnt(T);
+    cudaEvent_t ev0, ev1, evf0, evf1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreate(&evf0));
+    CK(cudaEventCreate(&evf1));
+    struct EvGuard {
+      cudaEvent_t* e;
+      ~EvGuard() {
+        for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+      }
+    };
+    cudaEvent_t evs[4] = {ev0, ev1, evf0, evf1};
+    EvGuard eg{evs};
+    CK(cudaEventRecord(evf0, st.s));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      pf.alloc(cap);
+      pl.alloc(cap);
+      pt.alloc(cap);
+      pv.alloc(cap);
+      pr.alloc(cap);
+      a.pool_feature = pf.p;
+      a.pool_left = pl.p;
+      a.pool_thr = pt.p;
+      a.pool_value = pv.p;
+      a.pool_rank = pr.p;
+      a.pool_used = used.p;
+      a.pool_cap = cap;
+      CK(cudaMemsetAsync(queue.p, 0, 4, st.s));
+      CK(cudaMemsetAsync(err.p, 0, 4, st.s));
+      CK(cudaMemsetAsync(used.p, 0, 8, st.s));
+      CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
+      CK(cudaEventRecord(ev0, st.s));
+      CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
+      CK(cudaEventRecord(ev1, st.s));
+      g_launches += 1;
+      f->grow_launches += 1;
+      int herr = 0;
+      unsigned long long hused = 0;
+      CK(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st.s));
+      CK(cudaMemcpyAsync(&hused, used.p, 8, cudaMemcpyDeviceToHost, st.s));
+      CK(cudaStreamSynchronize(st.s));
+      {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        f->grow_ms += ms;
+      }
+      if (herr == 1 && attempt == 0) {  // pool overflow: exact size is now known
+        cap = hused;
+        continue;
+      }
+      if (herr == 2) throw Status(AIWC_EEXEC, "in-bag row count exceeded the slot bound");
+      if (herr == 3) throw Status(AIWC_EEXEC, "frontier/node capacity exceeded");
+      if (herr) throw Status(AIWC_EEXEC, "grow kernel error " + std::to_string(herr));
+      break;
+    }
+    CK(cudaMemcpy(cnt.data(), tree_cnt.p, size_t{T} * 4, cudaMemcpyDeviceToHost));
+    f->off.assign(T + 1, 0);
+    for (uint32_t t = 0; t < T; ++t) f->off[t + 1] = f->off[t] + cnt[t];
+    const uint64_t N = f->off[T];
+    f->feature.alloc(N);
+    f->left.alloc(N);
+    f->thr.alloc(N);
+    f->value.alloc(N);
+    f->packed.alloc(N);
+    f->d_off.alloc(T + 1);
+    CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, st.s));
+    compact_kernel<<<T, 256, 0, st.s>>>(pf.p, pt.p, pl.p, pv.p, tree_off.p, f->d_off.p,
+                                        f->feature.p, f->thr.p, f->left.p, f->value.p,
+                                        f->packed.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaStreamSynchronize(st.s));
+    if (compute_oob && tree_begin == 0 && tree_end == num_trees) {
+      std::vector<double> sum(n, 0.0);
+      std::vector<uint32_t> count(n, 0);
+      oob_accumulate_device(f.get(), sum.data(), count.data(), st.s);
+      f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
+      f->has_oob = true;
+    }
+    CK(cudaEventRecord(evf1, st.s));
+    CK(cudaEventSynchronize(evf1));
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, evf0, evf1));
+      f->fit_ms = ms;
+    }
+    *out = f.release();
+  });
+}
+
+int aiwc_forest_free(aiwc_forest* f) {
+  if (!f) return AIWC_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(f->device);
+  delete f;
+  cudaSetDevice(prev);
+  return AIWC_OK;
+}
+
+int aiwc_forest_info(const aiwc_forest* f, uint32_t* trees, uint64_t* total_nodes,
+                     uint32_t* tree_begin) {
+  return guard([&] {
+    if (!f) throw Status(AIWC_EARG, "forest is NULL");
+    if (trees) *trees = f->trees;
+    if (total_nodes) *total_nodes = f->off.back();
+    if (tree_begin) *tree_begin = f->tree_begin;
+  });
+}
+
+int aiwc_forest_node_counts(const aiwc_forest* f, uint64_t* counts) {
+  return guard([&] {
+    if (!f || !counts) throw Status(AIWC_EARG, "NULL argument");
+    for (uint32_t t = 0; t < f->trees; ++t) counts[t] = f->off[t + 1] - f->off[t];
+  });
+}
+
+int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature,
+                       double* threshold, int32_t* left, int32_t* right, double* value) {
+  return guard([&] {
+    if (!f) throw Status(AIWC_EARG, "forest is NULL");
+    DeviceGuard dg(f->device);
+    const uint64_t N = f->off.back();
+    if (offsets) std::copy(f->off.begin(), f->off.end(), offsets);
+    std::vector<int32_t> tmp;
+    if (feature) CK(cudaMemcpy(feature, f->feature.p, N * 4, cudaMemcpyDeviceToHost));
+    if (threshold) CK(cudaMemcpy(threshold, f->thr.p, N * 8, cudaMemcpyDeviceToHost));
+    if (left || right) {
+      tmp.resize(N);
+      CK(cudaMemcpy(tmp.data(), f->left.p, N * 4, cudaMemcpyDeviceToHost));
+      if (left) std::copy(tmp.begin(), tmp.end(), left);
+      if (right)
+        for (uint64_t i = 0; i < N; ++i) right[i] = tmp[i] < 0 ? -1 : tmp[i] + 1;
+    }
+    if (value) CK(cudaMemcpy(value, f->value.p, N * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag) {
+  return guard([&] {
+    if (!f || !inbag) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
+    DeviceGuard dg(f->device);
+    CK(cudaMemcpy(inbag, f->inbag.p, size_t{f->trees} * f->n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int aiwc_forest_oob_stats(const aiwc_forest* f, aiwc_oob_stats* out) {
+  return guard([&] {
+    if (!f || !out) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->has_oob) throw Status(AIWC_EEXEC, "forest has no OOB statistics (partial range?)");
+    *out = f->oob;
+  });
+}
+
+int aiwc_forest_import(uint32_t trees, const uint64_t* offsets, const int32_t* feature,
+                       const double* threshold, const int32_t* left, const int32_t* right,
+                       const double* value, const uint32_t* inbag, uint64_t n, int device,
+                       aiwc_forest** out) {
+  return guard([&] {
+    if (!offsets || !feature || !threshold || !left || !value || !out || trees < 1)
+      throw Status(AIWC_EARG, "NULL argument or zero trees");
+    DeviceGuard dg(device);
+    auto f = std::make_unique<aiwc_forest>();
+    f->device = device;
+    f->n = n;
+    f->trees = trees;
+    f->num_trees = trees;
+    f->off.assign(offsets, offsets + trees + 1);
+    const uint64_t N = f->off[trees];
+    std::vector<PredNode> pk(N);
+    for (uint32_t t = 0; t < trees; ++t) {
+      const uint64_t b = f->off[t], e = f->off[t + 1];
+      if (e <= b) throw Status(AIWC_EPARSE, "empty tree in model");
+      for (uint64_t i = b; i < e; ++i) {
+        const int64_t cnt = static_cast<int64_t>(e - b);
+        if (feature[i] >= 0) {
+          // BFS layout: right == left + 1, children inside the tree
+          if (left[i] < 1 || left[i] + 1 >= cnt || (right && right[i] != left[i] + 1))
+            throw Status(AIWC_EPARSE, "model tree is not in canonical BFS layout");
+        }
+        pk[i] = PredNode{feature[i] >= 0 ? threshold[i] : value[i], feature[i], left[i]};
+      }
+    }
+    f->feature.alloc(N);
+    f->left.alloc(N);
+    f->thr.alloc(N);
+    f->value.alloc(N);
+    f->packed.alloc(N);
+    f->d_off.alloc(trees + 1);
+    CK(cudaMemcpy(f->feature.p, feature, N * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->left.p, left, N * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->thr.p, threshold, N * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->value.p, value, N * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->packed.p, pk.data(), N * sizeof(PredNode), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f->d_off.p, f->off.data(), (trees + 1) * 8, cudaMemcpyHostToDevice));
+    if (inbag && n) {
+      f->inbag.alloc(size_t{trees} * n);
+      CK(cudaMemcpy(f->inbag.p, inbag, size_t{trees} * n * 4, cudaMemcpyHostToDevice));
+    }
+    *out = f.release();
+  });
+}
+
+int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum,
+             uint32_t* row_count) {
+  return guard([&] {
+    if (!ctx || !f || !out) throw Status(AIWC_EARG, "NULL argument");
+    if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    const uint64_t n = ctx->n;
+    if (!f->oobval.p) {
+      f->oobval.alloc(size_t{f->trees} * n);
+      DevBuf<uint8_t> flags(size_t{f->trees} * n);
+      CK(cudaMemsetAsync(flags.p, 0, size_t{f->trees} * n, st.s));
+      const dim3 grid(static_cast<unsigned>((n + 255) / 256), f->trees);
+      inbag_flags_kernel<<<grid, 256, 0, st.s>>>(f->inbag.p, f->trees, n, flags.p);
+      oob_walk_kernel<<<grid, 256, 0, st.s>>>(f->packed.p, f->d_off.p, flags.p, ctx->col.p, n,
+                                              f->oobval.p);
+      CK(cudaGetLastError());
+      g_launches += 2;
+      CK(cudaStreamSynchronize(st.s));
+    }
+    std::vector<double> sum(n, 0.0);
+    std::vector<uint32_t> count(n, 0);
+    oob_accumulate_device(f, sum.data(), count.data(), st.s);
+    *out = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
+    if (row_sum) std::copy(sum.begin(), sum.end(), row_sum);
+    if (row_count) std::copy(count.begin(), count.end(), row_count);
+  });
+}
+
+int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum, uint32_t* row_count) {
+  return guard([&] {
+    if (!ctx || !f || !row_sum || !row_count) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    oob_accumulate_device(f, row_sum, row_count, st.s);
+  });
+}
+
+int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
+                      const uint32_t* row_count, aiwc_oob_stats* out) {
+  return guard([&] {
+    if (!y || !row_sum || !row_count || !out) throw Status(AIWC_EARG, "NULL argument");
+    *out = finalize_oob(y, n, row_sum, row_count);
+  });
+}
+
+int aiwc_predict_device(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
+                        double* d_out) {
+  return guard([&] {
+    if (!f || (!d_rows && q) || (!d_out && q)) throw Status(AIWC_EARG, "NULL argument");
+    if (q == 0) return;
+    DeviceGuard dg(f->device);
+    Stream st;
+    predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st.s>>>(
+        f->packed.p, f->d_off.p, f->trees, d_rows, q, p, d_out);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    CK(cudaStreamSynchronize(st.s));
+  });
+}
+
+int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
+                 double* out_response) {
+  return guard([&] {
+    if (!f || (!rows && q) || (!out_response && q)) throw Status(AIWC_EARG, "NULL argument");
+    if (q == 0) return;
+    DeviceGuard dg(f->device);
+    Stream st;
+    DevBuf<double> dr(q * p), dout(q);
+    CK(cudaMemcpyAsync(dr.p, rows, q * p * 8, cudaMemcpyHostToDevice, st.s));
+    predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st.s>>>(
+        f->packed.p, f->d_off.p, f->trees, dr.p, q, p, dout.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    CK(cudaMemcpyAsync(out_response, dout.p, q * 8, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaStreamSynchronize(st.s));
+  });
+}
+
+int aiwc_evaluate(const double* col, const double* y, uint64_t n, uint32_t p,
+                  const uint32_t* kernel_of_row, uint32_t K, uint32_t num_trees,
+                  uint32_t mtry, uint32_t min_node_size, uint64_t seed, int device,
+                  double* predicted_seconds) {
+  return guard([&] {
+    if (!col || !y || !kernel_of_row || !predicted_seconds)
+      throw Status(AIWC_EARG, "NULL argument");
+    for (uint32_t k = 0; k < K; ++k) {
+      std::vector<uint64_t> train, test;
+      for (uint64_t i = 0; i < n; ++i) (kernel_of_row[i] == k ? test : train).push_back(i);
+      if (test.empty()) continue;
+      const uint64_t m = train.size();
+      std::vector<double> tc(m * p), ty(m), rows(test.size() * p), resp(test.size());
+      for (uint32_t c = 0; c < p; ++c)
+        for (uint64_t i = 0; i < m; ++i) tc[c * m + i] = col[c * n + train[i]];
+      for (uint64_t i = 0; i < m; ++i) ty[i] = y[train[i]];
+      for (uint64_t j = 0; j < test.size(); ++j)
+        for (uint32_t c = 0; c < p; ++c) rows[j * p + c] = col[c * n + test[j]];
+      aiwc_ctx* ctx = nullptr;
+      int rc = aiwc_ctx_create(tc.data(), ty.data(), m, p, device, &ctx);
+      if (rc) throw Status(rc, g_last_error);
+      std::unique_ptr<aiwc_ctx, int (*)(aiwc_ctx*)> cg(ctx, aiwc_ctx_free);
+      aiwc_forest* f = nullptr;
+      rc = aiwc_fit(ctx, num_trees, mtry, min_node_size, host_derive_seed(seed, "holdout", k),
+                    0, num_trees, 0, &f);
+      if (rc) throw Status(rc, g_last_error);
+      std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> fg(f, aiwc_forest_free);
+      rc = aiwc_predict(f, rows.data(), test.size(), p, resp.data());
+      if (rc) throw Status(rc, g_last_error);
+      for (uint64_t j = 0; j < test.size(); ++j)
+        predicted_seconds[test[j]] = std::pow(10.0, resp[j]);  // from_response, dataset.hpp:89-91
+    }
+  });
+}
+
+uint64_t aiwc_launch_count(void) { return g_launches.load(); }
+
+int aiwc_forest_profile(const aiwc_forest* f, double* grow_ms, double* fit_ms,
+                        uint64_t* split_rows, uint32_t* grow_launches) {
+  return guard([&] {
+    if (!f) throw Status(AIWC_EARG, "forest is NULL");
+    if (grow_ms) *grow_ms = f->grow_ms;
+    if (fit_ms) *fit_ms = f->fit_ms;
+    if (split_rows) *split_rows = f->split_rows;
+    if (grow_launches) *grow_launches = f->grow_launches;
+  });
+}
+
+int aiwc_make_queries(const double* d_rows, uint64_t n, uint32_t p, uint64_t q, uint64_t seed,
+                      int device, double* d_out) {
+  return guard([&] {
+    if (!d_rows || !d_out || n == 0) throw Status(AIWC_EARG, "bad argument");
+    DeviceGuard dg(device);
+    Stream st;
+    const uint64_t tag = host_fnv1a64("query", 5);
+    const uint64_t total = q * p;
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 1u << 20));
+    make_queries_kernel<<<blocks, 256, 0, st.s>>>(d_rows, n, p, q, seed, tag, d_out);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    CK(cudaStreamSynchronize(st.s));
+  });
+}
+
+}  // extern "C"

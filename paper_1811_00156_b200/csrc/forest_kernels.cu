@@ -1,0 +1,118 @@
+// Forest-level kernels: pool compaction into tree order, out-of-bag reduction,
+// out-of-bag walks for imported forests, and batched predict.
+#include <cmath>
+
+#include "device_common.cuh"
+#include "forest_kernels.cuh"
+
+namespace aiwc_b200 {
+
+// one CTA per tree: pool (completion order) -> forest arrays (tree order)
+__global__ void compact_kernel(const int32_t* __restrict__ pf, const double* __restrict__ pt,
+                               const int32_t* __restrict__ pl, const double* __restrict__ pv,
+                               const uint64_t* __restrict__ src_off,
+                               const uint64_t* __restrict__ dst_off, int32_t* __restrict__ f,
+                               double* __restrict__ thr, int32_t* __restrict__ left,
+                               double* __restrict__ val, PredNode* __restrict__ packed) {
+  const uint32_t t = blockIdx.x;
+  const uint64_t s = src_off[t], o = dst_off[t], cnt = dst_off[t + 1] - o;
+  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const int32_t fi = pf[s + i];
+    const double th = pt[s + i];
+    const int32_t le = pl[s + i];
+    const double v = pv[s + i];
+    f[o + i] = fi;
+    thr[o + i] = th;
+    left[o + i] = le;
+    val[o + i] = v;
+    packed[o + i] = PredNode{fi >= 0 ? th : v, fi, le};
+  }
+}
+
+// per row, tree-ordered sum of OOB leaf values (forest.hpp:418-435); NaN marks in-bag.
+// Continues from (sum, count) so chained partial forests reproduce the order.
+__global__ void oob_reduce_kernel(const double* __restrict__ oobval, uint32_t T, uint64_t n,
+                                  double* __restrict__ sum, uint32_t* __restrict__ count) {
+  const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  double s = sum[i];
+  uint32_t c = count[i];
+  for (uint32_t t = 0; t < T; ++t) {
+    const double v = __ldg(oobval + t * n + i);
+    if (v == v) {
+      s = __dadd_rn(s, v);
+      ++c;
+    }
+  }
+  sum[i] = s;
+  count[i] = c;
+}
+
+// OOB leaf values of an imported forest: in-bag flags from the draws, then a walk
+// over the column store with the stored f64 thresholds (Tree::predict semantics)
+__global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t T, uint64_t n,
+                                   uint8_t* __restrict__ flags) {
+  const uint64_t j = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  const uint32_t t = blockIdx.y;
+  if (j < n) flags[t * n + inbag[t * n + j]] = 1;
+}
+
+__global__ void oob_walk_kernel(const PredNode* __restrict__ nodes,
+                                const uint64_t* __restrict__ off, const uint8_t* __restrict__ flags,
+                                const double* __restrict__ col, uint64_t n,
+                                double* __restrict__ oobval) {
+  const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  const uint32_t t = blockIdx.y;
+  if (i >= n) return;
+  double v = __longlong_as_double(-1ll);  // NaN
+  if (!flags[t * n + i]) {
+    const PredNode* nd = nodes + off[t];
+    int32_t k = 0;
+    PredNode x = nd[0];
+    while (x.feature >= 0) {
+      k = col[static_cast<uint64_t>(x.feature) * n + i] <= x.thr ? x.left : x.left + 1;
+      x = nd[k];
+    }
+    v = x.thr;
+  }
+  oobval[t * n + i] = v;
+}
+
+// predict_response for q row-major rows: mean over trees, summed in tree order
+// (forest.hpp:77-81).  One query per thread; nodes stream from L2.
+__global__ void predict_kernel(const PredNode* __restrict__ nodes,
+                               const uint64_t* __restrict__ off, uint32_t T,
+                               const double* __restrict__ rows, uint64_t q, uint32_t p,
+                               double* __restrict__ out) {
+  const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  if (i >= q) return;
+  const double* x = rows + i * p;
+  double s = 0.0;
+  for (uint32_t t = 0; t < T; ++t) {
+    const PredNode* nd = nodes + __ldg(off + t);
+    PredNode v = nd[0];
+    while (v.feature >= 0) {
+      const int32_t k = __ldg(x + v.feature) <= v.thr ? v.left : v.left + 1;
+      v = nd[k];
+    }
+    s = __dadd_rn(s, v.thr);
+  }
+  out[i] = __ddiv_rn(s, static_cast<double>(T));
+}
+
+// C5 query generator: query i copies table row Rng(derive_seed(seed,"query",i)).bounded(n)
+// (first draw of that stream; rng.hpp:32-59)
+__global__ void make_queries_kernel(const double* __restrict__ rows, uint64_t n, uint32_t p,
+                                    uint64_t q, uint64_t seed, uint64_t tag,
+                                    double* __restrict__ out) {
+  const uint64_t total = q * p;
+  for (uint64_t g = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; g < total;
+       g += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t i = g / p, c = g - i * p;
+    const uint64_t key = dmix64(seed ^ tag ^ dmix64(i));
+    const uint64_t r = draw_bounded(key, 1, n);
+    out[g] = rows[r * p + c];
+  }
+}
+
+}  // namespace aiwc_b200

@@ -1,0 +1,920 @@
+// Forest grower: one persistent CTA per tree, level-synchronous growth inside the CTA.
+//
+// Reproduces TreeGrower::grow (forest.hpp:179-376) bit-exactly:
+//   * bootstrap: n counter-based splitmix64 draws (forest.hpp:184-195, rng.hpp:45-59);
+//   * per tree, the in-bag rows live in a node-grouped "payload" array and every
+//     column keeps a list of payload positions in (value, row) order, partitioned
+//     stably by node each level -- the reference's presort/partition invariant
+//     (forest.hpp:163-166, 197-209, 355-371), realised as flat CTA-wide
+//     scan+scatter passes over compacted arrays instead of per-bucket loops;
+//   * split scan: one warp (or, for nodes < kLaneMax rows, one lane) per
+//     (node, sampled column) chain; the running sum sl is accumulated strictly
+//     sequentially in FP64 (warp-shuffle chain, no reassociation) so every gain is
+//     bit-identical to forest.hpp:277-296; wl is an exact integer prefix;
+//   * first-max argmax over (column slot, position), threshold midpoint rule
+//     (forest.hpp:282-283, 287);
+//   * children numbered in frontier order (BFS ids, forest.hpp:310-318);
+//   * child sums accumulated in column-0 list order (forest.hpp:326-344);
+//   * mtry draws: exactly mtry per eligible node, counter = n + mtry*(BFS index
+//     among eligible nodes) (forest.hpp:255-266).
+// All FP64 arithmetic uses explicit _rn intrinsics (no FMA contraction).
+// Row routing compares dense value ranks: x <= thr  <=>  rank(x) <= thr_rank,
+// thr_rank = largest distinct-value rank with value <= thr (exact for every
+// training row).
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+
+#include "device_common.cuh"
+#include "forest_kernels.cuh"
+#include "grow.cuh"
+
+namespace aiwc_b200 {
+
+namespace {
+
+constexpr uint32_t kLaneMax = 48;  // nodes below this size use one lane per chain
+constexpr uint32_t kMaxP = 1024;
+
+__device__ __forceinline__ uint32_t get_bit(const uint32_t* bits, uint32_t i) {
+  return (bits[i >> 5] >> (i & 31u)) & 1u;
+}
+
+__device__ __forceinline__ void put_bit(uint32_t* bits, uint32_t i, bool v) {
+  const uint32_t m = 1u << (i & 31u);
+  if (v)
+    atomicOr(bits + (i >> 5), m);
+  else
+    atomicAnd(bits + (i >> 5), ~m);
+}
+
+template <typename RankT>
+__device__ __forceinline__ uint32_t rank_of(const RankT* rank_c, uint32_t row) {
+  return static_cast<uint32_t>(__ldg(rank_c + row));
+}
+
+__device__ __forceinline__ double gain_at(double sl, double wl, double W, double S) {
+  // sl*sl/wl + (sum-sl)*(sum-sl)/wr   (forest.hpp:284-286)
+  const double wr = __dsub_rn(W, wl);
+  const double d = __dsub_rn(S, sl);
+  return __dadd_rn(__ddiv_rn(__dmul_rn(sl, sl), wl), __ddiv_rn(__dmul_rn(d, d), wr));
+}
+
+// ---- split chain, warp-cooperative (large nodes) --------------------------------
+template <typename RankT, int G>
+__device__ void chain_warp(const uint32_t* __restrict__ list, uint32_t b, uint32_t e,
+                           const Payload* __restrict__ pay, const RankT* __restrict__ rk_c,
+                           double W, double S, double& best_gain, uint32_t& best_pos) {
+  const unsigned lane = lane_id();
+  double sl = 0.0;
+  uint32_t wl = 0, prev_rank = 0;
+  bool first = true;
+  double bg = -INFINITY;
+  uint32_t bp = 0xffffffffu;
+  for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
+    uint32_t q[G], rk[G], mu[G];
+    double wy[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      q[g] = k < e ? __ldg(list + k) : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      if (k < e) {
+        const Payload P = pay[q[g]];
+        q[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+      } else {
+        mu[g] = 0;
+        wy[g] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      rk[g] = k < e ? rank_of(rk_c, q[g]) : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      if (t0 >= e) break;
+      const uint32_t nv = min(32u, e - t0);
+      const bool valid = lane < nv;
+      const uint32_t inc = warp_incl_scan(mu[g]);
+      const uint32_t wl_before = wl + inc - mu[g];
+      double run = sl, mine = 0.0;
+      for (uint32_t j = 0; j < nv; ++j) {
+        const double a = __shfl_sync(kFull, wy[g], j);
+        if (lane == j) mine = run;
+        run = __dadd_rn(run, a);
+      }
+      uint32_t pr = __shfl_up_sync(kFull, rk[g], 1);
+      if (lane == 0) pr = first ? rk[g] : prev_rank;
+      if (valid && rk[g] != pr) {
+        const double gn = gain_at(mine, static_cast<double>(wl_before), W, S);
+        if (gn > bg) {
+          bg = gn;
+          bp = t0 + lane;
+        }
+      }
+      sl = run;
+      wl += __shfl_sync(kFull, inc, 31);
+      prev_rank = __shfl_sync(kFull, rk[g], nv - 1);
+      first = false;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double og = __shfl_xor_sync(kFull, bg, o);
+    const uint32_t op = __shfl_xor_sync(kFull, bp, o);
+    if (og > bg || (og == bg && op < bp)) {
+      bg = og;
+      bp = op;
+    }
+  }
+  best_gain = bg;
+  best_pos = bp;
+}
+
+// ---- split chain, one lane (small nodes) ----------------------------------------
+template <typename RankT>
+__device__ void chain_lane(const uint32_t* __restrict__ list, uint32_t b, uint32_t e,
+                           const Payload* __restrict__ pay, const RankT* __restrict__ rk_c,
+                           double W, double S, double& best_gain, uint32_t& best_pos) {
+  double sl = 0.0, bg = -INFINITY;
+  uint32_t wl = 0, prev = 0, bp = 0xffffffffu;
+  for (uint32_t k = b; k < e; k += 4) {
+    uint32_t q[4], rk[4], mu[4];
+    double wy[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? __ldg(list + k + g) : 0u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (k + g < e) {
+        const Payload P = pay[q[g]];
+        q[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+      } else {
+        mu[g] = 0;
+        wy[g] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) rk[g] = k + g < e ? rank_of(rk_c, q[g]) : 0u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint32_t kk = k + g;
+      if (kk >= e) break;
+      if (kk > b && rk[g] != prev) {
+        const double gn = gain_at(sl, static_cast<double>(wl), W, S);
+        if (gn > bg) {
+          bg = gn;
+          bp = kk;
+        }
+      }
+      wl += mu[g];
+      sl = __dadd_rn(sl, wy[g]);
+      prev = rk[g];
+    }
+  }
+  best_gain = bg;
+  best_pos = bp;
+}
+
+struct RouteOut {
+  uint32_t nl;
+  uint32_t wl, wr;
+  double sl, ql, sr, qr;
+};
+
+// ---- route + child sums in column-0 order, warp-cooperative ---------------------
+template <typename RankT, int G>
+__device__ RouteOut route_warp(const uint32_t* __restrict__ list0, uint32_t b, uint32_t e,
+                               const Payload* __restrict__ pay,
+                               const double* __restrict__ wyy,
+                               const RankT* __restrict__ rk_f, uint32_t thr_rank,
+                               uint32_t* bits) {
+  const unsigned lane = lane_id();
+  RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+  for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
+    uint32_t q[G], row[G], mu[G];
+    double wy[G], yy[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      q[g] = k < e ? __ldg(list0 + k) : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      if (k < e) {
+        const Payload P = pay[q[g]];
+        row[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+        yy[g] = wyy[q[g]];
+      } else {
+        row[g] = 0;
+        mu[g] = 0;
+        wy[g] = 0.0;
+        yy[g] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      if (t0 >= e) break;
+      const uint32_t nv = min(32u, e - t0);
+      const bool valid = lane < nv;
+      const bool left = valid && rank_of(rk_f, row[g]) <= thr_rank;
+      if (valid) put_bit(bits, q[g], left);
+      const unsigned bl = __ballot_sync(kFull, left);
+      o.nl += __popc(bl);
+      o.wl += warp_sum(left ? mu[g] : 0u);
+      o.wr += warp_sum((valid && !left) ? mu[g] : 0u);
+      for (uint32_t j = 0; j < nv; ++j) {
+        const double a = __shfl_sync(kFull, wy[g], j);
+        const double c = __shfl_sync(kFull, yy[g], j);
+        if ((bl >> j) & 1u) {
+          o.sl = __dadd_rn(o.sl, a);
+          o.ql = __dadd_rn(o.ql, c);
+        } else {
+          o.sr = __dadd_rn(o.sr, a);
+          o.qr = __dadd_rn(o.qr, c);
+        }
+      }
+    }
+  }
+  return o;
+}
+
+template <typename RankT>
+__device__ RouteOut route_lane(const uint32_t* __restrict__ list0, uint32_t b, uint32_t e,
+                               const Payload* __restrict__ pay,
+                               const double* __restrict__ wyy,
+                               const RankT* __restrict__ rk_f, uint32_t thr_rank,
+                               uint32_t* bits) {
+  RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+  for (uint32_t k = b; k < e; k += 4) {
+    uint32_t q[4], row[4], mu[4];
+    double wy[4], yy[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? __ldg(list0 + k + g) : 0u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (k + g < e) {
+        const Payload P = pay[q[g]];
+        row[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+        yy[g] = wyy[q[g]];
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (k + g >= e) break;
+      const bool left = rank_of(rk_f, row[g]) <= thr_rank;
+      put_bit(bits, q[g], left);
+      if (left) {
+        ++o.nl;
+        o.wl += mu[g];
+        o.sl = __dadd_rn(o.sl, wy[g]);
+        o.ql = __dadd_rn(o.ql, yy[g]);
+      } else {
+        o.wr += mu[g];
+        o.sr = __dadd_rn(o.sr, wy[g]);
+        o.qr = __dadd_rn(o.qr, yy[g]);
+      }
+    }
+  }
+  return o;
+}
+
+// sequential FP64 sums over the payload in row order (root stats, forest.hpp:221-226)
+template <int G>
+__device__ void root_sums_warp(const Payload* __restrict__ pay, const double* __restrict__ wyy,
+                               uint32_t A, double& s_out, double& q_out) {
+  const unsigned lane = lane_id();
+  double s = 0.0, q = 0.0;
+  for (uint32_t k0 = 0; k0 < A; k0 += 32 * G) {
+    double a[G], c[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      a[g] = k < A ? pay[k].wy : 0.0;
+      c[g] = k < A ? wyy[k] : 0.0;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      if (t0 >= A) break;
+      const uint32_t nv = min(32u, A - t0);
+      for (uint32_t j = 0; j < nv; ++j) {
+        s = __dadd_rn(s, __shfl_sync(kFull, a[g], j));
+        q = __dadd_rn(q, __shfl_sync(kFull, c[g], j));
+      }
+    }
+  }
+  s_out = s;
+  q_out = q;
+}
+
+}  // namespace
+
+template <int NT, typename RankT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const GrowArgs a) {
+  constexpr int NW = NT / 32;
+  constexpr int G = 4;
+  extern __shared__ uint32_t dyn_smem[];
+  __shared__ uint32_t sh_scan[NW + 2];
+  __shared__ uint32_t s_tree, s_A, s_F, s_E, s_S, s_nodes, s_totL, s_err;
+  __shared__ double s_root[2];
+  __shared__ unsigned long long s_pool;
+
+  const DevData& d = a.d;
+  const uint32_t n = static_cast<uint32_t>(d.n);
+  const uint32_t p = d.p;
+  const uint32_t m = a.mtry;
+  const uint32_t tid = threadIdx.x;
+  const unsigned lane = lane_id();
+  const unsigned wid = warp_id();
+  const SlotLayout& L = a.L;
+  const uint32_t stride = L.stride;
+
+  char* slot = a.scratch + static_cast<size_t>(blockIdx.x) * L.bytes;
+  uint32_t* mult_g = reinterpret_cast<uint32_t*>(slot + L.off_mult);
+  Payload* pay[2] = {reinterpret_cast<Payload*>(slot + L.off_pay0),
+                     reinterpret_cast<Payload*>(slot + L.off_pay1)};
+  double* wyy[2] = {reinterpret_cast<double*>(slot + L.off_wyy0),
+                    reinterpret_cast<double*>(slot + L.off_wyy1)};
+  uint32_t* lists[2] = {reinterpret_cast<uint32_t*>(slot + L.off_list0),
+                        reinterpret_cast<uint32_t*>(slot + L.off_list1)};
+  uint32_t* newpos = reinterpret_cast<uint32_t*>(slot + L.off_newpos);
+  uint32_t* seg[2] = {reinterpret_cast<uint32_t*>(slot + L.off_seg0),
+                      reinterpret_cast<uint32_t*>(slot + L.off_seg1)};
+  NodeWork* front[2] = {reinterpret_cast<NodeWork*>(slot + L.off_front0),
+                        reinterpret_cast<NodeWork*>(slot + L.off_front1)};
+  SegTab* segtab = reinterpret_cast<SegTab*>(slot + L.off_segtab);
+  uint32_t* e2f = reinterpret_cast<uint32_t*>(slot + L.off_e2f);
+  uint16_t* samp = reinterpret_cast<uint16_t*>(slot + L.off_samp);
+  ChainRes* res = reinterpret_cast<ChainRes*>(slot + L.off_res);
+  SplitInfo* spl = reinterpret_cast<SplitInfo*>(slot + L.off_split);
+  int32_t* nf = reinterpret_cast<int32_t*>(slot + L.off_nf);
+  double* nthr = reinterpret_cast<double*>(slot + L.off_nthr);
+  int32_t* nleft = reinterpret_cast<int32_t*>(slot + L.off_nleft);
+  double* nval = reinterpret_cast<double*>(slot + L.off_nval);
+  uint32_t* nrank = reinterpret_cast<uint32_t*>(slot + L.off_nrank);
+  const uint32_t nwords = (n + 31u) / 32u;
+  const uint32_t nblk64 = (n + 63u) / 64u;
+  uint32_t* bits = a.bits_in_smem ? dyn_smem : reinterpret_cast<uint32_t*>(slot + L.off_gbits);
+  uint32_t* pref = a.bits_in_smem ? dyn_smem + ((nwords + 1u) & ~1u)
+                                  : reinterpret_cast<uint32_t*>(slot + L.off_gpref);
+  const RankT* rank = static_cast<const RankT*>(d.rank);
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) {
+      s_tree = atomicAdd(a.queue, 1u);
+      s_err = 0;
+    }
+    __syncthreads();
+    const uint32_t tl = s_tree;
+    if (tl >= a.tree_end - a.tree_begin) break;
+    const uint64_t t = a.tree_begin + tl;
+    const uint64_t key = dmix64(a.seed ^ a.tag_tree ^ dmix64(t));
+
+    // ---- bootstrap (forest.hpp:184-195) ----
+    for (uint32_t i = tid; i < n; i += NT) mult_g[i] = 0u;
+    __syncthreads();
+    for (uint32_t j = tid; j < n; j += NT) {
+      const uint32_t r = static_cast<uint32_t>(draw_bounded(key, uint64_t{j} + 1u, n));
+      if (a.inbag) a.inbag[static_cast<size_t>(tl) * n + j] = r;
+      atomicAdd(mult_g + r, 1u);
+    }
+    __syncthreads();
+    // in-bag bitmap by row + 64-row prefix counts
+    for (uint32_t w = wid; w < nwords; w += NW) {
+      const uint32_t r = w * 32u + lane;
+      const unsigned bl = __ballot_sync(kFull, r < n && mult_g[r] > 0u);
+      if (lane == 0) bits[w] = bl;
+    }
+    __syncthreads();
+    {
+      uint32_t carry = 0;
+      for (uint32_t base = 0; base < nblk64; base += NT) {
+        const uint32_t i = base + tid;
+        uint32_t v = 0;
+        if (i < nblk64)
+          v = __popc(bits[2 * i]) + (2 * i + 1 < nwords ? __popc(bits[2 * i + 1]) : 0u);
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan<NT>(v, sh_scan, &tot);
+        if (i < nblk64) pref[i] = carry + ex;
+        carry += tot;
+      }
+      if (tid == 0) s_A = carry;
+    }
+    __syncthreads();
+    const uint32_t A0 = s_A;
+    if (A0 > stride) {
+      if (tid == 0) atomicExch(a.err, 2);
+      continue;
+    }
+    // payload in row order (forest.hpp:194-195: weighted_y = mult*y)
+    for (uint32_t r = tid; r < n; r += NT) {
+      if (!get_bit(bits, r)) continue;
+      const uint32_t w = r >> 5;
+      const uint32_t pos = pref[r >> 6] + ((w & 1u) ? __popc(bits[w - 1]) : 0u) +
+                           __popc(bits[w] & ((1u << (r & 31u)) - 1u));
+      const uint32_t mu = mult_g[r];
+      const double yr = __ldg(d.y + r);
+      const double wy = __dmul_rn(static_cast<double>(mu), yr);
+      pay[0][pos] = Payload{r, mu, wy};
+      wyy[0][pos] = __dmul_rn(wy, yr);
+      seg[0][pos] = 0u;
+    }
+    __syncthreads();
+    // root sums (warp 0) || per-column in-bag filter of the presort (other warps)
+    if (wid == 0) {
+      double s, q;
+      root_sums_warp<G>(pay[0], wyy[0], A0, s, q);
+      if (lane == 0) {
+        s_root[0] = s;
+        s_root[1] = q;
+      }
+    } else {
+      for (uint32_t c = wid - 1; c < p; c += NW - 1) {
+        const uint32_t* ord = d.order + static_cast<size_t>(c) * n;
+        uint32_t* out = lists[0] + static_cast<size_t>(c) * stride;
+        uint32_t o = 0;
+        for (uint32_t k0 = 0; k0 < n; k0 += 32 * G) {
+          uint32_t r[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t k = k0 + g * 32 + lane;
+            r[g] = k < n ? __ldg(ord + k) : 0u;
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t k = k0 + g * 32 + lane;
+            const bool in = k < n && get_bit(bits, r[g]);
+            const unsigned bl = __ballot_sync(kFull, in);
+            if (in) {
+              const uint32_t rr = r[g], w = rr >> 5;
+              const uint32_t pos = pref[rr >> 6] + ((w & 1u) ? __popc(bits[w - 1]) : 0u) +
+                                   __popc(bits[w] & ((1u << (rr & 31u)) - 1u));
+              out[o + __popc(bl & lanemask_lt())] = pos;
+            }
+            o += __popc(bl);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      front[0][0] = NodeWork{0u, A0, 0u, 0u, static_cast<double>(n), s_root[0], s_root[1]};
+      nf[0] = -1;
+      nthr[0] = 0.0;
+      nleft[0] = -1;
+      nval[0] = 0.0;
+      nrank[0] = 0u;
+      s_F = 1;
+      s_nodes = 1;
+    }
+    __syncthreads();
+
+    // ---- level loop (forest.hpp:233-374) ----
+    uint32_t cur = 0, A = A0;
+    uint64_t elig_base = 0;
+    unsigned long long split_rows_acc = 0;  // meaningful in thread 0 only
+    for (;;) {
+      const uint32_t F = s_F;
+      const NodeWork* fr = front[cur];
+      // leaf tests + eligible compaction (forest.hpp:244-253)
+      {
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < F; base += NT) {
+          const uint32_t f = base + tid;
+          uint32_t el = 0;
+          if (f < F) {
+            const NodeWork nw = fr[f];
+            const double sse = __dsub_rn(nw.q, __ddiv_rn(__dmul_rn(nw.s, nw.s), nw.w));
+            const bool too_small = nw.w < 2.0 * static_cast<double>(a.mns);
+            const bool pure = sse <= __dmul_rn(1e-12, nw.q > 1.0 ? nw.q : 1.0);
+            if (too_small || pure)
+              nval[nw.id] = __ddiv_rn(nw.s, nw.w);
+            else
+              el = 1;
+            segtab[f].offL = INT_MIN;
+          }
+          uint32_t tot;
+          const uint32_t ex = block_excl_scan<NT>(el, sh_scan, &tot);
+          if (el) e2f[carry + ex] = f;
+          carry += tot;
+        }
+        if (tid == 0) s_E = carry;
+      }
+      __syncthreads();
+      const uint32_t E = s_E;
+      // mtry sampling: partial Fisher-Yates over a fresh pool, then ascending
+      // (forest.hpp:258-266); counters continue the tree's stream after the n
+      // bootstrap draws, m per eligible node in BFS order
+      for (uint32_t e = tid; e < E; e += NT) {
+        uint16_t pool[kMaxP];
+        for (uint32_t c = 0; c < p; ++c) pool[c] = static_cast<uint16_t>(c);
+        const uint64_t ctr = uint64_t{n} + (elig_base + e) * m;
+        for (uint32_t i = 0; i < m; ++i) {
+          const uint32_t j = i + static_cast<uint32_t>(draw_bounded(key, ctr + i + 1, p - i));
+          const uint16_t tmp = pool[i];
+          pool[i] = pool[j];
+          pool[j] = tmp;
+        }
+        for (uint32_t i = 1; i < m; ++i)
+          for (uint32_t k = i; k > 0 && pool[k - 1] > pool[k]; --k) {
+            const uint16_t tmp = pool[k];
+            pool[k] = pool[k - 1];
+            pool[k - 1] = tmp;
+          }
+        for (uint32_t i = 0; i < m; ++i) samp[static_cast<size_t>(e) * m + i] = pool[i];
+      }
+      __syncthreads();
+      // split chains (forest.hpp:268-297)
+      const uint32_t ntask = E * m;
+      for (uint32_t k = wid; k < ntask; k += NW) {
+        const NodeWork nw = fr[e2f[k / m]];
+        if (nw.e - nw.b < kLaneMax) continue;
+        const uint32_t c = samp[k];
+        double bg;
+        uint32_t bp;
+        chain_warp<RankT, G>(lists[cur] + static_cast<size_t>(c) * stride, nw.b, nw.e,
+                             pay[cur], rank + static_cast<size_t>(c) * n, nw.w, nw.s, bg,
+                             bp);
+        if (lane == 0) res[k] = ChainRes{bg, bp, 0u};
+      }
+      for (uint32_t k = tid; k < ntask; k += NT) {
+        const NodeWork nw = fr[e2f[k / m]];
+        if (nw.e - nw.b >= kLaneMax) continue;
+        const uint32_t c = samp[k];
+        double bg;
+        uint32_t bp;
+        chain_lane<RankT>(lists[cur] + static_cast<size_t>(c) * stride, nw.b, nw.e,
+                          pay[cur], rank + static_cast<size_t>(c) * n, nw.w, nw.s, bg, bp);
+        res[k] = ChainRes{bg, bp, 0u};
+      }
+      __syncthreads();
+      // decide + number children in frontier order (forest.hpp:299-319)
+      {
+        const uint32_t nodes0 = s_nodes;
+        uint32_t carry = 0, ccarry = 0;
+        for (uint32_t base = 0; base < E; base += NT) {
+          const uint32_t e = base + tid;
+          uint32_t sp = 0, c = 0, thr_rank = 0;
+          double thr = 0.0;
+          NodeWork nw{};
+          if (e < E) {
+            nw = fr[e2f[e]];
+            double bg = -INFINITY;
+            uint32_t bi = 0, bp = 0;
+            for (uint32_t i = 0; i < m; ++i) {
+              const ChainRes r = res[static_cast<size_t>(e) * m + i];
+              if (r.gain > bg) {
+                bg = r.gain;
+                bi = i;
+                bp = r.pos;
+              }
+            }
+            if (bg == -INFINITY) {
+              nval[nw.id] = __ddiv_rn(nw.s, nw.w);  // all sampled columns constant
+            } else {
+              sp = 1;
+              c = samp[static_cast<size_t>(e) * m + bi];
+              const uint32_t* lc = lists[cur] + static_cast<size_t>(c) * stride;
+              const uint32_t r1 = pay[cur][lc[bp - 1]].row;
+              const uint32_t r0 = pay[cur][lc[bp]].row;
+              const double prev = d.col[static_cast<size_t>(c) * n + r1];
+              const double v = d.col[static_cast<size_t>(c) * n + r0];
+              thr = __dadd_rn(prev, __ddiv_rn(__dsub_rn(v, prev), 2.0));
+              if (thr >= v) thr = prev;
+              // largest distinct-value rank whose value <= thr
+              const double* vals = d.vals + d.vals_off[c];
+              uint32_t lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
+              uint32_t hi = rank_of(rank + static_cast<size_t>(c) * n, r0);  // vals[hi] > thr
+              while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (vals[mid] <= thr) lo = mid; else hi = mid;
+              }
+              thr_rank = lo;
+            }
+          }
+          uint32_t tot;
+          const uint32_t ex = block_excl_scan<NT>(sp, sh_scan, &tot);
+          const uint32_t cnt = sp ? nw.e - nw.b : 0u;
+          uint32_t ctot;
+          const uint32_t cex = block_excl_scan<NT>(cnt, sh_scan, &ctot);
+          if (sp) {
+            const uint32_t s = carry + ex;
+            const uint32_t child = nodes0 + 2 * s;
+            nf[nw.id] = static_cast<int32_t>(c);
+            nthr[nw.id] = thr;
+            nleft[nw.id] = static_cast<int32_t>(child);
+            nrank[nw.id] = thr_rank;
+            for (uint32_t h = 0; h < 2; ++h) {
+              nf[child + h] = -1;
+              nthr[child + h] = 0.0;
+              nleft[child + h] = -1;
+              nval[child + h] = 0.0;
+              nrank[child + h] = 0u;
+            }
+            spl[s] = SplitInfo{e2f[e], c, thr_rank, cnt, 0u, ccarry + cex, 0u, 0u};
+          }
+          carry += tot;
+          ccarry += ctot;
+        }
+        if (tid == 0) {
+          s_S = carry;
+          s_nodes = nodes0 + 2 * carry;
+          s_A = ccarry;
+          split_rows_acc += ccarry;
+        }
+      }
+      __syncthreads();
+      const uint32_t S = s_S;
+      elig_base += E;
+      if (S == 0) break;
+      if (s_nodes > L.nodes_cap || 2 * S > L.fmax) {
+        if (tid == 0) atomicExch(a.err, 3);
+        s_err = 1;
+        break;
+      }
+      const uint32_t nxt = cur ^ 1u;
+      // route rows of every split node through column-0 order (forest.hpp:323-352)
+      {
+        const uint32_t* l0 = lists[cur];
+        for (uint32_t s = wid; s < S; s += NW) {
+          const SplitInfo si = spl[s];
+          const NodeWork nw = fr[si.f];
+          if (si.cnt < kLaneMax) continue;
+          const RouteOut o = route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], wyy[cur],
+                                                  rank + static_cast<size_t>(si.c) * n,
+                                                  si.thr_rank, bits);
+          if (lane == 0) {
+            spl[s].nl = o.nl;
+            const uint32_t child = static_cast<uint32_t>(nleft[nw.id]);
+            front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
+                                         static_cast<double>(o.wl), o.sl, o.ql};
+            front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1,
+                                             0u, static_cast<double>(o.wr), o.sr, o.qr};
+          }
+        }
+        for (uint32_t s = tid; s < S; s += NT) {
+          const SplitInfo si = spl[s];
+          if (si.cnt >= kLaneMax) continue;
+          const NodeWork nw = fr[si.f];
+          const RouteOut o = route_lane<RankT>(l0, nw.b, nw.e, pay[cur], wyy[cur],
+                                               rank + static_cast<size_t>(si.c) * n,
+                                               si.thr_rank, bits);
+          spl[s].nl = o.nl;
+          const uint32_t child = static_cast<uint32_t>(nleft[nw.id]);
+          front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
+                                       static_cast<double>(o.wl), o.sl, o.ql};
+          front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
+                                           static_cast<double>(o.wr), o.sr, o.qr};
+        }
+      }
+      __syncthreads();
+      // segment table: offsets of the stable partition into compacted children
+      {
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < S; base += NT) {
+          const uint32_t s = base + tid;
+          const uint32_t nl = s < S ? spl[s].nl : 0u;
+          uint32_t tot;
+          const uint32_t ex = block_excl_scan<NT>(nl, sh_scan, &tot);
+          if (s < S) {
+            const SplitInfo si = spl[s];
+            const uint32_t bL = carry + ex;  // lefts before this segment
+            const uint32_t b = fr[si.f].b;
+            segtab[si.f] = SegTab{static_cast<int32_t>(si.base) - static_cast<int32_t>(bL),
+                                  static_cast<int32_t>(si.base + nl) -
+                                      static_cast<int32_t>(b) + static_cast<int32_t>(bL),
+                                  2 * s, 0u};
+          }
+          carry += tot;
+        }
+        if (tid == 0) s_totL = carry;
+      }
+      __syncthreads();
+      // payload pass: stable multi-segment partition of the payload (+ newpos map)
+      {
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < A; base += NT * 4) {
+          uint32_t f4[4], lf = 0, keep = 0;
+          const uint32_t k0 = base + tid * 4;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t k = k0 + g;
+            f4[g] = k < A ? seg[cur][k] : 0u;
+            const bool kp = k < A && segtab[f4[g]].offL != INT_MIN;
+            const bool l = kp && get_bit(bits, k);
+            keep |= (kp ? 1u : 0u) << g;
+            lf |= (l ? 1u : 0u) << g;
+          }
+          uint32_t tot;
+          uint32_t pl = carry + block_excl_scan<NT>(__popc(lf), sh_scan, &tot);
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t k = k0 + g;
+            if (!((keep >> g) & 1u)) continue;
+            const SegTab tb = segtab[f4[g]];
+            const bool l = (lf >> g) & 1u;
+            const uint32_t dst = l ? static_cast<uint32_t>(tb.offL + static_cast<int32_t>(pl))
+                                   : static_cast<uint32_t>(tb.offR + static_cast<int32_t>(k) -
+                                                           static_cast<int32_t>(pl));
+            if (l) ++pl;
+            pay[nxt][dst] = pay[cur][k];
+            wyy[nxt][dst] = wyy[cur][k];
+            seg[nxt][dst] = tb.child + (l ? 0u : 1u);
+            newpos[k] = dst;
+          }
+          carry += tot;
+        }
+      }
+      __syncthreads();
+      // list pass: the same partition applied to every column list, flattened
+      // over (column, position) with a per-column left-count offset c*totL
+      {
+        const uint32_t A4 = (A + 3u) & ~3u;
+        const uint64_t total = uint64_t{p} * A4;
+        const uint32_t totL = s_totL;
+        uint64_t carry = 0;
+        for (uint64_t base = 0; base < total; base += NT * 4) {
+          const uint64_t g0 = base + uint64_t{tid} * 4;
+          uint32_t q4[4] = {0, 0, 0, 0}, f4[4] = {0, 0, 0, 0}, lf = 0, keep = 0;
+          uint32_t c = 0, k0 = 0;
+          if (g0 < total) {
+            c = static_cast<uint32_t>(g0 / A4);
+            k0 = static_cast<uint32_t>(g0 - uint64_t{c} * A4);
+            const uint4 v = *reinterpret_cast<const uint4*>(lists[cur] +
+                                                            static_cast<size_t>(c) * stride + k0);
+            q4[0] = v.x; q4[1] = v.y; q4[2] = v.z; q4[3] = v.w;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const uint32_t k = k0 + g;
+              if (k < A) {
+                f4[g] = seg[cur][k];
+                const bool kp = segtab[f4[g]].offL != INT_MIN;
+                keep |= (kp ? 1u : 0u) << g;
+                lf |= ((kp && get_bit(bits, q4[g])) ? 1u : 0u) << g;
+              }
+            }
+          }
+          uint32_t tot;
+          const uint32_t ex = block_excl_scan<NT>(__popc(lf), sh_scan, &tot);
+          uint32_t pl = static_cast<uint32_t>(carry + ex - uint64_t{c} * totL);
+          uint32_t* dstl = lists[nxt] + static_cast<size_t>(c) * stride;
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            if (!((keep >> g) & 1u)) continue;
+            const uint32_t k = k0 + g;
+            const SegTab tb = segtab[f4[g]];
+            const bool l = (lf >> g) & 1u;
+            const uint32_t dst = l ? static_cast<uint32_t>(tb.offL + static_cast<int32_t>(pl))
+                                   : static_cast<uint32_t>(tb.offR + static_cast<int32_t>(k) -
+                                                           static_cast<int32_t>(pl));
+            if (l) ++pl;
+            dstl[dst] = newpos[q4[g]];
+          }
+          carry += tot;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) s_F = 2 * S;
+      A = s_A;
+      cur = nxt;
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_err) continue;
+
+    // ---- emit the tree: BFS node SoA into the forest pool ----
+    const uint32_t count = s_nodes;
+    if (tid == 0) {
+      const unsigned long long off = atomicAdd(a.pool_used, static_cast<unsigned long long>(count));
+      s_pool = off;
+      a.tree_off[tl] = off;
+      a.tree_cnt[tl] = count;
+      atomicAdd(a.split_rows, split_rows_acc);
+      if (off + count > a.pool_cap) atomicExch(a.err, 1);
+    }
+    __syncthreads();
+    const unsigned long long off = s_pool;
+    if (off + count <= a.pool_cap) {
+      for (uint32_t i = tid; i < count; i += NT) {
+        const int32_t fi = nf[i];
+        a.pool_feature[off + i] = fi;
+        a.pool_thr[off + i] = nthr[i];
+        a.pool_left[off + i] = nleft[i];
+        a.pool_value[off + i] = nval[i];
+        a.pool_rank[off + i] = nrank[i];
+      }
+    }
+    // ---- out-of-bag leaf values (walk per OOB row, forest.hpp:418-435) ----
+    if (a.oobval) {
+      double* ov = a.oobval + static_cast<size_t>(tl) * n;
+      for (uint32_t r = tid; r < n; r += NT) {
+        if (mult_g[r]) continue;
+        int32_t i = 0;
+        int32_t fi = nf[0];
+        while (fi >= 0) {
+          const bool left = rank_of(rank + static_cast<size_t>(fi) * n, r) <= nrank[i];
+          i = nleft[i] + (left ? 0 : 1);
+          fi = nf[i];
+        }
+        ov[r] = nval[i];
+      }
+    }
+  }
+}
+
+namespace {
+template <int NT, typename RankT>
+cudaError_t launch_t(const GrowArgs& a, int slots, size_t smem, cudaStream_t st,
+                     int* blocks_per_sm) {
+  auto k = grow_kernel<NT, RankT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  if (blocks_per_sm) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k, NT, smem);
+  k<<<slots, NT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+}  // namespace
+
+// slots == 0 with blocks_per_sm != nullptr: occupancy query only
+cudaError_t launch_grow(int nt, int rank_bytes, const GrowArgs& a, int slots, size_t smem,
+                        cudaStream_t st, int* blocks_per_sm) {
+  if (nt == 512)
+    return rank_bytes == 2 ? launch_t<512, uint16_t>(a, slots, smem, st, blocks_per_sm)
+                           : launch_t<512, uint32_t>(a, slots, smem, st, blocks_per_sm);
+  return rank_bytes == 2 ? launch_t<256, uint16_t>(a, slots, smem, st, blocks_per_sm)
+                         : launch_t<256, uint32_t>(a, slots, smem, st, blocks_per_sm);
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool gbits) {
+  SlotLayout L{};
+  // in-bag distinct rows: 0.632 n on average; bound it generously (checked at run time)
+  const double exp_a = 0.6322 * static_cast<double>(n) + 8.0 * std::sqrt(static_cast<double>(n)) + 64.0;
+  uint64_t stride = static_cast<uint64_t>(exp_a);
+  if (stride > n) stride = n;
+  stride = (stride + 3) & ~uint64_t{3};
+  L.stride = static_cast<uint32_t>(stride);
+  // a splittable node weighs >= 2*mns, so a level has <= n/(2 mns) eligible nodes
+  // and <= n/mns frontier nodes
+  const uint64_t emax = std::min<uint64_t>(stride, n / (2 * uint64_t{mns}) + 2);
+  const uint64_t fmax = std::min<uint64_t>(stride + 2, 2 * emax + 2);
+  L.emax = static_cast<uint32_t>(emax);
+  L.fmax = static_cast<uint32_t>(fmax);
+  L.nodes_cap = static_cast<uint32_t>(2 * stride + 2);
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.off_mult = take(n * 4);
+  L.off_pay0 = take(stride * sizeof(Payload));
+  L.off_pay1 = take(stride * sizeof(Payload));
+  L.off_wyy0 = take(stride * 8);
+  L.off_wyy1 = take(stride * 8);
+  L.off_list0 = take(size_t{p} * stride * 4);
+  L.off_list1 = take(size_t{p} * stride * 4);
+  L.off_newpos = take(stride * 4);
+  L.off_seg0 = take(stride * 4);
+  L.off_seg1 = take(stride * 4);
+  L.off_front0 = take(fmax * sizeof(NodeWork));
+  L.off_front1 = take(fmax * sizeof(NodeWork));
+  L.off_segtab = take(fmax * sizeof(SegTab));
+  L.off_e2f = take(emax * 4);
+  L.off_samp = take(emax * mtry * 2);
+  L.off_res = take(emax * mtry * sizeof(ChainRes));
+  L.off_split = take(emax * sizeof(SplitInfo));
+  L.off_nf = take(size_t{L.nodes_cap} * 4);
+  L.off_nthr = take(size_t{L.nodes_cap} * 8);
+  L.off_nleft = take(size_t{L.nodes_cap} * 4);
+  L.off_nval = take(size_t{L.nodes_cap} * 8);
+  L.off_nrank = take(size_t{L.nodes_cap} * 4);
+  if (gbits) {
+    L.off_gbits = take(((n + 31) / 32 + 2) * 4);
+    L.off_gpref = take(((n + 63) / 64 + 2) * 4);
+  }
+  L.bytes = o;
+  return L;
+}
+
+}  // namespace aiwc_b200

@@ -1,0 +1,100 @@
+// Layout shared by the forest grower kernel (grow.cu) and its host driver (capi.cu).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace aiwc_b200 {
+
+// One frontier node: its compacted range [b, e) in the level's payload / list
+// order, its BFS node id and its (weight, sum, sumsq) -- NodeWork, forest.hpp:211-215.
+struct NodeWork {
+  uint32_t b, e, id, pad;
+  double w, s, q;
+};
+
+// Per in-bag row of a tree, in node-grouped order: global row, bootstrap
+// multiplicity, weighted response mult*y (forest.hpp:194-195).
+struct Payload {
+  uint32_t row, mult;
+  double wy;
+};
+
+struct ChainRes {
+  double gain;
+  uint32_t pos;
+  uint32_t pad;
+};
+
+struct SplitInfo {
+  uint32_t f;         // frontier index of the split node
+  uint32_t c;         // chosen column
+  uint32_t thr_rank;  // largest global value rank <= threshold
+  uint32_t cnt;       // rows of the node
+  uint32_t nl;        // rows going left (route result)
+  uint32_t base;      // compacted start of the children
+  uint32_t pad0, pad1;
+};
+
+// per segment (frontier node) partition offsets; offL == INT32_MIN => leaf (drop)
+struct SegTab {
+  int32_t offL, offR;
+  uint32_t child;  // next-frontier index of the left child
+  uint32_t pad;
+};
+
+// Device view of a PreparedDataset (forest.hpp:134-161): column store, responses,
+// per-column (value,row) argsort, dense value ranks and the distinct values.
+struct DevData {
+  uint64_t n;
+  uint32_t p;
+  uint32_t rank_bytes;  // 2 or 4
+  const double* col;     // p x n
+  const double* y;       // n
+  const uint32_t* order; // p x n
+  const void* rank;      // p x n (uint16 or uint32)
+  const double* vals;    // concatenated distinct sorted values per column
+  const uint64_t* vals_off;  // p+1
+};
+
+struct SlotLayout {
+  uint32_t stride;  // max in-bag rows per tree (payload / list length)
+  uint32_t fmax;    // max frontier width
+  uint32_t emax;    // max eligible nodes per level
+  uint32_t nodes_cap;
+  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1,
+      off_newpos, off_seg0, off_seg1, off_front0, off_front1, off_segtab, off_e2f,
+      off_samp, off_res, off_split, off_nf, off_nthr, off_nleft, off_nval, off_nrank,
+      off_gbits, off_gpref;
+  size_t bytes;
+};
+
+struct GrowArgs {
+  DevData d;
+  uint32_t mtry, mns;
+  uint64_t seed;
+  uint64_t tag_tree;  // fnv1a64("tree")
+  uint32_t tree_begin, tree_end;
+  uint32_t* queue;    // dynamic tree counter
+  char* scratch;      // slots x layout.bytes
+  SlotLayout L;
+  int bits_in_smem;
+  // outputs (indexed by local tree t - tree_begin)
+  uint32_t* inbag;    // T x n, may be null
+  double* oobval;     // T x n (NaN = in bag), may be null
+  int32_t* pool_feature;
+  double* pool_thr;
+  int32_t* pool_left;
+  double* pool_value;
+  uint32_t* pool_rank;
+  unsigned long long* pool_used;
+  uint64_t pool_cap;
+  uint64_t* tree_off;
+  uint32_t* tree_cnt;
+  unsigned long long* split_rows;  // sum over split nodes of their in-bag distinct rows
+  int* err;  // 1 = pool overflow, 2 = in-bag rows exceed stride, 3 = frontier overflow
+};
+
+SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool gbits);
+
+}  // namespace aiwc_b200

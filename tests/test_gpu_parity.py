@@ -1,0 +1,209 @@
+"""GPU parity: the sm_100a forest path (through the C-ABI) against the reference goldens
+(tests/golden, made by the unmodified reference) and the oracle.  Tree structure,
+thresholds, leaf values and in-bag draws must be bit-identical; OOB statistics and
+predictions too (the GPU sums in the reference's order, no FMA)."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import paper_1811_00156_b200 as pkg
+from oracle_lib import ForestSoA, Oracle, forests_equal
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def soa_of(forest: pkg.Forest, with_inbag=True) -> ForestSoA:
+    off, f, th, le, ri, va = forest.export()
+    return ForestSoA(off, f, th, le, ri, va, inbag=forest.inbag() if with_inbag else None)
+
+
+def soa_sha(s: ForestSoA) -> str:
+    h = hashlib.sha256()
+    for a in (s.offsets, s.feature, s.threshold, s.left, s.right, s.value):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def oob_list(st: pkg.OobStats):
+    return [float(st.degenerate), st.mse, st.response_variance, st.error_pct, st.r_squared,
+            float(st.rows_evaluated)]
+
+
+@pytest.fixture(scope="module")
+def c1():
+    t = pkg.Table()
+    return t, pkg.PreparedDataset.from_table(t)
+
+
+@pytest.fixture(scope="module")
+def seed(golden):
+    return golden["forest_seed"]
+
+
+def test_c1_first20_bit_exact(c1, seed):
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(20, 6, 5, seed))
+    z = np.load(os.path.join(GOLD, "c1_t20_m6_n5.npz"))
+    g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"], z["value"])
+    s = soa_of(f)
+    assert forests_equal(g, s, check_inbag=False) is None
+    assert hashlib.sha256(s.inbag.tobytes()).digest() == z["inbag_sha"].tobytes()
+    assert oob_list(f.oob) == list(z["oob"])
+
+
+def test_c1_500_forest_matches_reference(c1, seed, golden):
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(500, 6, 5, seed))
+    s = soa_of(f)
+    g = golden["c1_500_6_5"]
+    assert np.diff(s.offsets).tolist() == g["node_counts"]
+    assert soa_sha(s) == g["soa_sha"]
+    assert hashlib.sha256(s.inbag.tobytes()).hexdigest() == g["inbag_sha"]
+    assert oob_list(f.oob) == g["oob"]
+    # batched predict_response over every C1 row, summed in tree order
+    pred = f.predict_response(t.predictor_rows())
+    ref = np.load(os.path.join(GOLD, "c1_500_predict.npy"))
+    assert np.array_equal(pred.view(np.uint64), ref.view(np.uint64))
+
+
+def test_c1_paper_params(c1, seed, golden):
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(505, 30, 9, seed))
+    g = golden["c1_505_30_9"]
+    s = soa_of(f)
+    assert soa_sha(s) == g["soa_sha"]
+    assert hashlib.sha256(s.inbag.tobytes()).hexdigest() == g["inbag_sha"]
+    assert oob_list(f.oob) == g["oob"]
+
+
+@pytest.mark.parametrize("cell", range(5))
+def test_c2_grid_cells(c1, seed, golden, cell):
+    t, prep = c1
+    g = golden["c2_cells"][cell]
+    f = pkg.fit(prep, pkg.ForestParams(g["T"], g["mtry"], g["mns"], seed))
+    s = soa_of(f)
+    assert soa_sha(s) == g["soa_sha"]
+    assert oob_list(f.oob) == g["oob"]
+
+
+@pytest.mark.parametrize("name", ["step", "ties", "constcol", "singleleaf", "tworows", "wide"])
+def test_edge_tables(name, seed, golden):
+    z = np.load(os.path.join(GOLD, f"edge_{name}.npz"))
+    col, y = z["col"], z["y"]
+    p, n = col.shape
+    prm = golden["edges"][name]
+    prep = pkg.PreparedDataset(col, y, n, p)
+    f = pkg.fit(prep, pkg.ForestParams(prm["T"], prm["mtry"], prm["mns"], seed))
+    g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"], z["value"],
+                  inbag=z["inbag"])
+    assert forests_equal(g, soa_of(f)) is None
+    assert oob_list(f.oob) == list(z["oob"])
+
+
+def test_random_tables_vs_oracle():
+    rng = np.random.default_rng(99)
+    for case in range(8):
+        n = int(rng.integers(2, 700))
+        p = int(rng.integers(1, 20))
+        col = (rng.normal(size=(p, n)) if case % 2 else
+               rng.integers(0, 5, size=(p, n)).astype(float))
+        y = rng.normal(size=n)
+        T, m, mns = int(rng.integers(1, 16)), int(rng.integers(1, p + 1)), int(rng.integers(1, 7))
+        seed = int(rng.integers(0, 2**63))
+        prep = pkg.PreparedDataset(col, y, n, p)
+        try:
+            f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
+        except pkg.ExecutionError as e:  # "no out-of-bag rows" like compute_oob
+            assert "out-of-bag" in str(e)
+            f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed), compute_oob_stats=False)
+        o = Oracle.fit(col, y, n, p, T, m, mns, seed)
+        assert forests_equal(o, soa_of(f)) is None, (case, n, p, T, m, mns)
+
+
+def test_tree_ranges_and_chained_oob(c1, seed):
+    """Sharding by tree range (the multi-GPU path) reproduces the one-shot forest and,
+    with chained per-row OOB accumulation, bit-identical OOB statistics."""
+    t, prep = c1
+    params = pkg.ForestParams(90, 6, 5, seed)
+    full = pkg.fit(prep, params)
+    a = pkg.fit(prep, params, 0, 40, compute_oob_stats=False)
+    b = pkg.fit(prep, params, 40, 90, compute_oob_stats=False)
+    sf, sa, sb = soa_of(full), soa_of(a), soa_of(b)
+    cat = ForestSoA(np.concatenate([sa.offsets, sb.offsets[1:] + sa.offsets[-1]]),
+                    *(np.concatenate([getattr(sa, k), getattr(sb, k)])
+                      for k in ("feature", "threshold", "left", "right", "value")),
+                    inbag=np.concatenate([sa.inbag, sb.inbag]))
+    assert forests_equal(sf, cat) is None
+    rs = np.zeros(t.n)
+    rc = np.zeros(t.n, np.uint32)
+    pkg.oob_accumulate(a, prep, rs, rc)
+    pkg.oob_accumulate(b, prep, rs, rc)
+    assert oob_list(pkg.oob_finalize(t.y, rs, rc)) == oob_list(full.oob)
+
+
+def test_import_predict_and_oob(c1, seed):
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(40, 6, 5, seed))
+    s = soa_of(f)
+    g = pkg.Forest.from_arrays(s.offsets, s.feature, s.threshold, s.left, s.right, s.value,
+                               inbag=s.inbag, n=t.n)
+    rows = t.predictor_rows()
+    assert np.array_equal(g.predict_response(rows), f.predict_response(rows))
+    assert np.array_equal(g.predict_response(rows), Oracle.predict(rows, s))
+    assert oob_list(pkg.compute_oob(g, prep)) == oob_list(f.oob)
+    # arbitrary (non-training) query rows go through the f64 thresholds
+    q = rows[:64] * np.random.default_rng(3).uniform(0.5, 1.5, size=(64, t.p))
+    assert np.array_equal(f.predict_response(q), Oracle.predict(q, s))
+
+
+def test_evaluate_c3_small(c1, seed, golden):
+    t, _ = c1
+    pred = pkg.evaluate(t, pkg.ForestParams(50, 6, 5, 0), seed)
+    ref = np.load(os.path.join(GOLD, "c3_50_6_5_pred.npy"))
+    assert np.array_equal(pred.view(np.uint64), ref.view(np.uint64))
+
+
+def test_evaluate_c3_paper(c1, seed, golden):
+    """C3: leave-one-kernel-out at 505/30/9 -- per-kernel MAPE of the reference."""
+    t, _ = c1
+    pred = pkg.evaluate(t, pkg.ForestParams(505, 30, 9, 0), seed)
+    ref = np.load(os.path.join(GOLD, "c3_505_30_9_pred.npy"))
+    assert np.array_equal(pred.view(np.uint64), ref.view(np.uint64))
+    err = 100.0 * np.abs(pred - t.seconds) / t.seconds
+    g = golden["c3_505_30_9"]
+    assert err.mean() == g["mape"]
+
+
+def test_parameter_errors(c1):
+    t, prep = c1
+    with pytest.raises(pkg.ExecutionError, match="mtry"):
+        pkg.fit(prep, pkg.ForestParams(5, t.p + 1, 5, 1))
+    with pytest.raises(pkg.ExecutionError, match="num_trees"):
+        pkg.fit(prep, pkg.ForestParams(0, 2, 5, 1))
+    with pytest.raises(pkg.ExecutionError, match="min_node_size"):
+        pkg.fit(prep, pkg.ForestParams(5, 2, 0, 1))
+
+
+def test_degenerate_response():
+    n, p = 50, 3
+    col = np.random.default_rng(1).normal(size=(p, n))
+    prep = pkg.PreparedDataset(col, np.full(n, 0.25), n, p)
+    f = pkg.fit(prep, pkg.ForestParams(10, 2, 1, 3))
+    assert f.oob.degenerate
+
+
+@pytest.mark.slow
+def test_c4_first8_trees(seed, golden):
+    """C4 (1,000,036 x 64): first 8 trees of the 1000-tree m=8 mns=5 forest."""
+    t = pkg.Table(6757, 37)
+    prep = pkg.PreparedDataset.from_table(t)
+    f = pkg.fit(prep, pkg.ForestParams(8, 8, 5, seed))
+    g = golden["c4_8_8_5"]
+    s = soa_of(f)
+    assert np.diff(s.offsets).tolist() == g["node_counts"]
+    assert soa_sha(s) == g["soa_sha"]
+    assert hashlib.sha256(s.inbag.tobytes()).hexdigest() == g["inbag_sha"]
+    assert oob_list(f.oob) == g["oob"]
