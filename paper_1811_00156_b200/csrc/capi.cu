@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -45,13 +46,16 @@ struct DevBuf {
   size_t count = 0;
   DevBuf() = default;
   explicit DevBuf(size_t c) { alloc(c); }
+  // stream-ordered allocation from the device's default pool (kept warm, see
+  // warm_pool): fits in tuning loops allocate/free without device-wide syncs.  Every
+  // API call synchronises its stream before returning, so a buffer is idle when freed.
   void alloc(size_t c) {
     release();
-    if (c) CK(cudaMalloc(&p, c * sizeof(T)));
+    if (c) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), 0));
     count = c;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, 0);
     p = nullptr;
     count = 0;
   }
@@ -82,6 +86,19 @@ struct DeviceGuard {
       throw Status(AIWC_EARG, "device index " + std::to_string(dev) + " out of range");
     cudaGetDevice(&prev);
     CK(cudaSetDevice(dev));
+    warm_pool(dev);
+  }
+  // keep freed pool memory cached instead of returning it to the driver
+  static void warm_pool(int dev) {
+    static std::once_flag flags[64];
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(flags[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
@@ -109,17 +126,23 @@ struct aiwc_ctx {
   uint32_t p = 0;
   uint32_t rank_bytes = 2;
   std::vector<double> y;  // host copy (OOB finalize runs the reference's row-order sums)
+  uint32_t nlisted = 0, order_stride = 0;
   DevBuf<double> col, dy, vals;
-  DevBuf<uint32_t> order;
+  DevBuf<uint32_t> order, listed;
+  DevBuf<int32_t> list_of;
   DevBuf<uint8_t> rank;
   DevBuf<uint64_t> vals_off;
-  // grow scratch, reused across fits on this dataset (serialised by `mu`)
+  // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
   DevBuf<char> scratch;
-  DevBuf<char> gbits;
+  cudaStream_t stream = nullptr;
+  ~aiwc_ctx() {
+    if (stream) cudaStreamDestroy(stream);
+  }
 
   DevData view() const {
-    return DevData{n, p, rank_bytes, col.p, dy.p, order.p, rank.p, vals.p, vals_off.p};
+    return DevData{n, p, rank_bytes, nlisted, order_stride, col.p, dy.p, order.p, rank.p,
+                   vals.p, vals_off.p, list_of.p, listed.p};
   }
 };
 
@@ -130,7 +153,7 @@ namespace {
 void presort(const double* col, uint64_t n, uint32_t p, std::vector<uint32_t>& order,
              std::vector<uint32_t>& rank, std::vector<double>& vals,
              std::vector<uint64_t>& vals_off) {
-  order.resize(size_t{p} * n);
+  order.resize(size_t{p} * n);  // dense p x n argsorts (packed for the device later)
   rank.resize(size_t{p} * n);
   std::vector<std::vector<double>> distinct(p);
   const unsigned hw = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
@@ -235,15 +258,36 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
     uint64_t maxk = 0;
     for (uint32_t c = 0; c < p; ++c) maxk = std::max(maxk, voff[c + 1] - voff[c]);
     ctx->rank_bytes = maxk <= 65536 ? 2 : 4;
+    // listed columns: >= 3 distinct values (two-level columns are read off the payload)
+    std::vector<int32_t> list_of(p, -1);
+    std::vector<uint32_t> listed;
+    for (uint32_t c = 0; c < p; ++c)
+      if (voff[c + 1] - voff[c] >= 3) {
+        list_of[c] = static_cast<int32_t>(listed.size());
+        listed.push_back(c);
+      }
+    ctx->nlisted = static_cast<uint32_t>(listed.size());
+    ctx->order_stride = static_cast<uint32_t>((n + 15) & ~uint64_t{15});
+    std::vector<uint32_t> packed(size_t{ctx->nlisted} * ctx->order_stride, 0u);
+    for (uint32_t i = 0; i < ctx->nlisted; ++i)
+      std::copy(order.begin() + size_t{listed[i]} * n, order.begin() + size_t{listed[i] + 1} * n,
+                packed.begin() + size_t{i} * ctx->order_stride);
     ctx->col.alloc(size_t{p} * n);
     ctx->dy.alloc(n);
-    ctx->order.alloc(size_t{p} * n);
+    ctx->order.alloc(std::max<size_t>(packed.size(), 16));
+    ctx->list_of.alloc(p);
+    ctx->listed.alloc(std::max<size_t>(listed.size(), 1));
+    CK(cudaMemcpy(ctx->list_of.p, list_of.data(), p * 4, cudaMemcpyHostToDevice));
+    if (!listed.empty())
+      CK(cudaMemcpy(ctx->listed.p, listed.data(), listed.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     ctx->rank.alloc(size_t{p} * n * ctx->rank_bytes);
     ctx->vals.alloc(vals.size());
     ctx->vals_off.alloc(voff.size());
     CK(cudaMemcpy(ctx->col.p, col, size_t{p} * n * 8, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->dy.p, y, n * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->order.p, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+    if (!packed.empty())
+      CK(cudaMemcpy(ctx->order.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
     if (ctx->rank_bytes == 2) {
       std::vector<uint16_t> r16(rank.begin(), rank.end());
       CK(cudaMemcpy(ctx->rank.p, r16.data(), r16.size() * 2, cudaMemcpyHostToDevice));
@@ -354,7 +398,9 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
       throw Status(AIWC_EARG, "bad tree range");
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dg(ctx->device);
-    Stream st;
+    struct {
+      cudaStream_t s;
+    } st{ctx->stream};
     const uint64_t n = ctx->n;
     const uint32_t p = ctx->p;
     const uint32_t T = tree_end - tree_begin;
@@ -363,11 +409,11 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     int dev = ctx->device, sms = 0, max_optin = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const size_t nwords = (n + 31) / 32, nblk = (n + 63) / 64;
-    const size_t bits_smem = (((nwords + 1) & ~size_t{1}) + nblk + 2) * 4;
+    SlotLayout L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, false);
+    const size_t bits_smem = (grow_bits_words(n, L.stride) + grow_pref_words(n, L.stride)) * 4;
     const bool smem_bits = bits_smem + 4096 <= static_cast<size_t>(max_optin);
     const size_t dyn = smem_bits ? bits_smem : 0;
-    SlotLayout L = make_layout(n, p, mtry, min_node_size, !smem_bits);
+    if (!smem_bits) L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
 
     GrowArgs a{};
     a.d = ctx->view();
@@ -422,8 +468,14 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     DevBuf<int32_t> pf, pl;
     DevBuf<double> pt, pv;
     DevBuf<uint32_t> pr;
-    DevBuf<unsigned long long> used(1), split_rows(1);
+    DevBuf<unsigned long long> used(1), split_rows(1), prof;
     a.split_rows = split_rows.p;
+    const bool want_prof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
+    if (want_prof) {
+      prof.alloc(16);
+      CK(cudaMemset(prof.p, 0, 16 * 8));
+      a.prof = prof.p;
+    }
     std::vector<uint32_t> cnt(T);
     cudaEvent_t ev0, ev1, evf0, evf1;
     CK(cudaEventCreate(&ev0));
@@ -481,6 +533,19 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
       break;
     }
     CK(cudaMemcpy(cnt.data(), tree_cnt.p, size_t{T} * 4, cudaMemcpyDeviceToHost));
+    if (want_prof) {
+      unsigned long long h[16];
+      CK(cudaMemcpy(h, prof.p, 16 * 8, cudaMemcpyDeviceToHost));
+      static const char* names[14] = {"bootstrap", "bitmap", "payload0", "lists0+root",
+                                      "-", "elig", "sample", "chains", "decide", "route",
+                                      "segtab", "paypass", "listpass", "emit+oob"};
+      double tot = 0;
+      for (int i = 0; i < 14; ++i) tot += static_cast<double>(h[i]);
+      std::fprintf(stderr, "[aiwc grow phases] slots=%d trees=%u total=%.3g cycles:", slots, T, tot);
+      for (int i = 0; i < 14; ++i)
+        if (h[i]) std::fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * h[i] / tot);
+      std::fprintf(stderr, "\n");
+    }
     f->off.assign(T + 1, 0);
     for (uint32_t t = 0; t < T; ++t) f->off[t + 1] = f->off[t] + cnt[t];
     const uint64_t N = f->off[T];

@@ -2,11 +2,13 @@
 //
 // Reproduces TreeGrower::grow (forest.hpp:179-376) bit-exactly:
 //   * bootstrap: n counter-based splitmix64 draws (forest.hpp:184-195, rng.hpp:45-59);
-//   * per tree, the in-bag rows live in a node-grouped "payload" array and every
-//     column keeps a list of payload positions in (value, row) order, partitioned
-//     stably by node each level -- the reference's presort/partition invariant
-//     (forest.hpp:163-166, 197-209, 355-371), realised as flat CTA-wide
-//     scan+scatter passes over compacted arrays instead of per-bucket loops;
+//   * per tree, the in-bag rows live in a node-grouped, row-ordered "payload" array;
+//     every column with >= 3 distinct values keeps a list of payload positions in
+//     (value, row) order, partitioned stably by node each level -- the reference's
+//     presort/partition invariant (forest.hpp:163-166, 197-209, 355-371) realised
+//     as flat CTA-wide scan+scatter passes over compacted arrays.  Columns with <= 2
+//     distinct values (the one-hot device columns) need no list: their (value,row)
+//     order is "value-0 rows in row order, then value-1 rows", read off the payload;
 //   * split scan: one warp (or, for nodes < kLaneMax rows, one lane) per
 //     (node, sampled column) chain; the running sum sl is accumulated strictly
 //     sequentially in FP64 (warp-shuffle chain, no reassociation) so every gain is
@@ -14,9 +16,12 @@
 //   * first-max argmax over (column slot, position), threshold midpoint rule
 //     (forest.hpp:282-283, 287);
 //   * children numbered in frontier order (BFS ids, forest.hpp:310-318);
-//   * child sums accumulated in column-0 list order (forest.hpp:326-344);
+//   * child sums accumulated in column-0 order (forest.hpp:326-344);
 //   * mtry draws: exactly mtry per eligible node, counter = n + mtry*(BFS index
 //     among eligible nodes) (forest.hpp:255-266).
+// Partition destinations come from a shared-memory bitmap of "goes left" flags over
+// payload positions plus per-word prefix counts, so no per-element index map is
+// gathered from global memory.
 // All FP64 arithmetic uses explicit _rn intrinsics (no FMA contraction).
 // Row routing compares dense value ranks: x <= thr  <=>  rank(x) <= thr_rank,
 // thr_rank = largest distinct-value rank with value <= thr (exact for every
@@ -36,17 +41,25 @@ namespace {
 
 constexpr uint32_t kLaneMax = 48;  // nodes below this size use one lane per chain
 constexpr uint32_t kMaxP = 1024;
+constexpr int kPhases = 14;
+constexpr int kE = 16;  // elements per thread in the flat partition passes
 
 __device__ __forceinline__ uint32_t get_bit(const uint32_t* bits, uint32_t i) {
   return (bits[i >> 5] >> (i & 31u)) & 1u;
 }
 
-__device__ __forceinline__ void put_bit(uint32_t* bits, uint32_t i, bool v) {
-  const uint32_t m = 1u << (i & 31u);
-  if (v)
-    atomicOr(bits + (i >> 5), m);
-  else
-    atomicAnd(bits + (i >> 5), ~m);
+// set bits strictly before position q (per-word prefix counts)
+__device__ __forceinline__ uint32_t bits_before(const uint32_t* bits, const uint32_t* pref,
+                                                uint32_t q) {
+  return pref[q >> 5] + __popc(bits[q >> 5] & ((1u << (q & 31u)) - 1u));
+}
+
+// in-bag rank of row r (per-64-row prefix counts)
+__device__ __forceinline__ uint32_t inbag_pos(const uint32_t* bits, const uint32_t* pref64,
+                                              uint32_t r) {
+  const uint32_t w = r >> 5;
+  return pref64[r >> 6] + ((w & 1u) ? __popc(bits[w - 1]) : 0u) +
+         __popc(bits[w] & ((1u << (r & 31u)) - 1u));
 }
 
 template <typename RankT>
@@ -61,10 +74,22 @@ __device__ __forceinline__ double gain_at(double sl, double wl, double W, double
   return __dadd_rn(__ddiv_rn(__dmul_rn(sl, sl), wl), __ddiv_rn(__dmul_rn(d, d), wr));
 }
 
-// ---- split chain, warp-cooperative (large nodes) --------------------------------
+__device__ __forceinline__ void warp_best(double& bg, uint32_t& bp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double og = __shfl_xor_sync(kFull, bg, o);
+    const uint32_t op = __shfl_xor_sync(kFull, bp, o);
+    if (og > bg || (og == bg && op < bp)) {
+      bg = og;
+      bp = op;
+    }
+  }
+}
+
+// ---- split chain over a sorted list, warp-cooperative (large nodes) ---------------
 template <typename RankT, int G>
-__device__ void chain_warp(const uint32_t* __restrict__ list, uint32_t b, uint32_t e,
-                           const Payload* __restrict__ pay, const RankT* __restrict__ rk_c,
+__device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
+                           const Payload* pay, const RankT* __restrict__ rk_c,
                            double W, double S, double& best_gain, uint32_t& best_pos) {
   const unsigned lane = lane_id();
   double sl = 0.0;
@@ -78,7 +103,7 @@ __device__ void chain_warp(const uint32_t* __restrict__ list, uint32_t b, uint32
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      q[g] = k < e ? __ldg(list + k) : 0u;
+      q[g] = k < e ? list[k] : 0u;
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -108,9 +133,9 @@ __device__ void chain_warp(const uint32_t* __restrict__ list, uint32_t b, uint32
       const uint32_t wl_before = wl + inc - mu[g];
       double run = sl, mine = 0.0;
       for (uint32_t j = 0; j < nv; ++j) {
-        const double a = __shfl_sync(kFull, wy[g], j);
+        const double x = __shfl_sync(kFull, wy[g], j);
         if (lane == j) mine = run;
-        run = __dadd_rn(run, a);
+        run = __dadd_rn(run, x);
       }
       uint32_t pr = __shfl_up_sync(kFull, rk[g], 1);
       if (lane == 0) pr = first ? rk[g] : prev_rank;
@@ -127,23 +152,15 @@ __device__ void chain_warp(const uint32_t* __restrict__ list, uint32_t b, uint32
       first = false;
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double og = __shfl_xor_sync(kFull, bg, o);
-    const uint32_t op = __shfl_xor_sync(kFull, bp, o);
-    if (og > bg || (og == bg && op < bp)) {
-      bg = og;
-      bp = op;
-    }
-  }
+  warp_best(bg, bp);
   best_gain = bg;
   best_pos = bp;
 }
 
-// ---- split chain, one lane (small nodes) ----------------------------------------
+// ---- split chain over a sorted list, one lane (small nodes) -----------------------
 template <typename RankT>
-__device__ void chain_lane(const uint32_t* __restrict__ list, uint32_t b, uint32_t e,
-                           const Payload* __restrict__ pay, const RankT* __restrict__ rk_c,
+__device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
+                           const Payload* pay, const RankT* __restrict__ rk_c,
                            double W, double S, double& best_gain, uint32_t& best_pos) {
   double sl = 0.0, bg = -INFINITY;
   uint32_t wl = 0, prev = 0, bp = 0xffffffffu;
@@ -151,7 +168,7 @@ __device__ void chain_lane(const uint32_t* __restrict__ list, uint32_t b, uint32
     uint32_t q[4], rk[4], mu[4];
     double wy[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? __ldg(list + k + g) : 0u;
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list[k + g] : 0u;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       if (k + g < e) {
@@ -186,28 +203,111 @@ __device__ void chain_lane(const uint32_t* __restrict__ list, uint32_t b, uint32
   best_pos = bp;
 }
 
+// ---- split chain of a two-level column: the only boundary sits after the value-0
+// rows, and sl there is their sequential sum in row (= payload) order --------------
+template <typename RankT, int G>
+__device__ void chain_bin_warp(const Payload* pay, uint32_t b, uint32_t e,
+                               const RankT* __restrict__ rk_c, double W, double S,
+                               double& best_gain, uint32_t& best_pos) {
+  const unsigned lane = lane_id();
+  double s0 = 0.0;
+  uint32_t w0 = 0, n0 = 0;
+  for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
+    uint32_t row[G], mu[G];
+    double wy[G];
+    bool z[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      if (k < e) {
+        const Payload P = pay[k];
+        row[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+      } else {
+        row[g] = 0;
+        mu[g] = 0;
+        wy[g] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) z[g] = (k0 + g * 32 + lane < e) && rank_of(rk_c, row[g]) == 0u;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      if (t0 >= e) break;
+      const uint32_t nv = min(32u, e - t0);
+      const unsigned bz = __ballot_sync(kFull, z[g]);
+      n0 += __popc(bz);
+      w0 += warp_sum(z[g] ? mu[g] : 0u);
+      for (uint32_t j = 0; j < nv; ++j) {
+        const double x = __shfl_sync(kFull, wy[g], j);
+        if ((bz >> j) & 1u) s0 = __dadd_rn(s0, x);
+      }
+    }
+  }
+  const uint32_t R = e - b;
+  if (n0 == 0 || n0 == R) {
+    best_gain = -INFINITY;
+    best_pos = 0xffffffffu;
+  } else {
+    best_gain = gain_at(s0, static_cast<double>(w0), W, S);
+    best_pos = b + n0;
+  }
+}
+
+template <typename RankT>
+__device__ void chain_bin_lane(const Payload* pay, uint32_t b, uint32_t e,
+                               const RankT* __restrict__ rk_c, double W, double S,
+                               double& best_gain, uint32_t& best_pos) {
+  double s0 = 0.0;
+  uint32_t w0 = 0, n0 = 0;
+  for (uint32_t k = b; k < e; k += 4) {
+    Payload P[4];
+    bool z[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (k + g < e) P[g] = pay[k + g];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) z[g] = k + g < e && rank_of(rk_c, P[g].row) == 0u;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      if (!z[g]) continue;
+      ++n0;
+      w0 += P[g].mult;
+      s0 = __dadd_rn(s0, P[g].wy);
+    }
+  }
+  const uint32_t R = e - b;
+  if (n0 == 0 || n0 == R) {
+    best_gain = -INFINITY;
+    best_pos = 0xffffffffu;
+  } else {
+    best_gain = gain_at(s0, static_cast<double>(w0), W, S);
+    best_pos = b + n0;
+  }
+}
+
 struct RouteOut {
   uint32_t nl;
   uint32_t wl, wr;
   double sl, ql, sr, qr;
 };
 
-// ---- route + child sums in column-0 order, warp-cooperative ---------------------
+// ---- route + child sums in column-0 order (list of column 0), warp-cooperative -----
 template <typename RankT, int G>
-__device__ RouteOut route_warp(const uint32_t* __restrict__ list0, uint32_t b, uint32_t e,
-                               const Payload* __restrict__ pay,
-                               const double* __restrict__ wyy,
-                               const RankT* __restrict__ rk_f, uint32_t thr_rank,
-                               uint32_t* bits) {
+__device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
+                           const Payload* pay, const double* wyy,
+                           const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
+                           RouteOut& o) {
   const unsigned lane = lane_id();
-  RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
   for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
     uint32_t q[G], row[G], mu[G];
     double wy[G], yy[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      q[g] = k < e ? __ldg(list0 + k) : 0u;
+      q[g] = k < e ? list0[k] : 0u;
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -232,39 +332,36 @@ __device__ RouteOut route_warp(const uint32_t* __restrict__ list0, uint32_t b, u
       const uint32_t nv = min(32u, e - t0);
       const bool valid = lane < nv;
       const bool left = valid && rank_of(rk_f, row[g]) <= thr_rank;
-      if (valid) put_bit(bits, q[g], left);
+      if (left) atomicOr(bits + (q[g] >> 5), 1u << (q[g] & 31u));
       const unsigned bl = __ballot_sync(kFull, left);
       o.nl += __popc(bl);
       o.wl += warp_sum(left ? mu[g] : 0u);
       o.wr += warp_sum((valid && !left) ? mu[g] : 0u);
       for (uint32_t j = 0; j < nv; ++j) {
-        const double a = __shfl_sync(kFull, wy[g], j);
+        const double x = __shfl_sync(kFull, wy[g], j);
         const double c = __shfl_sync(kFull, yy[g], j);
         if ((bl >> j) & 1u) {
-          o.sl = __dadd_rn(o.sl, a);
+          o.sl = __dadd_rn(o.sl, x);
           o.ql = __dadd_rn(o.ql, c);
         } else {
-          o.sr = __dadd_rn(o.sr, a);
+          o.sr = __dadd_rn(o.sr, x);
           o.qr = __dadd_rn(o.qr, c);
         }
       }
     }
   }
-  return o;
 }
 
 template <typename RankT>
-__device__ RouteOut route_lane(const uint32_t* __restrict__ list0, uint32_t b, uint32_t e,
-                               const Payload* __restrict__ pay,
-                               const double* __restrict__ wyy,
-                               const RankT* __restrict__ rk_f, uint32_t thr_rank,
-                               uint32_t* bits) {
-  RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+__device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
+                           const Payload* pay, const double* wyy,
+                           const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
+                           RouteOut& o) {
   for (uint32_t k = b; k < e; k += 4) {
     uint32_t q[4], row[4], mu[4];
     double wy[4], yy[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? __ldg(list0 + k + g) : 0u;
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list0[k + g] : 0u;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       if (k + g < e) {
@@ -279,8 +376,8 @@ __device__ RouteOut route_lane(const uint32_t* __restrict__ list0, uint32_t b, u
     for (int g = 0; g < 4; ++g) {
       if (k + g >= e) break;
       const bool left = rank_of(rk_f, row[g]) <= thr_rank;
-      put_bit(bits, q[g], left);
       if (left) {
+        atomicOr(bits + (q[g] >> 5), 1u << (q[g] & 31u));
         ++o.nl;
         o.wl += mu[g];
         o.sl = __dadd_rn(o.sl, wy[g]);
@@ -292,21 +389,90 @@ __device__ RouteOut route_lane(const uint32_t* __restrict__ list0, uint32_t b, u
       }
     }
   }
-  return o;
+}
+
+// ---- route when column 0 has <= 2 distinct values: its order is the payload rows
+// with rank 0, then those with rank 1 (one pass per level of column 0) -------------
+template <typename RankT, int G>
+__device__ void route_groups_warp(const Payload* pay,
+                                  const double* wyy, uint32_t b, uint32_t e,
+                                  const RankT* __restrict__ rk0, uint32_t k0levels,
+                                  const RankT* __restrict__ rk_f, uint32_t thr_rank,
+                                  uint32_t* bits, RouteOut& o) {
+  const unsigned lane = lane_id();
+  for (uint32_t grp = 0; grp < k0levels; ++grp) {
+    for (uint32_t k0 = b; k0 < e; k0 += 32) {
+      const uint32_t k = k0 + lane;
+      const uint32_t nv = min(32u, e - k0);
+      Payload P{0, 0, 0.0};
+      double yy = 0.0;
+      bool sel = false, left = false;
+      if (k < e) {
+        P = pay[k];
+        yy = wyy[k];
+        sel = k0levels == 1 || rank_of(rk0, P.row) == grp;
+        left = sel && rank_of(rk_f, P.row) <= thr_rank;
+      }
+      if (left) atomicOr(bits + (k >> 5), 1u << (k & 31u));
+      const unsigned bl = __ballot_sync(kFull, left);
+      const unsigned bs = __ballot_sync(kFull, sel);
+      o.nl += __popc(bl);
+      o.wl += warp_sum(left ? P.mult : 0u);
+      o.wr += warp_sum((sel && !left) ? P.mult : 0u);
+      for (uint32_t j = 0; j < nv; ++j) {
+        const double x = __shfl_sync(kFull, P.wy, j);
+        const double c = __shfl_sync(kFull, yy, j);
+        if (!((bs >> j) & 1u)) continue;
+        if ((bl >> j) & 1u) {
+          o.sl = __dadd_rn(o.sl, x);
+          o.ql = __dadd_rn(o.ql, c);
+        } else {
+          o.sr = __dadd_rn(o.sr, x);
+          o.qr = __dadd_rn(o.qr, c);
+        }
+      }
+    }
+  }
+}
+
+template <typename RankT>
+__device__ void route_groups_lane(const Payload* pay,
+                                  const double* wyy, uint32_t b, uint32_t e,
+                                  const RankT* __restrict__ rk0, uint32_t k0levels,
+                                  const RankT* __restrict__ rk_f, uint32_t thr_rank,
+                                  uint32_t* bits, RouteOut& o) {
+  for (uint32_t grp = 0; grp < k0levels; ++grp) {
+    for (uint32_t k = b; k < e; ++k) {
+      const Payload P = pay[k];
+      if (k0levels != 1 && rank_of(rk0, P.row) != grp) continue;
+      const double yy = wyy[k];
+      if (rank_of(rk_f, P.row) <= thr_rank) {
+        atomicOr(bits + (k >> 5), 1u << (k & 31u));
+        ++o.nl;
+        o.wl += P.mult;
+        o.sl = __dadd_rn(o.sl, P.wy);
+        o.ql = __dadd_rn(o.ql, yy);
+      } else {
+        o.wr += P.mult;
+        o.sr = __dadd_rn(o.sr, P.wy);
+        o.qr = __dadd_rn(o.qr, yy);
+      }
+    }
+  }
 }
 
 // sequential FP64 sums over the payload in row order (root stats, forest.hpp:221-226)
 template <int G>
-__device__ void root_sums_warp(const Payload* __restrict__ pay, const double* __restrict__ wyy,
+__device__ void root_sums_warp(const Payload* pay, const double* wyy,
                                uint32_t A, double& s_out, double& q_out) {
   const unsigned lane = lane_id();
   double s = 0.0, q = 0.0;
   for (uint32_t k0 = 0; k0 < A; k0 += 32 * G) {
-    double a[G], c[G];
+    double x[G], c[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      a[g] = k < A ? pay[k].wy : 0.0;
+      x[g] = k < A ? pay[k].wy : 0.0;
       c[g] = k < A ? wyy[k] : 0.0;
     }
 #pragma unroll
@@ -315,7 +481,7 @@ __device__ void root_sums_warp(const Payload* __restrict__ pay, const double* __
       if (t0 >= A) break;
       const uint32_t nv = min(32u, A - t0);
       for (uint32_t j = 0; j < nv; ++j) {
-        s = __dadd_rn(s, __shfl_sync(kFull, a[g], j));
+        s = __dadd_rn(s, __shfl_sync(kFull, x[g], j));
         q = __dadd_rn(q, __shfl_sync(kFull, c[g], j));
       }
     }
@@ -333,7 +499,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   extern __shared__ uint32_t dyn_smem[];
   __shared__ uint32_t sh_scan[NW + 2];
   __shared__ uint32_t s_tree, s_A, s_F, s_E, s_S, s_nodes, s_totL, s_err;
-  __shared__ double s_root[2];
   __shared__ unsigned long long s_pool;
 
   const DevData& d = a.d;
@@ -345,6 +510,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   const unsigned wid = warp_id();
   const SlotLayout& L = a.L;
   const uint32_t stride = L.stride;
+  const uint32_t nl_cols = d.nlisted;
+  const uint32_t ostride = d.order_stride;
 
   char* slot = a.scratch + static_cast<size_t>(blockIdx.x) * L.bytes;
   uint32_t* mult_g = reinterpret_cast<uint32_t*>(slot + L.off_mult);
@@ -354,7 +521,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
                     reinterpret_cast<double*>(slot + L.off_wyy1)};
   uint32_t* lists[2] = {reinterpret_cast<uint32_t*>(slot + L.off_list0),
                         reinterpret_cast<uint32_t*>(slot + L.off_list1)};
-  uint32_t* newpos = reinterpret_cast<uint32_t*>(slot + L.off_newpos);
   uint32_t* seg[2] = {reinterpret_cast<uint32_t*>(slot + L.off_seg0),
                       reinterpret_cast<uint32_t*>(slot + L.off_seg1)};
   NodeWork* front[2] = {reinterpret_cast<NodeWork*>(slot + L.off_front0),
@@ -371,13 +537,30 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   uint32_t* nrank = reinterpret_cast<uint32_t*>(slot + L.off_nrank);
   const uint32_t nwords = (n + 31u) / 32u;
   const uint32_t nblk64 = (n + 63u) / 64u;
+  const size_t bw = grow_bits_words(n, stride);
   uint32_t* bits = a.bits_in_smem ? dyn_smem : reinterpret_cast<uint32_t*>(slot + L.off_gbits);
-  uint32_t* pref = a.bits_in_smem ? dyn_smem + ((nwords + 1u) & ~1u)
-                                  : reinterpret_cast<uint32_t*>(slot + L.off_gpref);
+  uint32_t* pref = a.bits_in_smem ? dyn_smem + bw : reinterpret_cast<uint32_t*>(slot + L.off_gpref);
   const RankT* rank = static_cast<const RankT*>(d.rank);
+  const int32_t list0 = d.list_of[0];
+  const uint32_t k0levels =
+      static_cast<uint32_t>(d.vals_off[1] - d.vals_off[0]);  // distinct values of column 0
+
+  // optional per-phase cycle accounting (thread 0, clock64), enabled by a.prof
+  long long ph_acc[kPhases];
+  long long ph_last = clock64();
+  for (int i = 0; i < kPhases; ++i) ph_acc[i] = 0;
+#define PHASE(k)                        \
+  do {                                  \
+    if (a.prof && tid == 0) {           \
+      const long long now_ = clock64(); \
+      ph_acc[(k)] += now_ - ph_last;    \
+      ph_last = now_;                   \
+    }                                   \
+  } while (0)
 
   for (;;) {
     __syncthreads();
+    PHASE(13);
     if (tid == 0) {
       s_tree = atomicAdd(a.queue, 1u);
       s_err = 0;
@@ -397,6 +580,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       atomicAdd(mult_g + r, 1u);
     }
     __syncthreads();
+    PHASE(0);
     // in-bag bitmap by row + 64-row prefix counts
     for (uint32_t w = wid; w < nwords; w += NW) {
       const uint32_t r = w * 32u + lane;
@@ -419,6 +603,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       if (tid == 0) s_A = carry;
     }
     __syncthreads();
+    PHASE(1);
     const uint32_t A0 = s_A;
     if (A0 > stride) {
       if (tid == 0) atomicExch(a.err, 2);
@@ -427,9 +612,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     // payload in row order (forest.hpp:194-195: weighted_y = mult*y)
     for (uint32_t r = tid; r < n; r += NT) {
       if (!get_bit(bits, r)) continue;
-      const uint32_t w = r >> 5;
-      const uint32_t pos = pref[r >> 6] + ((w & 1u) ? __popc(bits[w - 1]) : 0u) +
-                           __popc(bits[w] & ((1u << (r & 31u)) - 1u));
+      const uint32_t pos = inbag_pos(bits, pref, r);
       const uint32_t mu = mult_g[r];
       const double yr = __ldg(d.y + r);
       const double wy = __dmul_rn(static_cast<double>(mu), yr);
@@ -438,54 +621,58 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       seg[0][pos] = 0u;
     }
     __syncthreads();
-    // root sums (warp 0) || per-column in-bag filter of the presort (other warps)
+    PHASE(2);
+    // per listed column: stable in-bag filter of the presort, flattened over
+    // (list, position); every list holds exactly A0 in-bag rows
+    {
+      const uint64_t total = uint64_t{nl_cols} * ostride;
+      uint64_t carry = 0;
+      for (uint64_t base = 0; base < total; base += uint64_t{NT} * kE) {
+        const uint64_t g0 = base + uint64_t{tid} * kE;
+        uint32_t r[kE], in = 0, li = 0, k0 = 0;
+        if (g0 < total) {
+          li = static_cast<uint32_t>(g0 / ostride);
+          k0 = static_cast<uint32_t>(g0 - uint64_t{li} * ostride);
+          const uint4* src = reinterpret_cast<const uint4*>(d.order + g0);
+#pragma unroll
+          for (int v = 0; v < kE / 4; ++v) {
+            const uint4 x = __ldg(src + v);
+            r[4 * v] = x.x;
+            r[4 * v + 1] = x.y;
+            r[4 * v + 2] = x.z;
+            r[4 * v + 3] = x.w;
+          }
+#pragma unroll
+          for (int g = 0; g < kE; ++g)
+            if (k0 + g < n && get_bit(bits, r[g])) in |= 1u << g;
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan<NT>(__popc(in), sh_scan, &tot);
+        uint32_t o = static_cast<uint32_t>(carry + ex - uint64_t{li} * A0);
+        uint32_t* out = lists[0] + static_cast<size_t>(li) * stride;
+#pragma unroll
+        for (int g = 0; g < kE; ++g)
+          if ((in >> g) & 1u) out[o++] = inbag_pos(bits, pref, r[g]);
+        carry += tot;
+      }
+    }
+    __syncthreads();
     if (wid == 0) {
       double s, q;
       root_sums_warp<G>(pay[0], wyy[0], A0, s, q);
       if (lane == 0) {
-        s_root[0] = s;
-        s_root[1] = q;
-      }
-    } else {
-      for (uint32_t c = wid - 1; c < p; c += NW - 1) {
-        const uint32_t* ord = d.order + static_cast<size_t>(c) * n;
-        uint32_t* out = lists[0] + static_cast<size_t>(c) * stride;
-        uint32_t o = 0;
-        for (uint32_t k0 = 0; k0 < n; k0 += 32 * G) {
-          uint32_t r[G];
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t k = k0 + g * 32 + lane;
-            r[g] = k < n ? __ldg(ord + k) : 0u;
-          }
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const uint32_t k = k0 + g * 32 + lane;
-            const bool in = k < n && get_bit(bits, r[g]);
-            const unsigned bl = __ballot_sync(kFull, in);
-            if (in) {
-              const uint32_t rr = r[g], w = rr >> 5;
-              const uint32_t pos = pref[rr >> 6] + ((w & 1u) ? __popc(bits[w - 1]) : 0u) +
-                                   __popc(bits[w] & ((1u << (rr & 31u)) - 1u));
-              out[o + __popc(bl & lanemask_lt())] = pos;
-            }
-            o += __popc(bl);
-          }
-        }
+        front[0][0] = NodeWork{0u, A0, 0u, 0u, static_cast<double>(n), s, q};
+        nf[0] = -1;
+        nthr[0] = 0.0;
+        nleft[0] = -1;
+        nval[0] = 0.0;
+        nrank[0] = 0u;
+        s_F = 1;
+        s_nodes = 1;
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      front[0][0] = NodeWork{0u, A0, 0u, 0u, static_cast<double>(n), s_root[0], s_root[1]};
-      nf[0] = -1;
-      nthr[0] = 0.0;
-      nleft[0] = -1;
-      nval[0] = 0.0;
-      nrank[0] = 0u;
-      s_F = 1;
-      s_nodes = 1;
-    }
-    __syncthreads();
+    PHASE(3);
 
     // ---- level loop (forest.hpp:233-374) ----
     uint32_t cur = 0, A = A0;
@@ -519,6 +706,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         if (tid == 0) s_E = carry;
       }
       __syncthreads();
+      PHASE(5);
       const uint32_t E = s_E;
       // mtry sampling: partial Fisher-Yates over a fresh pool, then ascending
       // (forest.hpp:258-266); counters continue the tree's stream after the n
@@ -542,30 +730,41 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         for (uint32_t i = 0; i < m; ++i) samp[static_cast<size_t>(e) * m + i] = pool[i];
       }
       __syncthreads();
+      PHASE(6);
       // split chains (forest.hpp:268-297)
       const uint32_t ntask = E * m;
       for (uint32_t k = wid; k < ntask; k += NW) {
         const NodeWork nw = fr[e2f[k / m]];
         if (nw.e - nw.b < kLaneMax) continue;
         const uint32_t c = samp[k];
+        const int32_t li = d.list_of[c];
+        const RankT* rk_c = rank + static_cast<size_t>(c) * n;
         double bg;
         uint32_t bp;
-        chain_warp<RankT, G>(lists[cur] + static_cast<size_t>(c) * stride, nw.b, nw.e,
-                             pay[cur], rank + static_cast<size_t>(c) * n, nw.w, nw.s, bg,
-                             bp);
+        if (li >= 0)
+          chain_warp<RankT, G>(lists[cur] + static_cast<size_t>(li) * stride, nw.b, nw.e,
+                               pay[cur], rk_c, nw.w, nw.s, bg, bp);
+        else
+          chain_bin_warp<RankT, G>(pay[cur], nw.b, nw.e, rk_c, nw.w, nw.s, bg, bp);
         if (lane == 0) res[k] = ChainRes{bg, bp, 0u};
       }
       for (uint32_t k = tid; k < ntask; k += NT) {
         const NodeWork nw = fr[e2f[k / m]];
         if (nw.e - nw.b >= kLaneMax) continue;
         const uint32_t c = samp[k];
+        const int32_t li = d.list_of[c];
+        const RankT* rk_c = rank + static_cast<size_t>(c) * n;
         double bg;
         uint32_t bp;
-        chain_lane<RankT>(lists[cur] + static_cast<size_t>(c) * stride, nw.b, nw.e,
-                          pay[cur], rank + static_cast<size_t>(c) * n, nw.w, nw.s, bg, bp);
+        if (li >= 0)
+          chain_lane<RankT>(lists[cur] + static_cast<size_t>(li) * stride, nw.b, nw.e,
+                            pay[cur], rk_c, nw.w, nw.s, bg, bp);
+        else
+          chain_bin_lane<RankT>(pay[cur], nw.b, nw.e, rk_c, nw.w, nw.s, bg, bp);
         res[k] = ChainRes{bg, bp, 0u};
       }
       __syncthreads();
+      PHASE(7);
       // decide + number children in frontier order (forest.hpp:299-319)
       {
         const uint32_t nodes0 = s_nodes;
@@ -592,17 +791,27 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
             } else {
               sp = 1;
               c = samp[static_cast<size_t>(e) * m + bi];
-              const uint32_t* lc = lists[cur] + static_cast<size_t>(c) * stride;
-              const uint32_t r1 = pay[cur][lc[bp - 1]].row;
-              const uint32_t r0 = pay[cur][lc[bp]].row;
-              const double prev = d.col[static_cast<size_t>(c) * n + r1];
-              const double v = d.col[static_cast<size_t>(c) * n + r0];
+              const int32_t li = d.list_of[c];
+              const double* vals = d.vals + d.vals_off[c];
+              double prev, v;
+              uint32_t lo, hi;
+              if (li >= 0) {
+                const uint32_t* lc = lists[cur] + static_cast<size_t>(li) * stride;
+                const uint32_t r1 = pay[cur][lc[bp - 1]].row;
+                const uint32_t r0 = pay[cur][lc[bp]].row;
+                prev = d.col[static_cast<size_t>(c) * n + r1];
+                v = d.col[static_cast<size_t>(c) * n + r0];
+                lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
+                hi = rank_of(rank + static_cast<size_t>(c) * n, r0);
+              } else {  // two-level column: the boundary is between its two values
+                prev = vals[0];
+                v = vals[1];
+                lo = 0;
+                hi = 1;
+              }
               thr = __dadd_rn(prev, __ddiv_rn(__dsub_rn(v, prev), 2.0));
               if (thr >= v) thr = prev;
-              // largest distinct-value rank whose value <= thr
-              const double* vals = d.vals + d.vals_off[c];
-              uint32_t lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
-              uint32_t hi = rank_of(rank + static_cast<size_t>(c) * n, r0);  // vals[hi] > thr
+              // largest distinct-value rank whose value <= thr (vals[lo] <= thr < vals[hi])
               while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
                 if (vals[mid] <= thr) lo = mid; else hi = mid;
@@ -641,7 +850,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
           split_rows_acc += ccarry;
         }
       }
+      // the goes-left bitmap over payload positions starts empty each level
+      for (uint32_t w = tid; w < (A + 31u) / 32u; w += NT) bits[w] = 0u;
       __syncthreads();
+      PHASE(8);
       const uint32_t S = s_S;
       elig_base += E;
       if (S == 0) break;
@@ -653,40 +865,47 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       const uint32_t nxt = cur ^ 1u;
       // route rows of every split node through column-0 order (forest.hpp:323-352)
       {
-        const uint32_t* l0 = lists[cur];
-        for (uint32_t s = wid; s < S; s += NW) {
-          const SplitInfo si = spl[s];
-          const NodeWork nw = fr[si.f];
-          if (si.cnt < kLaneMax) continue;
-          const RouteOut o = route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], wyy[cur],
-                                                  rank + static_cast<size_t>(si.c) * n,
-                                                  si.thr_rank, bits);
-          if (lane == 0) {
+        const uint32_t* l0 = list0 >= 0 ? lists[cur] + static_cast<size_t>(list0) * stride
+                                        : nullptr;
+        const RankT* rk0 = rank;  // column 0
+        for (int pass = 0; pass < 2; ++pass) {
+          // pass 0: warps take large nodes; pass 1: lanes take small ones
+          const uint32_t step = pass == 0 ? NW : NT;
+          for (uint32_t s = pass == 0 ? wid : tid; s < S; s += step) {
+            const SplitInfo si = spl[s];
+            if ((pass == 0) != (si.cnt >= kLaneMax)) continue;
+            const NodeWork nw = fr[si.f];
+            const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+            RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+            if (pass == 0) {
+              if (l0)
+                route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank,
+                                     bits, o);
+              else
+                route_groups_warp<RankT, G>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels,
+                                            rk_f, si.thr_rank, bits, o);
+              if (lane != 0) continue;
+            } else {
+              if (l0)
+                route_lane<RankT>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank, bits,
+                                  o);
+              else
+                route_groups_lane<RankT>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels, rk_f,
+                                         si.thr_rank, bits, o);
+            }
             spl[s].nl = o.nl;
             const uint32_t child = static_cast<uint32_t>(nleft[nw.id]);
             front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
                                          static_cast<double>(o.wl), o.sl, o.ql};
-            front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1,
-                                             0u, static_cast<double>(o.wr), o.sr, o.qr};
+            front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
+                                             static_cast<double>(o.wr), o.sr, o.qr};
           }
-        }
-        for (uint32_t s = tid; s < S; s += NT) {
-          const SplitInfo si = spl[s];
-          if (si.cnt >= kLaneMax) continue;
-          const NodeWork nw = fr[si.f];
-          const RouteOut o = route_lane<RankT>(l0, nw.b, nw.e, pay[cur], wyy[cur],
-                                               rank + static_cast<size_t>(si.c) * n,
-                                               si.thr_rank, bits);
-          spl[s].nl = o.nl;
-          const uint32_t child = static_cast<uint32_t>(nleft[nw.id]);
-          front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
-                                       static_cast<double>(o.wl), o.sl, o.ql};
-          front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
-                                           static_cast<double>(o.wr), o.sr, o.qr};
         }
       }
       __syncthreads();
-      // segment table: offsets of the stable partition into compacted children
+      PHASE(9);
+      // segment table (stable partition offsets into compacted children) and
+      // per-word prefix counts of the goes-left bitmap
       {
         uint32_t carry = 0;
         for (uint32_t base = 0; base < S; base += NT) {
@@ -706,92 +925,88 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
           carry += tot;
         }
         if (tid == 0) s_totL = carry;
-      }
-      __syncthreads();
-      // payload pass: stable multi-segment partition of the payload (+ newpos map)
-      {
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < A; base += NT * 4) {
-          uint32_t f4[4], lf = 0, keep = 0;
-          const uint32_t k0 = base + tid * 4;
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint32_t k = k0 + g;
-            f4[g] = k < A ? seg[cur][k] : 0u;
-            const bool kp = k < A && segtab[f4[g]].offL != INT_MIN;
-            const bool l = kp && get_bit(bits, k);
-            keep |= (kp ? 1u : 0u) << g;
-            lf |= (l ? 1u : 0u) << g;
-          }
+        const uint32_t aw = (A + 31u) / 32u;
+        carry = 0;
+        for (uint32_t base = 0; base < aw; base += NT) {
+          const uint32_t w = base + tid;
+          const uint32_t v = w < aw ? __popc(bits[w]) : 0u;
           uint32_t tot;
-          uint32_t pl = carry + block_excl_scan<NT>(__popc(lf), sh_scan, &tot);
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const uint32_t k = k0 + g;
-            if (!((keep >> g) & 1u)) continue;
-            const SegTab tb = segtab[f4[g]];
-            const bool l = (lf >> g) & 1u;
-            const uint32_t dst = l ? static_cast<uint32_t>(tb.offL + static_cast<int32_t>(pl))
-                                   : static_cast<uint32_t>(tb.offR + static_cast<int32_t>(k) -
-                                                           static_cast<int32_t>(pl));
-            if (l) ++pl;
-            pay[nxt][dst] = pay[cur][k];
-            wyy[nxt][dst] = wyy[cur][k];
-            seg[nxt][dst] = tb.child + (l ? 0u : 1u);
-            newpos[k] = dst;
-          }
+          const uint32_t ex = block_excl_scan<NT>(v, sh_scan, &tot);
+          if (w < aw) pref[w] = carry + ex;
           carry += tot;
         }
       }
       __syncthreads();
-      // list pass: the same partition applied to every column list, flattened
-      // over (column, position) with a per-column left-count offset c*totL
+      PHASE(10);
+      // payload pass: element k goes to offL + lefts-before-k, or offR + k - that
+      for (uint32_t k = tid; k < A; k += NT) {
+        const uint32_t f = seg[cur][k];
+        const SegTab tb = segtab[f];
+        if (tb.offL == INT_MIN) continue;
+        const bool l = get_bit(bits, k);
+        const int32_t lp = static_cast<int32_t>(bits_before(bits, pref, k));
+        const uint32_t dst = static_cast<uint32_t>(l ? tb.offL + lp
+                                                     : tb.offR + static_cast<int32_t>(k) - lp);
+        pay[nxt][dst] = pay[cur][k];
+        wyy[nxt][dst] = wyy[cur][k];
+        seg[nxt][dst] = tb.child + (l ? 0u : 1u);
+      }
+      __syncthreads();
+      PHASE(11);
+      // list pass: the same partition applied to every listed column, flattened
+      // over (list, position) with a per-list left-count offset li*totL; the new
+      // entry (payload position in the next level) comes from the same bitmap
       {
-        const uint32_t A4 = (A + 3u) & ~3u;
-        const uint64_t total = uint64_t{p} * A4;
+        const uint32_t A16 = (A + 15u) & ~15u;
+        const uint64_t total = uint64_t{nl_cols} * A16;
         const uint32_t totL = s_totL;
         uint64_t carry = 0;
-        for (uint64_t base = 0; base < total; base += NT * 4) {
-          const uint64_t g0 = base + uint64_t{tid} * 4;
-          uint32_t q4[4] = {0, 0, 0, 0}, f4[4] = {0, 0, 0, 0}, lf = 0, keep = 0;
-          uint32_t c = 0, k0 = 0;
+        for (uint64_t base = 0; base < total; base += uint64_t{NT} * kE) {
+          const uint64_t g0 = base + uint64_t{tid} * kE;
+          uint32_t q[kE], f[kE], lf = 0, keep = 0, li = 0, k0 = 0;
           if (g0 < total) {
-            c = static_cast<uint32_t>(g0 / A4);
-            k0 = static_cast<uint32_t>(g0 - uint64_t{c} * A4);
-            const uint4 v = *reinterpret_cast<const uint4*>(lists[cur] +
-                                                            static_cast<size_t>(c) * stride + k0);
-            q4[0] = v.x; q4[1] = v.y; q4[2] = v.z; q4[3] = v.w;
+            li = static_cast<uint32_t>(g0 / A16);
+            k0 = static_cast<uint32_t>(g0 - uint64_t{li} * A16);
+            const uint4* src =
+                reinterpret_cast<const uint4*>(lists[cur] + static_cast<size_t>(li) * stride + k0);
+            const uint4* sg = reinterpret_cast<const uint4*>(seg[cur] + k0);
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const uint32_t k = k0 + g;
-              if (k < A) {
-                f4[g] = seg[cur][k];
-                const bool kp = segtab[f4[g]].offL != INT_MIN;
-                keep |= (kp ? 1u : 0u) << g;
-                lf |= ((kp && get_bit(bits, q4[g])) ? 1u : 0u) << g;
+            for (int v = 0; v < kE / 4; ++v) {
+              const uint4 x = src[v];
+              const uint4 y = sg[v];
+              q[4 * v] = x.x; q[4 * v + 1] = x.y; q[4 * v + 2] = x.z; q[4 * v + 3] = x.w;
+              f[4 * v] = y.x; f[4 * v + 1] = y.y; f[4 * v + 2] = y.z; f[4 * v + 3] = y.w;
+            }
+#pragma unroll
+            for (int g = 0; g < kE; ++g) {
+              if (k0 + g < A && segtab[f[g]].offL != INT_MIN) {
+                keep |= 1u << g;
+                lf |= get_bit(bits, q[g]) << g;
               }
             }
           }
           uint32_t tot;
           const uint32_t ex = block_excl_scan<NT>(__popc(lf), sh_scan, &tot);
-          uint32_t pl = static_cast<uint32_t>(carry + ex - uint64_t{c} * totL);
-          uint32_t* dstl = lists[nxt] + static_cast<size_t>(c) * stride;
+          int32_t pl = static_cast<int32_t>(carry + ex - uint64_t{li} * totL);
+          uint32_t* dstl = lists[nxt] + static_cast<size_t>(li) * stride;
 #pragma unroll
-          for (int g = 0; g < 4; ++g) {
+          for (int g = 0; g < kE; ++g) {
             if (!((keep >> g) & 1u)) continue;
-            const uint32_t k = k0 + g;
-            const SegTab tb = segtab[f4[g]];
+            const SegTab tb = segtab[f[g]];
             const bool l = (lf >> g) & 1u;
-            const uint32_t dst = l ? static_cast<uint32_t>(tb.offL + static_cast<int32_t>(pl))
-                                   : static_cast<uint32_t>(tb.offR + static_cast<int32_t>(k) -
-                                                           static_cast<int32_t>(pl));
+            const int32_t lq = static_cast<int32_t>(bits_before(bits, pref, q[g]));
+            const uint32_t nq = static_cast<uint32_t>(
+                l ? tb.offL + lq : tb.offR + static_cast<int32_t>(q[g]) - lq);
+            const uint32_t dst = static_cast<uint32_t>(
+                l ? tb.offL + pl : tb.offR + static_cast<int32_t>(k0 + g) - pl);
             if (l) ++pl;
-            dstl[dst] = newpos[q4[g]];
+            dstl[dst] = nq;
           }
           carry += tot;
         }
       }
       __syncthreads();
+      PHASE(12);
       if (tid == 0) s_F = 2 * S;
       A = s_A;
       cur = nxt;
@@ -814,8 +1029,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     const unsigned long long off = s_pool;
     if (off + count <= a.pool_cap) {
       for (uint32_t i = tid; i < count; i += NT) {
-        const int32_t fi = nf[i];
-        a.pool_feature[off + i] = fi;
+        a.pool_feature[off + i] = nf[i];
         a.pool_thr[off + i] = nthr[i];
         a.pool_left[off + i] = nleft[i];
         a.pool_value[off + i] = nval[i];
@@ -838,6 +1052,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       }
     }
   }
+  if (a.prof && tid == 0)
+    for (int i = 0; i < kPhases; ++i)
+      atomicAdd(a.prof + i, static_cast<unsigned long long>(ph_acc[i]));
+#undef PHASE
 }
 
 namespace {
@@ -866,13 +1084,15 @@ cudaError_t launch_grow(int nt, int rank_bytes, const GrowArgs& a, int slots, si
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool gbits) {
+SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, uint32_t mns,
+                       bool gbits) {
+  (void)p;
   SlotLayout L{};
   // in-bag distinct rows: 0.632 n on average; bound it generously (checked at run time)
   const double exp_a = 0.6322 * static_cast<double>(n) + 8.0 * std::sqrt(static_cast<double>(n)) + 64.0;
   uint64_t stride = static_cast<uint64_t>(exp_a);
   if (stride > n) stride = n;
-  stride = (stride + 3) & ~uint64_t{3};
+  stride = (stride + 15) & ~uint64_t{15};
   L.stride = static_cast<uint32_t>(stride);
   // a splittable node weighs >= 2*mns, so a level has <= n/(2 mns) eligible nodes
   // and <= n/mns frontier nodes
@@ -892,11 +1112,10 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool
   L.off_pay1 = take(stride * sizeof(Payload));
   L.off_wyy0 = take(stride * 8);
   L.off_wyy1 = take(stride * 8);
-  L.off_list0 = take(size_t{p} * stride * 4);
-  L.off_list1 = take(size_t{p} * stride * 4);
-  L.off_newpos = take(stride * 4);
-  L.off_seg0 = take(stride * 4);
-  L.off_seg1 = take(stride * 4);
+  L.off_list0 = take(size_t{nlisted} * stride * 4 + 64);
+  L.off_list1 = take(size_t{nlisted} * stride * 4 + 64);
+  L.off_seg0 = take(stride * 4 + 64);
+  L.off_seg1 = take(stride * 4 + 64);
   L.off_front0 = take(fmax * sizeof(NodeWork));
   L.off_front1 = take(fmax * sizeof(NodeWork));
   L.off_segtab = take(fmax * sizeof(SegTab));
@@ -910,8 +1129,8 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool
   L.off_nval = take(size_t{L.nodes_cap} * 8);
   L.off_nrank = take(size_t{L.nodes_cap} * 4);
   if (gbits) {
-    L.off_gbits = take(((n + 31) / 32 + 2) * 4);
-    L.off_gpref = take(((n + 63) / 64 + 2) * 4);
+    L.off_gbits = take(grow_bits_words(n, L.stride) * 4);
+    L.off_gpref = take(grow_pref_words(n, L.stride) * 4);
   }
   L.bytes = o;
   return L;

@@ -13,7 +13,7 @@ struct NodeWork {
   double w, s, q;
 };
 
-// Per in-bag row of a tree, in node-grouped order: global row, bootstrap
+// Per in-bag row of a tree, in node-grouped row order: global row, bootstrap
 // multiplicity, weighted response mult*y (forest.hpp:194-195).
 struct Payload {
   uint32_t row, mult;
@@ -45,16 +45,24 @@ struct SegTab {
 
 // Device view of a PreparedDataset (forest.hpp:134-161): column store, responses,
 // per-column (value,row) argsort, dense value ranks and the distinct values.
+// Columns with <= 2 distinct values ("two-level" columns, e.g. the one-hot device
+// columns) keep no sorted list: their (value,row) order is the row order of the
+// value-0 rows followed by the value-1 rows, which the grower reads off the
+// row-ordered payload directly.
 struct DevData {
   uint64_t n;
   uint32_t p;
-  uint32_t rank_bytes;  // 2 or 4
-  const double* col;     // p x n
-  const double* y;       // n
-  const uint32_t* order; // p x n
-  const void* rank;      // p x n (uint16 or uint32)
-  const double* vals;    // concatenated distinct sorted values per column
-  const uint64_t* vals_off;  // p+1
+  uint32_t rank_bytes;      // 2 or 4
+  uint32_t nlisted;         // columns with >= 3 distinct values
+  uint32_t order_stride;    // padded row stride of `order` (multiple of 4)
+  const double* col;        // p x n
+  const double* y;          // n
+  const uint32_t* order;    // nlisted x order_stride, listed columns only
+  const void* rank;         // p x n (uint16 or uint32)
+  const double* vals;       // concatenated distinct sorted values per column
+  const uint64_t* vals_off; // p+1
+  const int32_t* list_of;   // p: list slot of column c, or -1
+  const uint32_t* listed;   // nlisted: column of list slot i
 };
 
 struct SlotLayout {
@@ -62,10 +70,9 @@ struct SlotLayout {
   uint32_t fmax;    // max frontier width
   uint32_t emax;    // max eligible nodes per level
   uint32_t nodes_cap;
-  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1,
-      off_newpos, off_seg0, off_seg1, off_front0, off_front1, off_segtab, off_e2f,
-      off_samp, off_res, off_split, off_nf, off_nthr, off_nleft, off_nval, off_nrank,
-      off_gbits, off_gpref;
+  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
+      off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
+      off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_gbits, off_gpref;
   size_t bytes;
 };
 
@@ -92,9 +99,21 @@ struct GrowArgs {
   uint64_t* tree_off;
   uint32_t* tree_cnt;
   unsigned long long* split_rows;  // sum over split nodes of their in-bag distinct rows
+  unsigned long long* prof;  // optional: kPhases per-phase cycle totals (all CTAs)
   int* err;  // 1 = pool overflow, 2 = in-bag rows exceed stride, 3 = frontier overflow
 };
 
-SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t mtry, uint32_t mns, bool gbits);
+// bitmap words + prefix words the grower keeps in shared memory (or global)
+__host__ __device__ inline size_t grow_bits_words(uint64_t n, uint32_t stride) {
+  const size_t a = (n + 31) / 32, b = (stride + 31) / 32;
+  return (((a > b ? a : b) + 2) + 1) & ~size_t{1};
+}
+__host__ __device__ inline size_t grow_pref_words(uint64_t n, uint32_t stride) {
+  const size_t a = (n + 63) / 64, b = (stride + 31) / 32;
+  return (a > b ? a : b) + 2;
+}
+
+SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, uint32_t mns,
+                       bool gbits);
 
 }  // namespace aiwc_b200
