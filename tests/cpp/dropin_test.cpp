@@ -1,0 +1,52 @@
+// Drop-in check: the reference's UNMODIFIED experiments.hpp / tuner.hpp / synth.hpp
+// compiled against include/aiwc/forest.hpp (this repo) instead of the reference's
+// forest.hpp, linked to libaiwc_cuda.so.  Built by oracle/Makefile (target `dropin`,
+// needs /root/reference) into oracle/_ref/dropin_test; tests/test_dropin.py runs it on
+// the GPU box and compares its JSON line with the reference goldens.
+#include <aiwc/experiments.hpp>
+#include <aiwc/synth.hpp>
+#include <aiwc/tuner.hpp>
+
+#include <cstdio>
+#include <string>
+
+using namespace aiwc;
+
+int main() {
+  try {
+    const SynthResult s = synthesize(SynthConfig{});
+    const Dataset d = make_dataset(s.features, s.runtimes);
+    const std::uint64_t seed = derive_seed(1, "forest");
+    // forest.hpp:511 entry point
+    const Forest f = fit(d, ForestParams{500, 6, 5, seed});
+    const std::string js = f.to_json().dump();
+    // tuner.hpp:247-253 objective path: PreparedDataset + fit(prepared, params, jobs)
+    const PreparedDataset prep(d, ResponseTransform::Log10);
+    const double obj = fit(prep, ParamsPoint{505, 30, 9}.to_forest_params(seed), 8).oob.error_pct;
+    // experiments.hpp:383 evaluate (the reference's loop over folds, our fit/predict)
+    const EvaluateResult ev = evaluate(d, ForestParams{50, 6, 5, 0}, seed);
+    double mape = 0;
+    for (std::size_t i = 0; i < d.rows.size(); ++i)
+      mape += 100.0 * std::abs(ev.predicted_time_s[i] - d.rows[i].measured_time_s) /
+              d.rows[i].measured_time_s;
+    mape /= static_cast<double>(d.rows.size());
+    // model round trip through the canonical JSON (forest.hpp:524-604)
+    const Forest g = Forest::from_json(nlohmann::json::parse(js));
+    const bool same = g.to_json().dump() == js &&
+                      g.predict_time(d.predictor_row(7)) == f.predict_time(d.predictor_row(7));
+    // oob_error recomputes OOB from trees + in-bag lists (forest.hpp:518)
+    const OobStats o2 = oob_error(f, d);
+    std::printf(
+        "{\"json_fnv\": %llu, \"json_size\": %zu, \"oob_error_pct\": %.17g, \"r2\": %.17g, "
+        "\"oob_recomputed\": %.17g, \"obj_505_30_9\": %.17g, \"c3_50_mape\": %.17g, "
+        "\"pairs\": %llu, \"pairs_correct\": %llu, \"roundtrip\": %s}\n",
+        static_cast<unsigned long long>(fnv1a64(js)), js.size(), f.oob.error_pct,
+        f.oob.r_squared, o2.error_pct, obj, mape,
+        static_cast<unsigned long long>(ev.rank.pairs),
+        static_cast<unsigned long long>(ev.rank.pairs_correct), same ? "true" : "false");
+    return 0;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "dropin_test: %s\n", e.what());
+    return 3;
+  }
+}

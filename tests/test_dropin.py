@@ -1,0 +1,41 @@
+"""Drop-in boundary: the reference's unmodified experiments.hpp / tuner.hpp / synth.hpp
+compiled against include/aiwc/forest.hpp (this repo), linked to libaiwc_cuda.so
+(oracle/_ref/dropin_test, built by `make -C oracle dropin` where /root/reference exists)."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "dropin_test")
+# canonical model JSON of the C1 500/6/5 forest: 17,820,410 bytes, FNV-1a64 below
+# (SURVEY.md section 8c golden, reproduced by oracle/_ref in tests/golden)
+C1_JSON_FNV = 0x22EFBC8C4B207134
+C1_JSON_SIZE = 17820410
+
+needs_bin = pytest.mark.skipif(not os.path.exists(BIN), reason="dropin_test not built")
+
+
+@needs_bin
+def test_dropin_binary_links_product_library():
+    out = subprocess.run(["ldd", BIN], capture_output=True, text=True).stdout
+    line = [x for x in out.splitlines() if "libaiwc_cuda.so" in x]
+    assert line and "not found" not in line[0]
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_reference_callers_run_unchanged_on_gpu(golden):
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["json_fnv"] == C1_JSON_FNV and got["json_size"] == C1_JSON_SIZE
+    c1 = golden["c1_500_6_5"]["oob"]
+    assert got["oob_error_pct"] == c1[3] and got["r2"] == c1[4]
+    assert got["oob_recomputed"] == c1[3]
+    assert got["obj_505_30_9"] == golden["c1_505_30_9"]["oob"][3]
+    c3 = golden["c3_50_6_5"]
+    assert got["c3_50_mape"] == c3["mape"]
+    assert (got["pairs"], got["pairs_correct"]) == (c3["pairs"], c3["pairs_correct"])
+    assert got["roundtrip"] is True
