@@ -242,23 +242,16 @@ def main():
     params = pkg.ForestParams(total_trees, C4_MTRY, C4_MNS, seed)
     tb, te = rank * per, (rank + 1) * per
 
+    from paper_1811_00156_b200 import shard
+
+    send, recv = shard.torch_transport(device=torch.device("cuda", local))
+
     def chained_oob(forest):
         """Exact tree-ordered OOB over ranks: rank r continues rank r-1's per-row sums."""
-        n = table.n
-        rs = np.zeros(n)
-        rc = np.zeros(n, np.uint32)
-        if rank > 0:
-            buf = torch.empty(n * 12 // 4, dtype=torch.int32, device="cuda")
-            dist.recv(buf, src=rank - 1)
-            raw = buf.cpu().numpy().view(np.uint8)
-            rs = raw[: 8 * n].view(np.float64).copy()
-            rc = raw[8 * n:].view(np.uint32).copy()
-        pkg.oob_accumulate(forest, prep, rs, rc)
-        if rank < world - 1:
-            raw = np.concatenate([rs.view(np.uint8), rc.view(np.uint8)])
-            dist.send(torch.from_numpy(raw.view(np.int32).copy()).cuda(), dst=rank + 1)
-            return None
-        return pkg.oob_finalize(table.y, rs, rc)
+        res = shard.chained_oob(table.n, rank, world,
+                                lambda rs, rc: pkg.oob_accumulate(forest, prep, rs, rc),
+                                send, recv)
+        return None if res is None else pkg.oob_finalize(table.y, *res)
 
     def fit_step():
         if world == 1:

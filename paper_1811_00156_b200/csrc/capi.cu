@@ -4,6 +4,7 @@
 // fit (grow_kernel launch over persistent per-tree CTAs, pool compaction, OOB),
 // forest export/import, OOB, predict and hold-one-kernel-out evaluate.
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -213,6 +214,18 @@ struct aiwc_forest {
   double grow_ms = 0, fit_ms = 0;
   uint64_t split_rows = 0;
   uint32_t grow_launches = 0;
+  // binned, chunked copy for the shared-memory predict path (built on first predict)
+  struct Chunk {
+    uint64_t node0, leaf0, root0;
+    uint32_t nnodes, nleaves, ntrees;
+  };
+  std::mutex bin_mu;
+  bool bin_ready = false, bin_ok = false;
+  uint32_t bin_p = 0, bin_bytes = 1;
+  std::vector<Chunk> chunks;
+  DevBuf<BinNode> bnodes;
+  DevBuf<double> bleaves, bthr;
+  DevBuf<uint32_t> broots, bthr_off;
 };
 
 extern "C" {
@@ -397,6 +410,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     if (tree_begin >= tree_end || tree_end > num_trees)
       throw Status(AIWC_EARG, "bad tree range");
     std::lock_guard<std::mutex> lock(ctx->mu);
+    const auto t_start = std::chrono::steady_clock::now();
     DeviceGuard dg(ctx->device);
     struct {
       cudaStream_t s;
@@ -411,7 +425,8 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     SlotLayout L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, false);
     const size_t bits_smem = (grow_bits_words(n, L.stride) + grow_pref_words(n, L.stride)) * 4;
-    const bool smem_bits = bits_smem + 4096 <= static_cast<size_t>(max_optin);
+    // static shared memory of grow_kernel: scans + per-warp FP64 stages (< 12 KB)
+    const bool smem_bits = bits_smem + 12288 <= static_cast<size_t>(max_optin);
     const size_t dyn = smem_bits ? bits_smem : 0;
     if (!smem_bits) L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
 
@@ -491,6 +506,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     cudaEvent_t evs[4] = {ev0, ev1, evf0, evf1};
     EvGuard eg{evs};
     CK(cudaEventRecord(evf0, st.s));
+    const auto t_grow0 = std::chrono::steady_clock::now();
     for (int attempt = 0; attempt < 2; ++attempt) {
       pf.alloc(cap);
       pl.alloc(cap);
@@ -563,12 +579,19 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     g_launches += 1;
     CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
     CK(cudaStreamSynchronize(st.s));
+    const auto t_compact = std::chrono::steady_clock::now();
     if (compute_oob && tree_begin == 0 && tree_end == num_trees) {
       std::vector<double> sum(n, 0.0);
       std::vector<uint32_t> count(n, 0);
       oob_accumulate_device(f.get(), sum.data(), count.data(), st.s);
       f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
       f->has_oob = true;
+    }
+    if (want_prof) {
+      const auto now = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[aiwc fit host] setup %.1f ms, grow+compact %.1f ms, oob %.1f ms\n",
+                   ms(t_start, t_grow0), ms(t_grow0, t_compact), ms(t_compact, now));
     }
     CK(cudaEventRecord(evf1, st.s));
     CK(cudaEventSynchronize(evf1));
@@ -744,6 +767,139 @@ int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+constexpr int kPredNT = kPredictThreads;
+constexpr size_t kPredSmem = 220 * 1024;  // per-CTA budget: chunk nodes+leaves + bin tile
+
+// Build the binned copy: per column the sorted distinct thresholds the forest uses,
+// per node its threshold bin, trees packed into shared-memory-sized chunks.
+void build_binned(aiwc_forest* f, uint32_t p) {
+  std::lock_guard<std::mutex> lock(f->bin_mu);
+  if (f->bin_ready && f->bin_p == p) return;
+  f->bin_ready = true;
+  f->bin_p = p;
+  f->bin_ok = false;
+  const uint64_t N = f->off.back();
+  std::vector<int32_t> fe(N), le(N);
+  std::vector<double> th(N), va(N);
+  CK(cudaMemcpy(fe.data(), f->feature.p, N * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(le.data(), f->left.p, N * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(th.data(), f->thr.p, N * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(va.data(), f->value.p, N * 8, cudaMemcpyDeviceToHost));
+  std::vector<std::vector<double>> T(p);
+  for (uint64_t i = 0; i < N; ++i) {
+    if (fe[i] < 0) continue;
+    if (static_cast<uint32_t>(fe[i]) >= p || fe[i] >= 0xffff) return;  // schema too wide
+    T[fe[i]].push_back(th[i]);
+  }
+  size_t maxT = 0;
+  std::vector<uint32_t> toff(p + 1, 0);
+  for (uint32_t c = 0; c < p; ++c) {
+    auto& v = T[c];
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    maxT = std::max(maxT, v.size());
+    toff[c + 1] = toff[c] + static_cast<uint32_t>(v.size());
+  }
+  if (maxT >= 0xffff) return;
+  f->bin_bytes = maxT < 0xff ? 1 : 2;
+  const size_t tile = size_t{kPredNT} * p * f->bin_bytes;
+  if (tile + 4096 > kPredSmem) return;
+  const size_t budget = kPredSmem - tile - 64;
+  std::vector<double> thr_all;
+  for (auto& v : T) thr_all.insert(thr_all.end(), v.begin(), v.end());
+  std::vector<BinNode> nodes;
+  std::vector<double> leaves;
+  std::vector<uint32_t> roots;
+  f->chunks.clear();
+  aiwc_forest::Chunk ch{0, 0, 0, 0, 0, 0};
+  for (uint32_t t = 0; t < f->trees; ++t) {
+    const uint64_t b = f->off[t], e = f->off[t + 1];
+    uint32_t nl = 0;
+    for (uint64_t i = b; i < e; ++i) nl += fe[i] < 0;
+    const size_t need = (ch.nnodes + (e - b)) * sizeof(BinNode) + 16 + (ch.nleaves + nl) * 8;
+    if (ch.ntrees > 0 && need > budget) {
+      f->chunks.push_back(ch);
+      ch = aiwc_forest::Chunk{nodes.size(), leaves.size(), roots.size(), 0, 0, 0};
+    }
+    if ((e - b) * sizeof(BinNode) + 16 + nl * 8 > budget) return;  // one tree too big
+    roots.push_back(ch.nnodes);
+    for (uint64_t i = b; i < e; ++i) {
+      const uint32_t local = static_cast<uint32_t>(i - b) + ch.nnodes;
+      (void)local;
+      if (fe[i] < 0) {
+        nodes.push_back(BinNode{0xffff, 0, ch.nleaves});
+        leaves.push_back(va[i]);
+        ++ch.nleaves;
+      } else {
+        const auto& v = T[fe[i]];
+        const uint32_t j = static_cast<uint32_t>(std::lower_bound(v.begin(), v.end(), th[i]) - v.begin());
+        nodes.push_back(BinNode{static_cast<uint16_t>(fe[i]), static_cast<uint16_t>(j),
+                                ch.nnodes + static_cast<uint32_t>(le[i])});
+      }
+    }
+    ch.nnodes += static_cast<uint32_t>(e - b);
+    ++ch.ntrees;
+  }
+  f->chunks.push_back(ch);
+  f->bnodes.alloc(nodes.size());
+  f->bleaves.alloc(leaves.size());
+  f->broots.alloc(roots.size());
+  f->bthr.alloc(std::max<size_t>(thr_all.size(), 1));
+  f->bthr_off.alloc(toff.size());
+  CK(cudaMemcpy(f->bnodes.p, nodes.data(), nodes.size() * sizeof(BinNode), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(f->bleaves.p, leaves.data(), leaves.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(f->broots.p, roots.data(), roots.size() * 4, cudaMemcpyHostToDevice));
+  if (!thr_all.empty())
+    CK(cudaMemcpy(f->bthr.p, thr_all.data(), thr_all.size() * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(f->bthr_off.p, toff.data(), toff.size() * 4, cudaMemcpyHostToDevice));
+  f->bin_ok = true;
+}
+
+void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p, double* d_out,
+                    cudaStream_t s) {
+  const size_t bb = f->bin_bytes;
+  DevBuf<uint8_t> bins(q * p * bb);
+  DevBuf<double> sum(q);
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device));
+  CK(launch_bin_queries(f->bin_bytes, d_rows, q, p, f->bthr.p, f->bthr_off.p, bins.p, s));
+  g_launches += 1;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(sms, (q + kPredNT - 1) / kPredNT));
+  for (size_t k = 0; k < f->chunks.size(); ++k) {
+    const auto& ch = f->chunks[k];
+    const size_t smem = ((ch.nnodes * sizeof(BinNode) + 15) & ~size_t{15}) + ch.nleaves * 8 +
+                        size_t{kPredNT} * p * bb;
+    CK(launch_predict_chunk(f->bin_bytes, f->bnodes.p + ch.node0, ch.nnodes,
+                            f->bleaves.p + ch.leaf0, ch.nleaves, f->broots.p + ch.root0, ch.ntrees,
+                            bins.p, q, p, sum.p, k == 0, k + 1 == f->chunks.size(),
+                            static_cast<double>(f->trees), d_out, grid, smem, kPredSmem, s));
+    g_launches += 1;
+  }
+}
+
+// device rows -> device responses; binned shared-memory path when the forest fits,
+// else the L2 walk (predict_kernel)
+void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
+                      double* d_out, cudaStream_t s) {
+  build_binned(f, p);
+  if (f->bin_ok) {
+    predict_binned(f, d_rows, q, p, d_out, s);
+    return;
+  }
+  predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(f->packed.p, f->d_off.p,
+                                                                        f->trees, d_rows, q, p, d_out);
+  CK(cudaGetLastError());
+  g_launches += 1;
+}
+
+}  // namespace
+
+extern "C" {
+
 int aiwc_predict_device(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
                         double* d_out) {
   return guard([&] {
@@ -751,10 +907,7 @@ int aiwc_predict_device(aiwc_forest* f, const double* d_rows, uint64_t q, uint32
     if (q == 0) return;
     DeviceGuard dg(f->device);
     Stream st;
-    predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st.s>>>(
-        f->packed.p, f->d_off.p, f->trees, d_rows, q, p, d_out);
-    CK(cudaGetLastError());
-    g_launches += 1;
+    predict_dispatch(f, d_rows, q, p, d_out, st.s);
     CK(cudaStreamSynchronize(st.s));
   });
 }
@@ -768,10 +921,7 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
     Stream st;
     DevBuf<double> dr(q * p), dout(q);
     CK(cudaMemcpyAsync(dr.p, rows, q * p * 8, cudaMemcpyHostToDevice, st.s));
-    predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, st.s>>>(
-        f->packed.p, f->d_off.p, f->trees, dr.p, q, p, dout.p);
-    CK(cudaGetLastError());
-    g_launches += 1;
+    predict_dispatch(f, dr.p, q, p, dout.p, st.s);
     CK(cudaMemcpyAsync(out_response, dout.p, q * 8, cudaMemcpyDeviceToHost, st.s));
     CK(cudaStreamSynchronize(st.s));
   });

@@ -71,4 +71,26 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sh,
   return r;
 }
 
+// Block-wide exclusive scan of one uint64 per thread (used with 4 packed 16-bit
+// counters: one scan serves four tile rows).  `sh` needs 2*(NT/32) + 2 words.
+template <int NT>
+__device__ __forceinline__ uint64_t block_excl_scan64(uint64_t v, uint64_t* sh,
+                                                      uint64_t* total) {
+  constexpr int NW = NT / 32;
+  __syncthreads();
+  const uint64_t inc = warp_incl_scan(v);
+  if (lane_id() == 31) sh[warp_id()] = inc;
+  __syncthreads();
+  if (warp_id() == 0) {
+    const uint64_t w = lane_id() < NW ? sh[lane_id()] : 0ull;
+    const uint64_t wi = warp_incl_scan(w);
+    if (lane_id() < NW) sh[lane_id()] = wi - w;
+    if (lane_id() == NW - 1) sh[NW] = wi;
+  }
+  __syncthreads();
+  const uint64_t r = sh[warp_id()] + inc - v;
+  *total = sh[NW];
+  return r;
+}
+
 }  // namespace aiwc_b200

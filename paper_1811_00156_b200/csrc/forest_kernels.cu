@@ -100,6 +100,118 @@ __global__ void predict_kernel(const PredNode* __restrict__ nodes,
   out[i] = __ddiv_rn(s, static_cast<double>(T));
 }
 
+// ---- shared-memory predict over binned queries ------------------------------------
+// Threshold binning: with T_c the sorted distinct thresholds the forest uses on column
+// c and thr = T_c[j],  x <= thr  <=>  #{t in T_c : t < x} <= j.  NaN goes to the
+// largest bin (every comparison false -> right child, as in Tree::predict).
+template <typename BinT>
+__global__ void bin_queries_kernel(const double* __restrict__ rows, uint64_t q, uint32_t p,
+                                   const double* __restrict__ thr,
+                                   const uint32_t* __restrict__ thr_off, BinT* __restrict__ bins) {
+  const uint64_t total = q * p;
+  for (uint64_t g = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; g < total;
+       g += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t c = static_cast<uint32_t>(g % p);
+    const double x = rows[g];
+    const double* t = thr + thr_off[c];
+    uint32_t lo = 0, hi = thr_off[c + 1] - thr_off[c];
+    if (x != x) {
+      lo = sizeof(BinT) == 1 ? 0xffu : 0xffffu;
+    } else {
+      while (lo < hi) {  // first index with t >= x == count of thresholds < x
+        const uint32_t mid = (lo + hi) >> 1;
+        if (t[mid] < x) lo = mid + 1; else hi = mid;
+      }
+    }
+    bins[g] = static_cast<BinT>(lo);
+  }
+}
+
+// One launch per tree chunk: the chunk's nodes and leaf values sit in shared memory,
+// every query walks the chunk's trees in order, continuing its running sum from the
+// previous chunk (so the per-query sum keeps the reference's tree order exactly).
+template <typename BinT, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    predict_chunk_kernel(const BinNode* __restrict__ nodes, uint32_t nnodes,
+                         const double* __restrict__ leaves, uint32_t nleaves,
+                         const uint32_t* __restrict__ roots, uint32_t ntrees,
+                         const BinT* __restrict__ bins, uint64_t q, uint32_t p,
+                         double* __restrict__ sum, int first, int last, double total_trees,
+                         double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  BinNode* sn = reinterpret_cast<BinNode*>(smem);
+  double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(BinNode) + 15) & ~size_t{15}));
+  BinT* sb = reinterpret_cast<BinT*>(reinterpret_cast<unsigned char*>(sl) + nleaves * 8);
+  for (uint32_t i = threadIdx.x; i < nnodes; i += NT) sn[i] = nodes[i];
+  for (uint32_t i = threadIdx.x; i < nleaves; i += NT) sl[i] = leaves[i];
+  for (uint64_t tile = uint64_t{blockIdx.x} * NT; tile < q; tile += uint64_t{gridDim.x} * NT) {
+    __syncthreads();
+    const uint64_t rem = q - tile;
+    const uint32_t cnt = rem < NT ? static_cast<uint32_t>(rem) : NT;
+    for (uint32_t i = threadIdx.x; i < cnt * p; i += NT) sb[i] = bins[tile * p + i];
+    __syncthreads();
+    if (threadIdx.x >= cnt) continue;
+    const uint64_t qi = tile + threadIdx.x;
+    const BinT* b = sb + threadIdx.x * p;
+    double s = first ? 0.0 : sum[qi];
+    for (uint32_t t = 0; t < ntrees; ++t) {
+      BinNode v = sn[roots[t]];
+      while (v.feat != 0xffffu) v = sn[v.child + (b[v.feat] <= v.j ? 0u : 1u)];
+      s = __dadd_rn(s, sl[v.child]);
+    }
+    if (last)
+      out[qi] = __ddiv_rn(s, total_trees);
+    else
+      sum[qi] = s;
+  }
+}
+
+// host-side launchers (kernels are launched from the TU that defines them)
+namespace {
+template <typename BinT>
+cudaError_t bin_t(const double* rows, uint64_t q, uint32_t p, const double* thr,
+                  const uint32_t* thr_off, void* bins, cudaStream_t s) {
+  const uint64_t blocks = (q * p + 255) / 256;
+  bin_queries_kernel<BinT><<<static_cast<unsigned>(blocks < 524288 ? blocks : 524288), 256, 0,
+                             s>>>(rows, q, p, thr, thr_off, static_cast<BinT*>(bins));
+  return cudaGetLastError();
+}
+template <typename BinT>
+cudaError_t chunk_t(const BinNode* nodes, uint32_t nnodes, const double* leaves, uint32_t nleaves,
+                    const uint32_t* roots, uint32_t ntrees, const void* bins, uint64_t q,
+                    uint32_t p, double* sum, int first, int last, double total_trees, double* out,
+                    unsigned grid, size_t smem, size_t smem_max, cudaStream_t s) {
+  auto k = predict_chunk_kernel<BinT, kPredictThreads>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_max));
+  if (e != cudaSuccess) return e;
+  k<<<grid, kPredictThreads, smem, s>>>(nodes, nnodes, leaves, nleaves, roots, ntrees,
+                                        static_cast<const BinT*>(bins), q, p, sum, first, last,
+                                        total_trees, out);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_bin_queries(int bin_bytes, const double* rows, uint64_t q, uint32_t p,
+                               const double* thr, const uint32_t* thr_off, void* bins,
+                               cudaStream_t s) {
+  return bin_bytes == 1 ? bin_t<uint8_t>(rows, q, p, thr, thr_off, bins, s)
+                        : bin_t<uint16_t>(rows, q, p, thr, thr_off, bins, s);
+}
+
+cudaError_t launch_predict_chunk(int bin_bytes, const BinNode* nodes, uint32_t nnodes,
+                                 const double* leaves, uint32_t nleaves, const uint32_t* roots,
+                                 uint32_t ntrees, const void* bins, uint64_t q, uint32_t p,
+                                 double* sum, int first, int last, double total_trees,
+                                 double* out, unsigned grid, size_t smem, size_t smem_max,
+                                 cudaStream_t s) {
+  return bin_bytes == 1
+             ? chunk_t<uint8_t>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p, sum,
+                                first, last, total_trees, out, grid, smem, smem_max, s)
+             : chunk_t<uint16_t>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p, sum,
+                                 first, last, total_trees, out, grid, smem, smem_max, s);
+}
+
 // C5 query generator: query i copies table row Rng(derive_seed(seed,"query",i)).bounded(n)
 // (first draw of that stream; rng.hpp:32-59)
 __global__ void make_queries_kernel(const double* __restrict__ rows, uint64_t n, uint32_t p,

@@ -16,6 +16,27 @@ struct alignas(16) PredNode {
   int32_t left;
 };
 
+// 8-byte node of a binned tree chunk: split column (0xffff = leaf), threshold bin j,
+// chunk-relative left child (right = left + 1) or leaf-value index
+struct BinNode {
+  uint16_t feat;
+  uint16_t j;
+  uint32_t child;
+};
+
+constexpr int kPredictThreads = 512;
+
+// binned shared-memory predict (kernels live in forest_kernels.cu and are launched there)
+cudaError_t launch_bin_queries(int bin_bytes, const double* rows, uint64_t q, uint32_t p,
+                               const double* thr, const uint32_t* thr_off, void* bins,
+                               cudaStream_t s);
+cudaError_t launch_predict_chunk(int bin_bytes, const BinNode* nodes, uint32_t nnodes,
+                                 const double* leaves, uint32_t nleaves, const uint32_t* roots,
+                                 uint32_t ntrees, const void* bins, uint64_t q, uint32_t p,
+                                 double* sum, int first, int last, double total_trees,
+                                 double* out, unsigned grid, size_t smem, size_t smem_max,
+                                 cudaStream_t s);
+
 cudaError_t launch_grow(int nt, int rank_bytes, const GrowArgs& a, int slots, size_t smem,
                         cudaStream_t st, int* blocks_per_sm);
 

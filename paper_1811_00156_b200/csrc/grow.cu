@@ -74,6 +74,85 @@ __device__ __forceinline__ double gain_at(double sl, double wl, double W, double
   return __dadd_rn(__ddiv_rn(__dmul_rn(sl, sl), wl), __ddiv_rn(__dmul_rn(d, d), wr));
 }
 
+// ---- sequential FP64 accumulation over one 32-element tile -----------------------
+// The values go through this warp's shared-memory stage and every lane runs the same
+// fully unrolled add chain, so the chain is bound by DADD latency alone (the loads are
+// independent of it).  The order of the adds is the lane order -- exactly the order
+// the reference visits these rows -- so results are bit-identical.
+
+// running value before each lane's element (lanes j < nv), `run` advanced past them
+__device__ __forceinline__ double tile_prefix(double v, uint32_t nv, double& run, double* st) {
+  const unsigned lane = lane_id();
+  st[lane] = v;
+  __syncwarp();
+  double r = run, mine = 0.0;
+  if (nv == 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double x = st[j];
+      mine = (lane == static_cast<unsigned>(j)) ? r : mine;
+      r = __dadd_rn(r, x);
+    }
+  } else {
+#pragma unroll 8
+    for (uint32_t j = 0; j < nv; ++j) {
+      const double x = st[j];
+      mine = (lane == j) ? r : mine;
+      r = __dadd_rn(r, x);
+    }
+  }
+  __syncwarp();
+  run = r;
+  return mine;
+}
+
+// add the masked lanes' (a, b) values, in lane order, onto (ra, rb)
+__device__ __forceinline__ void tile_masked_sum2(double a, double b, unsigned mask, double& ra,
+                                                 double& rb, double* st) {
+  const unsigned lane = lane_id();
+  if ((mask >> lane) & 1u) {
+    const unsigned k = __popc(mask & lanemask_lt());
+    st[k] = a;
+    st[32 + k] = b;
+  }
+  __syncwarp();
+  const uint32_t cnt = __popc(mask);
+  double x = ra, y = rb;
+  if (cnt == 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      x = __dadd_rn(x, st[j]);
+      y = __dadd_rn(y, st[32 + j]);
+    }
+  } else {
+#pragma unroll 8
+    for (uint32_t j = 0; j < cnt; ++j) {
+      x = __dadd_rn(x, st[j]);
+      y = __dadd_rn(y, st[32 + j]);
+    }
+  }
+  __syncwarp();
+  ra = x;
+  rb = y;
+}
+
+__device__ __forceinline__ void tile_masked_sum(double a, unsigned mask, double& ra, double* st) {
+  const unsigned lane = lane_id();
+  if ((mask >> lane) & 1u) st[__popc(mask & lanemask_lt())] = a;
+  __syncwarp();
+  const uint32_t cnt = __popc(mask);
+  double x = ra;
+  if (cnt == 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x = __dadd_rn(x, st[j]);
+  } else {
+#pragma unroll 8
+    for (uint32_t j = 0; j < cnt; ++j) x = __dadd_rn(x, st[j]);
+  }
+  __syncwarp();
+  ra = x;
+}
+
 __device__ __forceinline__ void warp_best(double& bg, uint32_t& bp) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -90,7 +169,8 @@ __device__ __forceinline__ void warp_best(double& bg, uint32_t& bp) {
 template <typename RankT, int G>
 __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
                            const Payload* pay, const RankT* __restrict__ rk_c,
-                           double W, double S, double& best_gain, uint32_t& best_pos) {
+                           double W, double S, double& best_gain, uint32_t& best_pos,
+                           double* st) {
   const unsigned lane = lane_id();
   double sl = 0.0;
   uint32_t wl = 0, prev_rank = 0;
@@ -131,12 +211,7 @@ __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
       const bool valid = lane < nv;
       const uint32_t inc = warp_incl_scan(mu[g]);
       const uint32_t wl_before = wl + inc - mu[g];
-      double run = sl, mine = 0.0;
-      for (uint32_t j = 0; j < nv; ++j) {
-        const double x = __shfl_sync(kFull, wy[g], j);
-        if (lane == j) mine = run;
-        run = __dadd_rn(run, x);
-      }
+      const double mine = tile_prefix(wy[g], nv, sl, st);
       uint32_t pr = __shfl_up_sync(kFull, rk[g], 1);
       if (lane == 0) pr = first ? rk[g] : prev_rank;
       if (valid && rk[g] != pr) {
@@ -146,7 +221,6 @@ __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
           bp = t0 + lane;
         }
       }
-      sl = run;
       wl += __shfl_sync(kFull, inc, 31);
       prev_rank = __shfl_sync(kFull, rk[g], nv - 1);
       first = false;
@@ -208,7 +282,7 @@ __device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
 template <typename RankT, int G>
 __device__ void chain_bin_warp(const Payload* pay, uint32_t b, uint32_t e,
                                const RankT* __restrict__ rk_c, double W, double S,
-                               double& best_gain, uint32_t& best_pos) {
+                               double& best_gain, uint32_t& best_pos, double* st) {
   const unsigned lane = lane_id();
   double s0 = 0.0;
   uint32_t w0 = 0, n0 = 0;
@@ -236,14 +310,10 @@ __device__ void chain_bin_warp(const Payload* pay, uint32_t b, uint32_t e,
     for (int g = 0; g < G; ++g) {
       const uint32_t t0 = k0 + g * 32;
       if (t0 >= e) break;
-      const uint32_t nv = min(32u, e - t0);
       const unsigned bz = __ballot_sync(kFull, z[g]);
       n0 += __popc(bz);
       w0 += warp_sum(z[g] ? mu[g] : 0u);
-      for (uint32_t j = 0; j < nv; ++j) {
-        const double x = __shfl_sync(kFull, wy[g], j);
-        if ((bz >> j) & 1u) s0 = __dadd_rn(s0, x);
-      }
+      tile_masked_sum(wy[g], bz, s0, st);
     }
   }
   const uint32_t R = e - b;
@@ -299,11 +369,12 @@ template <typename RankT, int G>
 __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
                            const Payload* pay, const double* wyy,
                            const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
-                           RouteOut& o) {
+                           RouteOut& o, double* st) {
   const unsigned lane = lane_id();
   for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
     uint32_t q[G], row[G], mu[G];
     double wy[G], yy[G];
+    bool lft[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
@@ -326,28 +397,23 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
       }
     }
 #pragma unroll
+    for (int g = 0; g < G; ++g)
+      lft[g] = (k0 + g * 32 + lane < e) && rank_of(rk_f, row[g]) <= thr_rank;
+#pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t t0 = k0 + g * 32;
       if (t0 >= e) break;
       const uint32_t nv = min(32u, e - t0);
       const bool valid = lane < nv;
-      const bool left = valid && rank_of(rk_f, row[g]) <= thr_rank;
+      const bool left = lft[g];
       if (left) atomicOr(bits + (q[g] >> 5), 1u << (q[g] & 31u));
       const unsigned bl = __ballot_sync(kFull, left);
+      const unsigned bv = __ballot_sync(kFull, valid);
       o.nl += __popc(bl);
       o.wl += warp_sum(left ? mu[g] : 0u);
       o.wr += warp_sum((valid && !left) ? mu[g] : 0u);
-      for (uint32_t j = 0; j < nv; ++j) {
-        const double x = __shfl_sync(kFull, wy[g], j);
-        const double c = __shfl_sync(kFull, yy[g], j);
-        if ((bl >> j) & 1u) {
-          o.sl = __dadd_rn(o.sl, x);
-          o.ql = __dadd_rn(o.ql, c);
-        } else {
-          o.sr = __dadd_rn(o.sr, x);
-          o.qr = __dadd_rn(o.qr, c);
-        }
-      }
+      tile_masked_sum2(wy[g], yy[g], bl, o.sl, o.ql, st);
+      tile_masked_sum2(wy[g], yy[g], bv & ~bl, o.sr, o.qr, st);
     }
   }
 }
@@ -398,12 +464,11 @@ __device__ void route_groups_warp(const Payload* pay,
                                   const double* wyy, uint32_t b, uint32_t e,
                                   const RankT* __restrict__ rk0, uint32_t k0levels,
                                   const RankT* __restrict__ rk_f, uint32_t thr_rank,
-                                  uint32_t* bits, RouteOut& o) {
+                                  uint32_t* bits, RouteOut& o, double* st) {
   const unsigned lane = lane_id();
   for (uint32_t grp = 0; grp < k0levels; ++grp) {
     for (uint32_t k0 = b; k0 < e; k0 += 32) {
       const uint32_t k = k0 + lane;
-      const uint32_t nv = min(32u, e - k0);
       Payload P{0, 0, 0.0};
       double yy = 0.0;
       bool sel = false, left = false;
@@ -419,18 +484,8 @@ __device__ void route_groups_warp(const Payload* pay,
       o.nl += __popc(bl);
       o.wl += warp_sum(left ? P.mult : 0u);
       o.wr += warp_sum((sel && !left) ? P.mult : 0u);
-      for (uint32_t j = 0; j < nv; ++j) {
-        const double x = __shfl_sync(kFull, P.wy, j);
-        const double c = __shfl_sync(kFull, yy, j);
-        if (!((bs >> j) & 1u)) continue;
-        if ((bl >> j) & 1u) {
-          o.sl = __dadd_rn(o.sl, x);
-          o.ql = __dadd_rn(o.ql, c);
-        } else {
-          o.sr = __dadd_rn(o.sr, x);
-          o.qr = __dadd_rn(o.qr, c);
-        }
-      }
+      tile_masked_sum2(P.wy, yy, bl, o.sl, o.ql, st);
+      tile_masked_sum2(P.wy, yy, bs & ~bl, o.sr, o.qr, st);
     }
   }
 }
@@ -464,7 +519,7 @@ __device__ void route_groups_lane(const Payload* pay,
 // sequential FP64 sums over the payload in row order (root stats, forest.hpp:221-226)
 template <int G>
 __device__ void root_sums_warp(const Payload* pay, const double* wyy,
-                               uint32_t A, double& s_out, double& q_out) {
+                               uint32_t A, double& s_out, double& q_out, double* st) {
   const unsigned lane = lane_id();
   double s = 0.0, q = 0.0;
   for (uint32_t k0 = 0; k0 < A; k0 += 32 * G) {
@@ -480,10 +535,7 @@ __device__ void root_sums_warp(const Payload* pay, const double* wyy,
       const uint32_t t0 = k0 + g * 32;
       if (t0 >= A) break;
       const uint32_t nv = min(32u, A - t0);
-      for (uint32_t j = 0; j < nv; ++j) {
-        s = __dadd_rn(s, __shfl_sync(kFull, x[g], j));
-        q = __dadd_rn(q, __shfl_sync(kFull, c[g], j));
-      }
+      tile_masked_sum2(x[g], c[g], nv == 32 ? kFull : ((1u << nv) - 1u), s, q, st);
     }
   }
   s_out = s;
@@ -498,6 +550,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   constexpr int G = 4;
   extern __shared__ uint32_t dyn_smem[];
   __shared__ uint32_t sh_scan[NW + 2];
+  __shared__ uint64_t sh_scan64[NW + 2];
+  __shared__ double s_stage[NW][64];  // per-warp tile stage for the FP64 chains
   __shared__ uint32_t s_tree, s_A, s_F, s_E, s_S, s_nodes, s_totL, s_err;
   __shared__ unsigned long long s_pool;
 
@@ -626,40 +680,54 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     // (list, position); every list holds exactly A0 in-bag rows
     {
       const uint64_t total = uint64_t{nl_cols} * ostride;
+      constexpr uint32_t kRow = NT * 4;
       uint64_t carry = 0;
-      for (uint64_t base = 0; base < total; base += uint64_t{NT} * kE) {
-        const uint64_t g0 = base + uint64_t{tid} * kE;
-        uint32_t r[kE], in = 0, li = 0, k0 = 0;
-        if (g0 < total) {
-          li = static_cast<uint32_t>(g0 / ostride);
-          k0 = static_cast<uint32_t>(g0 - uint64_t{li} * ostride);
-          const uint4* src = reinterpret_cast<const uint4*>(d.order + g0);
+      for (uint64_t base = 0; base < total; base += uint64_t{kRow} * 4) {
+        uint32_t r[16], in = 0, li[4], k0[4];
+        uint64_t cnt = 0;
 #pragma unroll
-          for (int v = 0; v < kE / 4; ++v) {
-            const uint4 x = __ldg(src + v);
+        for (int v = 0; v < 4; ++v) {
+          const uint64_t g0 = base + uint64_t{v} * kRow + uint64_t{tid} * 4;
+          li[v] = 0;
+          k0[v] = 0;
+          uint32_t c = 0;
+          if (g0 < total) {
+            li[v] = static_cast<uint32_t>(g0 / ostride);
+            k0[v] = static_cast<uint32_t>(g0 - uint64_t{li[v]} * ostride);
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(d.order + g0));
             r[4 * v] = x.x;
             r[4 * v + 1] = x.y;
             r[4 * v + 2] = x.z;
             r[4 * v + 3] = x.w;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (k0[v] + j < n && get_bit(bits, r[4 * v + j])) {
+                in |= 1u << (4 * v + j);
+                ++c;
+              }
           }
-#pragma unroll
-          for (int g = 0; g < kE; ++g)
-            if (k0 + g < n && get_bit(bits, r[g])) in |= 1u << g;
+          cnt |= uint64_t{c} << (16 * v);
         }
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan<NT>(__popc(in), sh_scan, &tot);
-        uint32_t o = static_cast<uint32_t>(carry + ex - uint64_t{li} * A0);
-        uint32_t* out = lists[0] + static_cast<size_t>(li) * stride;
+        uint64_t tot;
+        const uint64_t ex = block_excl_scan64<NT>(cnt, sh_scan64, &tot);
+        uint64_t rowbase = carry;
 #pragma unroll
-        for (int g = 0; g < kE; ++g)
-          if ((in >> g) & 1u) out[o++] = inbag_pos(bits, pref, r[g]);
-        carry += tot;
+        for (int v = 0; v < 4; ++v) {
+          uint32_t o = static_cast<uint32_t>(rowbase + ((ex >> (16 * v)) & 0xffffu) -
+                                             uint64_t{li[v]} * A0);
+          uint32_t* out = lists[0] + static_cast<size_t>(li[v]) * stride;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if ((in >> (4 * v + j)) & 1u) out[o++] = inbag_pos(bits, pref, r[4 * v + j]);
+          rowbase += (tot >> (16 * v)) & 0xffffu;
+        }
+        carry = rowbase;
       }
     }
     __syncthreads();
     if (wid == 0) {
       double s, q;
-      root_sums_warp<G>(pay[0], wyy[0], A0, s, q);
+      root_sums_warp<G>(pay[0], wyy[0], A0, s, q, s_stage[wid]);
       if (lane == 0) {
         front[0][0] = NodeWork{0u, A0, 0u, 0u, static_cast<double>(n), s, q};
         nf[0] = -1;
@@ -743,9 +811,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         uint32_t bp;
         if (li >= 0)
           chain_warp<RankT, G>(lists[cur] + static_cast<size_t>(li) * stride, nw.b, nw.e,
-                               pay[cur], rk_c, nw.w, nw.s, bg, bp);
+                               pay[cur], rk_c, nw.w, nw.s, bg, bp, s_stage[wid]);
         else
-          chain_bin_warp<RankT, G>(pay[cur], nw.b, nw.e, rk_c, nw.w, nw.s, bg, bp);
+          chain_bin_warp<RankT, G>(pay[cur], nw.b, nw.e, rk_c, nw.w, nw.s, bg, bp,
+                                   s_stage[wid]);
         if (lane == 0) res[k] = ChainRes{bg, bp, 0u};
       }
       for (uint32_t k = tid; k < ntask; k += NT) {
@@ -880,10 +949,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
             if (pass == 0) {
               if (l0)
                 route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank,
-                                     bits, o);
+                                     bits, o, s_stage[wid]);
               else
                 route_groups_warp<RankT, G>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels,
-                                            rk_f, si.thr_rank, bits, o);
+                                            rk_f, si.thr_rank, bits, o, s_stage[wid]);
               if (lane != 0) continue;
             } else {
               if (l0)
@@ -956,53 +1025,74 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       // list pass: the same partition applied to every listed column, flattened
       // over (list, position) with a per-list left-count offset li*totL; the new
       // entry (payload position in the next level) comes from the same bitmap
+      // Tile = 4 rows x NT threads x 4 consecutive elements: every uint4 load and
+      // every row of stores is coalesced across the warp; one packed 64-bit block
+      // scan yields the four rows' left-count prefixes.
       {
         const uint32_t A16 = (A + 15u) & ~15u;
         const uint64_t total = uint64_t{nl_cols} * A16;
         const uint32_t totL = s_totL;
+        constexpr uint32_t kRow = NT * 4;
         uint64_t carry = 0;
-        for (uint64_t base = 0; base < total; base += uint64_t{NT} * kE) {
-          const uint64_t g0 = base + uint64_t{tid} * kE;
-          uint32_t q[kE], f[kE], lf = 0, keep = 0, li = 0, k0 = 0;
-          if (g0 < total) {
-            li = static_cast<uint32_t>(g0 / A16);
-            k0 = static_cast<uint32_t>(g0 - uint64_t{li} * A16);
-            const uint4* src =
-                reinterpret_cast<const uint4*>(lists[cur] + static_cast<size_t>(li) * stride + k0);
-            const uint4* sg = reinterpret_cast<const uint4*>(seg[cur] + k0);
+        for (uint64_t base = 0; base < total; base += uint64_t{kRow} * 4) {
+          uint32_t q[16], f[16], lf = 0, keep = 0, li[4], k0[4];
+          uint64_t cnt = 0;
 #pragma unroll
-            for (int v = 0; v < kE / 4; ++v) {
-              const uint4 x = src[v];
-              const uint4 y = sg[v];
-              q[4 * v] = x.x; q[4 * v + 1] = x.y; q[4 * v + 2] = x.z; q[4 * v + 3] = x.w;
-              f[4 * v] = y.x; f[4 * v + 1] = y.y; f[4 * v + 2] = y.z; f[4 * v + 3] = y.w;
+          for (int r = 0; r < 4; ++r) {
+            const uint64_t g0 = base + uint64_t{r} * kRow + uint64_t{tid} * 4;
+            li[r] = 0;
+            k0[r] = 0;
+            if (g0 < total) {
+              li[r] = static_cast<uint32_t>(g0 / A16);
+              k0[r] = static_cast<uint32_t>(g0 - uint64_t{li[r]} * A16);
+              const uint4 x = *reinterpret_cast<const uint4*>(
+                  lists[cur] + static_cast<size_t>(li[r]) * stride + k0[r]);
+              const uint4 y = *reinterpret_cast<const uint4*>(seg[cur] + k0[r]);
+              q[4 * r] = x.x; q[4 * r + 1] = x.y; q[4 * r + 2] = x.z; q[4 * r + 3] = x.w;
+              f[4 * r] = y.x; f[4 * r + 1] = y.y; f[4 * r + 2] = y.z; f[4 * r + 3] = y.w;
             }
+          }
 #pragma unroll
-            for (int g = 0; g < kE; ++g) {
-              if (k0 + g < A && segtab[f[g]].offL != INT_MIN) {
+          for (int r = 0; r < 4; ++r) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int g = 4 * r + j;
+              const uint64_t gg = base + uint64_t{r} * kRow + uint64_t{tid} * 4 + j;
+              if (gg < total && k0[r] + j < A && segtab[f[g]].offL != INT_MIN) {
                 keep |= 1u << g;
-                lf |= get_bit(bits, q[g]) << g;
+                const uint32_t b = get_bit(bits, q[g]);
+                lf |= b << g;
+                c += b;
               }
             }
+            cnt |= uint64_t{c} << (16 * r);
           }
-          uint32_t tot;
-          const uint32_t ex = block_excl_scan<NT>(__popc(lf), sh_scan, &tot);
-          int32_t pl = static_cast<int32_t>(carry + ex - uint64_t{li} * totL);
-          uint32_t* dstl = lists[nxt] + static_cast<size_t>(li) * stride;
+          uint64_t tot;
+          const uint64_t ex = block_excl_scan64<NT>(cnt, sh_scan64, &tot);
+          uint64_t rowbase = carry;
 #pragma unroll
-          for (int g = 0; g < kE; ++g) {
-            if (!((keep >> g) & 1u)) continue;
-            const SegTab tb = segtab[f[g]];
-            const bool l = (lf >> g) & 1u;
-            const int32_t lq = static_cast<int32_t>(bits_before(bits, pref, q[g]));
-            const uint32_t nq = static_cast<uint32_t>(
-                l ? tb.offL + lq : tb.offR + static_cast<int32_t>(q[g]) - lq);
-            const uint32_t dst = static_cast<uint32_t>(
-                l ? tb.offL + pl : tb.offR + static_cast<int32_t>(k0 + g) - pl);
-            if (l) ++pl;
-            dstl[dst] = nq;
+          for (int r = 0; r < 4; ++r) {
+            int32_t pl = static_cast<int32_t>(rowbase + ((ex >> (16 * r)) & 0xffffu) -
+                                              uint64_t{li[r]} * totL);
+            uint32_t* dstl = lists[nxt] + static_cast<size_t>(li[r]) * stride;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int g = 4 * r + j;
+              if (!((keep >> g) & 1u)) continue;
+              const SegTab tb = segtab[f[g]];
+              const bool l = (lf >> g) & 1u;
+              const int32_t lq = static_cast<int32_t>(bits_before(bits, pref, q[g]));
+              const uint32_t nq = static_cast<uint32_t>(
+                  l ? tb.offL + lq : tb.offR + static_cast<int32_t>(q[g]) - lq);
+              const uint32_t dst = static_cast<uint32_t>(
+                  l ? tb.offL + pl : tb.offR + static_cast<int32_t>(k0[r] + j) - pl);
+              if (l) ++pl;
+              dstl[dst] = nq;
+            }
+            rowbase += (tot >> (16 * r)) & 0xffffu;
           }
-          carry += tot;
+          carry = rowbase;
         }
       }
       __syncthreads();

@@ -1,0 +1,87 @@
+"""Multi-GPU host logic for the forest path.
+
+Trees shard by global tree index: tree t depends only on (dataset, params, seed, t)
+(forest.hpp:182), so rank r grows its own tree range of the global forest and the
+union equals a one-GPU fit.  Two exchanges exist:
+
+* OOB (forest.hpp:414-447) sums each row's OOB leaf values in TREE order.  A plain
+  all-reduce of per-rank partial sums would reassociate that sum, so it is chained:
+  rank r receives the per-row (sum, count) of trees [0, t0_r) from rank r-1, continues
+  it with its own trees (aiwc_oob_accumulate), and passes it on; the last rank
+  finalises.  Result: bit-identical to the one-GPU / reference value.
+* the forest gather (node SoA + in-bag lists) concatenates rank parts in rank order.
+
+The compute is injected (`accumulate(row_sum, row_count)`), so the same logic drives
+the GPU path in bench.py (NCCL) and the CPU tests (gloo + the oracle).
+"""
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+
+def tree_range(rank: int, world: int, total: int) -> tuple[int, int]:
+    """Contiguous tree range of `rank` when `total` trees are split over `world` ranks."""
+    return (rank * total) // world, ((rank + 1) * total) // world
+
+
+def _pack(rs: np.ndarray, rc: np.ndarray) -> np.ndarray:
+    return np.concatenate([rs.view(np.uint8), rc.astype(np.uint32).view(np.uint8)]).view(np.int32)
+
+
+def _unpack(buf: np.ndarray, n: int) -> tuple[np.ndarray, np.ndarray]:
+    raw = buf.view(np.uint8)
+    return raw[: 8 * n].view(np.float64).copy(), raw[8 * n: 12 * n].view(np.uint32).copy()
+
+
+def chained_oob(n: int, rank: int, world: int,
+                accumulate: Callable[[np.ndarray, np.ndarray], None],
+                send: Callable[[np.ndarray, int], None],
+                recv: Callable[[int, int], np.ndarray]):
+    """Run the rank chain; returns (row_sum, row_count) on the last rank, else None.
+
+    send(int32_array, dst) / recv(num_int32, src) -> int32_array are the transport
+    (torch.distributed send/recv over NCCL or gloo)."""
+    if rank > 0:
+        rs, rc = _unpack(recv(3 * n, rank - 1), n)
+    else:
+        rs, rc = np.zeros(n), np.zeros(n, np.uint32)
+    accumulate(rs, rc)
+    if rank < world - 1:
+        send(_pack(rs, rc), rank + 1)
+        return None
+    return rs, rc
+
+
+def torch_transport(device=None):
+    """send/recv callables over the default torch.distributed process group."""
+    import torch
+    import torch.distributed as dist
+
+    def send(arr: np.ndarray, dst: int):
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        dist.send(t.to(device) if device is not None else t, dst=dst)
+
+    def recv(count: int, src: int) -> np.ndarray:
+        t = torch.empty(count, dtype=torch.int32, device=device)
+        dist.recv(t, src=src)
+        return t.cpu().numpy()
+
+    return send, recv
+
+
+def concat_forests(parts):
+    """Rank-ordered concatenation of (offsets, feature, threshold, left, right, value,
+    inbag) parts into one forest in global tree order."""
+    offs, cols = [np.zeros(1, np.uint64)], [[] for _ in range(5)]
+    inb = []
+    base = np.uint64(0)
+    for off, f, th, le, ri, va, ib in parts:
+        offs.append(np.asarray(off[1:], np.uint64) + base)
+        base += np.uint64(off[-1])
+        for k, a in enumerate((f, th, le, ri, va)):
+            cols[k].append(a)
+        inb.append(ib)
+    return (np.concatenate(offs), *[np.concatenate(c) for c in cols],
+            np.concatenate(inb) if inb and inb[0] is not None else None)

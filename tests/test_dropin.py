@@ -36,6 +36,8 @@ def test_reference_callers_run_unchanged_on_gpu(golden):
     assert got["oob_recomputed"] == c1[3]
     assert got["obj_505_30_9"] == golden["c1_505_30_9"]["oob"][3]
     c3 = golden["c3_50_6_5"]
-    assert got["c3_50_mape"] == c3["mape"]
+    # the golden MAPE is numpy's (pairwise) mean, the binary sums in row order; the
+    # per-row predictions themselves are compared bit-exactly in test_gpu_parity.py
+    assert got["c3_50_mape"] == pytest.approx(c3["mape"], rel=1e-13)
     assert (got["pairs"], got["pairs_correct"]) == (c3["pairs"], c3["pairs_correct"])
     assert got["roundtrip"] is True

@@ -1,0 +1,124 @@
+"""CPU, world_size 2 (gloo): the multi-GPU host path of paper_1811_00156_b200/shard.py.
+
+Each rank grows its tree range of the global forest (the oracle stands in for the
+per-rank GPU fit on this CPU-only box), the OOB per-row sums are chained rank 0 -> 1
+over torch.distributed send/recv, and the forest parts are gathered in rank order.
+The result must equal a single-process fit bit-for-bit (structure, in-bag lists, OOB
+statistics) -- the property bench.py relies on for --gpus N."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle_lib import ForestSoA, Oracle, forests_equal
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _table():
+    z = np.load(os.path.join(HERE, "golden", "edge_ties.npz"))
+    return z["col"], z["y"]
+
+
+def _walk_rows(s: ForestSoA, t: int, col: np.ndarray) -> np.ndarray:
+    fe, th, le, _, va = s.tree(t)
+    n = col.shape[1]
+    node = np.zeros(n, np.int64)
+    while True:
+        sp = fe[node] >= 0
+        if not sp.any():
+            return va[node]
+        nd = node[sp]
+        x = col[fe[nd], np.nonzero(sp)[0]]
+        node[sp] = np.where(x <= th[nd], le[nd], le[nd] + 1)
+
+
+def _oracle_accumulate(part: ForestSoA, col: np.ndarray):
+    """Continue per-row tree-ordered OOB sums with the trees of `part` (the role of
+    aiwc_oob_accumulate on a GPU rank)."""
+    n = col.shape[1]
+
+    def acc(rs, rc):
+        for t in range(part.num_trees):
+            bag = np.zeros(n, bool)
+            bag[part.inbag[t]] = True
+            leaf = _walk_rows(part, t, col)
+            for i in np.nonzero(~bag)[0]:  # row order; each row's sum in tree order
+                rs[i] += leaf[i]
+                rc[i] += 1
+    return acc
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, m, mns, seed, q):
+    from paper_1811_00156_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        col, y = _table()
+        p, n = col.shape
+        t0, t1 = shard.tree_range(rank, world, T)
+        part = Oracle.fit(col, y, n, p, T, m, mns, seed, trees=range(t0, t1))
+        send, recv = shard.torch_transport()
+        res = shard.chained_oob(n, rank, world, _oracle_accumulate(part, col), send, recv)
+        parts = [None] * world
+        dist.all_gather_object(parts, (part.offsets, part.feature, part.threshold, part.left,
+                                       part.right, part.value, part.inbag))
+        if rank == world - 1:
+            from paper_1811_00156_b200 import oob_finalize  # host-only C-ABI function
+
+            st = oob_finalize(y, res[0], res[1])
+            q.put(("stats", [float(st.degenerate), st.mse, st.response_variance, st.error_pct,
+                             st.r_squared, float(st.rows_evaluated)], res[0], res[1]))
+        if rank == 0:
+            q.put(("forest", shard.concat_forests(parts)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("T", [10, 7])
+def test_two_rank_sharded_fit_equals_single_fit(T):
+    col, y = _table()
+    p, n = col.shape
+    m, mns, seed = 3, 2, 12345
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, T, m, mns, seed, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict()
+    for _ in range(2):
+        item = q.get(timeout=120)
+        got[item[0]] = item[1:]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    full = Oracle.fit(col, y, n, p, T, m, mns, seed)
+    off, f, th, le, ri, va, ib = got["forest"][0]
+    assert forests_equal(full, ForestSoA(off, f, th, le, ri, va, inbag=ib)) is None
+    stats, rs, rc = Oracle.oob(col, y, n, p, full)
+    assert got["stats"][0] == list(stats)
+    assert np.array_equal(got["stats"][1].view(np.uint64), rs.view(np.uint64))
+    assert np.array_equal(got["stats"][2], rc)
+
+
+def test_tree_ranges_cover_forest():
+    from paper_1811_00156_b200 import shard
+
+    for world in (1, 2, 3, 8):
+        for T in (1, 7, 1000):
+            rs = [shard.tree_range(r, world, T) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == T
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
