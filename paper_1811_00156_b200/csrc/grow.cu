@@ -1028,28 +1028,31 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       // Tile = 4 rows x NT threads x 4 consecutive elements: every uint4 load and
       // every row of stores is coalesced across the warp; one packed 64-bit block
       // scan yields the four rows' left-count prefixes.
+      // Per element: one 8-byte segment-offset load and one shared bitmap word give
+      // both the side and the element's next-level payload position; both are kept in
+      // registers across the scan (32-bit index math: nlisted * A < 2^32).
       {
         const uint32_t A16 = (A + 15u) & ~15u;
-        const uint64_t total = uint64_t{nl_cols} * A16;
+        const uint32_t total = nl_cols * A16;
         const uint32_t totL = s_totL;
         constexpr uint32_t kRow = NT * 4;
-        uint64_t carry = 0;
-        for (uint64_t base = 0; base < total; base += uint64_t{kRow} * 4) {
+        uint32_t carry = 0;
+        for (uint32_t base = 0; base < total; base += kRow * 4) {
           uint32_t q[16], f[16], lf = 0, keep = 0, li[4], k0[4];
           uint64_t cnt = 0;
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const uint64_t g0 = base + uint64_t{r} * kRow + uint64_t{tid} * 4;
-            li[r] = 0;
-            k0[r] = 0;
+            const uint32_t g0 = base + r * kRow + tid * 4;
+            li[r] = g0 / A16;
+            k0[r] = g0 - li[r] * A16;
             if (g0 < total) {
-              li[r] = static_cast<uint32_t>(g0 / A16);
-              k0[r] = static_cast<uint32_t>(g0 - uint64_t{li[r]} * A16);
               const uint4 x = *reinterpret_cast<const uint4*>(
                   lists[cur] + static_cast<size_t>(li[r]) * stride + k0[r]);
               const uint4 y = *reinterpret_cast<const uint4*>(seg[cur] + k0[r]);
               q[4 * r] = x.x; q[4 * r + 1] = x.y; q[4 * r + 2] = x.z; q[4 * r + 3] = x.w;
               f[4 * r] = y.x; f[4 * r + 1] = y.y; f[4 * r + 2] = y.z; f[4 * r + 3] = y.w;
+            } else {
+              k0[r] = A;  // whole row is padding
             }
           }
 #pragma unroll
@@ -1058,39 +1061,46 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int g = 4 * r + j;
-              const uint64_t gg = base + uint64_t{r} * kRow + uint64_t{tid} * 4 + j;
-              if (gg < total && k0[r] + j < A && segtab[f[g]].offL != INT_MIN) {
-                keep |= 1u << g;
-                const uint32_t b = get_bit(bits, q[g]);
-                lf |= b << g;
-                c += b;
+              if (k0[r] + j < A) {
+                const int2 t = *reinterpret_cast<const int2*>(segtab + f[g]);
+                if (t.x != INT_MIN) {
+                  keep |= 1u << g;
+                  const uint32_t qq = q[g];
+                  const uint32_t w = bits[qq >> 5];
+                  const uint32_t b = (w >> (qq & 31u)) & 1u;
+                  const int32_t lq =
+                      static_cast<int32_t>(pref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u)));
+                  lf |= b << g;
+                  c += b;
+                  // new payload position of this entry, then the offset used for its
+                  // destination inside this list
+                  q[g] = static_cast<uint32_t>(b ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
+                  f[g] = static_cast<uint32_t>(b ? t.x : t.y);
+                }
               }
             }
             cnt |= uint64_t{c} << (16 * r);
           }
           uint64_t tot;
           const uint64_t ex = block_excl_scan64<NT>(cnt, sh_scan64, &tot);
-          uint64_t rowbase = carry;
+          uint32_t rowbase = carry;
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            int32_t pl = static_cast<int32_t>(rowbase + ((ex >> (16 * r)) & 0xffffu) -
-                                              uint64_t{li[r]} * totL);
+            int32_t pl = static_cast<int32_t>(rowbase + static_cast<uint32_t>((ex >> (16 * r)) & 0xffffu) -
+                                              li[r] * totL);
             uint32_t* dstl = lists[nxt] + static_cast<size_t>(li[r]) * stride;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int g = 4 * r + j;
               if (!((keep >> g) & 1u)) continue;
-              const SegTab tb = segtab[f[g]];
               const bool l = (lf >> g) & 1u;
-              const int32_t lq = static_cast<int32_t>(bits_before(bits, pref, q[g]));
-              const uint32_t nq = static_cast<uint32_t>(
-                  l ? tb.offL + lq : tb.offR + static_cast<int32_t>(q[g]) - lq);
+              const int32_t off = static_cast<int32_t>(f[g]);
               const uint32_t dst = static_cast<uint32_t>(
-                  l ? tb.offL + pl : tb.offR + static_cast<int32_t>(k0[r] + j) - pl);
-              if (l) ++pl;
-              dstl[dst] = nq;
+                  l ? off + pl : off + static_cast<int32_t>(k0[r] + j) - pl);
+              pl += l ? 1 : 0;
+              dstl[dst] = q[g];
             }
-            rowbase += (tot >> (16 * r)) & 0xffffu;
+            rowbase += static_cast<uint32_t>((tot >> (16 * r)) & 0xffffu);
           }
           carry = rowbase;
         }

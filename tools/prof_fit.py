@@ -13,7 +13,8 @@ import paper_1811_00156_b200 as pkg  # noqa: E402
 which = sys.argv[1] if len(sys.argv) > 1 else "c1"
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 500
 t0 = time.perf_counter()
-tab = pkg.Table() if which == "c1" else pkg.Table(6757, 37)
+tab = {"c1": lambda: pkg.Table(), "c4": lambda: pkg.Table(6757, 37),
+       "c4s": lambda: pkg.Table(1500, 37)}[which]()
 m = int(sys.argv[3]) if len(sys.argv) > 3 else (6 if which == "c1" else 8)
 mns = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 prep = pkg.PreparedDataset.from_table(tab)
