@@ -43,6 +43,10 @@ constexpr uint32_t kLaneMax = 48;  // nodes below this size use one lane per cha
 constexpr uint32_t kMaxP = 1024;
 constexpr int kPhases = 14;
 constexpr int kE = 16;  // elements per thread in the flat partition passes
+}  // namespace
+constexpr uint32_t kListChunk = 4096;  // list-pass chunk (flat elements) per warp task
+namespace {
+constexpr uint32_t kChunk = kListChunk;
 
 __device__ __forceinline__ uint32_t get_bit(const uint32_t* bits, uint32_t i) {
   return (bits[i >> 5] >> (i & 31u)) & 1u;
@@ -151,6 +155,58 @@ __device__ __forceinline__ void tile_masked_sum(double a, unsigned mask, double&
   }
   __syncwarp();
   ra = x;
+}
+
+// ---- list-pass element quads -------------------------------------------------------
+// Four consecutive positions of one list (flat index g0 over (list, position)).
+struct ListQuad {
+  uint32_t q[4];  // list entries (payload positions); after side_quad: next-level entries
+  uint32_t f[4];  // after side_quad: the destination offset (offL or offR)
+  int2 t[4];      // (offL, offR) of each position's segment (offL == INT_MIN: leaf)
+  uint32_t li, k0, keep;
+};
+
+// off2: per position of this level, its segment's (offL, offR) -- expanded once per
+// level so the list pass has no dependent segment-table lookup
+__device__ __forceinline__ void load_quad(ListQuad& v, uint32_t g0, uint32_t A16, uint32_t A,
+                                          uint32_t end, uint32_t stride, const uint32_t* lists,
+                                          const int2* off2) {
+  v.keep = 0;
+  v.li = g0 / A16;
+  v.k0 = g0 - v.li * A16;
+  if (g0 < end && v.k0 < A) {
+    const uint4 x = *reinterpret_cast<const uint4*>(lists + static_cast<size_t>(v.li) * stride + v.k0);
+    const int4 y0 = *reinterpret_cast<const int4*>(off2 + v.k0);
+    const int4 y1 = *reinterpret_cast<const int4*>(off2 + v.k0 + 2);
+    v.q[0] = x.x; v.q[1] = x.y; v.q[2] = x.z; v.q[3] = x.w;
+    v.t[0] = make_int2(y0.x, y0.y); v.t[1] = make_int2(y0.z, y0.w);
+    v.t[2] = make_int2(y1.x, y1.y); v.t[3] = make_int2(y1.z, y1.w);
+    const uint32_t left = A - v.k0;
+    v.keep = left >= 4 ? 0xfu : ((1u << left) - 1u);
+  }
+}
+
+// side bits of the quad's kept entries (entries of leaf segments are dropped); also
+// rewrites q to the entries' next-level payload positions and f to their offsets
+__device__ __forceinline__ uint32_t side_quad(ListQuad& v, const uint32_t* bits,
+                                              const uint32_t* pref) {
+  uint32_t lf = 0, keep = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (!((v.keep >> j) & 1u)) continue;
+    const int2 t = v.t[j];
+    if (t.x == INT_MIN) continue;
+    keep |= 1u << j;
+    const uint32_t qq = v.q[j];
+    const uint32_t w = bits[qq >> 5];
+    const uint32_t b = (w >> (qq & 31u)) & 1u;
+    const int32_t lq = static_cast<int32_t>(pref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u)));
+    lf |= b << j;
+    v.q[j] = static_cast<uint32_t>(b ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
+    v.f[j] = static_cast<uint32_t>(b ? t.x : t.y);
+  }
+  v.keep = keep;
+  return lf;
 }
 
 __device__ __forceinline__ void warp_best(double& bg, uint32_t& bp) {
@@ -589,6 +645,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   int32_t* nleft = reinterpret_cast<int32_t*>(slot + L.off_nleft);
   double* nval = reinterpret_cast<double*>(slot + L.off_nval);
   uint32_t* nrank = reinterpret_cast<uint32_t*>(slot + L.off_nrank);
+  uint32_t* chunk_cnt = reinterpret_cast<uint32_t*>(slot + L.off_chunk);
+  int2* off2 = reinterpret_cast<int2*>(slot + L.off_off2);
   const uint32_t nwords = (n + 31u) / 32u;
   const uint32_t nblk64 = (n + 63u) / 64u;
   const size_t bw = grow_bits_words(n, stride);
@@ -1008,9 +1066,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       __syncthreads();
       PHASE(10);
       // payload pass: element k goes to offL + lefts-before-k, or offR + k - that
+      // (it also expands the segment offsets per position for the list pass)
       for (uint32_t k = tid; k < A; k += NT) {
         const uint32_t f = seg[cur][k];
         const SegTab tb = segtab[f];
+        off2[k] = make_int2(tb.offL, tb.offR);
         if (tb.offL == INT_MIN) continue;
         const bool l = get_bit(bits, k);
         const int32_t lp = static_cast<int32_t>(bits_before(bits, pref, k));
@@ -1031,78 +1091,65 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       // Per element: one 8-byte segment-offset load and one shared bitmap word give
       // both the side and the element's next-level payload position; both are kept in
       // registers across the scan (32-bit index math: nlisted * A < 2^32).
+      // Two phases, no block barrier per tile: (1) every warp counts the kept-left
+      // entries of its chunks (kChunk flat elements), (2) one block scan over the chunk
+      // counts, (3) every warp re-reads its chunks and scatters with its own running
+      // prefix (warp-level scans only), so warps stream independently with several
+      // loads in flight.
       {
         const uint32_t A16 = (A + 15u) & ~15u;
         const uint32_t total = nl_cols * A16;
         const uint32_t totL = s_totL;
-        constexpr uint32_t kRow = NT * 4;
-        uint32_t carry = 0;
-        for (uint32_t base = 0; base < total; base += kRow * 4) {
-          uint32_t q[16], f[16], lf = 0, keep = 0, li[4], k0[4];
-          uint64_t cnt = 0;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const uint32_t g0 = base + r * kRow + tid * 4;
-            li[r] = g0 / A16;
-            k0[r] = g0 - li[r] * A16;
-            if (g0 < total) {
-              const uint4 x = *reinterpret_cast<const uint4*>(
-                  lists[cur] + static_cast<size_t>(li[r]) * stride + k0[r]);
-              const uint4 y = *reinterpret_cast<const uint4*>(seg[cur] + k0[r]);
-              q[4 * r] = x.x; q[4 * r + 1] = x.y; q[4 * r + 2] = x.z; q[4 * r + 3] = x.w;
-              f[4 * r] = y.x; f[4 * r + 1] = y.y; f[4 * r + 2] = y.z; f[4 * r + 3] = y.w;
-            } else {
-              k0[r] = A;  // whole row is padding
-            }
+        const uint32_t nchunk = (total + kChunk - 1) / kChunk;
+        for (uint32_t c = wid; c < nchunk; c += NW) {
+          const uint32_t ce = min(total, (c + 1) * kChunk);
+          uint32_t cnt = 0;
+#pragma unroll 2
+          for (uint32_t s = c * kChunk; s < ce; s += 128) {
+            ListQuad v;
+            load_quad(v, s + lane * 4, A16, A, ce, stride, lists[cur], off2);
+            cnt += __popc(side_quad(v, bits, pref));
           }
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            uint32_t c = 0;
+          cnt = warp_sum(cnt);
+          if (lane == 0) chunk_cnt[c] = cnt;
+        }
+        __syncthreads();
+        {
+          uint32_t carry = 0;
+          for (uint32_t base = 0; base < nchunk; base += NT) {
+            const uint32_t c = base + tid;
+            const uint32_t v = c < nchunk ? chunk_cnt[c] : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_excl_scan<NT>(v, sh_scan, &tot);
+            if (c < nchunk) chunk_cnt[c] = carry + ex;
+            carry += tot;
+          }
+        }
+        __syncthreads();
+        for (uint32_t c = wid; c < nchunk; c += NW) {
+          const uint32_t ce = min(total, (c + 1) * kChunk);
+          uint32_t run = chunk_cnt[c];
+#pragma unroll 2
+          for (uint32_t s = c * kChunk; s < ce; s += 128) {
+            ListQuad v;
+            load_quad(v, s + lane * 4, A16, A, ce, stride, lists[cur], off2);
+            const uint32_t lf = side_quad(v, bits, pref);
+            const uint32_t mine = __popc(lf);
+            const uint32_t inc = warp_incl_scan(mine);
+            int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
+            uint32_t* dstl = lists[nxt] + static_cast<size_t>(v.li) * stride;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const int g = 4 * r + j;
-              if (k0[r] + j < A) {
-                const int2 t = *reinterpret_cast<const int2*>(segtab + f[g]);
-                if (t.x != INT_MIN) {
-                  keep |= 1u << g;
-                  const uint32_t qq = q[g];
-                  const uint32_t w = bits[qq >> 5];
-                  const uint32_t b = (w >> (qq & 31u)) & 1u;
-                  const int32_t lq =
-                      static_cast<int32_t>(pref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u)));
-                  lf |= b << g;
-                  c += b;
-                  // new payload position of this entry, then the offset used for its
-                  // destination inside this list
-                  q[g] = static_cast<uint32_t>(b ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
-                  f[g] = static_cast<uint32_t>(b ? t.x : t.y);
-                }
-              }
-            }
-            cnt |= uint64_t{c} << (16 * r);
-          }
-          uint64_t tot;
-          const uint64_t ex = block_excl_scan64<NT>(cnt, sh_scan64, &tot);
-          uint32_t rowbase = carry;
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            int32_t pl = static_cast<int32_t>(rowbase + static_cast<uint32_t>((ex >> (16 * r)) & 0xffffu) -
-                                              li[r] * totL);
-            uint32_t* dstl = lists[nxt] + static_cast<size_t>(li[r]) * stride;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int g = 4 * r + j;
-              if (!((keep >> g) & 1u)) continue;
-              const bool l = (lf >> g) & 1u;
-              const int32_t off = static_cast<int32_t>(f[g]);
+              if (!((v.keep >> j) & 1u)) continue;
+              const bool l = (lf >> j) & 1u;
+              const int32_t off = static_cast<int32_t>(v.f[j]);
               const uint32_t dst = static_cast<uint32_t>(
-                  l ? off + pl : off + static_cast<int32_t>(k0[r] + j) - pl);
+                  l ? off + pl : off + static_cast<int32_t>(v.k0 + j) - pl);
               pl += l ? 1 : 0;
-              dstl[dst] = q[g];
+              dstl[dst] = v.q[j];
             }
-            rowbase += static_cast<uint32_t>((tot >> (16 * r)) & 0xffffu);
+            run += __shfl_sync(kFull, inc, 31);
           }
-          carry = rowbase;
         }
       }
       __syncthreads();
@@ -1228,6 +1275,8 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_nleft = take(size_t{L.nodes_cap} * 4);
   L.off_nval = take(size_t{L.nodes_cap} * 8);
   L.off_nrank = take(size_t{L.nodes_cap} * 4);
+  L.off_chunk = take((size_t{nlisted} * stride / kListChunk + 4) * 4);
+  L.off_off2 = take(stride * 8 + 64);
   if (gbits) {
     L.off_gbits = take(grow_bits_words(n, L.stride) * 4);
     L.off_gpref = take(grow_pref_words(n, L.stride) * 4);
