@@ -389,7 +389,10 @@ void oob_accumulate_device(aiwc_forest* f, double* row_sum, uint32_t* row_count,
   CK(cudaStreamSynchronize(s));
 }
 
-int pick_threads(uint64_t n) { return n >= 65536 ? 512 : 256; }
+int pick_threads(uint64_t n) {
+  if (const char* e = std::getenv("AIWC_GROW_NT")) return std::atoi(e) == 512 ? 512 : 256;
+  return n >= 65536 ? 512 : 256;
+}
 
 }  // namespace
 
@@ -426,7 +429,8 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     SlotLayout L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, false);
     const size_t bits_smem = (grow_bits_words(n, L.stride) + grow_pref_words(n, L.stride)) * 4;
     // static shared memory of grow_kernel: scans + per-warp FP64 stages (< 12 KB)
-    const bool smem_bits = bits_smem + 12288 <= static_cast<size_t>(max_optin);
+    const bool smem_bits = bits_smem + 12288 <= static_cast<size_t>(max_optin) &&
+                           std::getenv("AIWC_GROW_GBITS") == nullptr;
     const size_t dyn = smem_bits ? bits_smem : 0;
     if (!smem_bits) L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
 
@@ -441,8 +445,20 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     a.L = L;
     a.bits_in_smem = smem_bits ? 1 : 0;
 
+    // large tables grow batches of trees level-synchronously with one grid-wide kernel
+    // per phase (grow_wide.cuh); small ones keep one persistent CTA per tree
+    bool wide = n >= 65536;
+    if (const char* e = std::getenv("AIWC_GROW_WIDE")) wide = std::atoi(e) != 0;
+    if (wide) {
+      L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
+      a.L = L;
+      a.bits_in_smem = 0;
+    }
     int per_sm = 0;
-    CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
+    if (wide)
+      per_sm = 4;  // batch up to 4 trees per SM (bounded by memory below)
+    else
+      CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
     if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
@@ -472,6 +488,15 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     const size_t need = size_t(slots) * L.bytes;
     if (ctx->scratch.count < need) ctx->scratch.alloc(need);
     a.scratch = ctx->scratch.p;
+    DevBuf<TreeState> wts(wide ? slots : 0);
+    DevBuf<uint32_t> woff(wide ? 4 * (size_t(slots) + 1) : 0), wactive(wide ? 1 : 0);
+    std::unique_ptr<uint32_t, void (*)(uint32_t*)> h_active(
+        [] {
+          uint32_t* p = nullptr;
+          cudaMallocHost(&p, 4);
+          return p;
+        }(),
+        [](uint32_t* p) { cudaFreeHost(p); });
 
     DevBuf<uint32_t> queue(1), tree_cnt(T);
     DevBuf<int> err(1);
@@ -525,9 +550,25 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
       CK(cudaMemsetAsync(used.p, 0, 8, st.s));
       CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
       CK(cudaEventRecord(ev0, st.s));
-      CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
+      if (wide) {
+        // batched multi-kernel grower: batches of `slots` trees, level-synchronous
+        for (uint32_t t0 = 0; t0 < T; t0 += static_cast<uint32_t>(slots)) {
+          WideArgs w{};
+          w.g = a;
+          w.ts = wts.p;
+          w.B = std::min<uint32_t>(static_cast<uint32_t>(slots), T - t0);
+          w.t0 = t0;
+          for (int i = 0; i < 4; ++i) w.off[i] = woff.p + size_t{i} * (slots + 1);
+          w.active = wactive.p;
+          uint64_t nl = 0;
+          CK(run_wide(ctx->rank_bytes, w, st.s, sms, h_active.get(), &nl));
+          g_launches += nl;
+        }
+      } else {
+        CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
+        g_launches += 1;
+      }
       CK(cudaEventRecord(ev1, st.s));
-      g_launches += 1;
       f->grow_launches += 1;
       int herr = 0;
       unsigned long long hused = 0;

@@ -37,6 +37,10 @@ cudaError_t launch_predict_chunk(int bin_bytes, const BinNode* nodes, uint32_t n
                                  double* out, unsigned grid, size_t smem, size_t smem_max,
                                  cudaStream_t s);
 
+// batched multi-kernel grower for one batch of trees (grow_wide.cuh)
+cudaError_t run_wide(int rank_bytes, const WideArgs& a, cudaStream_t st, int sms,
+                     uint32_t* h_active, uint64_t* launches);
+
 cudaError_t launch_grow(int nt, int rank_bytes, const GrowArgs& a, int slots, size_t smem,
                         cudaStream_t st, int* blocks_per_sm);
 

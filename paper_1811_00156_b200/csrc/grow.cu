@@ -1275,7 +1275,10 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_nleft = take(size_t{L.nodes_cap} * 4);
   L.off_nval = take(size_t{L.nodes_cap} * 8);
   L.off_nrank = take(size_t{L.nodes_cap} * 4);
-  L.off_chunk = take((size_t{nlisted} * stride / kListChunk + 4) * 4);
+  // chunk counters: list pass (nlisted x stride) and the wide grower's list init
+  // (nlisted x padded n)
+  L.off_chunk = take((size_t{nlisted} * std::max<uint64_t>(stride, (n + 15) & ~uint64_t{15}) /
+                          kListChunk + 4) * 4);
   L.off_off2 = take(stride * 8 + 64);
   if (gbits) {
     L.off_gbits = take(grow_bits_words(n, L.stride) * 4);
@@ -1286,3 +1289,6 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
 }
 
 }  // namespace aiwc_b200
+
+// the batched (wide) grower shares this file's device helpers
+#include "grow_wide.cuh"

@@ -103,6 +103,24 @@ struct GrowArgs {
   int* err;  // 1 = pool overflow, 2 = in-bag rows exceed stride, 3 = frontier overflow
 };
 
+// per-tree level state of the wide (batched) grower
+struct TreeState {
+  uint32_t A, F, E, S;
+  uint32_t nodes, done, totL, A_next;
+  unsigned long long elig_base, split_rows;
+};
+
+struct WideArgs {
+  GrowArgs g;
+  TreeState* ts;     // [B]
+  uint32_t B;        // trees in this batch (slots 0..B-1)
+  uint32_t t0;       // local index of the batch's first tree
+  uint32_t cur;      // buffer parity of the current level
+  uint32_t pad;
+  uint32_t* off[4];  // [B+1] prefixes: chain tasks, splits, positions, list chunks
+  uint32_t* active;  // trees still splitting after this level's decide
+};
+
 // bitmap words + prefix words the grower keeps in shared memory (or global)
 __host__ __device__ inline size_t grow_bits_words(uint64_t n, uint32_t stride) {
   const size_t a = (n + 31) / 32, b = (stride + 31) / 32;

@@ -1,0 +1,827 @@
+// "Wide" forest grower for large tables -- included at the end of grow.cu (it uses
+// that file's device helpers).
+//
+// Same algorithm and the same bit-exact results as grow_kernel, but the batch of trees
+// advances level-synchronously and every phase of a level is its own grid-wide kernel
+// over ALL trees of the batch: per-tree bookkeeping (leaf tests, numbering scans,
+// segment tables) runs one CTA per tree, while the heavy passes (split chains, routing,
+// payload and list partitions) are flattened over (tree, task) and spread over the
+// whole GPU at full occupancy.  A tree's long sequential FP64 chain on a huge node no
+// longer idles the rest of its CTA: other trees' tasks fill the SMs.
+#pragma once
+
+namespace aiwc_b200 {
+
+struct SlotPtrs {
+  uint32_t* mult;
+  Payload* pay[2];
+  double* wyy[2];
+  uint32_t* lists[2];
+  uint32_t* seg[2];
+  NodeWork* front[2];
+  SegTab* segtab;
+  uint32_t* e2f;
+  uint16_t* samp;
+  ChainRes* res;
+  SplitInfo* spl;
+  int32_t* nf;
+  double* nthr;
+  int32_t* nleft;
+  double* nval;
+  uint32_t* nrank;
+  uint32_t* chunk;
+  int2* off2;
+  uint32_t* bits;
+  uint32_t* pref;
+};
+
+__device__ __forceinline__ SlotPtrs slot_ptrs(const GrowArgs& g, uint32_t b) {
+  const SlotLayout& L = g.L;
+  char* s = g.scratch + static_cast<size_t>(b) * L.bytes;
+  SlotPtrs p;
+  p.mult = reinterpret_cast<uint32_t*>(s + L.off_mult);
+  p.pay[0] = reinterpret_cast<Payload*>(s + L.off_pay0);
+  p.pay[1] = reinterpret_cast<Payload*>(s + L.off_pay1);
+  p.wyy[0] = reinterpret_cast<double*>(s + L.off_wyy0);
+  p.wyy[1] = reinterpret_cast<double*>(s + L.off_wyy1);
+  p.lists[0] = reinterpret_cast<uint32_t*>(s + L.off_list0);
+  p.lists[1] = reinterpret_cast<uint32_t*>(s + L.off_list1);
+  p.seg[0] = reinterpret_cast<uint32_t*>(s + L.off_seg0);
+  p.seg[1] = reinterpret_cast<uint32_t*>(s + L.off_seg1);
+  p.front[0] = reinterpret_cast<NodeWork*>(s + L.off_front0);
+  p.front[1] = reinterpret_cast<NodeWork*>(s + L.off_front1);
+  p.segtab = reinterpret_cast<SegTab*>(s + L.off_segtab);
+  p.e2f = reinterpret_cast<uint32_t*>(s + L.off_e2f);
+  p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
+  p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
+  p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
+  p.nf = reinterpret_cast<int32_t*>(s + L.off_nf);
+  p.nthr = reinterpret_cast<double*>(s + L.off_nthr);
+  p.nleft = reinterpret_cast<int32_t*>(s + L.off_nleft);
+  p.nval = reinterpret_cast<double*>(s + L.off_nval);
+  p.nrank = reinterpret_cast<uint32_t*>(s + L.off_nrank);
+  p.chunk = reinterpret_cast<uint32_t*>(s + L.off_chunk);
+  p.off2 = reinterpret_cast<int2*>(s + L.off_off2);
+  p.bits = reinterpret_cast<uint32_t*>(s + L.off_gbits);
+  p.pref = reinterpret_cast<uint32_t*>(s + L.off_gpref);
+  return p;
+}
+
+// tree index b of flattened item t given exclusive prefix off[0..B] (off[B] = total)
+__device__ __forceinline__ uint32_t owner(const uint32_t* off, uint32_t B, uint32_t t) {
+  uint32_t lo = 0, hi = B;  // off[lo] <= t < off[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint64_t tree_key(const GrowArgs& g, uint32_t tl) {
+  const uint64_t t = uint64_t{g.tree_begin} + tl;
+  return dmix64(g.seed ^ g.tag_tree ^ dmix64(t));
+}
+
+__device__ __forceinline__ uint32_t nchunks_of(uint32_t A, uint32_t nl) {
+  const uint32_t A16 = (A + 15u) & ~15u;
+  return (nl * A16 + kChunk - 1) / kChunk;
+}
+
+// ---- batch initialisation ---------------------------------------------------------
+__global__ void w_zero(const WideArgs a) {
+  const SlotPtrs P = slot_ptrs(a.g, blockIdx.y);
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    P.mult[i] = 0u;
+}
+
+// bootstrap draws (forest.hpp:184-195)
+__global__ void w_boot(const WideArgs a) {
+  const uint32_t b = blockIdx.y, tl = a.t0 + b;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const uint64_t key = tree_key(a.g, tl);
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(draw_bounded(key, uint64_t{j} + 1u, n));
+    if (a.g.inbag) a.g.inbag[static_cast<size_t>(tl) * n + j] = r;
+    atomicAdd(P.mult + r, 1u);
+  }
+}
+
+// in-bag bitmap + 64-row prefix counts + A0 (CTA per tree)
+template <int NT>
+__global__ void __launch_bounds__(NT) w_bits(const WideArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  const uint32_t b = blockIdx.x;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const uint32_t nwords = (n + 31u) / 32u, nblk64 = (n + 63u) / 64u;
+  for (uint32_t w = warp_id(); w < nwords; w += NW) {
+    const uint32_t r = w * 32u + lane_id();
+    const unsigned bl = __ballot_sync(kFull, r < n && P.mult[r] > 0u);
+    if (lane_id() == 0) P.bits[w] = bl;
+  }
+  __syncthreads();
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nblk64; base += NT) {
+    const uint32_t i = base + threadIdx.x;
+    uint32_t v = 0;
+    if (i < nblk64)
+      v = __popc(P.bits[2 * i]) + (2 * i + 1 < nwords ? __popc(P.bits[2 * i + 1]) : 0u);
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(v, sh, &tot);
+    if (i < nblk64) P.pref[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) {
+    TreeState& s = a.ts[b];
+    s.A = carry;
+    s.F = 1;
+    s.nodes = 1;
+    s.done = 0;
+    s.E = 0;
+    s.S = 0;
+    s.elig_base = 0;
+    s.split_rows = 0;
+    if (carry > a.g.L.stride) {
+      s.done = 1;
+      atomicExch(a.g.err, 2);
+    }
+  }
+}
+
+// payload in row order (forest.hpp:194-195)
+__global__ void w_payload(const WideArgs a) {
+  const uint32_t b = blockIdx.y;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (!get_bit(P.bits, r)) continue;
+    const uint32_t pos = inbag_pos(P.bits, P.pref, r);
+    const uint32_t mu = P.mult[r];
+    const double yr = __ldg(a.g.d.y + r);
+    const double wy = __dmul_rn(static_cast<double>(mu), yr);
+    P.pay[0][pos] = Payload{r, mu, wy};
+    P.wyy[0][pos] = __dmul_rn(wy, yr);
+    P.seg[0][pos] = 0u;
+  }
+}
+
+// per listed column: stable in-bag filter of the presort.  Items = (tree, chunk of the
+// flat (list, presort position) space); counts, then a per-tree scan, then scatter.
+__global__ void w_l0count(const WideArgs a) {
+  const uint32_t nl = a.g.d.nlisted, os = a.g.d.order_stride;
+  const uint32_t per = (nl * os + kChunk - 1) / kChunk;
+  const uint32_t total = per * a.B;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = gw; it < total; it += nw) {
+    const uint32_t b = it / per, c = it - b * per;
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const uint32_t ce = min(nl * os, (c + 1) * kChunk);
+    uint32_t cnt = 0;
+    for (uint32_t s = c * kChunk; s < ce; s += 128) {
+      const uint32_t g0 = s + lane_id() * 4;
+      if (g0 < ce) {
+        const uint32_t k0 = g0 % os;
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(a.g.d.order + g0));
+        const uint32_t r4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cnt += (k0 + j < n) ? get_bit(P.bits, r4[j]) : 0u;
+      }
+    }
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0) P.chunk[c] = cnt;
+  }
+}
+
+// exclusive scan of each tree's chunk counts (CTA per tree); `which` selects the
+// item space: 0 = list init, 1 = level list pass (also advances the tree's level state)
+template <int NT>
+__global__ void __launch_bounds__(NT) w_chunkscan(const WideArgs a, int which) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  const uint32_t b = blockIdx.x;
+  TreeState& s = a.ts[b];
+  const uint32_t nl = a.g.d.nlisted;
+  if (which == 1 && s.done) return;
+  const uint32_t per = which == 0 ? (nl * a.g.d.order_stride + kChunk - 1) / kChunk
+                                  : nchunks_of(s.A, nl);
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < per; base += NT) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < per ? P.chunk[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(v, sh, &tot);
+    if (i < per) P.chunk[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void w_l0scatter(const WideArgs a) {
+  const uint32_t nl = a.g.d.nlisted, os = a.g.d.order_stride;
+  const uint32_t per = (nl * os + kChunk - 1) / kChunk;
+  const uint32_t total = per * a.B;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const uint32_t stride = a.g.L.stride;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = gw; it < total; it += nw) {
+    const uint32_t b = it / per, c = it - b * per;
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const uint32_t A0 = a.ts[b].A;
+    const uint32_t ce = min(nl * os, (c + 1) * kChunk);
+    uint32_t run = P.chunk[c];
+    for (uint32_t s = c * kChunk; s < ce; s += 128) {
+      const uint32_t g0 = s + lane_id() * 4;
+      uint32_t in = 0, r4[4] = {0, 0, 0, 0}, li = 0;
+      if (g0 < ce) {
+        li = g0 / os;
+        const uint32_t k0 = g0 - li * os;
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(a.g.d.order + g0));
+        r4[0] = x.x; r4[1] = x.y; r4[2] = x.z; r4[3] = x.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (k0 + j < n && get_bit(P.bits, r4[j])) in |= 1u << j;
+      }
+      const uint32_t mine = __popc(in);
+      const uint32_t inc = warp_incl_scan(mine);
+      uint32_t o = run + inc - mine - li * A0;
+      uint32_t* out = P.lists[0] + static_cast<size_t>(li) * stride;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((in >> j) & 1u) out[o++] = inbag_pos(P.bits, P.pref, r4[j]);
+      run += __shfl_sync(kFull, inc, 31);
+    }
+  }
+}
+
+// root sums in row order (forest.hpp:221-226), warp per tree
+__global__ void w_root(const WideArgs a) {
+  __shared__ double st[64];
+  const uint32_t b = blockIdx.x;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  TreeState& s = a.ts[b];
+  if (s.done) return;
+  double sum, sq;
+  root_sums_warp<4>(P.pay[0], P.wyy[0], s.A, sum, sq, st);
+  if (lane_id() == 0) {
+    P.front[0][0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(a.g.d.n), sum, sq};
+    P.nf[0] = -1;
+    P.nthr[0] = 0.0;
+    P.nleft[0] = -1;
+    P.nval[0] = 0.0;
+    P.nrank[0] = 0u;
+  }
+}
+
+// ---- level kernels ----------------------------------------------------------------
+// leaf tests, eligible compaction, mtry sampling, bitmap reset (CTA per tree)
+template <int NT>
+__global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  const uint32_t b = blockIdx.x;
+  TreeState& s = a.ts[b];
+  if (s.done) return;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const NodeWork* fr = P.front[a.cur];
+  const uint32_t F = s.F, A = s.A, m = a.g.mtry, p = a.g.d.p;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < F; base += NT) {
+    const uint32_t f = base + threadIdx.x;
+    uint32_t el = 0;
+    if (f < F) {
+      const NodeWork nw = fr[f];
+      const double sse = __dsub_rn(nw.q, __ddiv_rn(__dmul_rn(nw.s, nw.s), nw.w));
+      const bool too_small = nw.w < 2.0 * static_cast<double>(a.g.mns);
+      const bool pure = sse <= __dmul_rn(1e-12, nw.q > 1.0 ? nw.q : 1.0);
+      if (too_small || pure)
+        P.nval[nw.id] = __ddiv_rn(nw.s, nw.w);
+      else
+        el = 1;
+      P.segtab[f].offL = INT_MIN;
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(el, sh, &tot);
+    if (el) P.e2f[carry + ex] = f;
+    carry += tot;
+  }
+  const uint32_t E = carry;
+  const uint64_t key = tree_key(a.g, a.t0 + b);
+  for (uint32_t e = threadIdx.x; e < E; e += NT) {
+    uint16_t pool[kMaxP];
+    for (uint32_t c = 0; c < p; ++c) pool[c] = static_cast<uint16_t>(c);
+    const uint64_t ctr = uint64_t{n} + (s.elig_base + e) * m;
+    for (uint32_t i = 0; i < m; ++i) {
+      const uint32_t j = i + static_cast<uint32_t>(draw_bounded(key, ctr + i + 1, p - i));
+      const uint16_t tmp = pool[i];
+      pool[i] = pool[j];
+      pool[j] = tmp;
+    }
+    for (uint32_t i = 1; i < m; ++i)
+      for (uint32_t k = i; k > 0 && pool[k - 1] > pool[k]; --k) {
+        const uint16_t tmp = pool[k];
+        pool[k] = pool[k - 1];
+        pool[k - 1] = tmp;
+      }
+    for (uint32_t i = 0; i < m; ++i) P.samp[static_cast<size_t>(e) * m + i] = pool[i];
+  }
+  for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
+  if (threadIdx.x == 0) s.E = E;
+}
+
+// exclusive prefixes over trees of this level's work items (one CTA)
+//   which 0: chain tasks E*m;  which 1: splits S, positions A, list chunks
+template <int NT>
+__global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  uint32_t c0 = 0, c1 = 0, c2 = 0;
+  for (uint32_t base = 0; base < a.B; base += NT) {
+    const uint32_t b = base + threadIdx.x;
+    uint32_t v0 = 0, v1 = 0, v2 = 0;
+    if (b < a.B && !a.ts[b].done) {
+      const TreeState& s = a.ts[b];
+      if (which == 0) {
+        v0 = s.E * a.g.mtry;
+      } else {
+        v0 = s.S;
+        v1 = s.A;
+        v2 = nchunks_of(s.A, a.g.d.nlisted);
+      }
+    }
+    uint32_t t0, t1, t2;
+    const uint32_t e0 = block_excl_scan<NT>(v0, sh, &t0);
+    const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
+    const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
+    if (b < a.B) {
+      if (which == 0) {
+        a.off[0][b] = c0 + e0;
+      } else {
+        a.off[1][b] = c0 + e0;
+        a.off[2][b] = c1 + e1;
+        a.off[3][b] = c2 + e2;
+      }
+    }
+    c0 += t0;
+    c1 += t1;
+    c2 += t2;
+  }
+  if (threadIdx.x == 0) {
+    if (which == 0) {
+      a.off[0][a.B] = c0;
+    } else {
+      a.off[1][a.B] = c0;
+      a.off[2][a.B] = c1;
+      a.off[3][a.B] = c2;
+    }
+  }
+}
+
+// split chains (forest.hpp:268-297): warps take tasks of nodes >= kLaneMax rows
+template <typename RankT>
+__global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
+  __shared__ double stage[8][64];
+  const uint32_t total = a.off[0][a.B];
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  for (uint32_t t = gw; t < total; t += nw) {
+    const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const NodeWork nw_ = P.front[a.cur][P.e2f[k / m]];
+    if (nw_.e - nw_.b < kLaneMax) continue;
+    const uint32_t c = P.samp[k];
+    const int32_t li = a.g.d.list_of[c];
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    double bg;
+    uint32_t bp;
+    if (li >= 0)
+      chain_warp<RankT, 4>(P.lists[a.cur] + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
+                           P.pay[a.cur], rk_c, nw_.w, nw_.s, bg, bp, stage[warp_id()]);
+    else
+      chain_bin_warp<RankT, 4>(P.pay[a.cur], nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp,
+                               stage[warp_id()]);
+    if (lane_id() == 0) P.res[k] = ChainRes{bg, bp, 0u};
+  }
+}
+
+template <typename RankT>
+__global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
+  const uint32_t total = a.off[0][a.B];
+  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const NodeWork nw_ = P.front[a.cur][P.e2f[k / m]];
+    if (nw_.e - nw_.b >= kLaneMax) continue;
+    const uint32_t c = P.samp[k];
+    const int32_t li = a.g.d.list_of[c];
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    double bg;
+    uint32_t bp;
+    if (li >= 0)
+      chain_lane<RankT>(P.lists[a.cur] + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
+                        P.pay[a.cur], rk_c, nw_.w, nw_.s, bg, bp);
+    else
+      chain_bin_lane<RankT>(P.pay[a.cur], nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp);
+    P.res[k] = ChainRes{bg, bp, 0u};
+  }
+}
+
+// decide + BFS numbering (forest.hpp:299-319), CTA per tree
+template <int NT, typename RankT>
+__global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  const uint32_t b = blockIdx.x;
+  TreeState& st = a.ts[b];
+  if (st.done) return;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const DevData& d = a.g.d;
+  const uint32_t n = static_cast<uint32_t>(d.n), m = a.g.mtry, stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(d.rank);
+  const NodeWork* fr = P.front[a.cur];
+  const uint32_t E = st.E, nodes0 = st.nodes;
+  uint32_t carry = 0, ccarry = 0;
+  for (uint32_t base = 0; base < E; base += NT) {
+    const uint32_t e = base + threadIdx.x;
+    uint32_t sp = 0, c = 0, thr_rank = 0;
+    double thr = 0.0;
+    NodeWork nw{};
+    if (e < E) {
+      nw = fr[P.e2f[e]];
+      double bg = -INFINITY;
+      uint32_t bi = 0, bp = 0;
+      for (uint32_t i = 0; i < m; ++i) {
+        const ChainRes r = P.res[static_cast<size_t>(e) * m + i];
+        if (r.gain > bg) {
+          bg = r.gain;
+          bi = i;
+          bp = r.pos;
+        }
+      }
+      if (bg == -INFINITY) {
+        P.nval[nw.id] = __ddiv_rn(nw.s, nw.w);
+      } else {
+        sp = 1;
+        c = P.samp[static_cast<size_t>(e) * m + bi];
+        const int32_t li = d.list_of[c];
+        const double* vals = d.vals + d.vals_off[c];
+        double prev, v;
+        uint32_t lo, hi;
+        if (li >= 0) {
+          const uint32_t* lc = P.lists[a.cur] + static_cast<size_t>(li) * stride;
+          const uint32_t r1 = P.pay[a.cur][lc[bp - 1]].row;
+          const uint32_t r0 = P.pay[a.cur][lc[bp]].row;
+          prev = d.col[static_cast<size_t>(c) * n + r1];
+          v = d.col[static_cast<size_t>(c) * n + r0];
+          lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
+          hi = rank_of(rank + static_cast<size_t>(c) * n, r0);
+        } else {
+          prev = vals[0];
+          v = vals[1];
+          lo = 0;
+          hi = 1;
+        }
+        thr = __dadd_rn(prev, __ddiv_rn(__dsub_rn(v, prev), 2.0));
+        if (thr >= v) thr = prev;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (vals[mid] <= thr) lo = mid; else hi = mid;
+        }
+        thr_rank = lo;
+      }
+    }
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(sp, sh, &tot);
+    const uint32_t cnt = sp ? nw.e - nw.b : 0u;
+    uint32_t ctot;
+    const uint32_t cex = block_excl_scan<NT>(cnt, sh, &ctot);
+    if (sp) {
+      const uint32_t s = carry + ex;
+      const uint32_t child = nodes0 + 2 * s;
+      if (child + 1 < a.g.L.nodes_cap) {
+        P.nf[nw.id] = static_cast<int32_t>(c);
+        P.nthr[nw.id] = thr;
+        P.nleft[nw.id] = static_cast<int32_t>(child);
+        P.nrank[nw.id] = thr_rank;
+        for (uint32_t h = 0; h < 2; ++h) {
+          P.nf[child + h] = -1;
+          P.nthr[child + h] = 0.0;
+          P.nleft[child + h] = -1;
+          P.nval[child + h] = 0.0;
+          P.nrank[child + h] = 0u;
+        }
+      }
+      P.spl[s] = SplitInfo{P.e2f[e], c, thr_rank, cnt, 0u, ccarry + cex, 0u, 0u};
+    }
+    carry += tot;
+    ccarry += ctot;
+  }
+  if (threadIdx.x == 0) {
+    st.S = carry;
+    st.A_next = ccarry;
+    st.split_rows += ccarry;
+    st.elig_base += E;
+    st.nodes = nodes0 + 2 * carry;
+    if (carry == 0) {
+      st.done = 1;
+    } else if (st.nodes > a.g.L.nodes_cap || 2 * carry > a.g.L.fmax) {
+      st.done = 1;
+      atomicExch(a.g.err, 3);
+    } else {
+      atomicAdd(a.active, 1u);
+    }
+  }
+}
+
+// route in column-0 order (forest.hpp:323-352): warps take split nodes >= kLaneMax
+template <typename RankT, bool kWarp>
+__global__ void __launch_bounds__(256) w_route(const WideArgs a) {
+  __shared__ double stage[8][64];
+  const uint32_t total = a.off[1][a.B];
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  const int32_t list0 = a.g.d.list_of[0];
+  const uint32_t k0levels = static_cast<uint32_t>(a.g.d.vals_off[1] - a.g.d.vals_off[0]);
+  const uint32_t id = kWarp ? (blockIdx.x * blockDim.x + threadIdx.x) >> 5
+                            : blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t step = kWarp ? (gridDim.x * blockDim.x) >> 5 : gridDim.x * blockDim.x;
+  const uint32_t nxt = a.cur ^ 1u;
+  for (uint32_t t = id; t < total; t += step) {
+    const uint32_t b = owner(a.off[1], a.B, t), s = t - a.off[1][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SplitInfo si = P.spl[s];
+    if (kWarp != (si.cnt >= kLaneMax)) continue;
+    const NodeWork nw = P.front[a.cur][si.f];
+    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+    const uint32_t* l0 = list0 >= 0 ? P.lists[a.cur] + static_cast<size_t>(list0) * stride : nullptr;
+    RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
+    if (kWarp) {
+      if (l0)
+        route_warp<RankT, 4>(l0, nw.b, nw.e, P.pay[a.cur], P.wyy[a.cur], rk_f, si.thr_rank,
+                             P.bits, o, stage[warp_id()]);
+      else
+        route_groups_warp<RankT, 4>(P.pay[a.cur], P.wyy[a.cur], nw.b, nw.e, rank, k0levels,
+                                    rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
+      if (lane_id() != 0) continue;
+    } else {
+      if (l0)
+        route_lane<RankT>(l0, nw.b, nw.e, P.pay[a.cur], P.wyy[a.cur], rk_f, si.thr_rank, P.bits, o);
+      else
+        route_groups_lane<RankT>(P.pay[a.cur], P.wyy[a.cur], nw.b, nw.e, rank, k0levels, rk_f,
+                                 si.thr_rank, P.bits, o);
+    }
+    P.spl[s].nl = o.nl;
+    const uint32_t child = static_cast<uint32_t>(P.nleft[nw.id]);
+    P.front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
+                                   static_cast<double>(o.wl), o.sl, o.ql};
+    P.front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
+                                       static_cast<double>(o.wr), o.sr, o.qr};
+  }
+}
+
+// segment table + per-word prefix of the goes-left bitmap (CTA per tree)
+template <int NT>
+__global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
+  constexpr int NW = NT / 32;
+  __shared__ uint32_t sh[NW + 2];
+  const uint32_t b = blockIdx.x;
+  TreeState& st = a.ts[b];
+  if (st.done) return;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const NodeWork* fr = P.front[a.cur];
+  const uint32_t S = st.S, A = st.A;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < S; base += NT) {
+    const uint32_t s = base + threadIdx.x;
+    const uint32_t nl = s < S ? P.spl[s].nl : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(nl, sh, &tot);
+    if (s < S) {
+      const SplitInfo si = P.spl[s];
+      const uint32_t bL = carry + ex;
+      const uint32_t bb = fr[si.f].b;
+      P.segtab[si.f] = SegTab{static_cast<int32_t>(si.base) - static_cast<int32_t>(bL),
+                              static_cast<int32_t>(si.base + nl) - static_cast<int32_t>(bb) +
+                                  static_cast<int32_t>(bL),
+                              2 * s, 0u};
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) st.totL = carry;
+  const uint32_t aw = (A + 31u) / 32u;
+  carry = 0;
+  for (uint32_t base = 0; base < aw; base += NT) {
+    const uint32_t w = base + threadIdx.x;
+    const uint32_t v = w < aw ? __popc(P.bits[w]) : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan<NT>(v, sh, &tot);
+    if (w < aw) P.pref[w] = carry + ex;
+    carry += tot;
+  }
+}
+
+// payload pass over flattened (tree, position) + per-position segment offsets
+__global__ void w_pay(const WideArgs a) {
+  const uint32_t total = a.off[2][a.B];
+  const uint32_t nxt = a.cur ^ 1u;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const uint32_t f = P.seg[a.cur][k];
+    const SegTab tb = P.segtab[f];
+    P.off2[k] = make_int2(tb.offL, tb.offR);
+    if (tb.offL == INT_MIN) continue;
+    const bool l = get_bit(P.bits, k);
+    const int32_t lp = static_cast<int32_t>(bits_before(P.bits, P.pref, k));
+    const uint32_t dst =
+        static_cast<uint32_t>(l ? tb.offL + lp : tb.offR + static_cast<int32_t>(k) - lp);
+    P.pay[nxt][dst] = P.pay[a.cur][k];
+    P.wyy[nxt][dst] = P.wyy[a.cur][k];
+    P.seg[nxt][dst] = tb.child + (l ? 0u : 1u);
+  }
+}
+
+// list pass, phase 1: kept-left counts per (tree, chunk)
+__global__ void w_lcount(const WideArgs a) {
+  const uint32_t total = a.off[3][a.B];
+  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = gw; it < total; it += nw) {
+    const uint32_t b = owner(a.off[3], a.B, it), c = it - a.off[3][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const uint32_t A = a.ts[b].A, A16 = (A + 15u) & ~15u;
+    const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
+    uint32_t cnt = 0;
+#pragma unroll 2
+    for (uint32_t s = c * kChunk; s < ce; s += 128) {
+      ListQuad v;
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2);
+      cnt += __popc(side_quad(v, P.bits, P.pref));
+    }
+    cnt = warp_sum(cnt);
+    if (lane_id() == 0) P.chunk[c] = cnt;
+  }
+}
+
+// list pass, phase 3: scatter with the scanned chunk prefixes
+__global__ void w_lscatter(const WideArgs a) {
+  const uint32_t total = a.off[3][a.B];
+  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
+  const uint32_t nxt = a.cur ^ 1u;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = gw; it < total; it += nw) {
+    const uint32_t b = owner(a.off[3], a.B, it), c = it - a.off[3][b];
+    const SlotPtrs P = slot_ptrs(a.g, b);
+    const TreeState& st = a.ts[b];
+    const uint32_t A = st.A, A16 = (A + 15u) & ~15u, totL = st.totL;
+    const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
+    uint32_t run = P.chunk[c];
+#pragma unroll 2
+    for (uint32_t s = c * kChunk; s < ce; s += 128) {
+      ListQuad v;
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2);
+      const uint32_t lf = side_quad(v, P.bits, P.pref);
+      const uint32_t mine = __popc(lf);
+      const uint32_t inc = warp_incl_scan(mine);
+      int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
+      uint32_t* dstl = P.lists[nxt] + static_cast<size_t>(v.li) * stride;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((v.keep >> j) & 1u)) continue;
+        const bool l = (lf >> j) & 1u;
+        const int32_t off = static_cast<int32_t>(v.f[j]);
+        const uint32_t dst =
+            static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(v.k0 + j) - pl);
+        pl += l ? 1 : 0;
+        dstl[dst] = v.q[j];
+      }
+      run += __shfl_sync(kFull, inc, 31);
+    }
+  }
+}
+
+// advance the per-tree level state (after the level's last per-tree read of A)
+__global__ void w_advance(const WideArgs a) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.B) return;
+  TreeState& s = a.ts[b];
+  if (s.done) return;
+  s.F = 2 * s.S;
+  s.A = s.A_next;
+}
+
+// ---- emit + OOB ----------------------------------------------------------------------
+__global__ void w_emit(const WideArgs a) {
+  __shared__ unsigned long long s_off;
+  const uint32_t b = blockIdx.x, tl = a.t0 + b;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const TreeState& st = a.ts[b];
+  const uint32_t count = st.nodes;
+  if (threadIdx.x == 0) {
+    const unsigned long long off = atomicAdd(a.g.pool_used, static_cast<unsigned long long>(count));
+    s_off = off;
+    a.g.tree_off[tl] = off;
+    a.g.tree_cnt[tl] = count;
+    atomicAdd(a.g.split_rows, st.split_rows);
+    if (off + count > a.g.pool_cap) atomicExch(a.g.err, 1);
+  }
+  __syncthreads();
+  const unsigned long long off = s_off;
+  if (off + count > a.g.pool_cap) return;
+  for (uint32_t i = threadIdx.x; i < count; i += blockDim.x) {
+    a.g.pool_feature[off + i] = P.nf[i];
+    a.g.pool_thr[off + i] = P.nthr[i];
+    a.g.pool_left[off + i] = P.nleft[i];
+    a.g.pool_value[off + i] = P.nval[i];
+    a.g.pool_rank[off + i] = P.nrank[i];
+  }
+}
+
+template <typename RankT>
+__global__ void w_oob(const WideArgs a) {
+  const uint32_t b = blockIdx.y, tl = a.t0 + b;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  double* ov = a.g.oobval + static_cast<size_t>(tl) * n;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    if (P.mult[r]) continue;
+    int32_t i = 0;
+    int32_t fi = P.nf[0];
+    while (fi >= 0) {
+      const bool left = rank_of(rank + static_cast<size_t>(fi) * n, r) <= P.nrank[i];
+      i = P.nleft[i] + (left ? 0 : 1);
+      fi = P.nf[i];
+    }
+    ov[r] = P.nval[i];
+  }
+}
+
+// ---- host driver for one batch of trees [t0, t0+B) (local indices) ----------------
+template <typename RankT>
+cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
+                       uint64_t* launches) {
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const dim3 rowsgrid((n + 1023) / 1024, a.B);
+  const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
+#define WCK(x)                              \
+  do {                                      \
+    x;                                      \
+    ++*launches;                            \
+    cudaError_t e_ = cudaGetLastError();    \
+    if (e_ != cudaSuccess) return e_;       \
+  } while (0)
+  WCK((w_zero<<<rowsgrid, 256, 0, st>>>(a)));
+  WCK((w_boot<<<rowsgrid, 256, 0, st>>>(a)));
+  WCK((w_bits<1024><<<a.B, 1024, 0, st>>>(a)));
+  WCK((w_payload<<<rowsgrid, 256, 0, st>>>(a)));
+  if (a.g.d.nlisted) {
+    WCK((w_l0count<<<wgrid, 256, 0, st>>>(a)));
+    WCK((w_chunkscan<1024><<<a.B, 1024, 0, st>>>(a, 0)));
+    WCK((w_l0scatter<<<wgrid, 256, 0, st>>>(a)));
+  }
+  WCK((w_root<<<a.B, 32, 0, st>>>(a)));
+  for (uint32_t level = 0;; ++level) {
+    a.cur = level & 1u;
+    WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
+    WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
+    WCK((w_chains_warp<RankT><<<wgrid, 256, 0, st>>>(a)));
+    WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
+    cudaMemsetAsync(a.active, 0, 4, st);
+    WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
+    cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    if (*h_active == 0) break;
+    WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 1)));
+    WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
+    WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
+    WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
+    WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
+    if (a.g.d.nlisted) {
+      WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
+      WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
+      WCK((w_lscatter<<<wgrid, 256, 0, st>>>(a)));
+    }
+    WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
+  }
+  WCK((w_emit<<<a.B, 256, 0, st>>>(a)));
+  if (a.g.oobval) WCK((w_oob<RankT><<<rowsgrid, 256, 0, st>>>(a)));
+#undef WCK
+  return cudaSuccess;
+}
+
+cudaError_t run_wide(int rank_bytes, const WideArgs& a, cudaStream_t st, int sms,
+                     uint32_t* h_active, uint64_t* launches) {
+  return rank_bytes == 2 ? run_wide_t<uint16_t>(a, st, sms, h_active, launches)
+                         : run_wide_t<uint32_t>(a, st, sms, h_active, launches);
+}
+
+}  // namespace aiwc_b200
