@@ -481,6 +481,18 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
     int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
     CK(cudaMemGetInfo(&free_b, &total_b));
+    {
+      // memory parked in the stream-ordered pool (and this ctx's scratch, which is
+      // reused or replaced) is available too; cudaMemGetInfo does not count it
+      cudaMemPool_t mp;
+      uint64_t reserved = 0, used_now = 0;
+      if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess &&
+          cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+          cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used_now) == cudaSuccess &&
+          reserved > used_now)
+        free_b += reserved - used_now;
+      free_b += ctx->scratch.count;
+    }
     const size_t pool_bytes = cap * 28;
     const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
     slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));

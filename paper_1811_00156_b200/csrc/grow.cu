@@ -170,17 +170,21 @@ struct ListQuad {
 // level so the list pass has no dependent segment-table lookup
 __device__ __forceinline__ void load_quad(ListQuad& v, uint32_t g0, uint32_t A16, uint32_t A,
                                           uint32_t end, uint32_t stride, const uint32_t* lists,
-                                          const int2* off2) {
+                                          const int2* off2, const int2* uniform = nullptr) {
   v.keep = 0;
   v.li = g0 / A16;
   v.k0 = g0 - v.li * A16;
   if (g0 < end && v.k0 < A) {
     const uint4 x = *reinterpret_cast<const uint4*>(lists + static_cast<size_t>(v.li) * stride + v.k0);
-    const int4 y0 = *reinterpret_cast<const int4*>(off2 + v.k0);
-    const int4 y1 = *reinterpret_cast<const int4*>(off2 + v.k0 + 2);
     v.q[0] = x.x; v.q[1] = x.y; v.q[2] = x.z; v.q[3] = x.w;
-    v.t[0] = make_int2(y0.x, y0.y); v.t[1] = make_int2(y0.z, y0.w);
-    v.t[2] = make_int2(y1.x, y1.y); v.t[3] = make_int2(y1.z, y1.w);
+    if (uniform) {  // the whole chunk lies in one segment: no per-position offsets
+      v.t[0] = v.t[1] = v.t[2] = v.t[3] = *uniform;
+    } else {
+      const int4 y0 = *reinterpret_cast<const int4*>(off2 + v.k0);
+      const int4 y1 = *reinterpret_cast<const int4*>(off2 + v.k0 + 2);
+      v.t[0] = make_int2(y0.x, y0.y); v.t[1] = make_int2(y0.z, y0.w);
+      v.t[2] = make_int2(y1.x, y1.y); v.t[3] = make_int2(y1.z, y1.w);
+    }
     const uint32_t left = A - v.k0;
     v.keep = left >= 4 ? 0xfu : ((1u << left) - 1u);
   }

@@ -87,6 +87,20 @@ __device__ __forceinline__ uint32_t nchunks_of(uint32_t A, uint32_t nl) {
   return (nl * A16 + kChunk - 1) / kChunk;
 }
 
+// true when list-pass chunk [cb, ce) lies inside one list and one segment; then `u`
+// holds that segment's (offL, offR) and the chunk needs no per-position offsets
+__device__ __forceinline__ bool chunk_uniform(uint32_t cb, uint32_t ce, uint32_t A16, uint32_t A,
+                                              const uint32_t* seg, const int2* off2, int2& u) {
+  const uint32_t li = cb / A16;
+  if ((ce - 1) / A16 != li) return false;
+  const uint32_t k0 = cb - li * A16;
+  if (k0 >= A) return false;
+  const uint32_t k1 = min(ce - 1 - li * A16, A - 1);
+  if (seg[k0] != seg[k1]) return false;
+  u = off2[k0];
+  return true;
+}
+
 // ---- batch initialisation ---------------------------------------------------------
 __global__ void w_zero(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a.g, blockIdx.y);
@@ -648,6 +662,64 @@ __global__ void w_pay(const WideArgs a) {
   }
 }
 
+// List pass with the tree's goes-left bitmap + prefix staged in shared memory: one CTA
+// per tree streams all of that tree's chunks (phase 1 counts, phase 3 scatter), so the
+// two random lookups per entry hit shared memory instead of L2.
+template <int NT, bool kScatter>
+__global__ void __launch_bounds__(NT) w_ltree(const WideArgs a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t b = blockIdx.x;
+  const TreeState& st = a.ts[b];
+  if (st.done) return;
+  const SlotPtrs P = slot_ptrs(a.g, b);
+  const uint32_t A = st.A, A16 = (A + 15u) & ~15u, aw = (A + 31u) / 32u;
+  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride, totL = st.totL;
+  uint32_t* sbits = sm;
+  uint32_t* spref = sm + aw;
+  for (uint32_t w = threadIdx.x; w < aw; w += NT) {
+    sbits[w] = P.bits[w];
+    spref[w] = P.pref[w];
+  }
+  __syncthreads();
+  const uint32_t nchunk = nchunks_of(A, nl), nxt = a.cur ^ 1u;
+  for (uint32_t c = warp_id(); c < nchunk; c += NT / 32) {
+    const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
+    int2 u;
+    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
+    uint32_t run = kScatter ? P.chunk[c] : 0u;
+#pragma unroll 2
+    for (uint32_t s = c * kChunk; s < ce; s += 128) {
+      ListQuad v;
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
+                uni ? &u : nullptr);
+      const uint32_t lf = side_quad(v, sbits, spref);
+      const uint32_t mine = __popc(lf);
+      if (!kScatter) {
+        run += mine;
+        continue;
+      }
+      const uint32_t inc = warp_incl_scan(mine);
+      int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
+      uint32_t* dstl = P.lists[nxt] + static_cast<size_t>(v.li) * stride;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((v.keep >> j) & 1u)) continue;
+        const bool l = (lf >> j) & 1u;
+        const int32_t off = static_cast<int32_t>(v.f[j]);
+        const uint32_t dst =
+            static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(v.k0 + j) - pl);
+        pl += l ? 1 : 0;
+        dstl[dst] = v.q[j];
+      }
+      run += __shfl_sync(kFull, inc, 31);
+    }
+    if (!kScatter) {
+      run = warp_sum(run);
+      if (lane_id() == 0) P.chunk[c] = run;
+    }
+  }
+}
+
 // list pass, phase 1: kept-left counts per (tree, chunk)
 __global__ void w_lcount(const WideArgs a) {
   const uint32_t total = a.off[3][a.B];
@@ -658,11 +730,14 @@ __global__ void w_lcount(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a.g, b);
     const uint32_t A = a.ts[b].A, A16 = (A + 15u) & ~15u;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
+    int2 u;
+    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
     uint32_t cnt = 0;
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
       ListQuad v;
-      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2);
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
+                uni ? &u : nullptr);
       cnt += __popc(side_quad(v, P.bits, P.pref));
     }
     cnt = warp_sum(cnt);
@@ -682,11 +757,14 @@ __global__ void w_lscatter(const WideArgs a) {
     const TreeState& st = a.ts[b];
     const uint32_t A = st.A, A16 = (A + 15u) & ~15u, totL = st.totL;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
+    int2 u;
+    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
     uint32_t run = P.chunk[c];
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
       ListQuad v;
-      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2);
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
+                uni ? &u : nullptr);
       const uint32_t lf = side_quad(v, P.bits, P.pref);
       const uint32_t mine = __popc(lf);
       const uint32_t inc = warp_incl_scan(mine);
@@ -771,6 +849,20 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const dim3 rowsgrid((n + 1023) / 1024, a.B);
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
+  // per-tree list pass with the bitmap + prefix in shared memory when they fit
+  size_t ltree_smem = (a.g.L.stride + 31) / 32 * 8;
+  {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (ltree_smem + 1024 > static_cast<size_t>(optin) ||
+        cudaFuncSetAttribute(w_ltree<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ltree_smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(w_ltree<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(ltree_smem)) != cudaSuccess)
+      ltree_smem = 0;
+    cudaGetLastError();
+  }
 #define WCK(x)                              \
   do {                                      \
     x;                                      \
@@ -806,9 +898,15 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
     if (a.g.d.nlisted) {
-      WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
-      WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
-      WCK((w_lscatter<<<wgrid, 256, 0, st>>>(a)));
+      if (ltree_smem) {
+        WCK((w_ltree<1024, false><<<a.B, 1024, ltree_smem, st>>>(a)));
+        WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
+        WCK((w_ltree<1024, true><<<a.B, 1024, ltree_smem, st>>>(a)));
+      } else {
+        WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
+        WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
+        WCK((w_lscatter<<<wgrid, 256, 0, st>>>(a)));
+      }
     }
     WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
   }
