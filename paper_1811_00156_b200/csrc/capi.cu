@@ -500,15 +500,34 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     const size_t need = size_t(slots) * L.bytes;
     if (ctx->scratch.count < need) ctx->scratch.alloc(need);
     a.scratch = ctx->scratch.p;
+    int nlanes = 1;
+    if (wide) {
+      nlanes = 2;
+      if (const char* e = std::getenv("AIWC_WIDE_LANES")) nlanes = std::max(1, std::atoi(e));
+      nlanes = std::max(1, std::min(nlanes, slots));
+    }
+    const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
     DevBuf<TreeState> wts(wide ? slots : 0);
-    DevBuf<uint32_t> woff(wide ? 4 * (size_t(slots) + 1) : 0), wactive(wide ? 1 : 0);
+    DevBuf<uint32_t> woff(wide ? 4 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0);
     std::unique_ptr<uint32_t, void (*)(uint32_t*)> h_active(
         [] {
           uint32_t* p = nullptr;
-          cudaMallocHost(&p, 4);
+          cudaMallocHost(&p, 64 * 4);
           return p;
         }(),
         [](uint32_t* p) { cudaFreeHost(p); });
+    std::vector<cudaStream_t> lane_streams;
+    struct StreamsGuard {
+      std::vector<cudaStream_t>& v;
+      ~StreamsGuard() {
+        for (auto s : v) cudaStreamDestroy(s);
+      }
+    } lsg{lane_streams};
+    for (int k = 1; k < nlanes; ++k) {
+      cudaStream_t s;
+      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+      lane_streams.push_back(s);
+    }
 
     DevBuf<uint32_t> queue(1), tree_cnt(T);
     DevBuf<int> err(1);
@@ -563,19 +582,42 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
       CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
       CK(cudaEventRecord(ev0, st.s));
       if (wide) {
-        // batched multi-kernel grower: batches of `slots` trees, level-synchronous
-        for (uint32_t t0 = 0; t0 < T; t0 += static_cast<uint32_t>(slots)) {
-          WideArgs w{};
-          w.g = a;
-          w.ts = wts.p;
-          w.B = std::min<uint32_t>(static_cast<uint32_t>(slots), T - t0);
-          w.t0 = t0;
-          for (int i = 0; i < 4; ++i) w.off[i] = woff.p + size_t{i} * (slots + 1);
-          w.active = wactive.p;
-          uint64_t nl = 0;
-          CK(run_wide(ctx->rank_bytes, w, st.s, sms, h_active.get(), &nl));
-          g_launches += nl;
+        // batched multi-kernel grower: K concurrent lanes (stream + host thread), each
+        // growing batches of `per` trees level-synchronously.  While one batch sits in
+        // the sequential tail of a level (a few long chains on huge nodes), the other
+        // lanes' kernels fill the SMs.
+        const int K = nlanes;
+        const uint32_t per = static_cast<uint32_t>(slots / K);
+        std::vector<cudaError_t> lane_err(K, cudaSuccess);
+        std::vector<std::thread> lanes;
+        for (int k = 0; k < K; ++k) {
+          lanes.emplace_back([&, k] {
+            cudaSetDevice(dev);
+            const cudaStream_t ls = k == 0 ? st.s : lane_streams[k - 1];
+            for (uint32_t t0 = k * per; t0 < T; t0 += K * per) {
+              WideArgs w{};
+              w.g = a;
+              w.g.scratch = a.scratch + size_t{k} * per * L.bytes;
+              w.ts = wts.p + size_t{k} * per;
+              w.B = std::min<uint32_t>(per, T - t0);
+              w.t0 = t0;
+              for (int i = 0; i < 4; ++i)
+                w.off[i] = woff.p + (size_t{k} * 4 + i) * (per + 1);
+              w.active = wactive.p + k;
+              uint64_t nl = 0;
+              cudaError_t e = run_wide(ctx->rank_bytes, w, ls, sms, h_active.get() + k, &nl);
+              g_launches += nl;
+              if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
+              if (e != cudaSuccess) {
+                lane_err[k] = e;
+                return;
+              }
+            }
+          });
         }
+        for (auto& th : lanes) th.join();
+        for (cudaError_t e : lane_err)
+          if (e != cudaSuccess) throw Status(AIWC_ECUDA, std::string("wide grower: ") + cudaGetErrorString(e));
       } else {
         CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
         g_launches += 1;

@@ -207,3 +207,26 @@ def test_c4_first8_trees(seed, golden):
     assert soa_sha(s) == g["soa_sha"]
     assert hashlib.sha256(s.inbag.tobytes()).hexdigest() == g["inbag_sha"]
     assert oob_list(f.oob) == g["oob"]
+
+
+@pytest.mark.parametrize("path", ["wide", "persistent"])
+def test_both_growers_bit_exact(path, seed, golden, monkeypatch):
+    """The batched wide grower (default for n >= 65536) and the per-tree persistent
+    grower (default below) produce the same forests; force each on C1 and edge tables."""
+    monkeypatch.setenv("AIWC_GROW_WIDE", "1" if path == "wide" else "0")
+    t = pkg.Table()
+    prep = pkg.PreparedDataset.from_table(t)
+    f = pkg.fit(prep, pkg.ForestParams(60, 6, 5, seed))
+    s = soa_of(f)
+    o = Oracle.fit(t.col, t.y, t.n, t.p, 60, 6, 5, seed)
+    assert forests_equal(o, s) is None
+    for name in ("ties", "tworows", "constcol"):
+        z = np.load(os.path.join(GOLD, f"edge_{name}.npz"))
+        col, y = z["col"], z["y"]
+        p, n = col.shape
+        prm = golden["edges"][name]
+        f = pkg.fit(pkg.PreparedDataset(col, y, n, p),
+                    pkg.ForestParams(prm["T"], prm["mtry"], prm["mns"], seed))
+        g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"],
+                      z["value"], inbag=z["inbag"])
+        assert forests_equal(g, soa_of(f)) is None
