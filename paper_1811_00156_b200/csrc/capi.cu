@@ -493,13 +493,21 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         free_b += reserved - used_now;
       free_b += ctx->scratch.count;
     }
-    const size_t pool_bytes = cap * 28;
+    // node pool (28 B/node) plus the compacted forest built from it after growth
+    // (feature, left, thr, value, PredNode: 40 B/node) stay outside the slot scratch
+    const size_t pool_bytes = cap * (28 + 40);
     const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
     slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
     if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
     const size_t need = size_t(slots) * L.bytes;
     if (ctx->scratch.count < need) ctx->scratch.alloc(need);
     a.scratch = ctx->scratch.p;
+    // hand the slots back to the stream-ordered pool when the fit ends (the pool keeps
+    // them reserved, so the next fit -- on this or another dataset -- reuses them)
+    struct ScratchRelease {
+      DevBuf<char>& b;
+      ~ScratchRelease() { b.release(); }
+    } scratch_release{ctx->scratch};
     int nlanes = 1;
     if (wide) {
       nlanes = 2;
