@@ -455,8 +455,10 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
       a.bits_in_smem = 0;
     }
     int per_sm = 0;
-    if (wide)
+    if (wide) {
       per_sm = 4;  // batch up to 4 trees per SM (bounded by memory below)
+      if (const char* e = std::getenv("AIWC_WIDE_PER_SM")) per_sm = std::max(1, std::atoi(e));
+    }
     else
       CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
     if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
@@ -596,6 +598,8 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         // lanes' kernels fill the SMs.
         const int K = nlanes;
         const uint32_t per = static_cast<uint32_t>(slots / K);
+        uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
+        if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
         std::vector<cudaError_t> lane_err(K, cudaSuccess);
         std::vector<std::thread> lanes;
         for (int k = 0; k < K; ++k) {
@@ -608,6 +612,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
               w.g.scratch = a.scratch + size_t{k} * per * L.bytes;
               w.ts = wts.p + size_t{k} * per;
               w.B = std::min<uint32_t>(per, T - t0);
+              w.big_min = big_min;
               w.t0 = t0;
               for (int i = 0; i < 4; ++i)
                 w.off[i] = woff.p + (size_t{k} * 4 + i) * (per + 1);

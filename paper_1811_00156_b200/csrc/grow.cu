@@ -291,6 +291,107 @@ __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
   best_pos = bp;
 }
 
+// Pipelined warp chains for the wide grower: tiles of 32*G positions; while tile i is
+// scanned, the payload gathers of tile i+1 and the list loads of tile i+2 are in
+// flight.  Same arithmetic (and order) as chain_warp / chain_bin_warp.
+template <typename RankT, int G>
+__device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint32_t e,
+                             const Payload* pay, const RankT* __restrict__ rk_c, double W,
+                             double S, double& best_gain, uint32_t& best_pos, double* st) {
+  const unsigned lane = lane_id();
+  double sl = 0.0, bg = -INFINITY;
+  uint32_t wl = 0, prev_rank = 0, bp = 0xffffffffu, n0 = 0;
+  bool first = true;
+  uint32_t qn[G], rowc[G], muc[G], rown[G], mun[G];
+  double wyc[G], wyn[G];
+  auto load_q = [&](uint32_t k0, uint32_t (&q)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      q[g] = k < e ? (listed ? list[k] : k) : 0u;
+    }
+  };
+  auto load_p = [&](uint32_t k0, const uint32_t (&q)[G], uint32_t (&row)[G], uint32_t (&mu)[G],
+                    double (&wy)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      if (k < e) {
+        const Payload P = pay[q[g]];
+        row[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+      } else {
+        row[g] = 0u;
+        mu[g] = 0u;
+        wy[g] = 0.0;
+      }
+    }
+  };
+  load_q(b, qn);
+  load_p(b, qn, rowc, muc, wyc);
+  load_q(b + 32 * G, qn);
+  for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
+    uint32_t rk[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) rk[g] = k0 + g * 32 + lane < e ? rank_of(rk_c, rowc[g]) : 0u;
+    load_p(k0 + 32 * G, qn, rown, mun, wyn);
+    load_q(k0 + 64 * G, qn);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      if (t0 >= e) break;
+      const uint32_t nv = min(32u, e - t0);
+      const bool valid = lane < nv;
+      if (listed) {
+        const uint32_t inc = warp_incl_scan(muc[g]);
+        const uint32_t wl_before = wl + inc - muc[g];
+        const double mine = tile_prefix(wyc[g], nv, sl, st);
+        uint32_t pr = __shfl_up_sync(kFull, rk[g], 1);
+        if (lane == 0) pr = first ? rk[g] : prev_rank;
+        if (valid && rk[g] != pr) {
+          const double gn = gain_at(mine, static_cast<double>(wl_before), W, S);
+          if (gn > bg) {
+            bg = gn;
+            bp = t0 + lane;
+          }
+        }
+        wl += __shfl_sync(kFull, inc, 31);
+        prev_rank = __shfl_sync(kFull, rk[g], nv - 1);
+        first = false;
+      } else {  // two-level column: value-0 rows in row order, +0.0 for the others
+        const bool z = valid && rk[g] == 0u;
+        n0 += __popc(__ballot_sync(kFull, z));
+        wl += warp_sum(z ? muc[g] : 0u);
+        st[lane] = z ? wyc[g] : 0.0;
+        __syncwarp();
+        double r = sl;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r = __dadd_rn(r, st[j]);
+        sl = r;
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      rowc[g] = rown[g];
+      muc[g] = mun[g];
+      wyc[g] = wyn[g];
+    }
+  }
+  if (listed) {
+    warp_best(bg, bp);
+    best_gain = bg;
+    best_pos = bp;
+  } else if (n0 == 0 || n0 == e - b) {
+    best_gain = -INFINITY;
+    best_pos = 0xffffffffu;
+  } else {
+    best_gain = gain_at(sl, static_cast<double>(wl), W, S);
+    best_pos = b + n0;
+  }
+}
+
 // ---- split chain over a sorted list, one lane (small nodes) -----------------------
 template <typename RankT>
 __device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
@@ -418,6 +519,174 @@ __device__ void chain_bin_lane(const Payload* pay, uint32_t b, uint32_t e,
   }
 }
 
+// ---- split chains of one node, G lanes per (node, column) -------------------------
+// A warp holds 32/G lane groups, each running one sampled column of the SAME node (so
+// every group walks the same range [b, e) and the warp stays converged).  A round
+// covers G*U consecutive positions; lane gl of a group owns positions
+// k0 + gl*U + u (u < U), so the visiting order is (gl, u) lexicographic.  The
+// sequential FP64 chain of a round runs in every lane of the group over a shared-memory
+// stage (each DADD instruction serves 32/G chains instead of one), the integer weight
+// prefix is a group scan, and gains are evaluated per lane at value boundaries.
+// `listed`: the column's sorted list gives the order (forest.hpp:268-297); otherwise the
+// column is two-level and its chain is the row-order sum of the value-0 rows (a masked
+// add of +0.0 is exact: the running sum starts at +0.0 and can never become -0.0).
+template <typename RankT, int G, int U>
+__device__ __forceinline__ void chain_grp(bool active, bool listed, const uint32_t* list,
+                                          uint32_t b, uint32_t e, const Payload* pay,
+                                          const RankT* __restrict__ rk_c, double W, double S,
+                                          double& best_gain, uint32_t& best_pos, double* st) {
+  static_assert(U % 4 == 0, "U must be a multiple of 4 (uint4 list loads)");
+  constexpr uint32_t R = G * U;  // positions per round
+  const unsigned gl = lane_id() & (G - 1);
+  double sl = 0.0, bg = -INFINITY;
+  uint32_t wl = 0, prev_rank = 0, bp = 0xffffffffu, n0 = 0;
+  bool pg[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) pg[g] = gl == static_cast<unsigned>(g);
+  // software pipeline over rounds: while round i is summed, the payload gathers of round
+  // i+1 and the list loads of round i+2 are in flight
+  auto load_q = [&](uint32_t kb, uint32_t (&q)[U]) {
+    if (active && listed) {
+#pragma unroll
+      for (int v = 0; v < U; v += 4) {
+        if (kb + v < e) {
+          const uint4 x = *reinterpret_cast<const uint4*>(list + kb + v);
+          q[v] = x.x; q[v + 1] = x.y; q[v + 2] = x.z; q[v + 3] = x.w;
+        } else {
+          q[v] = q[v + 1] = q[v + 2] = q[v + 3] = 0u;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) q[u] = kb + u;
+    }
+  };
+  auto load_p = [&](uint32_t kb, const uint32_t (&q)[U], uint32_t (&row)[U], uint32_t (&mu)[U],
+                    double (&wy)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + u;
+      if (active && k >= b && k < e) {
+        const Payload P = pay[q[u]];
+        row[u] = P.row;
+        mu[u] = P.mult;
+        wy[u] = P.wy;
+      } else {
+        row[u] = 0u;
+        mu[u] = 0u;
+        wy[u] = 0.0;
+      }
+    }
+  };
+  uint32_t k0 = b & ~3u;
+  uint32_t qn[U], rowc[U], muc[U], rown[U], mun[U];
+  double wyc[U], wyn[U];
+  load_q(k0 + gl * U, qn);
+  load_p(k0 + gl * U, qn, rowc, muc, wyc);
+  load_q(k0 + R + gl * U, qn);
+  for (; k0 < e; k0 += R) {
+    const uint32_t kb = k0 + gl * U;
+    uint32_t rk[U], mu[U];
+    double a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + u;
+      rk[u] = (active && k >= b && k < e) ? rank_of(rk_c, rowc[u]) : 0u;
+    }
+    // prefetch: payload of round i+1, list of round i+2
+    load_p(kb + R, qn, rown, mun, wyn);
+    load_q(kb + 2 * R, qn);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      mu[u] = muc[u];
+      a[u] = wyc[u];
+      if (!listed) {  // two-level column: only value-0 rows enter the chain
+        const uint32_t k = kb + u;
+        const bool z = active && k >= b && k < e && rk[u] == 0u;
+        n0 += z ? 1u : 0u;
+        if (!z) {
+          mu[u] = 0u;
+          a[u] = 0.0;
+        }
+      }
+    }
+    // integer weight prefix (exact): lane-local, then across the group
+    uint32_t loc = 0, wb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      wb[u] = loc;
+      loc += mu[u];
+    }
+    uint32_t inc = loc;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, inc, o, G);
+      if (gl >= static_cast<unsigned>(o)) inc += t;
+    }
+    const uint32_t wbase = wl + inc - loc;
+    wl += __shfl_sync(kFull, inc, G - 1, G);
+    // sequential FP64 chain of the round
+#pragma unroll
+    for (int u = 0; u < U; ++u) st[gl * U + u] = a[u];
+    __syncwarp();
+    double mine[U];
+    double r = sl;
+#pragma unroll
+    for (int j = 0; j < static_cast<int>(R); ++j) {
+      if (pg[j / U]) mine[j % U] = r;
+      r = __dadd_rn(r, st[j]);
+    }
+    sl = r;
+    __syncwarp();
+    // (shuffles stay outside the `listed` branch: groups of one warp may differ)
+    uint32_t pr = __shfl_up_sync(kFull, rk[U - 1], 1, G);
+    if (gl == 0) pr = prev_rank;
+    prev_rank = __shfl_sync(kFull, rk[U - 1], G - 1, G);
+    if (listed) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t k = kb + u;
+        const uint32_t pru = u == 0 ? pr : rk[u - 1];
+        if (active && k > b && k < e && rk[u] != pru) {
+          const double gn = gain_at(mine[u], static_cast<double>(wbase + wb[u]), W, S);
+          if (gn > bg) {
+            bg = gn;
+            bp = k;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      rowc[u] = rown[u];
+      muc[u] = mun[u];
+      wyc[u] = wyn[u];
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    const double og = __shfl_xor_sync(kFull, bg, o, G);
+    const uint32_t op = __shfl_xor_sync(kFull, bp, o, G);
+    if (og > bg || (og == bg && op < bp)) {
+      bg = og;
+      bp = op;
+    }
+    n0 += __shfl_xor_sync(kFull, n0, o, G);
+  }
+  if (listed) {
+    best_gain = bg;
+    best_pos = bp;
+  } else {
+    if (n0 == 0 || n0 == e - b) {
+      best_gain = -INFINITY;
+      best_pos = 0xffffffffu;
+    } else {
+      best_gain = gain_at(sl, static_cast<double>(wl), W, S);
+      best_pos = b + n0;
+    }
+  }
+}
+
 struct RouteOut {
   uint32_t nl;
   uint32_t wl, wr;
@@ -476,6 +745,94 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
       tile_masked_sum2(wy[g], yy[g], bv & ~bl, o.sr, o.qr, st);
     }
   }
+}
+
+// Pipelined variant for the wide grower: tiles of 32*G positions; while tile i is
+// summed, the payload gathers of tile i+1 and the list loads of tile i+2 are in flight.
+// The four sequential sums (left/right x sum/sumsq) run in four 8-lane groups over a
+// staged tile in which elements of the other side are +0.0 (an exact no-op, see
+// chain_grp), so every tile costs 32 dependent DADDs per group and no masked loops.
+template <typename RankT, int G>
+__device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
+                             const Payload* pay, const double* wyy,
+                             const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
+                             RouteOut& o, double* st /* 4*32 doubles */) {
+  const unsigned lane = lane_id(), grp = lane >> 3;
+  double acc = 0.0;  // this lane's group chain: 0 sl, 1 ql, 2 sr, 3 qr
+  uint32_t qn[G], qc[G], rowc[G], muc[G], rown[G], mun[G];
+  double wyc[G], yyc[G], wyn[G], yyn[G];
+  auto load_q = [&](uint32_t k0, uint32_t (&q)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      q[g] = k < e ? list0[k] : 0u;
+    }
+  };
+  auto load_p = [&](uint32_t k0, const uint32_t (&q)[G], uint32_t (&row)[G], uint32_t (&mu)[G],
+                    double (&wy)[G], double (&yy)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t k = k0 + g * 32 + lane;
+      if (k < e) {
+        const Payload P = pay[q[g]];
+        row[g] = P.row;
+        mu[g] = P.mult;
+        wy[g] = P.wy;
+        yy[g] = wyy[q[g]];
+      } else {
+        row[g] = 0u;
+        mu[g] = 0u;
+        wy[g] = 0.0;
+        yy[g] = 0.0;
+      }
+    }
+  };
+  load_q(b, qc);
+  load_p(b, qc, rowc, muc, wyc, yyc);
+  load_q(b + 32 * G, qn);
+  for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
+    bool lft[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      lft[g] = (k0 + g * 32 + lane < e) && rank_of(rk_f, rowc[g]) <= thr_rank;
+    uint32_t qnn[G];
+    load_p(k0 + 32 * G, qn, rown, mun, wyn, yyn);
+    load_q(k0 + 64 * G, qnn);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t t0 = k0 + g * 32;
+      const bool valid = t0 + lane < e;
+      const bool left = lft[g];
+      if (left) atomicOr(bits + (qc[g] >> 5), 1u << (qc[g] & 31u));
+      o.nl += __popc(__ballot_sync(kFull, left));
+      o.wl += warp_sum(left ? muc[g] : 0u);
+      o.wr += warp_sum((valid && !left) ? muc[g] : 0u);
+      st[lane] = left ? wyc[g] : 0.0;
+      st[32 + lane] = left ? yyc[g] : 0.0;
+      st[64 + lane] = (valid && !left) ? wyc[g] : 0.0;
+      st[96 + lane] = (valid && !left) ? yyc[g] : 0.0;
+      __syncwarp();
+      const double* sg = st + grp * 32;
+      double r = acc;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) r = __dadd_rn(r, sg[j]);
+      acc = r;
+      __syncwarp();
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      qc[g] = qn[g];
+      qn[g] = qnn[g];
+      rowc[g] = rown[g];
+      muc[g] = mun[g];
+      wyc[g] = wyn[g];
+      yyc[g] = yyn[g];
+    }
+  }
+  o.sl = __shfl_sync(kFull, acc, 0);
+  o.ql = __shfl_sync(kFull, acc, 8);
+  o.sr = __shfl_sync(kFull, acc, 16);
+  o.qr = __shfl_sync(kFull, acc, 24);
 }
 
 template <typename RankT>
@@ -1271,6 +1628,7 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_front1 = take(fmax * sizeof(NodeWork));
   L.off_segtab = take(fmax * sizeof(SegTab));
   L.off_e2f = take(emax * 4);
+  L.off_ecls = take(emax * 4);
   L.off_samp = take(emax * mtry * 2);
   L.off_res = take(emax * mtry * sizeof(ChainRes));
   L.off_split = take(emax * sizeof(SplitInfo));

@@ -72,7 +72,8 @@ struct SlotLayout {
   uint32_t nodes_cap;
   size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
-      off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref;
+      off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
+      off_ecls;
   size_t bytes;
 };
 
@@ -107,6 +108,7 @@ struct GrowArgs {
 struct TreeState {
   uint32_t A, F, E, S;
   uint32_t nodes, done, totL, A_next;
+  uint32_t E0, E1;  // eligible nodes by size class: small (lane chains), mid (group chains)
   unsigned long long elig_base, split_rows;
 };
 
@@ -116,7 +118,7 @@ struct WideArgs {
   uint32_t B;        // trees in this batch (slots 0..B-1)
   uint32_t t0;       // local index of the batch's first tree
   uint32_t cur;      // buffer parity of the current level
-  uint32_t pad;
+  uint32_t big_min;  // nodes with >= big_min rows run one warp per chain (else lane groups)
   uint32_t* off[4];  // [B+1] prefixes: chain tasks, splits, positions, list chunks
   uint32_t* active;  // trees still splitting after this level's decide
 };

@@ -12,15 +12,19 @@
 
 namespace aiwc_b200 {
 
+// Pointers of slot b for the current level (cur) and the next one (suffix _n).  The
+// double buffers are resolved here, with selects, so no kernel indexes a pointer array
+// dynamically (that would put the whole struct in local memory).
 struct SlotPtrs {
   uint32_t* mult;
-  Payload* pay[2];
-  double* wyy[2];
-  uint32_t* lists[2];
-  uint32_t* seg[2];
-  NodeWork* front[2];
+  Payload *pay, *pay_n;
+  double *wyy, *wyy_n;
+  uint32_t *lists, *lists_n;
+  uint32_t *seg, *seg_n;
+  NodeWork *front, *front_n;
   SegTab* segtab;
   uint32_t* e2f;
+  uint32_t* ecls;
   uint16_t* samp;
   ChainRes* res;
   SplitInfo* spl;
@@ -35,23 +39,25 @@ struct SlotPtrs {
   uint32_t* pref;
 };
 
-__device__ __forceinline__ SlotPtrs slot_ptrs(const GrowArgs& g, uint32_t b) {
-  const SlotLayout& L = g.L;
-  char* s = g.scratch + static_cast<size_t>(b) * L.bytes;
+__device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
+  const SlotLayout& L = a.g.L;
+  char* s = a.g.scratch + static_cast<size_t>(b) * L.bytes;
+  const bool c = a.cur != 0u;
   SlotPtrs p;
   p.mult = reinterpret_cast<uint32_t*>(s + L.off_mult);
-  p.pay[0] = reinterpret_cast<Payload*>(s + L.off_pay0);
-  p.pay[1] = reinterpret_cast<Payload*>(s + L.off_pay1);
-  p.wyy[0] = reinterpret_cast<double*>(s + L.off_wyy0);
-  p.wyy[1] = reinterpret_cast<double*>(s + L.off_wyy1);
-  p.lists[0] = reinterpret_cast<uint32_t*>(s + L.off_list0);
-  p.lists[1] = reinterpret_cast<uint32_t*>(s + L.off_list1);
-  p.seg[0] = reinterpret_cast<uint32_t*>(s + L.off_seg0);
-  p.seg[1] = reinterpret_cast<uint32_t*>(s + L.off_seg1);
-  p.front[0] = reinterpret_cast<NodeWork*>(s + L.off_front0);
-  p.front[1] = reinterpret_cast<NodeWork*>(s + L.off_front1);
+  p.pay = reinterpret_cast<Payload*>(s + (c ? L.off_pay1 : L.off_pay0));
+  p.pay_n = reinterpret_cast<Payload*>(s + (c ? L.off_pay0 : L.off_pay1));
+  p.wyy = reinterpret_cast<double*>(s + (c ? L.off_wyy1 : L.off_wyy0));
+  p.wyy_n = reinterpret_cast<double*>(s + (c ? L.off_wyy0 : L.off_wyy1));
+  p.lists = reinterpret_cast<uint32_t*>(s + (c ? L.off_list1 : L.off_list0));
+  p.lists_n = reinterpret_cast<uint32_t*>(s + (c ? L.off_list0 : L.off_list1));
+  p.seg = reinterpret_cast<uint32_t*>(s + (c ? L.off_seg1 : L.off_seg0));
+  p.seg_n = reinterpret_cast<uint32_t*>(s + (c ? L.off_seg0 : L.off_seg1));
+  p.front = reinterpret_cast<NodeWork*>(s + (c ? L.off_front1 : L.off_front0));
+  p.front_n = reinterpret_cast<NodeWork*>(s + (c ? L.off_front0 : L.off_front1));
   p.segtab = reinterpret_cast<SegTab*>(s + L.off_segtab);
   p.e2f = reinterpret_cast<uint32_t*>(s + L.off_e2f);
+  p.ecls = reinterpret_cast<uint32_t*>(s + L.off_ecls);
   p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
   p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
   p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
@@ -75,6 +81,18 @@ __device__ __forceinline__ uint32_t owner(const uint32_t* off, uint32_t B, uint3
     if (off[mid] <= t) lo = mid; else hi = mid;
   }
   return lo;
+}
+
+// lane-group width of the mid-size chain kernel: the widest power of two that still
+// fits all m sampled columns of a node in one warp (G = 32 / pow2ceil(m), >= 1)
+__host__ __device__ inline uint32_t grp_width(uint32_t m) {
+  uint32_t c = 1;
+  while (c < m && c < 32) c <<= 1;
+  return 32u / c;
+}
+__host__ __device__ inline uint32_t grp_tasks_per_node(uint32_t m) {
+  const uint32_t ng = 32u / grp_width(m);  // chains per warp
+  return (m + ng - 1) / ng;
 }
 
 __device__ __forceinline__ uint64_t tree_key(const GrowArgs& g, uint32_t tl) {
@@ -103,7 +121,7 @@ __device__ __forceinline__ bool chunk_uniform(uint32_t cb, uint32_t ce, uint32_t
 
 // ---- batch initialisation ---------------------------------------------------------
 __global__ void w_zero(const WideArgs a) {
-  const SlotPtrs P = slot_ptrs(a.g, blockIdx.y);
+  const SlotPtrs P = slot_ptrs(a, blockIdx.y);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     P.mult[i] = 0u;
@@ -112,7 +130,7 @@ __global__ void w_zero(const WideArgs a) {
 // bootstrap draws (forest.hpp:184-195)
 __global__ void w_boot(const WideArgs a) {
   const uint32_t b = blockIdx.y, tl = a.t0 + b;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const uint64_t key = tree_key(a.g, tl);
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -128,7 +146,7 @@ __global__ void __launch_bounds__(NT) w_bits(const WideArgs a) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
   const uint32_t b = blockIdx.x;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const uint32_t nwords = (n + 31u) / 32u, nblk64 = (n + 63u) / 64u;
   for (uint32_t w = warp_id(); w < nwords; w += NW) {
@@ -168,7 +186,7 @@ __global__ void __launch_bounds__(NT) w_bits(const WideArgs a) {
 // payload in row order (forest.hpp:194-195)
 __global__ void w_payload(const WideArgs a) {
   const uint32_t b = blockIdx.y;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
     if (!get_bit(P.bits, r)) continue;
@@ -176,9 +194,9 @@ __global__ void w_payload(const WideArgs a) {
     const uint32_t mu = P.mult[r];
     const double yr = __ldg(a.g.d.y + r);
     const double wy = __dmul_rn(static_cast<double>(mu), yr);
-    P.pay[0][pos] = Payload{r, mu, wy};
-    P.wyy[0][pos] = __dmul_rn(wy, yr);
-    P.seg[0][pos] = 0u;
+    P.pay[pos] = Payload{r, mu, wy};
+    P.wyy[pos] = __dmul_rn(wy, yr);
+    P.seg[pos] = 0u;
   }
 }
 
@@ -192,7 +210,7 @@ __global__ void w_l0count(const WideArgs a) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = gw; it < total; it += nw) {
     const uint32_t b = it / per, c = it - b * per;
-    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t ce = min(nl * os, (c + 1) * kChunk);
     uint32_t cnt = 0;
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
@@ -222,7 +240,7 @@ __global__ void __launch_bounds__(NT) w_chunkscan(const WideArgs a, int which) {
   if (which == 1 && s.done) return;
   const uint32_t per = which == 0 ? (nl * a.g.d.order_stride + kChunk - 1) / kChunk
                                   : nchunks_of(s.A, nl);
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   uint32_t carry = 0;
   for (uint32_t base = 0; base < per; base += NT) {
     const uint32_t i = base + threadIdx.x;
@@ -243,7 +261,7 @@ __global__ void w_l0scatter(const WideArgs a) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = gw; it < total; it += nw) {
     const uint32_t b = it / per, c = it - b * per;
-    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t A0 = a.ts[b].A;
     const uint32_t ce = min(nl * os, (c + 1) * kChunk);
     uint32_t run = P.chunk[c];
@@ -262,7 +280,7 @@ __global__ void w_l0scatter(const WideArgs a) {
       const uint32_t mine = __popc(in);
       const uint32_t inc = warp_incl_scan(mine);
       uint32_t o = run + inc - mine - li * A0;
-      uint32_t* out = P.lists[0] + static_cast<size_t>(li) * stride;
+      uint32_t* out = P.lists + static_cast<size_t>(li) * stride;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if ((in >> j) & 1u) out[o++] = inbag_pos(P.bits, P.pref, r4[j]);
@@ -275,13 +293,13 @@ __global__ void w_l0scatter(const WideArgs a) {
 __global__ void w_root(const WideArgs a) {
   __shared__ double st[64];
   const uint32_t b = blockIdx.x;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   TreeState& s = a.ts[b];
   if (s.done) return;
   double sum, sq;
-  root_sums_warp<4>(P.pay[0], P.wyy[0], s.A, sum, sq, st);
+  root_sums_warp<4>(P.pay, P.wyy, s.A, sum, sq, st);
   if (lane_id() == 0) {
-    P.front[0][0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(a.g.d.n), sum, sq};
+    P.front[0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(a.g.d.n), sum, sq};
     P.nf[0] = -1;
     P.nthr[0] = 0.0;
     P.nleft[0] = -1;
@@ -299,8 +317,8 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   const uint32_t b = blockIdx.x;
   TreeState& s = a.ts[b];
   if (s.done) return;
-  const SlotPtrs P = slot_ptrs(a.g, b);
-  const NodeWork* fr = P.front[a.cur];
+  const SlotPtrs P = slot_ptrs(a, b);
+  const NodeWork* fr = P.front;
   const uint32_t F = s.F, A = s.A, m = a.g.mtry, p = a.g.d.p;
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   uint32_t carry = 0;
@@ -343,8 +361,35 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       }
     for (uint32_t i = 0; i < m; ++i) P.samp[static_cast<size_t>(e) * m + i] = pool[i];
   }
+  // eligible nodes by size class, BFS order inside each: [0, E0) small (< kLaneMax
+  // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain)
+  uint32_t base = 0, E0 = 0, E1 = 0;
+  for (uint32_t cls = 0; cls < 3; ++cls) {
+    carry = 0;
+    for (uint32_t b0 = 0; b0 < E; b0 += NT) {
+      const uint32_t e = b0 + threadIdx.x;
+      uint32_t in = 0;
+      if (e < E) {
+        const NodeWork& nw = fr[P.e2f[e]];
+        const uint32_t R = nw.e - nw.b;
+        const uint32_t c = R < kLaneMax ? 0u : (R < a.big_min ? 1u : 2u);
+        in = c == cls;
+      }
+      uint32_t tot;
+      const uint32_t ex = block_excl_scan<NT>(in, sh, &tot);
+      if (in) P.ecls[base + carry + ex] = e;
+      carry += tot;
+    }
+    if (cls == 0) E0 = carry;
+    if (cls == 1) E1 = carry;
+    base += carry;
+  }
   for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
-  if (threadIdx.x == 0) s.E = E;
+  if (threadIdx.x == 0) {
+    s.E = E;
+    s.E0 = E0;
+    s.E1 = E1;
+  }
 }
 
 // exclusive prefixes over trees of this level's work items (one CTA)
@@ -359,8 +404,10 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     uint32_t v0 = 0, v1 = 0, v2 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
-      if (which == 0) {
-        v0 = s.E * a.g.mtry;
+      if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
+        v0 = s.E0 * a.g.mtry;
+        v1 = s.E1 * grp_tasks_per_node(a.g.mtry);
+        v2 = (s.E - s.E0 - s.E1) * a.g.mtry;
       } else {
         v0 = s.S;
         v1 = s.A;
@@ -374,6 +421,8 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     if (b < a.B) {
       if (which == 0) {
         a.off[0][b] = c0 + e0;
+        a.off[1][b] = c1 + e1;
+        a.off[2][b] = c2 + e2;
       } else {
         a.off[1][b] = c0 + e0;
         a.off[2][b] = c1 + e1;
@@ -387,6 +436,8 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   if (threadIdx.x == 0) {
     if (which == 0) {
       a.off[0][a.B] = c0;
+      a.off[1][a.B] = c1;
+      a.off[2][a.B] = c2;
     } else {
       a.off[1][a.B] = c0;
       a.off[2][a.B] = c1;
@@ -395,34 +446,64 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   }
 }
 
-// split chains (forest.hpp:268-297): warps take tasks of nodes >= kLaneMax rows
+// split chains (forest.hpp:268-297), three kernels over the size classes of w_front:
+// big nodes (>= big_min rows) run one warp per (node, column) ...
 template <typename RankT>
 __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
   __shared__ double stage[8][64];
-  const uint32_t total = a.off[0][a.B];
+  const uint32_t total = a.off[2][a.B];
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   for (uint32_t t = gw; t < total; t += nw) {
-    const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
-    const NodeWork nw_ = P.front[a.cur][P.e2f[k / m]];
-    if (nw_.e - nw_.b < kLaneMax) continue;
-    const uint32_t c = P.samp[k];
+    const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const TreeState& st = a.ts[b];
+    const uint32_t e = P.ecls[st.E0 + st.E1 + k / m];
+    const uint32_t slot = e * m + k % m;
+    const NodeWork nw_ = P.front[P.e2f[e]];
+    const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     double bg;
     uint32_t bp;
-    if (li >= 0)
-      chain_warp<RankT, 4>(P.lists[a.cur] + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
-                           P.pay[a.cur], rk_c, nw_.w, nw_.s, bg, bp, stage[warp_id()]);
-    else
-      chain_bin_warp<RankT, 4>(P.pay[a.cur], nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp,
-                               stage[warp_id()]);
-    if (lane_id() == 0) P.res[k] = ChainRes{bg, bp, 0u};
+    chain_warp_p<RankT, 2>(li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride,
+                           nw_.b, nw_.e, P.pay, rk_c, nw_.w, nw_.s, bg, bp, stage[warp_id()]);
+    if (lane_id() == 0) P.res[slot] = ChainRes{bg, bp, 0u};
   }
 }
 
+// ... mid nodes run one warp per node (or per group of 32/G of its columns), G lanes
+// per column (chain_grp) ...
+template <typename RankT, int G, int U>
+__global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
+  __shared__ double stage[8][32 * U];
+  const uint32_t total = a.off[1][a.B];
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const uint32_t tpn = grp_tasks_per_node(m), grp = lane_id() / G;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  for (uint32_t t = gw; t < total; t += nw) {
+    const uint32_t b = owner(a.off[1], a.B, t), k = t - a.off[1][b];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const TreeState& st = a.ts[b];
+    const uint32_t e = P.ecls[st.E0 + k / tpn];
+    const uint32_t j = (k % tpn) * (32 / G) + grp;  // sampled-column index of this group
+    const bool act = j < m;
+    const NodeWork nw_ = P.front[P.e2f[e]];
+    const uint32_t c = act ? P.samp[e * m + j] : 0u;
+    const int32_t li = a.g.d.list_of[c];
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const uint32_t* list = P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride;
+    double bg;
+    uint32_t bp;
+    chain_grp<RankT, G, U>(act, li >= 0, list, nw_.b, nw_.e, P.pay, rk_c, nw_.w, nw_.s,
+                           bg, bp, stage[warp_id()] + grp * G * U);
+    if (act && (lane_id() & (G - 1)) == 0) P.res[e * m + j] = ChainRes{bg, bp, 0u};
+  }
+}
+
+// ... and small nodes (< kLaneMax rows) one lane per chain
 template <typename RankT>
 __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
   const uint32_t total = a.off[0][a.B];
@@ -430,20 +511,21 @@ __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
-    const NodeWork nw_ = P.front[a.cur][P.e2f[k / m]];
-    if (nw_.e - nw_.b >= kLaneMax) continue;
-    const uint32_t c = P.samp[k];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const uint32_t e = P.ecls[k / m];
+    const uint32_t slot = e * m + k % m;
+    const NodeWork nw_ = P.front[P.e2f[e]];
+    const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     double bg;
     uint32_t bp;
     if (li >= 0)
-      chain_lane<RankT>(P.lists[a.cur] + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
-                        P.pay[a.cur], rk_c, nw_.w, nw_.s, bg, bp);
+      chain_lane<RankT>(P.lists + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
+                        P.pay, rk_c, nw_.w, nw_.s, bg, bp);
     else
-      chain_bin_lane<RankT>(P.pay[a.cur], nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp);
-    P.res[k] = ChainRes{bg, bp, 0u};
+      chain_bin_lane<RankT>(P.pay, nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp);
+    P.res[slot] = ChainRes{bg, bp, 0u};
   }
 }
 
@@ -455,11 +537,11 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const uint32_t b = blockIdx.x;
   TreeState& st = a.ts[b];
   if (st.done) return;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const DevData& d = a.g.d;
   const uint32_t n = static_cast<uint32_t>(d.n), m = a.g.mtry, stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(d.rank);
-  const NodeWork* fr = P.front[a.cur];
+  const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
   uint32_t carry = 0, ccarry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
@@ -489,9 +571,9 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
         double prev, v;
         uint32_t lo, hi;
         if (li >= 0) {
-          const uint32_t* lc = P.lists[a.cur] + static_cast<size_t>(li) * stride;
-          const uint32_t r1 = P.pay[a.cur][lc[bp - 1]].row;
-          const uint32_t r0 = P.pay[a.cur][lc[bp]].row;
+          const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
+          const uint32_t r1 = P.pay[lc[bp - 1]].row;
+          const uint32_t r0 = P.pay[lc[bp]].row;
           prev = d.col[static_cast<size_t>(c) * n + r1];
           v = d.col[static_cast<size_t>(c) * n + r0];
           lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
@@ -557,7 +639,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
 // route in column-0 order (forest.hpp:323-352): warps take split nodes >= kLaneMax
 template <typename RankT, bool kWarp>
 __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
-  __shared__ double stage[8][64];
+  __shared__ double stage[8][128];
   const uint32_t total = a.off[1][a.B];
   const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
@@ -566,36 +648,35 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
   const uint32_t id = kWarp ? (blockIdx.x * blockDim.x + threadIdx.x) >> 5
                             : blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t step = kWarp ? (gridDim.x * blockDim.x) >> 5 : gridDim.x * blockDim.x;
-  const uint32_t nxt = a.cur ^ 1u;
   for (uint32_t t = id; t < total; t += step) {
     const uint32_t b = owner(a.off[1], a.B, t), s = t - a.off[1][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SlotPtrs P = slot_ptrs(a, b);
     const SplitInfo si = P.spl[s];
     if (kWarp != (si.cnt >= kLaneMax)) continue;
-    const NodeWork nw = P.front[a.cur][si.f];
+    const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
-    const uint32_t* l0 = list0 >= 0 ? P.lists[a.cur] + static_cast<size_t>(list0) * stride : nullptr;
+    const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
       if (l0)
-        route_warp<RankT, 4>(l0, nw.b, nw.e, P.pay[a.cur], P.wyy[a.cur], rk_f, si.thr_rank,
-                             P.bits, o, stage[warp_id()]);
+        route_warp_p<RankT, 2>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
+                               P.bits, o, stage[warp_id()]);
       else
-        route_groups_warp<RankT, 4>(P.pay[a.cur], P.wyy[a.cur], nw.b, nw.e, rank, k0levels,
+        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels,
                                     rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
       if (lane_id() != 0) continue;
     } else {
       if (l0)
-        route_lane<RankT>(l0, nw.b, nw.e, P.pay[a.cur], P.wyy[a.cur], rk_f, si.thr_rank, P.bits, o);
+        route_lane<RankT>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank, P.bits, o);
       else
-        route_groups_lane<RankT>(P.pay[a.cur], P.wyy[a.cur], nw.b, nw.e, rank, k0levels, rk_f,
+        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels, rk_f,
                                  si.thr_rank, P.bits, o);
     }
     P.spl[s].nl = o.nl;
     const uint32_t child = static_cast<uint32_t>(P.nleft[nw.id]);
-    P.front[nxt][2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
+    P.front_n[2 * s] = NodeWork{si.base, si.base + o.nl, child, 0u,
                                    static_cast<double>(o.wl), o.sl, o.ql};
-    P.front[nxt][2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
+    P.front_n[2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
                                        static_cast<double>(o.wr), o.sr, o.qr};
   }
 }
@@ -608,8 +689,8 @@ __global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
   const uint32_t b = blockIdx.x;
   TreeState& st = a.ts[b];
   if (st.done) return;
-  const SlotPtrs P = slot_ptrs(a.g, b);
-  const NodeWork* fr = P.front[a.cur];
+  const SlotPtrs P = slot_ptrs(a, b);
+  const NodeWork* fr = P.front;
   const uint32_t S = st.S, A = st.A;
   uint32_t carry = 0;
   for (uint32_t base = 0; base < S; base += NT) {
@@ -644,11 +725,10 @@ __global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
 // payload pass over flattened (tree, position) + per-position segment offsets
 __global__ void w_pay(const WideArgs a) {
   const uint32_t total = a.off[2][a.B];
-  const uint32_t nxt = a.cur ^ 1u;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
-    const uint32_t f = P.seg[a.cur][k];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const uint32_t f = P.seg[k];
     const SegTab tb = P.segtab[f];
     P.off2[k] = make_int2(tb.offL, tb.offR);
     if (tb.offL == INT_MIN) continue;
@@ -656,66 +736,114 @@ __global__ void w_pay(const WideArgs a) {
     const int32_t lp = static_cast<int32_t>(bits_before(P.bits, P.pref, k));
     const uint32_t dst =
         static_cast<uint32_t>(l ? tb.offL + lp : tb.offR + static_cast<int32_t>(k) - lp);
-    P.pay[nxt][dst] = P.pay[a.cur][k];
-    P.wyy[nxt][dst] = P.wyy[a.cur][k];
-    P.seg[nxt][dst] = tb.child + (l ? 0u : 1u);
+    P.pay_n[dst] = P.pay[k];
+    P.wyy_n[dst] = P.wyy[k];
+    P.seg_n[dst] = tb.child + (l ? 0u : 1u);
   }
 }
 
-// List pass with the tree's goes-left bitmap + prefix staged in shared memory: one CTA
-// per tree streams all of that tree's chunks (phase 1 counts, phase 3 scatter), so the
-// two random lookups per entry hit shared memory instead of L2.
-template <int NT, bool kScatter>
-__global__ void __launch_bounds__(NT) w_ltree(const WideArgs a) {
+// List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix in
+// shared memory and one warp per sorted list.  A warp walks its list in position order,
+// 256 positions per step (8 per lane), so the count of left-going entries before each
+// entry is the warp's running carry plus a warp scan -- no count pass, no chunk scan.
+// The (offL, offR) of each position's segment come from off2 (shared by all lists, so
+// the CTA's warps hit it in L1/L2) or, when a step lies inside one segment, from that
+// segment alone.  The next step's entries and offsets are loaded before this step's
+// are scattered.
+constexpr uint32_t kLwStep = 256;
+constexpr int kLwWarps = 28;
+constexpr bool kLwUniProbe = false;  // warps per list-pass CTA (<= 73 registers per thread)
+struct LwStage {
+  uint32_t q[8];
+  int2 t[8];
+};
+
+__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
+                                        const uint32_t* seg, const int2* off2) {
+  const uint32_t kb = k0 + lane_id() * 8;
+  // one segment for the whole step?  (AIWC_LW_UNI: probe seg first; the probe makes the
+  // offsets' loads wait for it, so by default every position's offsets are loaded)
+  bool uni = false;
+  if (kLwUniProbe) {
+    const uint32_t klast = min(k0 + kLwStep, A) - 1;
+    uni = k0 < A && seg[k0] == seg[klast];
+  }
+  if (kb < A) {
+    const uint4 x0 = *reinterpret_cast<const uint4*>(list + kb);
+    const uint4 x1 = *reinterpret_cast<const uint4*>(list + kb + 4);
+    v.q[0] = x0.x; v.q[1] = x0.y; v.q[2] = x0.z; v.q[3] = x0.w;
+    v.q[4] = x1.x; v.q[5] = x1.y; v.q[6] = x1.z; v.q[7] = x1.w;
+    if (uni) {
+      const int2 u = off2[k0];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v.t[j] = u;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const int4 y = *reinterpret_cast<const int4*>(off2 + kb + j);
+        v.t[j] = make_int2(y.x, y.y);
+        v.t[j + 1] = make_int2(y.z, y.w);
+      }
+    }
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   extern __shared__ uint32_t sm[];
   const uint32_t b = blockIdx.x;
   const TreeState& st = a.ts[b];
   if (st.done) return;
-  const SlotPtrs P = slot_ptrs(a.g, b);
-  const uint32_t A = st.A, A16 = (A + 15u) & ~15u, aw = (A + 31u) / 32u;
-  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride, totL = st.totL;
+  const SlotPtrs P = slot_ptrs(a, b);
+  const uint32_t A = st.A, aw = (A + 31u) / 32u;
+  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
   uint32_t* sbits = sm;
   uint32_t* spref = sm + aw;
-  for (uint32_t w = threadIdx.x; w < aw; w += NT) {
+  for (uint32_t w = threadIdx.x; w < aw; w += blockDim.x) {
     sbits[w] = P.bits[w];
     spref[w] = P.pref[w];
   }
   __syncthreads();
-  const uint32_t nchunk = nchunks_of(A, nl), nxt = a.cur ^ 1u;
-  for (uint32_t c = warp_id(); c < nchunk; c += NT / 32) {
-    const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
-    int2 u;
-    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
-    uint32_t run = kScatter ? P.chunk[c] : 0u;
-#pragma unroll 2
-    for (uint32_t s = c * kChunk; s < ce; s += 128) {
-      ListQuad v;
-      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
-                uni ? &u : nullptr);
-      const uint32_t lf = side_quad(v, sbits, spref);
-      const uint32_t mine = __popc(lf);
-      if (!kScatter) {
-        run += mine;
-        continue;
-      }
-      const uint32_t inc = warp_incl_scan(mine);
-      int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
-      uint32_t* dstl = P.lists[nxt] + static_cast<size_t>(v.li) * stride;
+  const unsigned lane = lane_id();
+  for (uint32_t li = warp_id(); li < nl; li += blockDim.x >> 5) {
+    const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
+    uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
+    uint32_t carry = 0;  // left-going entries of this list before the step
+    LwStage cur, nxt;
+    lw_load(cur, 0, A, src, P.seg, P.off2);
+    for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
+      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.seg, P.off2);
+      const uint32_t kb = k0 + lane * 8;
+      uint32_t lf = 0, keep = 0;
+      if (kb < A) {
+        const uint32_t lim = A - kb;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (!((v.keep >> j) & 1u)) continue;
-        const bool l = (lf >> j) & 1u;
-        const int32_t off = static_cast<int32_t>(v.f[j]);
-        const uint32_t dst =
-            static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(v.k0 + j) - pl);
-        pl += l ? 1 : 0;
-        dstl[dst] = v.q[j];
+        for (int j = 0; j < 8; ++j) {
+          const int2 t = cur.t[j];
+          if (static_cast<uint32_t>(j) >= lim || t.x == INT_MIN) continue;
+          keep |= 1u << j;
+          const uint32_t qq = cur.q[j];
+          const uint32_t w = sbits[qq >> 5];
+          const uint32_t bit = (w >> (qq & 31u)) & 1u;
+          const int32_t lq = static_cast<int32_t>(spref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u)));
+          lf |= bit << j;
+          cur.q[j] = static_cast<uint32_t>(bit ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
+        }
       }
-      run += __shfl_sync(kFull, inc, 31);
-    }
-    if (!kScatter) {
-      run = warp_sum(run);
-      if (lane_id() == 0) P.chunk[c] = run;
+      const uint32_t mine = __popc(lf);
+      const uint32_t inc = warp_incl_scan(mine);
+      int32_t pl = static_cast<int32_t>(carry + inc - mine);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!((keep >> j) & 1u)) continue;
+        const bool l = (lf >> j) & 1u;
+        const int32_t off = l ? cur.t[j].x : cur.t[j].y;
+        const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(kb + j) - pl);
+        pl += l ? 1 : 0;
+        dstl[dst] = cur.q[j];
+      }
+      carry += __shfl_sync(kFull, inc, 31);
+      cur = nxt;
     }
   }
 }
@@ -727,16 +855,16 @@ __global__ void w_lcount(const WideArgs a) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = gw; it < total; it += nw) {
     const uint32_t b = owner(a.off[3], a.B, it), c = it - a.off[3][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t A = a.ts[b].A, A16 = (A + 15u) & ~15u;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
     int2 u;
-    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
+    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg, P.off2, u);
     uint32_t cnt = 0;
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
       ListQuad v;
-      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.off2,
                 uni ? &u : nullptr);
       cnt += __popc(side_quad(v, P.bits, P.pref));
     }
@@ -749,27 +877,26 @@ __global__ void w_lcount(const WideArgs a) {
 __global__ void w_lscatter(const WideArgs a) {
   const uint32_t total = a.off[3][a.B];
   const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
-  const uint32_t nxt = a.cur ^ 1u;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t it = gw; it < total; it += nw) {
     const uint32_t b = owner(a.off[3], a.B, it), c = it - a.off[3][b];
-    const SlotPtrs P = slot_ptrs(a.g, b);
+    const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
     const uint32_t A = st.A, A16 = (A + 15u) & ~15u, totL = st.totL;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
     int2 u;
-    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg[a.cur], P.off2, u);
+    const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg, P.off2, u);
     uint32_t run = P.chunk[c];
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
       ListQuad v;
-      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists[a.cur], P.off2,
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.off2,
                 uni ? &u : nullptr);
       const uint32_t lf = side_quad(v, P.bits, P.pref);
       const uint32_t mine = __popc(lf);
       const uint32_t inc = warp_incl_scan(mine);
       int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
-      uint32_t* dstl = P.lists[nxt] + static_cast<size_t>(v.li) * stride;
+      uint32_t* dstl = P.lists_n + static_cast<size_t>(v.li) * stride;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (!((v.keep >> j) & 1u)) continue;
@@ -799,7 +926,7 @@ __global__ void w_advance(const WideArgs a) {
 __global__ void w_emit(const WideArgs a) {
   __shared__ unsigned long long s_off;
   const uint32_t b = blockIdx.x, tl = a.t0 + b;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const TreeState& st = a.ts[b];
   const uint32_t count = st.nodes;
   if (threadIdx.x == 0) {
@@ -825,7 +952,7 @@ __global__ void w_emit(const WideArgs a) {
 template <typename RankT>
 __global__ void w_oob(const WideArgs a) {
   const uint32_t b = blockIdx.y, tl = a.t0 + b;
-  const SlotPtrs P = slot_ptrs(a.g, b);
+  const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   double* ov = a.g.oobval + static_cast<size_t>(tl) * n;
@@ -850,19 +977,18 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const dim3 rowsgrid((n + 1023) / 1024, a.B);
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
   // per-tree list pass with the bitmap + prefix in shared memory when they fit
-  size_t ltree_smem = (a.g.L.stride + 31) / 32 * 8;
+  size_t lw_smem = (a.g.L.stride + 31) / 32 * 8;
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (ltree_smem + 1024 > static_cast<size_t>(optin) ||
-        cudaFuncSetAttribute(w_ltree<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ltree_smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(w_ltree<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(ltree_smem)) != cudaSuccess)
-      ltree_smem = 0;
+    if (lw_smem + 1024 > static_cast<size_t>(optin) ||
+        cudaFuncSetAttribute(w_lwarp<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(lw_smem)) != cudaSuccess)
+      lw_smem = 0;
     cudaGetLastError();
   }
+  const int lw_warps = static_cast<int>(std::min<uint32_t>(kLwWarps, std::max<uint32_t>(1u, a.g.d.nlisted)));
 #define WCK(x)                              \
   do {                                      \
     x;                                      \
@@ -885,6 +1011,14 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
     WCK((w_chains_warp<RankT><<<wgrid, 256, 0, st>>>(a)));
+    switch (grp_width(a.g.mtry)) {
+      case 32: WCK((w_chains_grp<RankT, 32, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      case 16: WCK((w_chains_grp<RankT, 16, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      case 8: WCK((w_chains_grp<RankT, 8, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      case 4: WCK((w_chains_grp<RankT, 4, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      case 2: WCK((w_chains_grp<RankT, 2, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      default: WCK((w_chains_grp<RankT, 1, 4><<<wgrid, 256, 0, st>>>(a))); break;
+    }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
@@ -898,10 +1032,8 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
     if (a.g.d.nlisted) {
-      if (ltree_smem) {
-        WCK((w_ltree<1024, false><<<a.B, 1024, ltree_smem, st>>>(a)));
-        WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
-        WCK((w_ltree<1024, true><<<a.B, 1024, ltree_smem, st>>>(a)));
+      if (lw_smem) {
+        WCK((w_lwarp<kLwWarps><<<a.B, lw_warps * 32, lw_smem, st>>>(a)));
       } else {
         WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
         WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));

@@ -230,3 +230,31 @@ def test_both_growers_bit_exact(path, seed, golden, monkeypatch):
         g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"],
                       z["value"], inbag=z["inbag"])
         assert forests_equal(g, soa_of(f)) is None
+
+
+def test_wide_grower_random_tables(seed, monkeypatch):
+    """The wide grower's chain kernels (lane / lane-group / warp per chain) on random
+    tables mixing continuous, tied and two-level columns, over the whole mtry range
+    (group widths 32..1 and several groups per node when mtry > 32)."""
+    monkeypatch.setenv("AIWC_GROW_WIDE", "1")
+    rng = np.random.default_rng(1811)
+    cases = [(1, 1), (2, 2), (5, 3), (9, 8), (20, 16), (40, 33), (70, 64), (34, 6)]
+    for case, (p, m) in enumerate(cases):
+        n = int(rng.integers(300, 2500))
+        kinds = rng.integers(0, 3, size=p)
+        col = np.empty((p, n))
+        for c in range(p):
+            if kinds[c] == 0:
+                col[c] = rng.normal(size=n)
+            elif kinds[c] == 1:
+                col[c] = rng.integers(0, 7, size=n).astype(float)
+            else:
+                col[c] = rng.integers(0, 2, size=n).astype(float)
+        y = rng.normal(size=n)
+        T, mns = 6, int(rng.integers(1, 6))
+        for big_min in ("64", "1000000"):
+            monkeypatch.setenv("AIWC_BIG_MIN", big_min)
+            prep = pkg.PreparedDataset(col, y, n, p)
+            f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
+            o = Oracle.fit(col, y, n, p, T, m, mns, seed)
+            assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min)

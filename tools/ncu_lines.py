@@ -9,7 +9,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kn = sys.argv[3] if len(sys.argv) > 3 else None
+out = subprocess.run(["ncu", "-i", rep] + (["--kernel-name", "regex:" + kn, "--launch-count", "1"] if kn else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 cur_file, hdr, lines = None, None, []
