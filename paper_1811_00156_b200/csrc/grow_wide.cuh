@@ -742,48 +742,31 @@ __global__ void w_pay(const WideArgs a) {
   }
 }
 
-// List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix in
-// shared memory and one warp per sorted list.  A warp walks its list in position order,
-// 256 positions per step (8 per lane), so the count of left-going entries before each
-// entry is the warp's running carry plus a warp scan -- no count pass, no chunk scan.
-// The (offL, offR) of each position's segment come from off2 (shared by all lists, so
-// the CTA's warps hit it in L1/L2) or, when a step lies inside one segment, from that
-// segment alone.  The next step's entries and offsets are loaded before this step's
-// are scattered.
+// List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
+// staged in shared memory and one warp per sorted list.  A warp walks its list in
+// position order, 256 positions per step as 8 sub-rows of 32 consecutive positions
+// (lane i holds position k0 + 32j + i of sub-row j), so the count of left-going entries
+// before each entry is the warp's running carry plus ballot counts -- no count pass --
+// and each sub-row's left (right) entries land on consecutive destinations: every
+// store instruction writes at most two contiguous runs.  The next step's entries and
+// segment offsets are loaded before this step is scattered.
 constexpr uint32_t kLwStep = 256;
-constexpr int kLwWarps = 28;
-constexpr bool kLwUniProbe = false;  // warps per list-pass CTA (<= 73 registers per thread)
+constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
 struct LwStage {
   uint32_t q[8];
   int2 t[8];
 };
 
 __device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
-                                        const uint32_t* seg, const int2* off2) {
-  const uint32_t kb = k0 + lane_id() * 8;
-  // one segment for the whole step?  (AIWC_LW_UNI: probe seg first; the probe makes the
-  // offsets' loads wait for it, so by default every position's offsets are loaded)
-  bool uni = false;
-  if (kLwUniProbe) {
-    const uint32_t klast = min(k0 + kLwStep, A) - 1;
-    uni = k0 < A && seg[k0] == seg[klast];
-  }
-  if (kb < A) {
-    const uint4 x0 = *reinterpret_cast<const uint4*>(list + kb);
-    const uint4 x1 = *reinterpret_cast<const uint4*>(list + kb + 4);
-    v.q[0] = x0.x; v.q[1] = x0.y; v.q[2] = x0.z; v.q[3] = x0.w;
-    v.q[4] = x1.x; v.q[5] = x1.y; v.q[6] = x1.z; v.q[7] = x1.w;
-    if (uni) {
-      const int2 u = off2[k0];
+                                        const int2* off2) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v.t[j] = u;
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t k = k0 + 32u * j + lane_id();
+    if (k < A) {
+      v.q[j] = list[k];
+      v.t[j] = off2[k];
     } else {
-#pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const int4 y = *reinterpret_cast<const int4*>(off2 + kb + j);
-        v.t[j] = make_int2(y.x, y.y);
-        v.t[j + 1] = make_int2(y.z, y.w);
-      }
+      v.t[j] = make_int2(INT_MIN, 0);
     }
   }
 }
@@ -798,51 +781,54 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   const uint32_t A = st.A, aw = (A + 31u) / 32u;
   const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
   uint32_t* sbits = sm;
-  uint32_t* spref = sm + aw;
-  for (uint32_t w = threadIdx.x; w < aw; w += blockDim.x) {
-    sbits[w] = P.bits[w];
-    spref[w] = P.pref[w];
+  uint32_t* spref = sm + (aw + 3u) / 4u * 4u;
+  {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
+    const uint32_t aw4 = (aw + 3u) / 4u;
+    const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
+    const uint4* gp = reinterpret_cast<const uint4*>(P.pref);
+    for (uint32_t w = threadIdx.x; w < aw4; w += blockDim.x) {
+      const uint4 x = gb[w], y = gp[w];
+      sbits[4 * w] = x.x; sbits[4 * w + 1] = x.y; sbits[4 * w + 2] = x.z; sbits[4 * w + 3] = x.w;
+      spref[4 * w] = y.x; spref[4 * w + 1] = y.y; spref[4 * w + 2] = y.z; spref[4 * w + 3] = y.w;
+    }
   }
   __syncthreads();
-  const unsigned lane = lane_id();
+  const unsigned lane = lane_id(), lt = lanemask_lt();
   for (uint32_t li = warp_id(); li < nl; li += blockDim.x >> 5) {
     const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
     uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
-    uint32_t carry = 0;  // left-going entries of this list before the step
+    uint32_t carry = 0;  // left-going entries of this list before the sub-row
     LwStage cur, nxt;
-    lw_load(cur, 0, A, src, P.seg, P.off2);
+    lw_load(cur, 0, A, src, P.off2);
     for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
-      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.seg, P.off2);
-      const uint32_t kb = k0 + lane * 8;
-      uint32_t lf = 0, keep = 0;
-      if (kb < A) {
-        const uint32_t lim = A - kb;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int2 t = cur.t[j];
-          if (static_cast<uint32_t>(j) >= lim || t.x == INT_MIN) continue;
-          keep |= 1u << j;
-          const uint32_t qq = cur.q[j];
-          const uint32_t w = sbits[qq >> 5];
-          const uint32_t bit = (w >> (qq & 31u)) & 1u;
-          const int32_t lq = static_cast<int32_t>(spref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u)));
-          lf |= bit << j;
-          cur.q[j] = static_cast<uint32_t>(bit ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
-        }
-      }
-      const uint32_t mine = __popc(lf);
-      const uint32_t inc = warp_incl_scan(mine);
-      int32_t pl = static_cast<int32_t>(carry + inc - mine);
+      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
+      // all 16 shared-memory lookups of the lane first (branch-free), then the scatter
+      uint32_t wv[8], pv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (!((keep >> j) & 1u)) continue;
-        const bool l = (lf >> j) & 1u;
-        const int32_t off = l ? cur.t[j].x : cur.t[j].y;
-        const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(kb + j) - pl);
-        pl += l ? 1 : 0;
-        dstl[dst] = cur.q[j];
+        const uint32_t wi = cur.t[j].x != INT_MIN ? cur.q[j] >> 5 : 0u;
+        wv[j] = sbits[wi];
+        pv[j] = spref[wi];
       }
-      carry += __shfl_sync(kFull, inc, 31);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int2 t = cur.t[j];
+        const bool keep = t.x != INT_MIN;
+        const uint32_t qq = cur.q[j];
+        const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
+        const bool l = keep && bit;
+        const unsigned bl = __ballot_sync(kFull, l);
+        const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
+        if (keep) {
+          const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
+          const uint32_t k = k0 + 32u * j + lane;
+          const uint32_t nq = static_cast<uint32_t>(l ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
+          const uint32_t dst =
+              static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
+          dstl[dst] = nq;
+        }
+        carry += __popc(bl);
+      }
       cur = nxt;
     }
   }
@@ -977,7 +963,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const dim3 rowsgrid((n + 1023) / 1024, a.B);
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
   // per-tree list pass with the bitmap + prefix in shared memory when they fit
-  size_t lw_smem = (a.g.L.stride + 31) / 32 * 8;
+  size_t lw_smem = ((a.g.L.stride + 31) / 32 + 3) / 4 * 4 * 8;
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
