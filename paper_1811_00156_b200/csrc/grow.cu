@@ -328,15 +328,26 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
       }
     }
   };
+  // 3-stage pipeline: tile i is scanned while the rank gathers of tile i+1, the payload
+  // gathers of tile i+2 and the list loads of tile i+3 are in flight
+  auto load_r = [&](uint32_t k0, const uint32_t (&row)[G], uint32_t (&rk)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      rk[g] = k0 + g * 32 + lane < e ? rank_of(rk_c, row[g]) : 0u;
+  };
+  uint32_t rk[G], rkn[G];
   load_q(b, qn);
   load_p(b, qn, rowc, muc, wyc);
   load_q(b + 32 * G, qn);
+  load_p(b + 32 * G, qn, rown, mun, wyn);
+  load_q(b + 64 * G, qn);
+  load_r(b, rowc, rk);
   for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
-    uint32_t rk[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) rk[g] = k0 + g * 32 + lane < e ? rank_of(rk_c, rowc[g]) : 0u;
-    load_p(k0 + 32 * G, qn, rown, mun, wyn);
-    load_q(k0 + 64 * G, qn);
+    load_r(k0 + 32 * G, rown, rkn);
+    uint32_t rownn[G], munn[G];
+    double wynn[G];
+    load_p(k0 + 64 * G, qn, rownn, munn, wynn);
+    load_q(k0 + 96 * G, qn);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t t0 = k0 + g * 32;
@@ -374,9 +385,12 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      rowc[g] = rown[g];
       muc[g] = mun[g];
       wyc[g] = wyn[g];
+      rk[g] = rkn[g];
+      rown[g] = rownn[g];
+      mun[g] = munn[g];
+      wyn[g] = wynn[g];
     }
   }
   if (listed) {
@@ -578,24 +592,33 @@ __device__ __forceinline__ void chain_grp(bool active, bool listed, const uint32
       }
     }
   };
+  // 3-stage pipeline: round i is summed while the rank gathers of round i+1, the
+  // payload gathers of round i+2 and the list loads of round i+3 are in flight
+  auto load_r = [&](uint32_t kb, const uint32_t (&row)[U], uint32_t (&rk)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t k = kb + u;
+      rk[u] = (active && k >= b && k < e) ? rank_of(rk_c, row[u]) : 0u;
+    }
+  };
   uint32_t k0 = b & ~3u;
-  uint32_t qn[U], rowc[U], muc[U], rown[U], mun[U];
+  uint32_t qn[U], rowc[U], muc[U], rown[U], mun[U], rk[U], rkn[U];
   double wyc[U], wyn[U];
   load_q(k0 + gl * U, qn);
   load_p(k0 + gl * U, qn, rowc, muc, wyc);
   load_q(k0 + R + gl * U, qn);
+  load_p(k0 + R + gl * U, qn, rown, mun, wyn);
+  load_q(k0 + 2 * R + gl * U, qn);
+  load_r(k0 + gl * U, rowc, rk);
   for (; k0 < e; k0 += R) {
     const uint32_t kb = k0 + gl * U;
-    uint32_t rk[U], mu[U];
+    uint32_t mu[U];
     double a[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t k = kb + u;
-      rk[u] = (active && k >= b && k < e) ? rank_of(rk_c, rowc[u]) : 0u;
-    }
-    // prefetch: payload of round i+1, list of round i+2
-    load_p(kb + R, qn, rown, mun, wyn);
-    load_q(kb + 2 * R, qn);
+    load_r(kb + R, rown, rkn);
+    uint32_t rownn[U], munn[U];
+    double wynn[U];
+    load_p(kb + 2 * R, qn, rownn, munn, wynn);
+    load_q(kb + 3 * R, qn);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       mu[u] = muc[u];
@@ -658,9 +681,12 @@ __device__ __forceinline__ void chain_grp(bool active, bool listed, const uint32
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      rowc[u] = rown[u];
       muc[u] = mun[u];
       wyc[u] = wyn[u];
+      rk[u] = rkn[u];
+      rown[u] = rownn[u];
+      mun[u] = munn[u];
+      wyn[u] = wynn[u];
     }
   }
 #pragma unroll
@@ -787,22 +813,33 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
       }
     }
   };
+  // 3-stage pipeline: tile i is summed while the rank gathers of tile i+1, the payload
+  // gathers of tile i+2 and the list loads of tile i+3 are in flight
+  // (raw ranks are kept and compared at use, so the gathers never stall the issue)
+  auto load_s = [&](uint32_t k0, const uint32_t (&row)[G], uint32_t (&rk)[G]) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      rk[g] = (k0 + g * 32 + lane < e) ? rank_of(rk_f, row[g]) : 0xffffffffu;
+  };
+  uint32_t qnn[G];
+  uint32_t lft[G], lftn[G];
   load_q(b, qc);
   load_p(b, qc, rowc, muc, wyc, yyc);
   load_q(b + 32 * G, qn);
+  load_p(b + 32 * G, qn, rown, mun, wyn, yyn);
+  load_q(b + 64 * G, qnn);
+  load_s(b, rowc, lft);
   for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
-    bool lft[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      lft[g] = (k0 + g * 32 + lane < e) && rank_of(rk_f, rowc[g]) <= thr_rank;
-    uint32_t qnn[G];
-    load_p(k0 + 32 * G, qn, rown, mun, wyn, yyn);
-    load_q(k0 + 64 * G, qnn);
+    load_s(k0 + 32 * G, rown, lftn);
+    uint32_t rownn[G], munn[G], qnnn[G];
+    double wynn[G], yynn[G];
+    load_p(k0 + 64 * G, qnn, rownn, munn, wynn, yynn);
+    load_q(k0 + 96 * G, qnnn);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t t0 = k0 + g * 32;
       const bool valid = t0 + lane < e;
-      const bool left = lft[g];
+      const bool left = lft[g] <= thr_rank;
       if (left) atomicOr(bits + (qc[g] >> 5), 1u << (qc[g] & 31u));
       o.nl += __popc(__ballot_sync(kFull, left));
       o.wl += warp_sum(left ? muc[g] : 0u);
@@ -823,10 +860,15 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
     for (int g = 0; g < G; ++g) {
       qc[g] = qn[g];
       qn[g] = qnn[g];
-      rowc[g] = rown[g];
+      qnn[g] = qnnn[g];
       muc[g] = mun[g];
       wyc[g] = wyn[g];
       yyc[g] = yyn[g];
+      lft[g] = lftn[g];
+      rown[g] = rownn[g];
+      mun[g] = munn[g];
+      wyn[g] = wynn[g];
+      yyn[g] = yynn[g];
     }
   }
   o.sl = __shfl_sync(kFull, acc, 0);

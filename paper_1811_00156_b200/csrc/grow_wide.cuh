@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     if (kWarp != (si.cnt >= kLaneMax)) continue;
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
