@@ -224,6 +224,8 @@ struct aiwc_forest {
   uint32_t bin_p = 0, bin_bytes = 1;
   std::vector<Chunk> chunks;
   DevBuf<BinNode> bnodes;
+  DevBuf<uint32_t> bnodes4;  // packed 4-byte nodes (node_bytes == 4)
+  int node_bytes = 8;
   DevBuf<double> bleaves, bthr;
   DevBuf<uint32_t> broots, bthr_off;
 };
@@ -914,9 +916,12 @@ void build_binned(aiwc_forest* f, uint32_t p) {
   }
   if (maxT >= 0xffff) return;
   f->bin_bytes = maxT < 0xff ? 1 : 2;
-  const size_t tile = size_t{kPredNT} * p * f->bin_bytes;
+  const size_t tile = size_t{kPredNT} * kPredictQ * p * f->bin_bytes;
   if (tile + 4096 > kPredSmem) return;
   const size_t budget = kPredSmem - tile - 64;
+  // packed 4-byte nodes: column < 127, bin < 256, chunk-relative indices < 2^17
+  const bool node4 = p < 127 && maxT <= 256 && std::getenv("AIWC_PRED_NODE8") == nullptr;
+  const size_t nb = node4 ? 4 : sizeof(BinNode);
   std::vector<double> thr_all;
   for (auto& v : T) thr_all.insert(thr_all.end(), v.begin(), v.end());
   std::vector<BinNode> nodes;
@@ -928,12 +933,12 @@ void build_binned(aiwc_forest* f, uint32_t p) {
     const uint64_t b = f->off[t], e = f->off[t + 1];
     uint32_t nl = 0;
     for (uint64_t i = b; i < e; ++i) nl += fe[i] < 0;
-    const size_t need = (ch.nnodes + (e - b)) * sizeof(BinNode) + 16 + (ch.nleaves + nl) * 8;
+    const size_t need = (ch.nnodes + (e - b)) * nb + 16 + (ch.nleaves + nl) * 8;
     if (ch.ntrees > 0 && need > budget) {
       f->chunks.push_back(ch);
       ch = aiwc_forest::Chunk{nodes.size(), leaves.size(), roots.size(), 0, 0, 0};
     }
-    if ((e - b) * sizeof(BinNode) + 16 + nl * 8 > budget) return;  // one tree too big
+    if ((e - b) * nb + 16 + nl * 8 > budget) return;  // one tree too big
     roots.push_back(ch.nnodes);
     for (uint64_t i = b; i < e; ++i) {
       const uint32_t local = static_cast<uint32_t>(i - b) + ch.nnodes;
@@ -953,6 +958,24 @@ void build_binned(aiwc_forest* f, uint32_t p) {
     ++ch.ntrees;
   }
   f->chunks.push_back(ch);
+  f->node_bytes = 8;
+  if (node4) {
+    std::vector<uint32_t> n4(nodes.size());
+    bool ok = true;
+    for (size_t i = 0; i < nodes.size(); ++i) {
+      const BinNode& v = nodes[i];
+      if (v.child >= (1u << 17)) ok = false;
+      n4[i] = v.feat == 0xffff ? (127u | (v.child << 15))
+                               : (v.feat | (uint32_t{v.j} << 7) | (v.child << 15));
+    }
+    if (ok) {
+      f->node_bytes = 4;
+      f->bnodes4.alloc(n4.size());
+      CK(cudaMemcpy(f->bnodes4.p, n4.data(), n4.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  if (f->node_bytes == 4 && !node4) return;
+  if (node4 && f->node_bytes != 4) return;  // packed chunks were sized for 4-byte nodes
   f->bnodes.alloc(nodes.size());
   f->bleaves.alloc(leaves.size());
   f->broots.alloc(roots.size());
@@ -976,12 +999,15 @@ void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device));
   CK(launch_bin_queries(f->bin_bytes, d_rows, q, p, f->bthr.p, f->bthr_off.p, bins.p, s));
   g_launches += 1;
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(sms, (q + kPredNT - 1) / kPredNT));
+  const uint64_t tq = uint64_t{kPredNT} * kPredictQ;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(sms, (q + tq - 1) / tq));
   for (size_t k = 0; k < f->chunks.size(); ++k) {
     const auto& ch = f->chunks[k];
-    const size_t smem = ((ch.nnodes * sizeof(BinNode) + 15) & ~size_t{15}) + ch.nleaves * 8 +
-                        size_t{kPredNT} * p * bb;
-    CK(launch_predict_chunk(f->bin_bytes, f->bnodes.p + ch.node0, ch.nnodes,
+    const size_t smem = ((size_t{ch.nnodes} * f->node_bytes + 15) & ~size_t{15}) +
+                        ch.nleaves * 8 + size_t{kPredNT} * kPredictQ * p * bb;
+    const void* nodes = f->node_bytes == 4 ? static_cast<const void*>(f->bnodes4.p + ch.node0)
+                                           : static_cast<const void*>(f->bnodes.p + ch.node0);
+    CK(launch_predict_chunk(f->bin_bytes, f->node_bytes, nodes, ch.nnodes,
                             f->bleaves.p + ch.leaf0, ch.nleaves, f->broots.p + ch.root0, ch.ntrees,
                             bins.p, q, p, sum.p, k == 0, k + 1 == f->chunks.size(),
                             static_cast<double>(f->trees), d_out, grid, smem, kPredSmem, s));

@@ -127,42 +127,99 @@ __global__ void bin_queries_kernel(const double* __restrict__ rows, uint64_t q, 
   }
 }
 
+// Node accessors: 8-byte BinNode, or the packed 4-byte form (bits 0-6 column, 127 =
+// leaf; bits 7-14 threshold bin; bits 15-31 chunk-relative left child / leaf index)
+// used when the schema and the chunk are small enough -- half the shared-memory
+// wavefronts per visit and twice the trees per chunk.
+struct Node8 {
+  using T = BinNode;
+  static __device__ __forceinline__ bool leaf(const BinNode& v) { return v.feat == 0xffffu; }
+  static __device__ __forceinline__ uint32_t feat(const BinNode& v) { return v.feat; }
+  static __device__ __forceinline__ uint32_t j(const BinNode& v) { return v.j; }
+  static __device__ __forceinline__ uint32_t child(const BinNode& v) { return v.child; }
+};
+struct Node4 {
+  using T = uint32_t;
+  static __device__ __forceinline__ bool leaf(uint32_t v) { return (v & 127u) == 127u; }
+  static __device__ __forceinline__ uint32_t feat(uint32_t v) { return v & 127u; }
+  static __device__ __forceinline__ uint32_t j(uint32_t v) { return (v >> 7) & 255u; }
+  static __device__ __forceinline__ uint32_t child(uint32_t v) { return v >> 15; }
+};
+
 // One launch per tree chunk: the chunk's nodes and leaf values sit in shared memory,
 // every query walks the chunk's trees in order, continuing its running sum from the
 // previous chunk (so the per-query sum keeps the reference's tree order exactly).
-template <typename BinT, int NT>
+// A tile holds Q*NT queries; thread t walks queries t, t+NT, ... of it as Q independent
+// node chains, so their shared-memory latencies overlap.
+template <typename BinT, typename NA, int NT, int Q>
 __global__ void __launch_bounds__(NT, 1)
-    predict_chunk_kernel(const BinNode* __restrict__ nodes, uint32_t nnodes,
+    predict_chunk_kernel(const typename NA::T* __restrict__ nodes, uint32_t nnodes,
                          const double* __restrict__ leaves, uint32_t nleaves,
                          const uint32_t* __restrict__ roots, uint32_t ntrees,
                          const BinT* __restrict__ bins, uint64_t q, uint32_t p,
                          double* __restrict__ sum, int first, int last, double total_trees,
                          double* __restrict__ out) {
+  using NodeT = typename NA::T;
+  constexpr uint32_t TQ = NT * Q;
   extern __shared__ __align__(16) unsigned char smem[];
-  BinNode* sn = reinterpret_cast<BinNode*>(smem);
-  double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(BinNode) + 15) & ~size_t{15}));
+  NodeT* sn = reinterpret_cast<NodeT*>(smem);
+  double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(NodeT) + 15) & ~size_t{15}));
   BinT* sb = reinterpret_cast<BinT*>(reinterpret_cast<unsigned char*>(sl) + nleaves * 8);
   for (uint32_t i = threadIdx.x; i < nnodes; i += NT) sn[i] = nodes[i];
   for (uint32_t i = threadIdx.x; i < nleaves; i += NT) sl[i] = leaves[i];
-  for (uint64_t tile = uint64_t{blockIdx.x} * NT; tile < q; tile += uint64_t{gridDim.x} * NT) {
+  for (uint64_t tile = uint64_t{blockIdx.x} * TQ; tile < q; tile += uint64_t{gridDim.x} * TQ) {
     __syncthreads();
     const uint64_t rem = q - tile;
-    const uint32_t cnt = rem < NT ? static_cast<uint32_t>(rem) : NT;
+    const uint32_t cnt = rem < TQ ? static_cast<uint32_t>(rem) : TQ;
     for (uint32_t i = threadIdx.x; i < cnt * p; i += NT) sb[i] = bins[tile * p + i];
     __syncthreads();
     if (threadIdx.x >= cnt) continue;
-    const uint64_t qi = tile + threadIdx.x;
-    const BinT* b = sb + threadIdx.x * p;
-    double s = first ? 0.0 : sum[qi];
-    for (uint32_t t = 0; t < ntrees; ++t) {
-      BinNode v = sn[roots[t]];
-      while (v.feat != 0xffffu) v = sn[v.child + (b[v.feat] <= v.j ? 0u : 1u)];
-      s = __dadd_rn(s, sl[v.child]);
+    const BinT* bq[Q];
+    double s[Q];
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+      // a query slot past the tile's end re-walks query threadIdx.x (result dropped)
+      const uint32_t qi = threadIdx.x + u * NT < cnt ? threadIdx.x + u * NT : threadIdx.x;
+      bq[u] = sb + qi * p;
+      s[u] = first ? 0.0 : sum[tile + qi];
     }
-    if (last)
-      out[qi] = __ddiv_rn(s, total_trees);
-    else
-      sum[qi] = s;
+    for (uint32_t t = 0; t < ntrees; ++t) {
+      const uint32_t r = roots[t];
+      uint32_t idx[Q];
+      NodeT v[Q];
+      bool done = true;
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        idx[u] = r;
+        v[u] = sn[r];
+        done = done && NA::leaf(v[u]);
+      }
+      while (!done) {
+        done = true;
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          const bool lf = NA::leaf(v[u]);
+          const uint32_t bin = bq[u][lf ? 0u : NA::feat(v[u])];
+          idx[u] = lf ? idx[u] : NA::child(v[u]) + (bin <= NA::j(v[u]) ? 0u : 1u);
+        }
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          v[u] = sn[idx[u]];
+          done = done && NA::leaf(v[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < Q; ++u) s[u] = __dadd_rn(s[u], sl[NA::child(v[u])]);
+    }
+#pragma unroll
+    for (int u = 0; u < Q; ++u) {
+      if (threadIdx.x + u * NT >= cnt) continue;
+      const uint64_t qi = tile + threadIdx.x + u * NT;
+      if (last)
+        out[qi] = __ddiv_rn(s[u], total_trees);
+      else
+        sum[qi] = s[u];
+    }
   }
 }
 
@@ -176,16 +233,17 @@ cudaError_t bin_t(const double* rows, uint64_t q, uint32_t p, const double* thr,
                              s>>>(rows, q, p, thr, thr_off, static_cast<BinT*>(bins));
   return cudaGetLastError();
 }
-template <typename BinT>
-cudaError_t chunk_t(const BinNode* nodes, uint32_t nnodes, const double* leaves, uint32_t nleaves,
+template <typename BinT, typename NA>
+cudaError_t chunk_t(const void* nodes, uint32_t nnodes, const double* leaves, uint32_t nleaves,
                     const uint32_t* roots, uint32_t ntrees, const void* bins, uint64_t q,
                     uint32_t p, double* sum, int first, int last, double total_trees, double* out,
                     unsigned grid, size_t smem, size_t smem_max, cudaStream_t s) {
-  auto k = predict_chunk_kernel<BinT, kPredictThreads>;
+  auto k = predict_chunk_kernel<BinT, NA, kPredictThreads, kPredictQ>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_max));
   if (e != cudaSuccess) return e;
-  k<<<grid, kPredictThreads, smem, s>>>(nodes, nnodes, leaves, nleaves, roots, ntrees,
+  k<<<grid, kPredictThreads, smem, s>>>(static_cast<const typename NA::T*>(nodes), nnodes,
+                                        leaves, nleaves, roots, ntrees,
                                         static_cast<const BinT*>(bins), q, p, sum, first, last,
                                         total_trees, out);
   return cudaGetLastError();
@@ -199,17 +257,26 @@ cudaError_t launch_bin_queries(int bin_bytes, const double* rows, uint64_t q, ui
                         : bin_t<uint16_t>(rows, q, p, thr, thr_off, bins, s);
 }
 
-cudaError_t launch_predict_chunk(int bin_bytes, const BinNode* nodes, uint32_t nnodes,
-                                 const double* leaves, uint32_t nleaves, const uint32_t* roots,
-                                 uint32_t ntrees, const void* bins, uint64_t q, uint32_t p,
-                                 double* sum, int first, int last, double total_trees,
-                                 double* out, unsigned grid, size_t smem, size_t smem_max,
-                                 cudaStream_t s) {
+cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* nodes,
+                                 uint32_t nnodes, const double* leaves, uint32_t nleaves,
+                                 const uint32_t* roots, uint32_t ntrees, const void* bins,
+                                 uint64_t q, uint32_t p, double* sum, int first, int last,
+                                 double total_trees, double* out, unsigned grid, size_t smem,
+                                 size_t smem_max, cudaStream_t s) {
+  if (node_bytes == 4)
+    return bin_bytes == 1
+               ? chunk_t<uint8_t, Node4>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q,
+                                         p, sum, first, last, total_trees, out, grid, smem,
+                                         smem_max, s)
+               : chunk_t<uint16_t, Node4>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q,
+                                          p, sum, first, last, total_trees, out, grid, smem,
+                                          smem_max, s);
   return bin_bytes == 1
-             ? chunk_t<uint8_t>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p, sum,
-                                first, last, total_trees, out, grid, smem, smem_max, s)
-             : chunk_t<uint16_t>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p, sum,
-                                 first, last, total_trees, out, grid, smem, smem_max, s);
+             ? chunk_t<uint8_t, Node8>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p,
+                                       sum, first, last, total_trees, out, grid, smem, smem_max, s)
+             : chunk_t<uint16_t, Node8>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p,
+                                        sum, first, last, total_trees, out, grid, smem, smem_max,
+                                        s);
 }
 
 // C5 query generator: query i copies table row Rng(derive_seed(seed,"query",i)).bounded(n)

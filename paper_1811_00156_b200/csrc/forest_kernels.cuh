@@ -24,18 +24,21 @@ struct BinNode {
   uint32_t child;
 };
 
-constexpr int kPredictThreads = 512;
+constexpr int kPredictThreads = 1024;  // predict CTA size (one CTA per SM)
+constexpr int kPredictQ = 1;           // queries per thread (2 measured slower: the warp waits
+                                       // for the deepest of 64 paths)
 
 // binned shared-memory predict (kernels live in forest_kernels.cu and are launched there)
 cudaError_t launch_bin_queries(int bin_bytes, const double* rows, uint64_t q, uint32_t p,
                                const double* thr, const uint32_t* thr_off, void* bins,
                                cudaStream_t s);
-cudaError_t launch_predict_chunk(int bin_bytes, const BinNode* nodes, uint32_t nnodes,
-                                 const double* leaves, uint32_t nleaves, const uint32_t* roots,
-                                 uint32_t ntrees, const void* bins, uint64_t q, uint32_t p,
-                                 double* sum, int first, int last, double total_trees,
-                                 double* out, unsigned grid, size_t smem, size_t smem_max,
-                                 cudaStream_t s);
+// node_bytes 8: BinNode; 4: packed (column | bin << 7 | child << 15, column 127 = leaf)
+cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* nodes,
+                                 uint32_t nnodes, const double* leaves, uint32_t nleaves,
+                                 const uint32_t* roots, uint32_t ntrees, const void* bins,
+                                 uint64_t q, uint32_t p, double* sum, int first, int last,
+                                 double total_trees, double* out, unsigned grid, size_t smem,
+                                 size_t smem_max, cudaStream_t s);
 
 // batched multi-kernel grower for one batch of trees (grow_wide.cuh)
 cudaError_t run_wide(int rank_bytes, const WideArgs& a, cudaStream_t st, int sms,
