@@ -602,6 +602,9 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         const uint32_t per = static_cast<uint32_t>(slots / K);
         uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
         if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
+        uint32_t coop_min = 32768;  // rows from which a split node is routed by a CTA
+        if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
+        coop_min = std::max(coop_min, big_min);
         std::vector<cudaError_t> lane_err(K, cudaSuccess);
         std::vector<std::thread> lanes;
         for (int k = 0; k < K; ++k) {
@@ -615,6 +618,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
               w.ts = wts.p + size_t{k} * per;
               w.B = std::min<uint32_t>(per, T - t0);
               w.big_min = big_min;
+              w.coop_min = coop_min;
               w.t0 = t0;
               for (int i = 0; i < 4; ++i)
                 w.off[i] = woff.p + (size_t{k} * 4 + i) * (per + 1);

@@ -108,7 +108,9 @@ struct GrowArgs {
 struct TreeState {
   uint32_t A, F, E, S;
   uint32_t nodes, done, totL, A_next;
-  uint32_t E0, E1;  // eligible nodes by size class: small (lane chains), mid (group chains)
+  uint32_t E0, E1, E2;  // eligible nodes by size class: small (lane chains), mid (lane
+                        // groups), big (warp per chain)
+  uint32_t Sbig;        // split nodes routed by a CTA (column 0 listed, >= coop_min rows)
   unsigned long long elig_base, split_rows;
 };
 
@@ -119,6 +121,7 @@ struct WideArgs {
   uint32_t t0;       // local index of the batch's first tree
   uint32_t cur;      // buffer parity of the current level
   uint32_t big_min;  // nodes with >= big_min rows run one warp per chain (else lane groups)
+  uint32_t coop_min; // split nodes with >= coop_min rows are routed by one CTA each
   uint32_t* off[4];  // [B+1] prefixes: chain tasks, splits, positions, list chunks
   uint32_t* active;  // trees still splitting after this level's decide
 };

@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   }
   // eligible nodes by size class, BFS order inside each: [0, E0) small (< kLaneMax
   // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain)
-  uint32_t base = 0, E0 = 0, E1 = 0;
+  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0;
   for (uint32_t cls = 0; cls < 3; ++cls) {
     carry = 0;
     for (uint32_t b0 = 0; b0 < E; b0 += NT) {
@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     }
     if (cls == 0) E0 = carry;
     if (cls == 1) E1 = carry;
+    if (cls == 2) E2 = carry;
     base += carry;
   }
   for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
@@ -389,60 +390,55 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     s.E = E;
     s.E0 = E0;
     s.E1 = E1;
+    s.E2 = E2;
   }
 }
 
 // exclusive prefixes over trees of this level's work items (one CTA)
-//   which 0: chain tasks E*m;  which 1: splits S, positions A, list chunks
+//   which 0: chain tasks (lane, group, warp);  which 1: CTA-routed splits, splits S,
+//   positions A, list chunks
 template <int NT>
 __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
-  uint32_t c0 = 0, c1 = 0, c2 = 0;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
   for (uint32_t base = 0; base < a.B; base += NT) {
     const uint32_t b = base + threadIdx.x;
-    uint32_t v0 = 0, v1 = 0, v2 = 0;
+    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
         v0 = s.E0 * a.g.mtry;
         v1 = s.E1 * grp_tasks_per_node(a.g.mtry);
-        v2 = (s.E - s.E0 - s.E1) * a.g.mtry;
+        v2 = s.E2 * a.g.mtry;
       } else {
-        v0 = s.S;
-        v1 = s.A;
-        v2 = nchunks_of(s.A, a.g.d.nlisted);
+        v0 = s.Sbig;
+        v1 = s.S;
+        v2 = s.A;
+        v3 = nchunks_of(s.A, a.g.d.nlisted);
       }
     }
-    uint32_t t0, t1, t2;
+    uint32_t t0, t1, t2, t3;
     const uint32_t e0 = block_excl_scan<NT>(v0, sh, &t0);
     const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
     const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
+    const uint32_t e3 = block_excl_scan<NT>(v3, sh, &t3);
     if (b < a.B) {
-      if (which == 0) {
-        a.off[0][b] = c0 + e0;
-        a.off[1][b] = c1 + e1;
-        a.off[2][b] = c2 + e2;
-      } else {
-        a.off[1][b] = c0 + e0;
-        a.off[2][b] = c1 + e1;
-        a.off[3][b] = c2 + e2;
-      }
+      a.off[0][b] = c0 + e0;
+      a.off[1][b] = c1 + e1;
+      a.off[2][b] = c2 + e2;
+      a.off[3][b] = c3 + e3;
     }
     c0 += t0;
     c1 += t1;
     c2 += t2;
+    c3 += t3;
   }
   if (threadIdx.x == 0) {
-    if (which == 0) {
-      a.off[0][a.B] = c0;
-      a.off[1][a.B] = c1;
-      a.off[2][a.B] = c2;
-    } else {
-      a.off[1][a.B] = c0;
-      a.off[2][a.B] = c1;
-      a.off[3][a.B] = c2;
-    }
+    a.off[0][a.B] = c0;
+    a.off[1][a.B] = c1;
+    a.off[2][a.B] = c2;
+    a.off[3][a.B] = c3;
   }
 }
 
@@ -459,7 +455,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
-    const uint32_t e = P.ecls[st.E0 + st.E1 + k / m];
+    const uint32_t e = P.ecls[st.E0 + st.E1 + k / m];  // class 2
     const uint32_t slot = e * m + k % m;
     const NodeWork nw_ = P.front[P.e2f[e]];
     const uint32_t c = P.samp[slot];
@@ -472,6 +468,13 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     if (lane_id() == 0) P.res[slot] = ChainRes{bg, bp, 0u};
   }
 }
+
+// Huge split nodes (>= coop_min rows, column 0 listed) are routed by a whole CTA:
+// three producer warps gather blocks of kCoopBlock positions while warp 0 sums.
+// (A CTA per huge chain was measured slower than the pipelined warp chain: 8 warps'
+// three-stage pipelines keep more gathers in flight than one producer block.)
+constexpr int kCoopPerLane = 4;
+constexpr uint32_t kCoopBlock = 3 * 32 * kCoopPerLane;  // positions per block
 
 // ... mid nodes run one warp per node (or per group of 32/G of its columns), G lanes
 // per column (chain_grp) ...
@@ -543,7 +546,8 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const RankT* rank = static_cast<const RankT*>(d.rank);
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
-  uint32_t carry = 0, ccarry = 0;
+  const bool coop_route = d.list_of[0] >= 0;
+  uint32_t carry = 0, ccarry = 0, bcarry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
     const uint32_t e = base + threadIdx.x;
     uint32_t sp = 0, c = 0, thr_rank = 0;
@@ -598,6 +602,13 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     const uint32_t cnt = sp ? nw.e - nw.b : 0u;
     uint32_t ctot;
     const uint32_t cex = block_excl_scan<NT>(cnt, sh, &ctot);
+    // splits routed by a whole CTA (w_route_coop), compacted into ecls (free after the
+    // chain kernels)
+    const uint32_t big = sp && coop_route && cnt >= a.coop_min ? 1u : 0u;
+    uint32_t btot;
+    const uint32_t bex = block_excl_scan<NT>(big, sh, &btot);
+    if (big) P.ecls[bcarry + bex] = carry + ex;
+    bcarry += btot;
     if (sp) {
       const uint32_t s = carry + ex;
       const uint32_t child = nodes0 + 2 * s;
@@ -621,6 +632,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   }
   if (threadIdx.x == 0) {
     st.S = carry;
+    st.Sbig = bcarry;
     st.A_next = ccarry;
     st.split_rows += ccarry;
     st.elig_base += E;
@@ -653,9 +665,9 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a, b);
     const SplitInfo si = P.spl[s];
     if (kWarp != (si.cnt >= kLaneMax)) continue;
+    if (list0 >= 0 && si.cnt >= a.coop_min) continue;  // w_route_coop
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
-
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
@@ -679,6 +691,114 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
                                    static_cast<double>(o.wl), o.sl, o.ql};
     P.front_n[2 * s + 1] = NodeWork{si.base + o.nl, si.base + si.cnt, child + 1, 0u,
                                        static_cast<double>(o.wr), o.sr, o.qr};
+  }
+}
+
+// route of huge split nodes (column 0 listed): one CTA per node, three producer warps
+// gather blocks (list-0 entry -> payload, wyy -> split-column rank), set the goes-left
+// bits and stage the four masked addend streams; warp 0 runs the four sequential sums
+// (one 8-lane group each) over the previous block
+template <typename RankT>
+__global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
+  __shared__ double s_a[2][4][kCoopBlock];
+  __shared__ uint32_t s_cnt[3];
+  const uint32_t total = a.off[0][a.B];
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  const int32_t list0 = a.g.d.list_of[0];
+  const unsigned lane = lane_id(), wid = warp_id();
+  for (uint32_t t = blockIdx.x; t < total; t += gridDim.x) {
+    const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const uint32_t s = P.ecls[k];
+    const SplitInfo si = P.spl[s];
+    const NodeWork nw = P.front[si.f];
+    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+    const uint32_t* l0 = P.lists + static_cast<size_t>(list0) * stride;
+    const uint32_t nblk = (nw.e - nw.b + kCoopBlock - 1) / kCoopBlock;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    uint32_t c_nl = 0, c_wl = 0, c_wr = 0;  // producer lanes' integer counts
+    auto produce = [&](uint32_t blk) {
+      const uint32_t base = nw.b + blk * kCoopBlock + (wid - 1) * 32 * kCoopPerLane;
+      uint32_t q[kCoopPerLane];
+      Payload pv[kCoopPerLane];
+      double yy[kCoopPerLane];
+#pragma unroll
+      for (int j = 0; j < kCoopPerLane; ++j) {
+        const uint32_t kk = base + j * 32 + lane;
+        q[j] = kk < nw.e ? l0[kk] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kCoopPerLane; ++j)
+        if (base + j * 32 + lane < nw.e) {
+          pv[j] = P.pay[q[j]];
+          yy[j] = P.wyy[q[j]];
+        }
+#pragma unroll
+      for (int j = 0; j < kCoopPerLane; ++j) {
+        const uint32_t kk = base + j * 32 + lane;
+        if (kk >= nw.e) continue;
+        const uint32_t idx = kk - nw.b - blk * kCoopBlock;
+        const bool left = rank_of(rk_f, pv[j].row) <= si.thr_rank;
+        if (left) {
+          atomicOr(P.bits + (q[j] >> 5), 1u << (q[j] & 31u));
+          ++c_nl;
+          c_wl += pv[j].mult;
+        } else {
+          c_wr += pv[j].mult;
+        }
+        s_a[blk & 1u][0][idx] = left ? pv[j].wy : 0.0;
+        s_a[blk & 1u][1][idx] = left ? yy[j] : 0.0;
+        s_a[blk & 1u][2][idx] = left ? 0.0 : pv[j].wy;
+        s_a[blk & 1u][3][idx] = left ? 0.0 : yy[j];
+      }
+    };
+    if (wid > 0) produce(0);
+    __syncthreads();
+    double acc = 0.0;  // warp 0: group g = lane / 8 sums stream g
+    for (uint32_t blk = 0; blk < nblk; ++blk) {
+      if (wid == 0) {
+        const uint32_t cntb = min(kCoopBlock, nw.e - nw.b - blk * kCoopBlock);
+        const double* sg = s_a[blk & 1u][lane >> 3];
+        double r = acc;
+        uint32_t i = 0;
+        for (; i + 32 <= cntb; i += 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r = __dadd_rn(r, sg[i + j]);
+        }
+        for (; i < cntb; ++i) r = __dadd_rn(r, sg[i]);
+        acc = r;
+      } else if (blk + 1 < nblk) {
+        produce(blk + 1);
+      }
+      __syncthreads();
+    }
+    if (wid > 0) {
+      c_nl = warp_sum(c_nl);
+      c_wl = warp_sum(c_wl);
+      c_wr = warp_sum(c_wr);
+      if (lane == 0) {
+        atomicAdd(&s_cnt[0], c_nl);
+        atomicAdd(&s_cnt[1], c_wl);
+        atomicAdd(&s_cnt[2], c_wr);
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const double sl = __shfl_sync(kFull, acc, 0), ql = __shfl_sync(kFull, acc, 8);
+      const double sr = __shfl_sync(kFull, acc, 16), qr = __shfl_sync(kFull, acc, 24);
+      if (lane == 0) {
+        const uint32_t nl = s_cnt[0];
+        P.spl[s].nl = nl;
+        const uint32_t child = static_cast<uint32_t>(P.nleft[nw.id]);
+        P.front_n[2 * s] = NodeWork{si.base, si.base + nl, child, 0u,
+                                    static_cast<double>(s_cnt[1]), sl, ql};
+        P.front_n[2 * s + 1] = NodeWork{si.base + nl, si.base + si.cnt, child + 1, 0u,
+                                        static_cast<double>(s_cnt[2]), sr, qr};
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1014,6 +1134,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     if (e != cudaSuccess) return e;
     if (*h_active == 0) break;
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 1)));
+    WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));

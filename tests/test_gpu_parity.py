@@ -252,9 +252,11 @@ def test_wide_grower_random_tables(seed, monkeypatch):
                 col[c] = rng.integers(0, 2, size=n).astype(float)
         y = rng.normal(size=n)
         T, mns = 6, int(rng.integers(1, 6))
-        for big_min in ("64", "1000000"):
+        # (warp chains from 64 rows | CTA chains + routes from 200 rows | lane groups only)
+        for big_min, coop_min in (("64", "1000000"), ("64", "200"), ("1000000", "1000000")):
             monkeypatch.setenv("AIWC_BIG_MIN", big_min)
+            monkeypatch.setenv("AIWC_COOP_MIN", coop_min)
             prep = pkg.PreparedDataset(col, y, n, p)
             f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
             o = Oracle.fit(col, y, n, p, T, m, mns, seed)
-            assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min)
+            assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min, coop_min)

@@ -22,5 +22,6 @@ for _ in range(reps):
     dt = time.perf_counter() - s
     pr = f.profile()
     print(f"{which} T={T}: wall {dt*1e3:.1f} ms grow {pr['grow_ms']:.1f} ms "
-          f"{T/dt:.1f} trees/s nodes/tree {f.total_nodes/T:.1f} oob {f.oob.error_pct:.9f}",
+          f"{T/dt:.1f} trees/s nodes/tree {f.total_nodes/T:.1f} oob {f.oob.error_pct:.9f} "
+          f"split_rows {pr['split_rows']}",
           flush=True)

@@ -10,7 +10,8 @@ rows = list(csv.reader(open(sys.argv[1])))
 start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[start]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
+scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3,
+         "ms": 1.0}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[start + 1:]:
     if len(r) <= iv:
