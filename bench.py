@@ -34,6 +34,17 @@ C5_TREES, C5_MTRY, C5_MNS = 1000, 6, 5
 METRIC = "RF fit trees/s + predict rows/s at 1/2/4/8 B200 (% HBM roofline) vs host CPU"
 
 
+def traffic_per_launch(trees: int, launches: int):
+    """Measured DRAM bytes of the grow phase per launch (a launch = one fit's grow phase):
+    the committed ncu capture's bytes per tree times the trees each launch grew."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_grow_traffic.json")) as fh:
+            d = json.load(fh)
+        return d["dram_bytes_per_tree"] * trees / max(1, launches)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -342,8 +353,12 @@ def main():
         "oob_error_pct": None if oob is None else oob.error_pct,
         "nodes_per_tree": nodes_last / per,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "grow_kernel",
+                     "frac": achieved / peak, "traffic": traffic_per_launch(per * args.steps,
+                                                                            grow_launch),
+                     "traffic_source": "profiles/r1_grow_traffic.json (ncu dram__bytes of every "
+                                       "grow kernel, 148-tree fit, per tree x trees per launch)",
+                     "peak_kind": peak_kind,
+                     "kernel": "wide grower: the level kernels w_* of one fit (grow phase)",
                      "algorithmic_bytes_per_launch": alg_bytes / max(1, grow_launch),
                      "kernel_ms_per_launch": grow_ms / max(1, grow_launch),
                      "kernel_share_of_step": grow_ms / max(1e-9, ms)},
