@@ -171,11 +171,15 @@ def main():
     ap.add_argument("--predict-rows", type=int, default=100_000_000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--skip-predict", action="store_true")
+    ap.add_argument("--skip-grid", action="store_true")
+    ap.add_argument("--grid-cells", type=int, default=34)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-worker", action="store_true")
     ap.add_argument("--cpu-trees", type=int, default=0)
     ap.add_argument("--cpu-steps", type=int, default=1)
     args = ap.parse_args()
+    global ARGS
+    ARGS = args
 
     if args.cpu_worker:
         print(json.dumps(cpu_worker(args)))
@@ -332,6 +336,11 @@ def main():
     if not args.skip_predict:
         predict = bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
 
+    # ---------------- C2 grid + C3 hold-one-kernel-out (sharded by cell / fold) -----------
+    grid = loko = None
+    if not args.skip_grid:
+        grid, loko = bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks)
+
     if cpu_thread:
         cpu_thread.join(timeout=1200)
     if rank != 0:
@@ -371,6 +380,8 @@ def main():
         "cpu_baseline": ({k: cpu_res.get(k) for k in ("value", "unit", "cores", "kind", "sample")}
                          if cpu_res else None),
         "predict": predict,
+        "grid": grid,
+        "loko": loko,
     }
     if cpu_res.get("error"):
         line["cpu_baseline_error"] = cpu_res["error"]
@@ -420,6 +431,50 @@ def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
             "e2e": {"value": e2e, "unit": "rows/s", "rows": qe,
                     "h2d_bytes": qe * t.p * 8, "d2h_bytes": qe * 8}}
 
+
+def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
+    """C2: the num.trees x mtry x min.node.size OOB grid on the C1 table -- a bounded
+    sample of (mtry, mns) cells, each one 1000-tree fit whose 20 tree prefixes
+    (50..1000) give the 20 num.trees points (tree-prefix property); cell i on rank
+    i mod N.  C3: evaluate at the paper's 505/30/9, folds split over the ranks."""
+    from paper_1811_00156_b200 import shard
+
+    t = pkg.Table()
+    prep = pkg.PreparedDataset.from_table(t, device=local)
+    seed = pkg.derive_seed(1, "forest")
+    counts = list(range(50, 1001, 50))
+    ncell = max(1, ARGS.grid_cells)
+    cells = [(m, 1 + (7 * m) % 50) for m in range(1, 35)][:ncell]
+    allreduce = shard.torch_allreduce_sum(torch.device("cuda", local)) if world > 1 else (lambda a: a)
+    _ = pkg.grid_oob(prep, cells[:1], counts[:2], seed)  # warm-up
+    barrier()
+    s = time.perf_counter()
+    err = shard.grid_sharded(cells, counts, rank, world,
+                             lambda cs: pkg.grid_oob(prep, cs, counts, seed), allreduce)
+    barrier()
+    gs = max_over_ranks(time.perf_counter() - s)
+    grid = {"workload": f"C2 sample: {len(cells)} (mtry, min.node.size) cells x 20 num.trees "
+                        "values (50..1000) on the C1 table, one 1000-tree fit per cell",
+            "cells_per_s": len(cells) / gs, "grid_points_per_s": len(cells) * len(counts) / gs,
+            "s": gs, "full_grid_est_s": 1700 / (len(cells) / gs),
+            "best": {"error_pct": float(err.min()),
+                     "cell": cells[int(err.argmin() // len(counts))],
+                     "num_trees": counts[int(err.argmin() % len(counts))]}}
+    prm = pkg.ForestParams(505, 30, 9, 0)
+    barrier()
+    s = time.perf_counter()
+    part = pkg.evaluate(t, prm, seed, device=local, folds=shard.fold_range(rank, world, t.kernels))
+    pred = allreduce(part)
+    barrier()
+    ls = max_over_ranks(time.perf_counter() - s)
+    err_row = 100.0 * np.abs(pred - t.seconds) / t.seconds
+    loko = {"workload": "C3: evaluate(C1, 505/30/9): 37 folds x 60 held-out rows",
+            "folds_per_s": t.kernels / ls, "s": ls, "mape_pct": float(err_row.mean())}
+    del prep
+    return grid, loko
+
+
+ARGS = None
 
 if __name__ == "__main__":
     main()

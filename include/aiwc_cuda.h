@@ -113,6 +113,14 @@ int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum
  * rank 0 -> 1 -> ... reproduces the single-forest tree-order sum bit-exactly. */
 int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum,
                         uint32_t* row_count);
+/* OOB statistics of the forest's first tree_counts[i] trees, i < k (ascending counts,
+ * forest grown from tree 0): compute_oob (forest.hpp:393-454) of every T-tree fit of
+ * the same (data, mtry, min.node.size, seed) at once -- by the tree-prefix property a
+ * T-tree fit is the first T trees of a longer one (forest.hpp:182, 477-479).  This is
+ * the objective of tune_forest / heatmap_scan (tuner.hpp:247-253, experiments.hpp:
+ * 79-108) over the num.trees axis. */
+int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, uint32_t k,
+                    aiwc_oob_stats* out);
 /* finalize OOB stats from per-row sum/count (forest.hpp:396-453) */
 int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
                       const uint32_t* row_count, aiwc_oob_stats* out);
@@ -135,6 +143,15 @@ int aiwc_evaluate(const double* col, const double* y, uint64_t n, uint32_t p,
                   const uint32_t* kernel_of_row, uint32_t K, uint32_t num_trees,
                   uint32_t mtry, uint32_t min_node_size, uint64_t seed, int device,
                   double* predicted_seconds);
+
+/* folds [fold_begin, fold_end) only (rows of other folds are left untouched): the
+ * multi-GPU split of evaluate -- rank r takes a fold range and the predictions of the
+ * ranks are combined row-wise (each row belongs to exactly one fold). */
+int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t p,
+                        const uint32_t* kernel_of_row, uint32_t K, uint32_t fold_begin,
+                        uint32_t fold_end, uint32_t num_trees, uint32_t mtry,
+                        uint32_t min_node_size, uint64_t seed, int device,
+                        double* predicted_seconds);
 
 /* ---- measurement (not part of the reference API) ----------------------------------
  * grow-kernel device time of the fit (CUDA events on the launching stream), whole fit

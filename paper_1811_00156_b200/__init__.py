@@ -105,6 +105,9 @@ def lib():
         L.aiwc_predict_device.argtypes = [vp, vp, u64, u32, vp]
         L.aiwc_evaluate.argtypes = [P(f64), P(f64), u64, u32, P(u32), u32, u32, u32, u32, u64,
                                     C.c_int, P(f64)]
+        L.aiwc_evaluate_folds.argtypes = [P(f64), P(f64), u64, u32, P(u32), u32, u32, u32,
+                                          u32, u32, u32, u64, C.c_int, P(f64)]
+        L.aiwc_oob_prefix.argtypes = [vp, vp, P(u32), u32, P(OobStatsC)]
         L.aiwc_forest_profile.argtypes = [vp, P(f64), P(f64), P(u64), P(u32)]
         L.aiwc_launch_count.restype = u64
         L.aiwc_make_queries.argtypes = [vp, u64, u32, u64, u64, C.c_int, vp]
@@ -366,11 +369,40 @@ def make_queries(d_rows_ptr: int, n: int, p: int, q: int, seed: int, device: int
     _check(lib().aiwc_make_queries(d_rows_ptr, n, p, q, seed, device, d_out_ptr))
 
 
-def evaluate(table: Table, params: ForestParams, seed: int, device: int = 0) -> np.ndarray:
+def evaluate(table: Table, params: ForestParams, seed: int, device: int = 0,
+             folds: tuple[int, int] | None = None) -> np.ndarray:
     """experiments.hpp:383-408: predicted seconds per row, each row predicted by the
-    forest fit without its kernel (fold k seeded derive_seed(seed, "holdout", k))."""
+    forest fit without its kernel (fold k seeded derive_seed(seed, "holdout", k)).
+    `folds` = (begin, end) restricts the work to those folds (rows of other folds stay
+    0.0): the per-rank share of a multi-GPU evaluate (shard.fold_range)."""
     out = np.zeros(table.n)
-    _check(lib().aiwc_evaluate(_p(table.col, f64), _p(table.y, f64), table.n, table.p,
-                               _p(table.kernel_of_row, u32), table.kernels, params.num_trees,
-                               params.mtry, params.min_node_size, seed, device, _p(out, f64)))
+    fb, fe = (0, table.kernels) if folds is None else folds
+    _check(lib().aiwc_evaluate_folds(_p(table.col, f64), _p(table.y, f64), table.n, table.p,
+                                     _p(table.kernel_of_row, u32), table.kernels, fb, fe,
+                                     params.num_trees, params.mtry, params.min_node_size,
+                                     seed, device, _p(out, f64)))
+    return out
+
+
+def oob_prefix(forest: Forest, prepared: PreparedDataset, tree_counts) -> list:
+    """OOB statistics of the forest's first T trees for each T in `tree_counts`
+    (ascending): by the tree-prefix property (forest.hpp:182, 477-479) these equal
+    fit(prepared, {T, mtry, mns, seed}).oob -- the grid objective of tuner.hpp:247-253
+    over the num.trees axis, from one fit."""
+    cps = np.ascontiguousarray(tree_counts, np.uint32)
+    outs = (OobStatsC * len(cps))()
+    _check(lib().aiwc_oob_prefix(prepared._h, forest._h, _p(cps, u32), len(cps), outs))
+    return [OobStats._from_c(o) for o in outs]
+
+
+def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int) -> np.ndarray:
+    """C2 grid objective (tuner.hpp:247-253 / experiments.hpp:79-108): error_pct for
+    every (mtry, min_node_size) cell x num.trees value, one fit of max(tree_counts)
+    trees per cell.  Returns an array [len(cells), len(tree_counts)]."""
+    cps = sorted(int(t) for t in tree_counts)
+    out = np.zeros((len(cells), len(cps)))
+    for i, (m, mns) in enumerate(cells):
+        f = fit(prepared, ForestParams(cps[-1], m, mns, seed), compute_oob_stats=False)
+        out[i] = [s.error_pct for s in oob_prefix(f, prepared, cps)]
+        del f
     return out

@@ -873,6 +873,38 @@ int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum, uint32_t
   });
 }
 
+int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, uint32_t k,
+                    aiwc_oob_stats* out) {
+  return guard([&] {
+    if (!ctx || !f || !tree_counts || !out) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    if (f->tree_begin != 0) throw Status(AIWC_EARG, "tree prefixes need a forest from tree 0");
+    for (uint32_t i = 0; i < k; ++i)
+      if (tree_counts[i] < 1 || tree_counts[i] > f->trees || (i && tree_counts[i] < tree_counts[i - 1]))
+        throw Status(AIWC_EARG, "tree counts must ascend within [1, trees]");
+    if (k == 0) return;
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    const uint64_t n = f->n;
+    DevBuf<uint32_t> cps(k);
+    DevBuf<double> sums(size_t{k} * n);
+    DevBuf<uint32_t> counts(size_t{k} * n);
+    CK(cudaMemcpyAsync(cps.p, tree_counts, k * 4, cudaMemcpyHostToDevice, st.s));
+    oob_prefix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st.s>>>(
+        f->oobval.p, cps.p, k, n, sums.p, counts.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    std::vector<double> hs(size_t{k} * n);
+    std::vector<uint32_t> hc(size_t{k} * n);
+    CK(cudaMemcpyAsync(hs.data(), sums.p, hs.size() * 8, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaMemcpyAsync(hc.data(), counts.p, hc.size() * 4, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaStreamSynchronize(st.s));
+    for (uint32_t i = 0; i < k; ++i)
+      out[i] = finalize_oob(ctx->y.data(), n, hs.data() + size_t{i} * n, hc.data() + size_t{i} * n);
+  });
+}
+
 int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
                       const uint32_t* row_count, aiwc_oob_stats* out) {
   return guard([&] {
@@ -1069,10 +1101,20 @@ int aiwc_evaluate(const double* col, const double* y, uint64_t n, uint32_t p,
                   const uint32_t* kernel_of_row, uint32_t K, uint32_t num_trees,
                   uint32_t mtry, uint32_t min_node_size, uint64_t seed, int device,
                   double* predicted_seconds) {
+  return aiwc_evaluate_folds(col, y, n, p, kernel_of_row, K, 0, K, num_trees, mtry,
+                             min_node_size, seed, device, predicted_seconds);
+}
+
+int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t p,
+                        const uint32_t* kernel_of_row, uint32_t K, uint32_t fold_begin,
+                        uint32_t fold_end, uint32_t num_trees, uint32_t mtry,
+                        uint32_t min_node_size, uint64_t seed, int device,
+                        double* predicted_seconds) {
   return guard([&] {
     if (!col || !y || !kernel_of_row || !predicted_seconds)
       throw Status(AIWC_EARG, "NULL argument");
-    for (uint32_t k = 0; k < K; ++k) {
+    if (fold_begin > fold_end || fold_end > K) throw Status(AIWC_EARG, "fold range out of [0, K]");
+    for (uint32_t k = fold_begin; k < fold_end; ++k) {
       std::vector<uint64_t> train, test;
       for (uint64_t i = 0; i < n; ++i) (kernel_of_row[i] == k ? test : train).push_back(i);
       if (test.empty()) continue;

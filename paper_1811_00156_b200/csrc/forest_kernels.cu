@@ -48,6 +48,29 @@ __global__ void oob_reduce_kernel(const double* __restrict__ oobval, uint32_t T,
   count[i] = c;
 }
 
+// Per-row OOB (sum, count) after each of k ascending tree-count checkpoints, summed in
+// tree order: the OOB statistics of every tree prefix of one fit at once (a T-tree fit is
+// the first T trees of a longer fit with the same seed, forest.hpp:182, 477-479).
+__global__ void oob_prefix_kernel(const double* __restrict__ oobval,
+                                  const uint32_t* __restrict__ cps, uint32_t k, uint64_t n,
+                                  double* __restrict__ sums, uint32_t* __restrict__ counts) {
+  const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  uint32_t c = 0, t = 0;
+  for (uint32_t j = 0; j < k; ++j) {
+    for (const uint32_t te = cps[j]; t < te; ++t) {
+      const double v = __ldg(oobval + t * n + i);
+      if (v == v) {
+        s = __dadd_rn(s, v);
+        ++c;
+      }
+    }
+    sums[j * n + i] = s;
+    counts[j * n + i] = c;
+  }
+}
+
 // OOB leaf values of an imported forest: in-bag flags from the draws, then a walk
 // over the column store with the stored f64 thresholds (Tree::predict semantics)
 __global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t T, uint64_t n,

@@ -11,6 +11,10 @@ union equals a one-GPU fit.  Two exchanges exist:
   finalises.  Result: bit-identical to the one-GPU / reference value.
 * the forest gather (node SoA + in-bag lists) concatenates rank parts in rank order.
 
+The grid search (C2) and hold-one-kernel-out evaluate (C3) shard by cell / fold: each
+cell or fold is computed by exactly one rank into a zero-filled array, so a SUM
+all-reduce of the arrays combines them exactly (x + 0.0 == x).
+
 The compute is injected (`accumulate(row_sum, row_count)`), so the same logic drives
 the GPU path in bench.py (NCCL) and the CPU tests (gloo + the oracle).
 """
@@ -85,3 +89,43 @@ def concat_forests(parts):
         inb.append(ib)
     return (np.concatenate(offs), *[np.concatenate(c) for c in cols],
             np.concatenate(inb) if inb and inb[0] is not None else None)
+
+
+def cells_for_rank(cells, rank: int, world: int):
+    """Round-robin share of grid cells (cell i goes to rank i mod G):
+    returns [(index, cell)] for this rank."""
+    return [(i, c) for i, c in enumerate(cells) if i % world == rank]
+
+
+def fold_range(rank: int, world: int, folds: int) -> tuple[int, int]:
+    """Contiguous fold range of `rank` for a sharded evaluate."""
+    return tree_range(rank, world, folds)
+
+
+def grid_sharded(cells, tree_counts, rank: int, world: int,
+                 compute: Callable[[list], np.ndarray],
+                 allreduce_sum: Callable[[np.ndarray], np.ndarray]) -> np.ndarray:
+    """Grid objective over all ranks: rank r computes its round-robin cells with
+    `compute(list_of_cells) -> [k, len(tree_counts)]`, the per-rank results are placed
+    in a zero-filled [len(cells), len(tree_counts)] array and summed over ranks."""
+    mine = cells_for_rank(cells, rank, world)
+    out = np.zeros((len(cells), len(tree_counts)))
+    if mine:
+        res = compute([c for _, c in mine])
+        for j, (i, _) in enumerate(mine):
+            out[i] = res[j]
+    return allreduce_sum(out)
+
+
+def torch_allreduce_sum(device=None):
+    """SUM all-reduce of a float64 numpy array over the default process group."""
+    import torch
+    import torch.distributed as dist
+
+    def f(a: np.ndarray) -> np.ndarray:
+        t = torch.from_numpy(np.ascontiguousarray(a, np.float64))
+        t = t.to(device) if device is not None else t
+        dist.all_reduce(t)
+        return t.cpu().numpy()
+
+    return f

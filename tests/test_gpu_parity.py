@@ -260,3 +260,36 @@ def test_wide_grower_random_tables(seed, monkeypatch):
             f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
             o = Oracle.fit(col, y, n, p, T, m, mns, seed)
             assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min, coop_min)
+
+
+def test_oob_prefix_equals_separate_fits(c1, seed, golden):
+    """Tree-prefix OOB (one 500-tree fit) == the OOB of separate T-tree fits, and the
+    500-tree value == the reference golden (C1 500/6/5)."""
+    t, prep = c1
+    counts = [1, 7, 50, 123, 500]
+    f = pkg.fit(prep, pkg.ForestParams(500, 6, 5, seed), compute_oob_stats=False)
+    pre = pkg.oob_prefix(f, prep, counts)
+    for T, st in zip(counts[:-1], pre):
+        want = pkg.fit(prep, pkg.ForestParams(T, 6, 5, seed)).oob
+        assert oob_list(st) == oob_list(want), T
+    assert pre[-1].error_pct == golden["c1_500_6_5"]["oob"][3]
+
+
+def test_grid_oob_matches_reference_cells(c1, seed, golden):
+    """C2 objective through grid_oob on the reference's golden grid cells."""
+    t, prep = c1
+    for g in golden["c2_cells"]:
+        got = pkg.grid_oob(prep, [(g["mtry"], g["mns"])], [g["T"] // 2, g["T"]], seed)
+        assert got[0, 1] == g["oob"][3], g
+
+
+def test_evaluate_fold_ranges_combine(c1, seed):
+    """The multi-GPU split of evaluate: fold ranges of two ranks, summed row-wise, equal
+    the whole evaluate bit-for-bit (C3 at 50/6/5 against the reference golden)."""
+    from paper_1811_00156_b200 import shard
+    t, _ = c1
+    prm = pkg.ForestParams(50, 6, 5, 0)
+    parts = [pkg.evaluate(t, prm, seed, folds=shard.fold_range(r, 2, t.kernels))
+             for r in range(2)]
+    ref = np.load(os.path.join(GOLD, "c3_50_6_5_pred.npy"))
+    assert np.array_equal((parts[0] + parts[1]).view(np.uint64), ref.view(np.uint64))

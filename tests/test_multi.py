@@ -122,3 +122,61 @@ def test_tree_ranges_cover_forest():
             rs = [shard.tree_range(r, world, T) for r in range(world)]
             assert rs[0][0] == 0 and rs[-1][1] == T
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+GRID_CELLS = [(1, 1), (2, 3), (3, 2), (1, 5), (2, 1)]
+GRID_T = [3, 6, 10]
+
+
+def _grid_compute(cells):
+    """Oracle stand-in for grid_oob on one rank: error_pct per (cell, num.trees)."""
+    col, y = _table()
+    p, n = col.shape
+    out = np.zeros((len(cells), len(GRID_T)))
+    for i, (m, mns) in enumerate(cells):
+        for j, T in enumerate(GRID_T):
+            f = Oracle.fit(col, y, n, p, T, m, mns, 777)
+            out[i, j] = Oracle.oob(col, y, n, p, f)[0][3]
+    return out
+
+
+def _grid_worker(rank, world, port, q):
+    from paper_1811_00156_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = shard.grid_sharded(GRID_CELLS, GRID_T, rank, world, _grid_compute,
+                                 shard.torch_allreduce_sum())
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_grid_equals_single_process():
+    """C2 sharding (cell i on rank i mod 2) + SUM all-reduce == one process, exactly."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grid_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = _grid_compute(GRID_CELLS)
+    for r in range(2):
+        assert np.array_equal(got[r].view(np.uint64), want.view(np.uint64))
+
+
+def test_cells_and_folds_cover_once():
+    from paper_1811_00156_b200 import shard
+
+    for world in (1, 2, 3, 8):
+        cells = list(range(37))
+        seen = sorted(i for r in range(world) for i, _ in shard.cells_for_rank(cells, r, world))
+        assert seen == cells
+        fr = [shard.fold_range(r, world, 37) for r in range(world)]
+        assert fr[0][0] == 0 and fr[-1][1] == 37
+        assert all(a[1] == b[0] for a, b in zip(fr, fr[1:]))
