@@ -114,6 +114,108 @@ struct Stream {
   }
 };
 
+// Device -> pageable host copy through two pinned bounce buffers (allocated once per
+// process): the DMA of chunk i+1 overlaps the multi-threaded host copy of chunk i, so
+// large exports (10 GB of C4 nodes) run at PCIe speed instead of the driver's pageable
+// path.  Small copies go straight through cudaMemcpy.
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = size_t{64} << 20;
+  if (bytes < (size_t{8} << 20)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  static std::mutex mu;
+  static char* pin[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pin[0]) {
+    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[0]), kChunk));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[1]), kChunk));
+  }
+  cudaEvent_t ev[2];
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EvG {
+    cudaEvent_t* e;
+    ~EvG() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } eg{ev};
+  const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t i) {
+    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    CK(cudaMemcpyAsync(pin[i & 1], static_cast<const char*>(src) + off, len,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(ev[i & 1], s));
+  };
+  const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  issue(0);
+  for (size_t i = 0; i < nchunk; ++i) {
+    if (i + 1 < nchunk) issue(i + 1);  // buffer (i+1)&1 was drained in iteration i-1
+    CK(cudaEventSynchronize(ev[i & 1]));
+    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    char* d = static_cast<char*>(dst) + off;
+    const char* p = pin[i & 1];
+    std::vector<std::thread> th;
+    const size_t part = (len + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+      const size_t b = t * part;
+      if (b >= len) break;
+      th.emplace_back([=] { std::memcpy(d + b, p + b, std::min(part, len - b)); });
+    }
+    for (auto& x : th) x.join();
+  }
+}
+
+// Pageable host -> device copy through two pinned bounce buffers: the multi-threaded
+// host copy into one buffer overlaps the DMA out of the other.  Returns when the data
+// is on the device (the stream is synchronised).
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = size_t{64} << 20;
+  if (bytes < (size_t{8} << 20)) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    return;
+  }
+  static std::mutex mu;
+  static char* pin[2] = {nullptr, nullptr};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pin[0]) {
+    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[0]), kChunk));
+    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[1]), kChunk));
+  }
+  cudaEvent_t ev[2];
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EvG {
+    cudaEvent_t* e;
+    ~EvG() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } eg{ev};
+  const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+  for (size_t i = 0; i < nchunk; ++i) {
+    if (i >= 2) CK(cudaEventSynchronize(ev[i & 1]));  // DMA out of this buffer finished
+    const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+    const char* h = static_cast<const char*>(src) + off;
+    char* p = pin[i & 1];
+    std::vector<std::thread> th;
+    const size_t part = (len + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+      const size_t b = t * part;
+      if (b >= len) break;
+      th.emplace_back([=] { std::memcpy(p + b, h + b, std::min(part, len - b)); });
+    }
+    for (auto& x : th) x.join();
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, p, len, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ev[i & 1], s));
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
 }  // namespace aiwc_b200
 
 using namespace aiwc_b200;
@@ -751,18 +853,20 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
     if (!f) throw Status(AIWC_EARG, "forest is NULL");
     DeviceGuard dg(f->device);
     const uint64_t N = f->off.back();
+    Stream st;
     if (offsets) std::copy(f->off.begin(), f->off.end(), offsets);
-    std::vector<int32_t> tmp;
-    if (feature) CK(cudaMemcpy(feature, f->feature.p, N * 4, cudaMemcpyDeviceToHost));
-    if (threshold) CK(cudaMemcpy(threshold, f->thr.p, N * 8, cudaMemcpyDeviceToHost));
-    if (left || right) {
-      tmp.resize(N);
-      CK(cudaMemcpy(tmp.data(), f->left.p, N * 4, cudaMemcpyDeviceToHost));
-      if (left) std::copy(tmp.begin(), tmp.end(), left);
-      if (right)
-        for (uint64_t i = 0; i < N; ++i) right[i] = tmp[i] < 0 ? -1 : tmp[i] + 1;
+    if (feature) d2h(feature, f->feature.p, N * 4, st.s);
+    if (threshold) d2h(threshold, f->thr.p, N * 8, st.s);
+    if (left) d2h(left, f->left.p, N * 4, st.s);
+    if (right) {  // right = left + 1 (BFS numbering, forest.hpp:310-311), -1 for leaves
+      DevBuf<int32_t> r(N);
+      right_child_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 1u << 20)),
+                           256, 0, st.s>>>(f->left.p, N, r.p);
+      CK(cudaGetLastError());
+      g_launches += 1;
+      d2h(right, r.p, N * 4, st.s);
     }
-    if (value) CK(cudaMemcpy(value, f->value.p, N * 8, cudaMemcpyDeviceToHost));
+    if (value) d2h(value, f->value.p, N * 8, st.s);
   });
 }
 
@@ -771,7 +875,8 @@ int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag) {
     if (!f || !inbag) throw Status(AIWC_EARG, "NULL argument");
     if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
     DeviceGuard dg(f->device);
-    CK(cudaMemcpy(inbag, f->inbag.p, size_t{f->trees} * f->n * 4, cudaMemcpyDeviceToHost));
+    Stream st;
+    d2h(inbag, f->inbag.p, size_t{f->trees} * f->n * 4, st.s);
   });
 }
 
@@ -1026,14 +1131,26 @@ void build_binned(aiwc_forest* f, uint32_t p) {
   f->bin_ok = true;
 }
 
+// scratch of the binned path for up to q rows (bins + running sums); kernels using it
+// must have finished before it is freed (DevBuf frees on the legacy stream)
+struct PredScratch {
+  DevBuf<uint8_t> bins;
+  DevBuf<double> sum;
+  void reserve(uint64_t q, uint32_t p) {
+    if (bins.count < q * p * 2) bins.alloc(q * p * 2);
+    if (sum.count < q) sum.alloc(q);
+  }
+};
+
 void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p, double* d_out,
-                    cudaStream_t s) {
+                    cudaStream_t s, PredScratch& sc) {
   const size_t bb = f->bin_bytes;
-  DevBuf<uint8_t> bins(q * p * bb);
-  DevBuf<double> sum(q);
+  sc.reserve(q, p);
+  uint8_t* const bins = sc.bins.p;
+  double* const sum = sc.sum.p;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device));
-  CK(launch_bin_queries(f->bin_bytes, d_rows, q, p, f->bthr.p, f->bthr_off.p, bins.p, s));
+  CK(launch_bin_queries(f->bin_bytes, d_rows, q, p, f->bthr.p, f->bthr_off.p, bins, s));
   g_launches += 1;
   const uint64_t tq = uint64_t{kPredNT} * kPredictQ;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(sms, (q + tq - 1) / tq));
@@ -1045,19 +1162,21 @@ void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p
                                            : static_cast<const void*>(f->bnodes.p + ch.node0);
     CK(launch_predict_chunk(f->bin_bytes, f->node_bytes, nodes, ch.nnodes,
                             f->bleaves.p + ch.leaf0, ch.nleaves, f->broots.p + ch.root0, ch.ntrees,
-                            bins.p, q, p, sum.p, k == 0, k + 1 == f->chunks.size(),
+                            bins, q, p, sum, k == 0, k + 1 == f->chunks.size(),
                             static_cast<double>(f->trees), d_out, grid, smem, kPredSmem, s));
     g_launches += 1;
   }
 }
 
+void build_binned_once(aiwc_forest* f, uint32_t p) { build_binned(f, p); }
+
 // device rows -> device responses; binned shared-memory path when the forest fits,
 // else the L2 walk (predict_kernel)
 void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
-                      double* d_out, cudaStream_t s) {
+                      double* d_out, cudaStream_t s, PredScratch& sc) {
   build_binned(f, p);
   if (f->bin_ok) {
-    predict_binned(f, d_rows, q, p, d_out, s);
+    predict_binned(f, d_rows, q, p, d_out, s, sc);
     return;
   }
   predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(f->packed.p, f->d_off.p,
@@ -1077,8 +1196,9 @@ int aiwc_predict_device(aiwc_forest* f, const double* d_rows, uint64_t q, uint32
     if (q == 0) return;
     DeviceGuard dg(f->device);
     Stream st;
-    predict_dispatch(f, d_rows, q, p, d_out, st.s);
-    CK(cudaStreamSynchronize(st.s));
+    PredScratch sc;
+    predict_dispatch(f, d_rows, q, p, d_out, st.s, sc);
+    CK(cudaStreamSynchronize(st.s));  // before sc is freed
   });
 }
 
@@ -1088,12 +1208,26 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
     if (!f || (!rows && q) || (!out_response && q)) throw Status(AIWC_EARG, "NULL argument");
     if (q == 0) return;
     DeviceGuard dg(f->device);
-    Stream st;
-    DevBuf<double> dr(q * p), dout(q);
-    CK(cudaMemcpyAsync(dr.p, rows, q * p * 8, cudaMemcpyHostToDevice, st.s));
-    predict_dispatch(f, dr.p, q, p, dout.p, st.s);
-    CK(cudaMemcpyAsync(out_response, dout.p, q * 8, cudaMemcpyDeviceToHost, st.s));
-    CK(cudaStreamSynchronize(st.s));
+    // row chunks on two streams: the upload of chunk i+1 (host copy into pinned memory,
+    // DMA) overlaps the predict kernels of chunk i
+    Stream st[2];
+    const uint64_t chunk = std::max<uint64_t>(uint64_t{1} << 20, (q + 7) / 8);
+    PredScratch sc[2];
+    DevBuf<double> dr[2], dout(q);
+    dr[0].alloc(std::min(q, chunk) * p);
+    if (q > chunk) dr[1].alloc(chunk * p);
+    build_binned_once(f, p);
+    uint64_t i = 0;
+    for (uint64_t r0 = 0; r0 < q; r0 += chunk, ++i) {
+      const uint64_t rn = std::min(chunk, q - r0);
+      const cudaStream_t s = st[i & 1].s;
+      CK(cudaStreamSynchronize(s));  // chunk i-2's kernels are done with dr[i&1]
+      h2d(dr[i & 1].p, rows + r0 * p, rn * p * 8, s);
+      predict_dispatch(f, dr[i & 1].p, rn, p, dout.p + r0, s, sc[i & 1]);
+    }
+    CK(cudaStreamSynchronize(st[0].s));
+    CK(cudaStreamSynchronize(st[1].s));
+    d2h(out_response, dout.p, q * 8, st[0].s);
   });
 }
 

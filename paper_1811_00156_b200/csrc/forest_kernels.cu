@@ -71,6 +71,16 @@ __global__ void oob_prefix_kernel(const double* __restrict__ oobval,
   }
 }
 
+// right child of every node (left + 1, BFS numbering forest.hpp:310-311; -1 for leaves)
+__global__ void right_child_kernel(const int32_t* __restrict__ left, uint64_t N,
+                                   int32_t* __restrict__ right) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < N;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const int32_t l = left[i];
+    right[i] = l < 0 ? -1 : l + 1;
+  }
+}
+
 // OOB leaf values of an imported forest: in-bag flags from the draws, then a walk
 // over the column store with the stored f64 thresholds (Tree::predict semantics)
 __global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t T, uint64_t n,
