@@ -417,9 +417,13 @@ def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
     # e2e: host rows through aiwc_predict (H2D + kernel + D2H), bounded host buffer
     qe = min(q, 10_000_000)
     host = qbuf[:qe].cpu().numpy()
-    s = time.perf_counter()
-    _ = forest.predict_response(host)
-    e2e = qe / (time.perf_counter() - s)
+    _ = forest.predict_response(host[:1_000_000])  # warm: pinned staging, pool
+    ts = []
+    for _ in range(3):
+        s = time.perf_counter()
+        _ = forest.predict_response(host)
+        ts.append(time.perf_counter() - s)
+    e2e = qe / float(np.median(ts))
     del qbuf, out
     torch.cuda.empty_cache()
     return {"workload": "C5: 1000-tree C1 forest (m=6, mns=5), 100M device-selection queries "
