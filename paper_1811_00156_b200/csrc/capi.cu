@@ -249,50 +249,6 @@ struct aiwc_ctx {
   }
 };
 
-namespace {
-
-// per-column argsort by (value asc, row asc) (forest.hpp:148-159) + dense ranks +
-// distinct values; host threads over columns
-void presort(const double* col, uint64_t n, uint32_t p, std::vector<uint32_t>& order,
-             std::vector<uint32_t>& rank, std::vector<double>& vals,
-             std::vector<uint64_t>& vals_off) {
-  order.resize(size_t{p} * n);  // dense p x n argsorts (packed for the device later)
-  rank.resize(size_t{p} * n);
-  std::vector<std::vector<double>> distinct(p);
-  const unsigned hw = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
-  std::atomic<uint32_t> next{0};
-  auto work = [&] {
-    for (;;) {
-      const uint32_t c = next.fetch_add(1);
-      if (c >= p) return;
-      const double* v = col + size_t{c} * n;
-      uint32_t* o = order.data() + size_t{c} * n;
-      std::iota(o, o + n, 0u);
-      std::sort(o, o + n, [&](uint32_t a, uint32_t b) {
-        if (v[a] != v[b]) return v[a] < v[b];
-        return a < b;
-      });
-      uint32_t* rk = rank.data() + size_t{c} * n;
-      auto& dv = distinct[c];
-      for (uint64_t k = 0; k < n; ++k) {
-        const double x = v[o[k]];
-        if (k == 0 || x != dv.back()) dv.push_back(x);
-        rk[o[k]] = static_cast<uint32_t>(dv.size() - 1);
-      }
-    }
-  };
-  std::vector<std::thread> th;
-  for (unsigned i = 0; i < std::min<unsigned>(hw, p); ++i) th.emplace_back(work);
-  for (auto& t : th) t.join();
-  vals_off.assign(p + 1, 0);
-  for (uint32_t c = 0; c < p; ++c) vals_off[c + 1] = vals_off[c] + distinct[c].size();
-  vals.resize(vals_off[p]);
-  for (uint32_t c = 0; c < p; ++c)
-    std::copy(distinct[c].begin(), distinct[c].end(), vals.begin() + vals_off[c]);
-}
-
-}  // namespace
-
 // ---------------------------------------------------------------------------------
 // Forest
 // ---------------------------------------------------------------------------------
@@ -358,61 +314,81 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
     if (n < 2) throw Status(AIWC_EEXEC, "dataset must have at least 2 rows");
     if (p < 1 || p > 1024) throw Status(AIWC_EARG, "predictor count must be in [1, 1024]");
     if (n >= (uint64_t{1} << 31)) throw Status(AIWC_EARG, "too many rows (max 2^31-1)");
-    for (uint64_t i = 0; i < n * p; ++i)
-      if (!std::isfinite(col[i])) throw Status(AIWC_EEXEC, "non-finite predictor value");
-    for (uint64_t i = 0; i < n; ++i)
-      if (!std::isfinite(y[i])) throw Status(AIWC_EEXEC, "non-finite response value");
     DeviceGuard dg(device);
     auto ctx = std::make_unique<aiwc_ctx>();
     ctx->device = device;
     ctx->n = n;
     ctx->p = p;
     ctx->y.assign(y, y + n);
-    std::vector<uint32_t> order, rank;
-    std::vector<double> vals;
-    std::vector<uint64_t> voff;
-    presort(col, n, p, order, rank, vals, voff);
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    const cudaStream_t s = ctx->stream;
+    ctx->col.alloc(size_t{p} * n);
+    ctx->dy.alloc(n);
+    h2d(ctx->col.p, col, size_t{p} * n * 8, s);
+    h2d(ctx->dy.p, y, n * 8, s);
+    {  // the reference rejects nothing here, but a non-finite value has no total order
+      DevBuf<unsigned long long> bad(2);
+      CK(cudaMemsetAsync(bad.p, 0, 16, s));
+      CK(count_nonfinite(ctx->col.p, size_t{p} * n, bad.p, s));
+      CK(count_nonfinite(ctx->dy.p, n, bad.p + 1, s));
+      unsigned long long hb[2];
+      CK(cudaMemcpyAsync(hb, bad.p, 16, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      g_launches += 2;
+      if (hb[0]) throw Status(AIWC_EEXEC, "non-finite predictor value");
+      if (hb[1]) throw Status(AIWC_EEXEC, "non-finite response value");
+    }
+    // presort on the device (presort.cu): argsorts, dense ranks, distinct values
+    DevBuf<uint32_t> sorted(size_t{p} * n), rank32(size_t{p} * n), counts(p);
+    DevBuf<double> vals_tmp(size_t{p} * n);
+    uint64_t nl = 0;
+    CK(gpu_presort(ctx->col.p, n, p, s, sorted.p, rank32.p, vals_tmp.p, counts.p, &nl));
+    g_launches += nl;
+    std::vector<uint32_t> cnt(p);
+    CK(cudaMemcpyAsync(cnt.data(), counts.p, p * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<uint64_t> voff(p + 1, 0);
     uint64_t maxk = 0;
-    for (uint32_t c = 0; c < p; ++c) maxk = std::max(maxk, voff[c + 1] - voff[c]);
+    for (uint32_t c = 0; c < p; ++c) {
+      voff[c + 1] = voff[c] + cnt[c];
+      maxk = std::max<uint64_t>(maxk, cnt[c]);
+    }
     ctx->rank_bytes = maxk <= 65536 ? 2 : 4;
     // listed columns: >= 3 distinct values (two-level columns are read off the payload)
     std::vector<int32_t> list_of(p, -1);
     std::vector<uint32_t> listed;
     for (uint32_t c = 0; c < p; ++c)
-      if (voff[c + 1] - voff[c] >= 3) {
+      if (cnt[c] >= 3) {
         list_of[c] = static_cast<int32_t>(listed.size());
         listed.push_back(c);
       }
     ctx->nlisted = static_cast<uint32_t>(listed.size());
     ctx->order_stride = static_cast<uint32_t>((n + 15) & ~uint64_t{15});
-    std::vector<uint32_t> packed(size_t{ctx->nlisted} * ctx->order_stride, 0u);
+    const size_t osz = std::max<size_t>(size_t{ctx->nlisted} * ctx->order_stride, 16);
+    ctx->order.alloc(osz);
+    CK(cudaMemsetAsync(ctx->order.p, 0, osz * 4, s));
     for (uint32_t i = 0; i < ctx->nlisted; ++i)
-      std::copy(order.begin() + size_t{listed[i]} * n, order.begin() + size_t{listed[i] + 1} * n,
-                packed.begin() + size_t{i} * ctx->order_stride);
-    ctx->col.alloc(size_t{p} * n);
-    ctx->dy.alloc(n);
-    ctx->order.alloc(std::max<size_t>(packed.size(), 16));
+      CK(cudaMemcpyAsync(ctx->order.p + size_t{i} * ctx->order_stride,
+                         sorted.p + size_t{listed[i]} * n, n * 4, cudaMemcpyDeviceToDevice, s));
+    ctx->rank.alloc(size_t{p} * n * ctx->rank_bytes);
+    if (ctx->rank_bytes == 2) {
+      CK(narrow_ranks(rank32.p, size_t{p} * n, reinterpret_cast<uint16_t*>(ctx->rank.p), s));
+      g_launches += 1;
+    } else {
+      CK(cudaMemcpyAsync(ctx->rank.p, rank32.p, size_t{p} * n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    ctx->vals.alloc(std::max<uint64_t>(voff[p], 1));
+    for (uint32_t c = 0; c < p; ++c)
+      CK(cudaMemcpyAsync(ctx->vals.p + voff[c], vals_tmp.p + size_t{c} * n, cnt[c] * 8,
+                         cudaMemcpyDeviceToDevice, s));
     ctx->list_of.alloc(p);
     ctx->listed.alloc(std::max<size_t>(listed.size(), 1));
-    CK(cudaMemcpy(ctx->list_of.p, list_of.data(), p * 4, cudaMemcpyHostToDevice));
-    if (!listed.empty())
-      CK(cudaMemcpy(ctx->listed.p, listed.data(), listed.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    ctx->rank.alloc(size_t{p} * n * ctx->rank_bytes);
-    ctx->vals.alloc(vals.size());
     ctx->vals_off.alloc(voff.size());
-    CK(cudaMemcpy(ctx->col.p, col, size_t{p} * n * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->dy.p, y, n * 8, cudaMemcpyHostToDevice));
-    if (!packed.empty())
-      CK(cudaMemcpy(ctx->order.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice));
-    if (ctx->rank_bytes == 2) {
-      std::vector<uint16_t> r16(rank.begin(), rank.end());
-      CK(cudaMemcpy(ctx->rank.p, r16.data(), r16.size() * 2, cudaMemcpyHostToDevice));
-    } else {
-      CK(cudaMemcpy(ctx->rank.p, rank.data(), rank.size() * 4, cudaMemcpyHostToDevice));
-    }
-    CK(cudaMemcpy(ctx->vals.p, vals.data(), vals.size() * 8, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->vals_off.p, voff.data(), voff.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->list_of.p, list_of.data(), p * 4, cudaMemcpyHostToDevice, s));
+    if (!listed.empty())
+      CK(cudaMemcpyAsync(ctx->listed.p, listed.data(), listed.size() * 4, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->vals_off.p, voff.data(), voff.size() * 8, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // the temporaries above are freed on return
     *out = ctx.release();
   });
 }

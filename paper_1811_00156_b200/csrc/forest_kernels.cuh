@@ -40,6 +40,16 @@ cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* node
                                  double total_trees, double* out, unsigned grid, size_t smem,
                                  size_t smem_max, cudaStream_t s);
 
+// device presort of a dataset (presort.cu): per column (value, row) argsort into
+// d_sorted (p x n), dense ranks into d_rank (p x n), distinct values into d_vals
+// (column c at c*n), distinct counts into d_counts (p)
+cudaError_t gpu_presort(const double* d_col, uint64_t n, uint32_t p, cudaStream_t s,
+                        uint32_t* d_sorted, uint32_t* d_rank, double* d_vals,
+                        uint32_t* d_counts, uint64_t* launches);
+cudaError_t narrow_ranks(const uint32_t* d_in, uint64_t count, uint16_t* d_out, cudaStream_t s);
+cudaError_t count_nonfinite(const double* d_v, uint64_t count, unsigned long long* d_bad,
+                            cudaStream_t s);
+
 // batched multi-kernel grower for one batch of trees (grow_wide.cuh)
 cudaError_t run_wide(int rank_bytes, const WideArgs& a, cudaStream_t st, int sms,
                      uint32_t* h_active, uint64_t* launches);
