@@ -124,6 +124,7 @@ struct WideArgs {
   uint32_t coop_min; // split nodes with >= coop_min rows are routed by one CTA each
   uint32_t* off[4];  // [B+1] prefixes: chain tasks, splits, positions, list chunks
   uint32_t* active;  // trees still splitting after this level's decide
+  uint32_t* task_ctr;  // dynamic task counters of this level's chain kernels (zeroed by w_prefix)
 };
 
 // bitmap words + prefix words the grower keeps in shared memory (or global)

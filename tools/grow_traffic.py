@@ -25,7 +25,7 @@ per = collections.defaultdict(lambda: collections.defaultdict(float))
 for r in rows[start + 1:]:
     if len(r) <= iv:
         continue
-    k = r[ik].split("(")[0].replace("void ", "")
+    k = r[ik].split("(")[0].replace("void ", "").replace("aiwc_b200::", "")
     v = float(r[iv].replace(",", "")) * unit.get(r[iu], 1.0)
     per[k][r[im]] += v
     per[k]["launches"] += 1 if r[im] == "gpu__time_duration.sum" else 0

@@ -16,7 +16,7 @@ agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[start + 1:]:
     if len(r) <= iv:
         continue
-    k = r[ik].split("(")[0].replace("void ", "")
+    k = r[ik].split("(")[0].replace("void ", "").replace("aiwc_b200::", "")
     agg[k][0] += 1
     agg[k][1] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-6)
 tot = sum(v[1] for v in agg.values())

@@ -19,7 +19,7 @@ names = []
 for r in rows[start + 1:]:
     if len(r) <= iv:
         continue
-    k = r[ik].split("(")[0].replace("void ", "").split("<")[0]
+    k = r[ik].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
     if k == "w_front":
         lv += 1
     if k not in names:
