@@ -395,14 +395,46 @@ def oob_prefix(forest: Forest, prepared: PreparedDataset, tree_counts) -> list:
     return [OobStats._from_c(o) for o in outs]
 
 
-def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int) -> np.ndarray:
+def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
+             workers: int = 2) -> np.ndarray:
     """C2 grid objective (tuner.hpp:247-253 / experiments.hpp:79-108): error_pct for
     every (mtry, min_node_size) cell x num.trees value, one fit of max(tree_counts)
-    trees per cell.  Returns an array [len(cells), len(tree_counts)]."""
+    trees per cell.  Returns an array [len(cells), len(tree_counts)].  `workers` host
+    threads, each with its own device copy of the dataset (a context serialises its
+    fits), keep several cells' fits in flight on the GPU at once."""
+    import threading
+
     cps = sorted(int(t) for t in tree_counts)
     out = np.zeros((len(cells), len(cps)))
-    for i, (m, mns) in enumerate(cells):
-        f = fit(prepared, ForestParams(cps[-1], m, mns, seed), compute_oob_stats=False)
-        out[i] = [s.error_pct for s in oob_prefix(f, prepared, cps)]
-        del f
+    workers = max(1, min(workers, len(cells)))
+    preps = [prepared] + [PreparedDataset(prepared.col, prepared.y, prepared.n, prepared.p,
+                                          prepared.device) for _ in range(workers - 1)]
+    nxt = [0]
+    lock = threading.Lock()
+    errors = []
+
+    def run(prep):
+        try:
+            while True:
+                with lock:
+                    i = nxt[0]
+                    nxt[0] += 1
+                if i >= len(cells):
+                    return
+                m, mns = cells[i]
+                f = fit(prep, ForestParams(cps[-1], m, mns, seed), compute_oob_stats=False)
+                out[i] = [s.error_pct for s in oob_prefix(f, prep, cps)]
+                del f
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(pp,)) for pp in preps]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for pp in preps[1:]:
+        pp.close()
+    if errors:
+        raise errors[0]
     return out
