@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     c3 += t3;
   }
   if (threadIdx.x == 0) {
-    if (which == 0) a.task_ctr[0] = 0u;
+    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = 0u;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
     a.off[2][a.B] = c2;
@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     const uint32_t e = P.ecls[st.E0 + st.E1 + k / m];  // class 2
     const uint32_t slot = e * m + k % m;
     const NodeWork nw_ = P.front[P.e2f[e]];
+    if (nw_.e - nw_.b >= a.coop_min) continue;  // w_chains_coop
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
@@ -476,10 +477,245 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
 
 // Huge split nodes (>= coop_min rows, column 0 listed) are routed by a whole CTA:
 // three producer warps gather blocks of kCoopBlock positions while warp 0 sums.
-// (A CTA per huge chain was measured slower than the pipelined warp chain: 8 warps'
-// three-stage pipelines keep more gathers in flight than one producer block.)
+// (The CTA-per-node kernels shorten each node's critical path but spend 4 warps per
+// chain: they pay off only when a lane's batch is small; the host sets coop_min.)
 constexpr int kCoopPerLane = 4;
 constexpr uint32_t kCoopBlock = 3 * 32 * kCoopPerLane;  // positions per block
+
+// ... and huge nodes (>= coop_min rows) one CTA per (node, column), with the chain's
+// sequential FP64 adds alone on one warp: a chain step costs one DADD latency (8 cycles
+// on B200) only if nothing else sits on that warp's critical path, so three producer
+// warps gather each block of kCB positions (list -> payload -> rank) into shared memory,
+// warp 0 runs the chain over the block writing the running value before every position,
+// and the producers then derive the integer weight prefix, the value boundaries and the
+// gains of that block from it.  Blocks flow through three shared-memory stages: while
+// warp 0 chains block i, the producers fill block i+1 and score block i-1.
+constexpr int kCoopW = 3;                                // producer warps
+constexpr int kCoopE = 4;                                // positions per producer lane
+constexpr uint32_t kCB = kCoopW * 32 * kCoopE;           // positions per block
+struct CoopStage {
+  double wy[kCB];   // addends (two-level chains: +0.0 for value-1 rows)
+  double pre[kCB];  // running sum before each position (written by warp 0)
+  uint32_t mu[kCB];
+  uint32_t rk[kCB];
+};
+
+template <typename RankT>
+__global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
+  __shared__ CoopStage S[3];
+  __shared__ uint32_t s_task, s_wsum[kCoopW], s_n0;
+  __shared__ double s_sl, s_bg[kCoopW];
+  __shared__ uint32_t s_w0;
+  __shared__ uint32_t s_bp[kCoopW];
+  const uint32_t total = a.off[2][a.B];
+  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
+  const unsigned lane = lane_id(), wid = warp_id();
+  const uint32_t pt = threadIdx.x - 32;  // producer thread index (wid > 0)
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(a.task_ctr + 1, 1u);
+    __syncthreads();
+    const uint32_t t = s_task;
+    __syncthreads();
+    if (t >= total) break;
+    const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
+    const SlotPtrs P = slot_ptrs(a, b);
+    const TreeState& ts = a.ts[b];
+    const uint32_t e = P.ecls[ts.E0 + ts.E1 + k / m];
+    const uint32_t slot = e * m + k % m;
+    const NodeWork nw = P.front[P.e2f[e]];
+    if (nw.e - nw.b < a.coop_min) continue;  // CTA-uniform: w_chains_warp's task
+    const uint32_t c = P.samp[slot];
+    const int32_t li = a.g.d.list_of[c];
+    const bool listed = li >= 0;
+    const uint32_t* list = P.lists + static_cast<size_t>(listed ? li : 0) * stride;
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const uint32_t R = nw.e - nw.b, nblk = (R + kCB - 1) / kCB;
+    // producers: a register pipeline over blocks -- at step i a producer lane writes
+    // block i+1 (ranks gathered at step i-1) into its stage, gathers the ranks of block
+    // i+2, the payload of block i+3 and the list entries of block i+4
+    uint32_t q4[kCoopE] = {}, row3[kCoopE] = {}, mu3[kCoopE] = {}, mu2[kCoopE] = {},
+             rk2[kCoopE] = {}, mu1[kCoopE] = {}, rk1[kCoopE] = {};
+    double wy3[kCoopE] = {}, wy2[kCoopE] = {}, wy1[kCoopE] = {};
+    auto pos = [&](int64_t blk, int j) -> int64_t {
+      return blk * kCB + (wid - 1) * 32 * kCoopE + j * 32 + lane;
+    };
+    auto step = [&](int64_t i) {
+#pragma unroll
+      for (int j = 0; j < kCoopE; ++j) {  // (mu1, wy1, rk1) <- block i+1 (ranks from step i-1)
+        mu1[j] = mu2[j];
+        wy1[j] = wy2[j];
+        rk1[j] = rk2[j];
+      }
+      if (i + 1 >= 0 && i + 1 < nblk) {  // block i+1 -> shared memory
+        CoopStage& st = S[(i + 1) % 3];
+#pragma unroll
+        for (int j = 0; j < kCoopE; ++j) {
+          const int64_t x = pos(i + 1, j);
+          uint32_t mu = x < R ? mu1[j] : 0u;
+          double wy = x < R ? wy1[j] : 0.0;
+          if (!listed && rk1[j] != 0u) {  // two-level: only value-0 rows enter the chain
+            mu = 0u;
+            wy = 0.0;
+          }
+          const uint32_t idx = static_cast<uint32_t>(x - (i + 1) * kCB);
+          st.wy[idx] = wy;
+          st.mu[idx] = mu;
+          st.rk[idx] = rk1[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCoopE; ++j) {  // ranks of block i+2
+        const int64_t x = pos(i + 2, j);
+        mu2[j] = mu3[j];
+        wy2[j] = wy3[j];
+        rk2[j] = (x >= 0 && x < R) ? rank_of(rk_c, row3[j]) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kCoopE; ++j) {  // payload of block i+3
+        const int64_t x = pos(i + 3, j);
+        if (x >= 0 && x < R) {
+          const Payload pv = P.pay[q4[j]];
+          row3[j] = pv.row;
+          mu3[j] = pv.mult;
+          wy3[j] = pv.wy;
+        } else {
+          row3[j] = 0u;
+          mu3[j] = 0u;
+          wy3[j] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kCoopE; ++j) {  // list entries of block i+4
+        const int64_t x = pos(i + 4, j);
+        q4[j] = (x >= 0 && x < R) ? (listed ? list[nw.b + x] : nw.b + static_cast<uint32_t>(x)) : 0u;
+      }
+    };
+    // producer scoring state: weight prefix carry, last rank, best gain (first max)
+    uint32_t wcarry = 0, last_rk = 0, n0 = 0;
+    double bg = -INFINITY;
+    uint32_t bp = 0xffffffffu;
+    auto score = [&](uint32_t blk) {
+      const CoopStage& st = S[blk % 3];
+      const uint32_t i0 = blk * kCB + pt * kCoopE;  // kCoopE consecutive positions
+      uint32_t mu[kCoopE], loc = 0;
+#pragma unroll
+      for (int j = 0; j < kCoopE; ++j) {
+        mu[j] = i0 + j < R ? st.mu[pt * kCoopE + j] : 0u;
+        loc += mu[j];
+      }
+      // exclusive prefix of the producer threads' sums (3 warps, producer-only barrier)
+      const uint32_t inc = warp_incl_scan(loc);
+      if (lane == 31) s_wsum[wid - 1] = inc;
+      asm volatile("bar.sync 1, 96;" ::: "memory");
+      uint32_t wpre = 0, btot = 0;
+#pragma unroll
+      for (int w = 0; w < kCoopW; ++w) {
+        wpre += (w < static_cast<int>(wid) - 1) ? s_wsum[w] : 0u;
+        btot += s_wsum[w];
+      }
+      uint32_t wb = wcarry + wpre + inc - loc;
+      if (listed) {
+        uint32_t prk = pt == 0 ? last_rk : st.rk[pt * kCoopE - 1];
+#pragma unroll
+        for (int j = 0; j < kCoopE; ++j) {
+          const uint32_t i = i0 + j;
+          if (i >= R) break;
+          const uint32_t rk = st.rk[pt * kCoopE + j];
+          if (i > 0 && rk != prk) {
+            const double gn = gain_at(st.pre[pt * kCoopE + j], static_cast<double>(wb), nw.w, nw.s);
+            if (gn > bg) {
+              bg = gn;
+              bp = nw.b + i;
+            }
+          }
+          wb += mu[j];
+          prk = rk;
+        }
+        const uint32_t nlast = min(kCB, R - blk * kCB);
+        last_rk = st.rk[nlast - 1];
+      } else {
+#pragma unroll
+        for (int j = 0; j < kCoopE; ++j)
+          if (i0 + j < R && st.rk[pt * kCoopE + j] == 0u) ++n0;
+      }
+      wcarry += btot;
+      asm volatile("bar.sync 1, 96;" ::: "memory");  // s_wsum reuse
+    };
+    if (wid > 0)
+      for (int64_t i = -4; i < 0; ++i) step(i);
+    __syncthreads();
+    double r = 0.0;  // warp 0: the chain
+    for (uint32_t i = 0; i <= nblk; ++i) {
+      if (wid == 0) {
+        if (i < nblk) {
+          CoopStage& st = S[i % 3];
+          constexpr int kW = 8;
+          double buf[kW];
+#pragma unroll
+          for (int j = 0; j < kW; ++j) buf[j] = st.wy[j];
+#pragma unroll 16
+          for (uint32_t j = 0; j < kCB; ++j) {
+            const double x = buf[j % kW];
+            if (j + kW < kCB) buf[j % kW] = st.wy[j + kW];
+            if (lane == 0) st.pre[j] = r;
+            r = __dadd_rn(r, x);
+          }
+        }
+      } else {
+        step(i);
+        if (i >= 1) score(i - 1);
+      }
+      __syncthreads();
+    }
+    // reduce the producers' best (first max: larger gain, then smaller position)
+    if (wid > 0) {
+      double g = bg;
+      uint32_t q = bp;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double og = __shfl_xor_sync(kFull, g, o);
+        const uint32_t op = __shfl_xor_sync(kFull, q, o);
+        if (og > g || (og == g && op < q)) {
+          g = og;
+          q = op;
+        }
+        n0 += __shfl_xor_sync(kFull, n0, o);
+      }
+      if (lane == 0) {
+        s_bg[wid - 1] = g;
+        s_bp[wid - 1] = q;
+        s_wsum[wid - 1] = n0;
+      }
+      if (pt == 0) s_w0 = wcarry;  // every producer carries the same weight total
+    } else if (lane == 0) {
+      s_sl = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double g = -INFINITY;
+      uint32_t q = 0xffffffffu, z = 0;
+      for (int w = 0; w < kCoopW; ++w) {
+        if (s_bg[w] > g || (s_bg[w] == g && s_bp[w] < q)) {
+          g = s_bg[w];
+          q = s_bp[w];
+        }
+        z += s_wsum[w];
+      }
+      if (!listed) {
+        if (z == 0 || z == R) {
+          g = -INFINITY;
+          q = 0xffffffffu;
+        } else {
+          g = gain_at(s_sl, static_cast<double>(s_w0), nw.w, nw.s);
+          q = nw.b + z;
+        }
+      }
+      P.res[slot] = ChainRes{g, q, 0u};
+    }
+    __syncthreads();
+  }
+}
 
 // ... mid nodes run one warp per node (or per group of 32/G of its columns), G lanes
 // per column (chain_grp) ...
@@ -1123,6 +1359,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
     WCK((w_chains_warp<RankT><<<wgrid, 256, 0, st>>>(a)));
+    WCK((w_chains_coop<RankT><<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(a)));
     switch (grp_width(a.g.mtry)) {
       case 32: WCK((w_chains_grp<RankT, 32, 4><<<wgrid, 256, 0, st>>>(a))); break;
       case 16: WCK((w_chains_grp<RankT, 16, 4><<<wgrid, 256, 0, st>>>(a))); break;
