@@ -684,6 +684,10 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         // CTA-per-chain / CTA-per-route for nodes >= coop_min rows: shorter critical
         // paths, more warps per node -- a win only when a lane's batch is too small to
         // keep the GPU busy (measured at C4: 64 trees +5 %, 200 trees -6 %, 1000 -7 %)
+        // lanes per chain for big nodes: 32 (a warp each) or 16 / 8 (lane groups)
+        uint32_t big_lanes = 16;
+        if (const char* e = std::getenv("AIWC_BIG_LANES")) big_lanes = static_cast<uint32_t>(std::atoi(e));
+        if (big_lanes != 8 && big_lanes != 16) big_lanes = 32;
         uint32_t coop_min = per <= 48 ? 32768u : 0xffffffffu;
         if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
         coop_min = std::max(coop_min, big_min);
@@ -701,6 +705,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
               w.B = std::min<uint32_t>(per, T - t0);
               w.big_min = big_min;
               w.coop_min = coop_min;
+              w.pair_big = big_lanes;
               w.t0 = t0;
               for (int i = 0; i < 4; ++i)
                 w.off[i] = woff.p + (size_t{k} * 4 + i) * (per + 1);

@@ -445,9 +445,9 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 
 // split chains (forest.hpp:268-297), three kernels over the size classes of w_front:
 // big nodes (>= big_min rows) run one warp per (node, column) ...
-template <typename RankT>
+template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
 __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
-  __shared__ double stage[8][64];
+  __shared__ double stage[8][GB == 32 ? 64 : 128];
   const uint32_t total = a.off[2][a.B];
   const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
@@ -464,6 +464,23 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     const uint32_t slot = e * m + k % m;
     const NodeWork nw_ = P.front[P.e2f[e]];
     if (nw_.e - nw_.b >= a.coop_min) continue;  // w_chains_coop
+    if (GB < 32) {  // 32/GB lane groups: sampled columns j .. j+32/GB-1 of the node
+      constexpr uint32_t NG = 32 / GB;
+      const uint32_t j = k % m;
+      if (j % NG) continue;
+      const uint32_t grp = lane_id() / GB, jj = j + grp;
+      const bool act = jj < m;
+      const uint32_t c = act ? P.samp[e * m + jj] : 0u;
+      const int32_t li = a.g.d.list_of[c];
+      double bg;
+      uint32_t bp;
+      chain_grp<RankT, (GB < 32 ? GB : 16), 4>(
+          act, li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride, nw_.b,
+          nw_.e, P.pay, rank + static_cast<size_t>(c) * n, nw_.w, nw_.s, bg, bp,
+          stage[warp_id()] + grp * 4 * GB);
+      if (act && (lane_id() % GB) == 0) P.res[e * m + jj] = ChainRes{bg, bp, 0u};
+      continue;
+    }
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
@@ -1358,7 +1375,12 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     a.cur = level & 1u;
     WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
-    WCK((w_chains_warp<RankT><<<wgrid, 256, 0, st>>>(a)));
+    if (a.pair_big == 16)
+      WCK((w_chains_warp<RankT, 16><<<wgrid, 256, 0, st>>>(a)));
+    else if (a.pair_big == 8)
+      WCK((w_chains_warp<RankT, 8><<<wgrid, 256, 0, st>>>(a)));
+    else
+      WCK((w_chains_warp<RankT, 32><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_chains_coop<RankT><<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(a)));
     switch (grp_width(a.g.mtry)) {
       case 32: WCK((w_chains_grp<RankT, 32, 4><<<wgrid, 256, 0, st>>>(a))); break;

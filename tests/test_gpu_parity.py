@@ -252,14 +252,19 @@ def test_wide_grower_random_tables(seed, monkeypatch):
                 col[c] = rng.integers(0, 2, size=n).astype(float)
         y = rng.normal(size=n)
         T, mns = 6, int(rng.integers(1, 6))
-        # (warp chains from 64 rows | CTA chains + routes from 200 rows | lane groups only)
-        for big_min, coop_min in (("64", "1000000"), ("64", "200"), ("1000000", "1000000")):
+        # big-node chains from 64 rows with 16 / 8 / 32 lanes per chain | CTA chains +
+        # routes from 200 rows | lane groups only
+        for big_min, coop_min, lanes in (("64", "1000000", "16"), ("64", "1000000", "8"),
+                                         ("64", "1000000", "32"), ("64", "200", "16"),
+                                         ("1000000", "1000000", "16")):
             monkeypatch.setenv("AIWC_BIG_MIN", big_min)
             monkeypatch.setenv("AIWC_COOP_MIN", coop_min)
+            monkeypatch.setenv("AIWC_BIG_LANES", lanes)
             prep = pkg.PreparedDataset(col, y, n, p)
             f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
             o = Oracle.fit(col, y, n, p, T, m, mns, seed)
-            assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min, coop_min)
+            assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, mns, big_min, coop_min,
+                                                         lanes)
 
 
 def test_oob_prefix_equals_separate_fits(c1, seed, golden):
