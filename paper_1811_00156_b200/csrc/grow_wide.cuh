@@ -445,9 +445,11 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 
 // split chains (forest.hpp:268-297), three kernels over the size classes of w_front:
 // big nodes (>= big_min rows) run one warp per (node, column) ...
+constexpr int kBigU = 4;
 template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
 __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
-  __shared__ double stage[8][GB == 32 ? 64 : 128];
+  constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
+  __shared__ double stage[8][GB == 32 ? 64 : 32 * UB];
   const uint32_t total = a.off[2][a.B];
   const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
@@ -474,10 +476,10 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
       const int32_t li = a.g.d.list_of[c];
       double bg;
       uint32_t bp;
-      chain_grp<RankT, (GB < 32 ? GB : 16), 4>(
+      chain_grp<RankT, (GB < 32 ? GB : 16), UB>(
           act, li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride, nw_.b,
           nw_.e, P.pay, rank + static_cast<size_t>(c) * n, nw_.w, nw_.s, bg, bp,
-          stage[warp_id()] + grp * 4 * GB);
+          stage[warp_id()] + grp * UB * GB);
       if (act && (lane_id() % GB) == 0) P.res[e * m + jj] = ChainRes{bg, bp, 0u};
       continue;
     }
