@@ -10,11 +10,12 @@ rows = list(csv.reader(open(sys.argv[1])))
 start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[start]
 ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+im = h.index("Metric Name")
 scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3,
          "ms": 1.0}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[start + 1:]:
-    if len(r) <= iv:
+    if len(r) <= iv or r[im] != "gpu__time_duration.sum":
         continue
     k = r[ik].split("(")[0].replace("void ", "").replace("aiwc_b200::", "")
     agg[k][0] += 1
