@@ -598,7 +598,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     }
     const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
     DevBuf<TreeState> wts(wide ? slots : 0);
-    DevBuf<uint32_t> woff(wide ? 4 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
+    DevBuf<uint32_t> woff(wide ? 5 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
         wctr(wide ? 4 * nlanes : 0);
     std::unique_ptr<uint32_t, void (*)(uint32_t*)> h_active(
         [] {
@@ -707,8 +707,8 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
               w.coop_min = coop_min;
               w.pair_big = big_lanes;
               w.t0 = t0;
-              for (int i = 0; i < 4; ++i)
-                w.off[i] = woff.p + (size_t{k} * 4 + i) * (per + 1);
+              for (int i = 0; i < 5; ++i)
+                w.off[i] = woff.p + (size_t{k} * 5 + i) * (per + 1);
               w.active = wactive.p + k;
               w.task_ctr = wctr.p + 4 * k;
               uint64_t nl = 0;

@@ -73,7 +73,7 @@ struct SlotLayout {
   size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
       off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
-      off_ecls;
+      off_ecls, off_wsplit;
   size_t bytes;
 };
 
@@ -111,6 +111,7 @@ struct TreeState {
   uint32_t E0, E1, E2;  // eligible nodes by size class: small (lane chains), mid (lane
                         // groups), big (warp per chain)
   uint32_t Sbig;        // split nodes routed by a CTA (column 0 listed, >= coop_min rows)
+  uint32_t Swarp;       // split nodes routed by a warp (the rest of those >= kLaneMax rows)
   unsigned long long elig_base, split_rows;
 };
 
@@ -123,7 +124,7 @@ struct WideArgs {
   uint32_t big_min;  // nodes with >= big_min rows run one warp per chain (else lane groups)
   uint32_t coop_min; // split nodes with >= coop_min rows are routed by one CTA each
   uint32_t pair_big; // lanes per chain for big nodes: 32 (warp), 16 or 8 (lane groups)
-  uint32_t* off[4];  // [B+1] prefixes: chain tasks, splits, positions, list chunks
+  uint32_t* off[5];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp routes
   uint32_t* active;  // trees still splitting after this level's decide
   uint32_t* task_ctr;  // dynamic task counters of this level's chain kernels (zeroed by w_prefix)
 };

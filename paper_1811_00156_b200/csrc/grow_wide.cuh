@@ -25,6 +25,7 @@ struct SlotPtrs {
   SegTab* segtab;
   uint32_t* e2f;
   uint32_t* ecls;
+  uint32_t* wsplit;
   uint16_t* samp;
   ChainRes* res;
   SplitInfo* spl;
@@ -58,6 +59,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.segtab = reinterpret_cast<SegTab*>(s + L.off_segtab);
   p.e2f = reinterpret_cast<uint32_t*>(s + L.off_e2f);
   p.ecls = reinterpret_cast<uint32_t*>(s + L.off_ecls);
+  p.wsplit = reinterpret_cast<uint32_t*>(s + L.off_wsplit);
   p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
   p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
   p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
@@ -401,10 +403,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
   for (uint32_t base = 0; base < a.B; base += NT) {
     const uint32_t b = base + threadIdx.x;
-    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
@@ -416,6 +418,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
         v1 = s.S;
         v2 = s.A;
         v3 = nchunks_of(s.A, a.g.d.nlisted);
+        v4 = s.Swarp;
       }
     }
     uint32_t t0, t1, t2, t3;
@@ -423,18 +426,26 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
     const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
     const uint32_t e3 = block_excl_scan<NT>(v3, sh, &t3);
+    uint32_t t4;
+    const uint32_t e4 = block_excl_scan<NT>(v4, sh, &t4);
     if (b < a.B) {
       a.off[0][b] = c0 + e0;
       a.off[1][b] = c1 + e1;
       a.off[2][b] = c2 + e2;
       a.off[3][b] = c3 + e3;
+      if (which == 1) a.off[4][b] = c4 + e4;
     }
     c0 += t0;
     c1 += t1;
     c2 += t2;
     c3 += t3;
+    c4 += t4;
   }
   if (threadIdx.x == 0) {
+    if (which == 1) {
+      a.off[4][a.B] = c4;
+      a.task_ctr[2] = 0u;
+    }
     if (which == 0) a.task_ctr[0] = a.task_ctr[1] = 0u;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
@@ -807,7 +818,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
   const bool coop_route = d.list_of[0] >= 0;
-  uint32_t carry = 0, ccarry = 0, bcarry = 0;
+  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
     const uint32_t e = base + threadIdx.x;
     uint32_t sp = 0, c = 0, thr_rank = 0;
@@ -869,6 +880,11 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     const uint32_t bex = block_excl_scan<NT>(big, sh, &btot);
     if (big) P.ecls[bcarry + bex] = carry + ex;
     bcarry += btot;
+    const uint32_t wsp = sp && !big && cnt >= kLaneMax ? 1u : 0u;  // warp-routed splits
+    uint32_t wtot;
+    const uint32_t wex = block_excl_scan<NT>(wsp, sh, &wtot);
+    if (wsp) P.wsplit[wcarry + wex] = carry + ex;
+    wcarry += wtot;
     if (sp) {
       const uint32_t s = carry + ex;
       const uint32_t child = nodes0 + 2 * s;
@@ -893,6 +909,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   if (threadIdx.x == 0) {
     st.S = carry;
     st.Sbig = bcarry;
+    st.Swarp = wcarry;
     st.A_next = ccarry;
     st.split_rows += ccarry;
     st.elig_base += E;
@@ -917,15 +934,28 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   const int32_t list0 = a.g.d.list_of[0];
   const uint32_t k0levels = static_cast<uint32_t>(a.g.d.vals_off[1] - a.g.d.vals_off[0]);
-  const uint32_t id = kWarp ? (blockIdx.x * blockDim.x + threadIdx.x) >> 5
-                            : blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t step = kWarp ? (gridDim.x * blockDim.x) >> 5 : gridDim.x * blockDim.x;
-  for (uint32_t t = id; t < total; t += step) {
-    const uint32_t b = owner(a.off[1], a.B, t), s = t - a.off[1][b];
+  // warps claim the compacted warp-routed splits dynamically; lanes stride over all
+  // splits and take the small ones
+  const uint32_t wtotal = a.off[4][a.B];
+  const uint32_t id = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t it = id;; it += step) {
+    uint32_t b, s;
+    if (kWarp) {
+      uint32_t t = 0;
+      if (lane_id() == 0) t = atomicAdd(a.task_ctr + 2, 1u);
+      t = __shfl_sync(kFull, t, 0);
+      if (t >= wtotal) break;
+      b = owner(a.off[4], a.B, t);
+      s = slot_ptrs(a, b).wsplit[t - a.off[4][b]];
+    } else {
+      if (it >= total) break;
+      b = owner(a.off[1], a.B, it);
+      s = it - a.off[1][b];
+    }
     const SlotPtrs P = slot_ptrs(a, b);
     const SplitInfo si = P.spl[s];
-    if (kWarp != (si.cnt >= kLaneMax)) continue;
-    if (list0 >= 0 && si.cnt >= a.coop_min) continue;  // w_route_coop
+    if (!kWarp && si.cnt >= kLaneMax) continue;
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
