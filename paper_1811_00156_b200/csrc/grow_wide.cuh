@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
       a.off[4][a.B] = c4;
       a.task_ctr[2] = 0u;
     }
-    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = 0u;
+    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = 0u;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
     a.off[2][a.B] = c2;
@@ -753,11 +753,14 @@ template <typename RankT, int G, int U>
 __global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
   __shared__ double stage[8][32 * U];
   const uint32_t total = a.off[1][a.B];
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const uint32_t tpn = grp_tasks_per_node(m), grp = lane_id() / G;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
-  for (uint32_t t = gw; t < total; t += nw) {
+  for (;;) {  // tasks claimed dynamically
+    uint32_t t = 0;
+    if (lane_id() == 0) t = atomicAdd(a.task_ctr + 3, 1u);
+    t = __shfl_sync(kFull, t, 0);
+    if (t >= total) break;
     const uint32_t b = owner(a.off[1], a.B, t), k = t - a.off[1][b];
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
