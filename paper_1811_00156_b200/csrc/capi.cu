@@ -1009,6 +1009,7 @@ int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
 namespace {
 
 constexpr int kPredNT = kPredictThreads;
+constexpr uint64_t kSmallQ = 4096;  // up to this many rows predict without binning
 constexpr size_t kPredSmem = 220 * 1024;  // per-CTA budget: chunk nodes+leaves + bin tile
 
 // Build the binned copy: per column the sorted distinct thresholds the forest uses,
@@ -1160,6 +1161,13 @@ void build_binned_once(aiwc_forest* f, uint32_t p) { build_binned(f, p); }
 // else the L2 walk (predict_kernel)
 void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
                       double* d_out, cudaStream_t s, PredScratch& sc) {
+  if (q <= kSmallQ && !f->bin_ready) {  // a handful of rows: no binned copy
+    predict_small_kernel<<<static_cast<unsigned>((q + 7) / 8), 256, 0, s>>>(
+        f->packed.p, f->d_off.p, f->trees, d_rows, q, p, d_out);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    return;
+  }
   build_binned(f, p);
   if (f->bin_ok) {
     predict_binned(f, d_rows, q, p, d_out, s, sc);

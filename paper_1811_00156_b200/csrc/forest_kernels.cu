@@ -133,6 +133,42 @@ __global__ void predict_kernel(const PredNode* __restrict__ nodes,
   out[i] = __ddiv_rn(s, static_cast<double>(T));
 }
 
+// Few queries (e.g. the 60 held-out rows of an evaluate fold): one warp per query, the
+// lanes walk 32 trees at a time from L2, and the warp adds the 32 leaf values in tree
+// order (forest.hpp:77-81) -- no binned copy of the forest is built for them.
+__global__ void __launch_bounds__(256) predict_small_kernel(const PredNode* __restrict__ nodes,
+                                                            const uint64_t* __restrict__ off,
+                                                            uint32_t T,
+                                                            const double* __restrict__ rows,
+                                                            uint64_t q, uint32_t p,
+                                                            double* __restrict__ out) {
+  __shared__ double st[8][32];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+  const uint64_t i = blockIdx.x * uint64_t{8} + w;
+  if (i >= q) return;  // warp-uniform
+  const double* x = rows + i * p;
+  double s = 0.0;
+  for (uint32_t t0 = 0; t0 < T; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    double leaf = 0.0;
+    if (t < T) {
+      const PredNode* nd = nodes + __ldg(off + t);
+      PredNode v = nd[0];
+      while (v.feature >= 0) {
+        const int32_t k = __ldg(x + v.feature) <= v.thr ? v.left : v.left + 1;
+        v = nd[k];
+      }
+      leaf = v.thr;
+    }
+    st[w][lane] = leaf;
+    __syncwarp();
+    const uint32_t cnt = T - t0 < 32 ? T - t0 : 32;
+    for (uint32_t j = 0; j < cnt; ++j) s = __dadd_rn(s, st[w][j]);
+    __syncwarp();
+  }
+  if (lane == 0) out[i] = __ddiv_rn(s, static_cast<double>(T));
+}
+
 // ---- shared-memory predict over binned queries ------------------------------------
 // Threshold binning: with T_c the sorted distinct thresholds the forest uses on column
 // c and thr = T_c[j],  x <= thr  <=>  #{t in T_c : t < x} <= j.  NaN goes to the

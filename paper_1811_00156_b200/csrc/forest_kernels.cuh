@@ -73,6 +73,8 @@ __global__ void oob_walk_kernel(const PredNode* nodes, const uint64_t* off,
                                 double* oobval);
 __global__ void make_queries_kernel(const double* rows, uint64_t n, uint32_t p, uint64_t q,
                                     uint64_t seed, uint64_t tag, double* out);
+__global__ void predict_small_kernel(const PredNode* nodes, const uint64_t* off, uint32_t T,
+                                     const double* rows, uint64_t q, uint32_t p, double* out);
 __global__ void predict_kernel(const PredNode* nodes, const uint64_t* off, uint32_t T,
                                const double* rows, uint64_t q, uint32_t p, double* out);
 
