@@ -465,6 +465,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
                      "cell": cells[int(err.argmin() // len(counts))],
                      "num_trees": counts[int(err.argmin() % len(counts))]}}
     prm = pkg.ForestParams(505, 30, 9, 0)
+    _ = pkg.evaluate(t, prm, seed, device=local, folds=(0, 1))  # warm-up
     barrier()
     s = time.perf_counter()
     part = pkg.evaluate(t, prm, seed, device=local, folds=shard.fold_range(rank, world, t.kernels))
