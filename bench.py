@@ -337,9 +337,9 @@ def main():
         predict = bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
 
     # ---------------- C2 grid + C3 hold-one-kernel-out (sharded by cell / fold) -----------
-    grid = loko = None
+    grid = loko = c1 = None
     if not args.skip_grid:
-        grid, loko = bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks)
+        grid, loko, c1 = bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks)
 
     if cpu_thread:
         cpu_thread.join(timeout=1200)
@@ -380,6 +380,7 @@ def main():
         "cpu_baseline": ({k: cpu_res.get(k) for k in ("value", "unit", "cores", "kind", "sample")}
                          if cpu_res else None),
         "predict": predict,
+        "c1": c1,
         "grid": grid,
         "loko": loko,
     }
@@ -457,6 +458,22 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
                              lambda cs: pkg.grid_oob(prep, cs, counts, seed), allreduce)
     barrier()
     gs = max_over_ranks(time.perf_counter() - s)
+    # C1: the paper-shaped table itself -- 500-tree fit (OOB included) + predict of its
+    # 2220 rows, the reference's configs[0]
+    c1p = pkg.ForestParams(500, 6, 5, seed)
+    rows = t.predictor_rows()
+    _ = pkg.fit(prep, c1p).predict_response(rows)
+    ts = []
+    for _ in range(5):
+        s = time.perf_counter()
+        f1 = pkg.fit(prep, c1p)
+        _ = f1.oob
+        _ = f1.predict_response(rows)
+        ts.append(time.perf_counter() - s)
+    c1 = {"workload": "C1: 2220 x 42 paper-shaped table, 500 trees m=6 mns=5, fit (OOB "
+                      "included) + predict_response of all 2220 rows, host buffers",
+          "trees_per_s": 500 / float(np.median(ts)), "s": float(np.median(ts)),
+          "oob_error_pct": f1.oob.error_pct}
     grid = {"workload": f"C2 sample: {len(cells)} (mtry, min.node.size) cells x 20 num.trees "
                         "values (50..1000) on the C1 table, one 1000-tree fit per cell",
             "cells_per_s": len(cells) / gs, "grid_points_per_s": len(cells) * len(counts) / gs,
@@ -476,7 +493,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     loko = {"workload": "C3: evaluate(C1, 505/30/9): 37 folds x 60 held-out rows",
             "folds_per_s": t.kernels / ls, "s": ls, "mape_pct": float(err_row.mean())}
     del prep
-    return grid, loko
+    return grid, loko, c1
 
 
 ARGS = None
