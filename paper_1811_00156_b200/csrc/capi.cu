@@ -685,6 +685,8 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         // paths, more warps per node -- a win only when a lane's batch is too small to
         // keep the GPU busy (measured at C4: 64 trees +5 %, 200 trees -6 %, 1000 -7 %)
         // lanes per chain for big nodes: 32 (a warp each) or 16 / 8 (lane groups)
+        uint32_t lane_max = 16;  // rows below which a node's chains run one lane each (measured)
+        if (const char* e = std::getenv("AIWC_LANE_MAX")) lane_max = static_cast<uint32_t>(std::atoi(e));
         uint32_t big_lanes = 16;
         if (const char* e = std::getenv("AIWC_BIG_LANES")) big_lanes = static_cast<uint32_t>(std::atoi(e));
         if (big_lanes != 8 && big_lanes != 16) big_lanes = 32;
@@ -706,6 +708,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
               w.big_min = big_min;
               w.coop_min = coop_min;
               w.pair_big = big_lanes;
+              w.lane_max = lane_max;
               w.t0 = t0;
               for (int i = 0; i < 5; ++i)
                 w.off[i] = woff.p + (size_t{k} * 5 + i) * (per + 1);

@@ -124,6 +124,7 @@ struct WideArgs {
   uint32_t big_min;  // nodes with >= big_min rows run one warp per chain (else lane groups)
   uint32_t coop_min; // split nodes with >= coop_min rows are routed by one CTA each
   uint32_t pair_big; // lanes per chain for big nodes: 32 (warp), 16 or 8 (lane groups)
+  uint32_t lane_max; // nodes below this many rows run one lane per chain
   uint32_t* off[5];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp routes
   uint32_t* active;  // trees still splitting after this level's decide
   uint32_t* task_ctr;  // dynamic task counters of this level's chain kernels (zeroed by w_prefix)

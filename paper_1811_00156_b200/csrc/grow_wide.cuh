@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       if (e < E) {
         const NodeWork& nw = fr[P.e2f[e]];
         const uint32_t R = nw.e - nw.b;
-        const uint32_t c = R < kLaneMax ? 0u : (R < a.big_min ? 1u : 2u);
+        const uint32_t c = R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u);
         in = c == cls;
       }
       uint32_t tot;

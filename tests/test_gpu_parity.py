@@ -260,6 +260,7 @@ def test_wide_grower_random_tables(seed, monkeypatch):
             monkeypatch.setenv("AIWC_BIG_MIN", big_min)
             monkeypatch.setenv("AIWC_COOP_MIN", coop_min)
             monkeypatch.setenv("AIWC_BIG_LANES", lanes)
+            monkeypatch.setenv("AIWC_LANE_MAX", "48" if lanes == "8" else "16")
             prep = pkg.PreparedDataset(col, y, n, p)
             f = pkg.fit(prep, pkg.ForestParams(T, m, mns, seed))
             o = Oracle.fit(col, y, n, p, T, m, mns, seed)
