@@ -114,6 +114,16 @@ struct Stream {
   }
 };
 
+// host threads for the pinned <-> pageable copies (AIWC_COPY_THREADS, default 8)
+unsigned copy_threads() {
+  static const unsigned n = [] {
+    unsigned v = 8;
+    if (const char* e = std::getenv("AIWC_COPY_THREADS")) v = static_cast<unsigned>(std::atoi(e));
+    return std::max(1u, std::min(v, std::max(1u, std::thread::hardware_concurrency())));
+  }();
+  return n;
+}
+
 // Device -> pageable host copy through two pinned bounce buffers (allocated once per
 // process): the DMA of chunk i+1 overlaps the multi-threaded host copy of chunk i, so
 // large exports (10 GB of C4 nodes) run at PCIe speed instead of the driver's pageable
@@ -149,7 +159,7 @@ void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
                        cudaMemcpyDeviceToHost, s));
     CK(cudaEventRecord(ev[i & 1], s));
   };
-  const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned nt = copy_threads();
   issue(0);
   for (size_t i = 0; i < nchunk; ++i) {
     if (i + 1 < nchunk) issue(i + 1);  // buffer (i+1)&1 was drained in iteration i-1
@@ -195,7 +205,7 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
       cudaEventDestroy(e[1]);
     }
   } eg{ev};
-  const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned nt = copy_threads();
   const size_t nchunk = (bytes + kChunk - 1) / kChunk;
   for (size_t i = 0; i < nchunk; ++i) {
     if (i >= 2) CK(cudaEventSynchronize(ev[i & 1]));  // DMA out of this buffer finished
