@@ -114,10 +114,10 @@ struct Stream {
   }
 };
 
-// host threads for the pinned <-> pageable copies (AIWC_COPY_THREADS, default 8)
+// host threads for the pinned <-> pageable copies (AIWC_COPY_THREADS, default 16)
 unsigned copy_threads() {
   static const unsigned n = [] {
-    unsigned v = 8;
+    unsigned v = 16;
     if (const char* e = std::getenv("AIWC_COPY_THREADS")) v = static_cast<unsigned>(std::atoi(e));
     return std::max(1u, std::min(v, std::max(1u, std::thread::hardware_concurrency())));
   }();
