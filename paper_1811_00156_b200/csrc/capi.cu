@@ -602,7 +602,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     } scratch_release{ctx->scratch};
     int nlanes = 1;
     if (wide) {
-      nlanes = 2;
+      nlanes = 4;  // concurrent batches (streams + host threads); 2 -> 4 measured +3 %
       if (const char* e = std::getenv("AIWC_WIDE_LANES")) nlanes = std::max(1, std::atoi(e));
       nlanes = std::max(1, std::min(nlanes, slots));
     }
