@@ -300,7 +300,7 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
                              double S, double& best_gain, uint32_t& best_pos, double* st) {
   const unsigned lane = lane_id();
   double sl = 0.0, bg = -INFINITY;
-  uint32_t wl = 0, prev_rank = 0, bp = 0xffffffffu, n0 = 0;
+  uint32_t wl = 0, prev_rank = 0, bp = 0xffffffffu, n0 = 0, wl_lane = 0;
   bool first = true;
   uint32_t qn[G], rowc[G], muc[G], rown[G], mun[G];
   double wyc[G], wyn[G];
@@ -373,7 +373,7 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
       } else {  // two-level column: value-0 rows in row order, +0.0 for the others
         const bool z = valid && rk[g] == 0u;
         n0 += __popc(__ballot_sync(kFull, z));
-        wl += warp_sum(z ? muc[g] : 0u);
+        wl_lane += z ? muc[g] : 0u;  // integer: reduced once at the end
         st[lane] = z ? wyc[g] : 0.0;
         __syncwarp();
         double r = sl;
@@ -393,6 +393,7 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
       wyn[g] = wynn[g];
     }
   }
+  if (!listed) wl = warp_sum(wl_lane);
   if (listed) {
     warp_best(bg, bp);
     best_gain = bg;
@@ -785,6 +786,7 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
                              RouteOut& o, double* st /* 4*32 doubles */) {
   const unsigned lane = lane_id(), grp = lane >> 3;
   double acc = 0.0;  // this lane's group chain: 0 sl, 1 ql, 2 sr, 3 qr
+  uint32_t wl_lane = 0, wr_lane = 0;
   uint32_t qn[G], qc[G], rowc[G], muc[G], rown[G], mun[G];
   double wyc[G], yyc[G], wyn[G], yyn[G];
   auto load_q = [&](uint32_t k0, uint32_t (&q)[G]) {
@@ -842,8 +844,8 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
       const bool left = lft[g] <= thr_rank;
       if (left) atomicOr(bits + (qc[g] >> 5), 1u << (qc[g] & 31u));
       o.nl += __popc(__ballot_sync(kFull, left));
-      o.wl += warp_sum(left ? muc[g] : 0u);
-      o.wr += warp_sum((valid && !left) ? muc[g] : 0u);
+      wl_lane += left ? muc[g] : 0u;  // integer weights: reduced once at the end
+      wr_lane += (valid && !left) ? muc[g] : 0u;
       st[lane] = left ? wyc[g] : 0.0;
       st[32 + lane] = left ? yyc[g] : 0.0;
       st[64 + lane] = (valid && !left) ? wyc[g] : 0.0;
@@ -871,6 +873,8 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
       yyn[g] = yynn[g];
     }
   }
+  o.wl += warp_sum(wl_lane);
+  o.wr += warp_sum(wr_lane);
   o.sl = __shfl_sync(kFull, acc, 0);
   o.ql = __shfl_sync(kFull, acc, 8);
   o.sr = __shfl_sync(kFull, acc, 16);
