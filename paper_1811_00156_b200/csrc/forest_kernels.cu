@@ -233,14 +233,39 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ __align__(16) unsigned char smem[];
   NodeT* sn = reinterpret_cast<NodeT*>(smem);
   double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(NodeT) + 15) & ~size_t{15}));
-  BinT* sb = reinterpret_cast<BinT*>(reinterpret_cast<unsigned char*>(sl) + nleaves * 8);
+  BinT* sb = reinterpret_cast<BinT*>(reinterpret_cast<unsigned char*>(sl) +
+                                     ((size_t{nleaves} * 8 + 15) & ~size_t{15}));
   for (uint32_t i = threadIdx.x; i < nnodes; i += NT) sn[i] = nodes[i];
   for (uint32_t i = threadIdx.x; i < nleaves; i += NT) sl[i] = leaves[i];
   for (uint64_t tile = uint64_t{blockIdx.x} * TQ; tile < q; tile += uint64_t{gridDim.x} * TQ) {
     __syncthreads();
     const uint64_t rem = q - tile;
     const uint32_t cnt = rem < TQ ? static_cast<uint32_t>(rem) : TQ;
-    for (uint32_t i = threadIdx.x; i < cnt * p; i += NT) sb[i] = bins[tile * p + i];
+    {  // stage the tile's bins: 16-byte vector copies, all of a thread's loads in flight
+      const size_t bytes = size_t{cnt} * p * sizeof(BinT);
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(bins + tile * p);
+      unsigned char* dst = reinterpret_cast<unsigned char*>(sb);
+      const bool vec = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+      size_t done16 = 0;
+      if (vec) {
+        const size_t n16 = bytes / 16;
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+        size_t i = threadIdx.x;
+        for (; i + 3 * NT < n16; i += 4 * NT) {
+          const uint4 a0 = __ldg(s4 + i), a1 = __ldg(s4 + i + NT), a2 = __ldg(s4 + i + 2 * NT),
+                      a3 = __ldg(s4 + i + 3 * NT);
+          d4[i] = a0;
+          d4[i + NT] = a1;
+          d4[i + 2 * NT] = a2;
+          d4[i + 3 * NT] = a3;
+        }
+        for (; i < n16; i += NT) d4[i] = __ldg(s4 + i);
+        done16 = n16 * 16;
+      }
+      for (size_t i = done16 + threadIdx.x; i < bytes; i += NT) dst[i] = src[i];
+    }
     __syncthreads();
     if (threadIdx.x >= cnt) continue;
     const BinT* bq[Q];
