@@ -114,6 +114,35 @@ struct Stream {
   }
 };
 
+// 64 pinned uint32 flags, recycled through a process-wide free list
+struct PinnedFlags {
+  uint32_t* p = nullptr;
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<uint32_t*>& pool() {
+    static std::vector<uint32_t*> v;
+    return v;
+  }
+  PinnedFlags() {
+    {
+      std::lock_guard<std::mutex> g(mu());
+      if (!pool().empty()) {
+        p = pool().back();
+        pool().pop_back();
+        return;
+      }
+    }
+    CK(cudaMallocHost(reinterpret_cast<void**>(&p), 64 * 4));
+  }
+  ~PinnedFlags() {
+    std::lock_guard<std::mutex> g(mu());
+    pool().push_back(p);
+  }
+  uint32_t* get() const { return p; }
+};
+
 // host threads for the pinned <-> pageable copies (AIWC_COPY_THREADS, default 16)
 unsigned copy_threads() {
   static const unsigned n = [] {
@@ -610,13 +639,10 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     DevBuf<TreeState> wts(wide ? slots : 0);
     DevBuf<uint32_t> woff(wide ? 5 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
         wctr(wide ? 4 * nlanes : 0);
-    std::unique_ptr<uint32_t, void (*)(uint32_t*)> h_active(
-        [] {
-          uint32_t* p = nullptr;
-          cudaMallocHost(&p, 64 * 4);
-          return p;
-        }(),
-        [](uint32_t* p) { cudaFreeHost(p); });
+    // per-lane "trees still splitting" flags read back every level: a pinned buffer per
+    // fit, taken from a process-wide pool (cudaMallocHost / cudaFreeHost synchronise
+    // and cost milliseconds -- too much for the many small fits of a grid search)
+    PinnedFlags h_active;
     std::vector<cudaStream_t> lane_streams;
     struct StreamsGuard {
       std::vector<cudaStream_t>& v;
