@@ -581,8 +581,16 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     else
       CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
     if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
-    size_t free_b = 0, total_b = 0;
-    CK(cudaMemGetInfo(&free_b, &total_b));
+    const bool tprof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
+    auto tmark = [&](const char* what) {
+      if (!tprof) return;
+      static thread_local auto last = std::chrono::steady_clock::now();
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[aiwc setup] %s %.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - last).count());
+      last = now;
+    };
+    tmark("start");
     // outputs first: in-bag draws, OOB leaf values, node pool
     auto f = std::make_unique<aiwc_forest>();
     f->device = dev;
@@ -596,13 +604,30 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     f->inbag.alloc(size_t{T} * n);
     f->oobval.alloc(size_t{T} * n);
     CK(cudaMemsetAsync(f->oobval.p, 0xff, size_t{T} * n * 8, st.s));
+    tmark("inbag+oobval");
     a.inbag = f->inbag.p;
     a.oobval = f->oobval.p;
 
     uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
     int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
-    CK(cudaMemGetInfo(&free_b, &total_b));
-    {
+    // node pool (28 B/node) plus the compacted forest built from it after growth
+    // (feature, left, thr, value, PredNode: 40 B/node) stay outside the slot scratch
+    const size_t pool_bytes = cap * (28 + 40);
+    // cudaMemGetInfo can stall for tens of milliseconds: small fits (a grid search's
+    // thousands of C1-size fits) skip the free-memory budget when they need under 1/16
+    // of the device
+    static size_t total_mem[64] = {};
+    size_t free_b = 0, total_b = 0;
+    if (dev < 64 && total_mem[dev] == 0) {
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      total_mem[dev] = total_b;
+    }
+    const size_t dev_total = dev < 64 ? total_mem[dev] : 0;
+    const bool small = dev_total && pool_bytes + size_t(slots) * L.bytes < dev_total / 16;
+    if (small) {
+      free_b = dev_total;  // ample: the budget below keeps every slot
+    } else {
+      CK(cudaMemGetInfo(&free_b, &total_b));
       // memory parked in the stream-ordered pool (and this ctx's scratch, which is
       // reused or replaced) is available too; cudaMemGetInfo does not count it
       cudaMemPool_t mp;
@@ -614,14 +639,13 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
         free_b += reserved - used_now;
       free_b += ctx->scratch.count;
     }
-    // node pool (28 B/node) plus the compacted forest built from it after growth
-    // (feature, left, thr, value, PredNode: 40 B/node) stay outside the slot scratch
-    const size_t pool_bytes = cap * (28 + 40);
     const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
     slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
     if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
     const size_t need = size_t(slots) * L.bytes;
+    tmark("budget");
     if (ctx->scratch.count < need) ctx->scratch.alloc(need);
+    tmark("scratch");
     a.scratch = ctx->scratch.p;
     // hand the slots back to the stream-ordered pool when the fit ends (the pool keeps
     // them reserved, so the next fit -- on this or another dataset -- reuses them)
@@ -689,6 +713,7 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
     cudaEvent_t evs[4] = {ev0, ev1, evf0, evf1};
     EvGuard eg{evs};
     CK(cudaEventRecord(evf0, st.s));
+        tmark("streams+events+pool");
     const auto t_grow0 = std::chrono::steady_clock::now();
     for (int attempt = 0; attempt < 2; ++attempt) {
       pf.alloc(cap);
