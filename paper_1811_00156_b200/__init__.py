@@ -396,7 +396,7 @@ def oob_prefix(forest: Forest, prepared: PreparedDataset, tree_counts) -> list:
 
 
 def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
-             workers: int = 2) -> np.ndarray:
+             workers: int = 1) -> np.ndarray:
     """C2 grid objective (tuner.hpp:247-253 / experiments.hpp:79-108): error_pct for
     every (mtry, min_node_size) cell x num.trees value, one fit of max(tree_counts)
     trees per cell.  Returns an array [len(cells), len(tree_counts)].  `workers` host
