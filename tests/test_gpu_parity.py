@@ -299,3 +299,19 @@ def test_evaluate_fold_ranges_combine(c1, seed):
              for r in range(2)]
     ref = np.load(os.path.join(GOLD, "c3_50_6_5_pred.npy"))
     assert np.array_equal((parts[0] + parts[1]).view(np.uint64), ref.view(np.uint64))
+
+
+def test_wide_grower_u32_ranks(seed):
+    """A column with more than 65,536 distinct values switches the rank table to u32;
+    the wide grower (default for n >= 65,536) must stay bit-exact on it."""
+    rng = np.random.default_rng(4242)
+    n, p = 70_000, 3
+    col = np.vstack([rng.normal(size=n), rng.integers(0, 9, size=n).astype(float),
+                     rng.integers(0, 2, size=n).astype(float)])
+    y = rng.normal(size=n)
+    prep = pkg.PreparedDataset(col, y, n, p)
+    f = pkg.fit(prep, pkg.ForestParams(3, 2, 5, seed))
+    o = Oracle.fit(col, y, n, p, 3, 2, 5, seed)
+    assert forests_equal(o, soa_of(f)) is None
+    stats, _, _ = Oracle.oob(col, y, n, p, o)
+    assert [f.oob.mse, f.oob.error_pct] == [stats[1], stats[3]]
