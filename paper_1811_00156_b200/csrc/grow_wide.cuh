@@ -1382,7 +1382,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (lw_smem + 1024 > static_cast<size_t>(optin) ||
+    if (lw_smem + 1024 > static_cast<size_t>(optin) || std::getenv("AIWC_LW_GLOBAL") ||
         cudaFuncSetAttribute(w_lwarp<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(lw_smem)) != cudaSuccess)
       lw_smem = 0;

@@ -257,6 +257,12 @@ def test_wide_grower_random_tables(seed, monkeypatch):
         for big_min, coop_min, lanes in (("64", "1000000", "16"), ("64", "1000000", "8"),
                                          ("64", "1000000", "32"), ("64", "200", "16"),
                                          ("1000000", "1000000", "16")):
+            # the list pass with the bitmap in global memory (the path of tables whose
+            # bitmap exceeds shared memory) on the last configuration
+            if big_min == "1000000":
+                monkeypatch.setenv("AIWC_LW_GLOBAL", "1")
+            else:
+                monkeypatch.delenv("AIWC_LW_GLOBAL", raising=False)
             monkeypatch.setenv("AIWC_BIG_MIN", big_min)
             monkeypatch.setenv("AIWC_COOP_MIN", coop_min)
             monkeypatch.setenv("AIWC_BIG_LANES", lanes)
