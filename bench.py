@@ -129,8 +129,33 @@ def cpu_worker(args) -> dict:
         Ref.check(L.ref_grow_range(prep, 1000, C4_MTRY, C4_MNS, seed, 0, sample, cores,
                                    C.byref(nodes)))
         rates.append(sample / (time.perf_counter() - s))
+    # the other configurations, each a bounded sample, same cores
+    from oracle_lib import RefForest, ref_evaluate
+
+    extra = {}
+    try:
+        d1 = RefData()
+        rows1 = d1.rows_rowmajor()
+        s = time.perf_counter()
+        f1 = RefForest.fit(d1, 500, 6, 5, seed, jobs=cores)  # C1: fit (OOB included)
+        f1.predict(rows1, jobs=cores)
+        extra["c1_trees_per_s"] = 500 / (time.perf_counter() - s)
+        f5 = RefForest.fit(d1, 1000, 6, 5, seed, jobs=cores)  # C5 forest
+        q = 50_000
+        idx = np.array([Ref.bounded_draws(Ref.derive_seed(7, "query", i), 2220, 1)[0]
+                        for i in range(q)])
+        qrows = np.ascontiguousarray(rows1[idx])
+        s = time.perf_counter()
+        f5.predict(qrows, jobs=cores)
+        extra["c5_rows_per_s"] = q / (time.perf_counter() - s)
+        extra["c5_sample_rows"] = q
+        s = time.perf_counter()
+        ref_evaluate(d1, 505, 30, 9, seed, jobs=cores)  # C3: 37 folds
+        extra["c3_folds_per_s"] = 37 / (time.perf_counter() - s)
+    except Exception as e:  # noqa: BLE001
+        extra["extra_error"] = str(e)[-200:]
     return {"value": float(np.median(rates)), "unit": "trees/s", "cores": cores,
-            "kind": "reference", "rates": rates,
+            "kind": "reference", "rates": rates, **extra,
             "sample": f"C4 trees [0,{sample}) of the 1000-tree m=8 mns=5 forest, "
                       f"TreeGrower::grow via parallel_for_with_state (forest.hpp:500-505), "
                       f"jobs={cores}; synth+join {t1 - t0:.1f}s and PreparedDataset "
@@ -379,6 +404,10 @@ def main():
         "setup_s": setup_s,
         "cpu_baseline": ({k: cpu_res.get(k) for k in ("value", "unit", "cores", "kind", "sample")}
                          if cpu_res else None),
+        "cpu_baseline_other": ({k: cpu_res.get(k) for k in ("c1_trees_per_s", "c5_rows_per_s",
+                                                            "c5_sample_rows", "c3_folds_per_s",
+                                                            "extra_error") if k in cpu_res}
+                               if cpu_res else None),
         "predict": predict,
         "c1": c1,
         "grid": grid,
