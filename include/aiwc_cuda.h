@@ -121,6 +121,17 @@ int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum,
  * 79-108) over the num.trees axis. */
 int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, uint32_t k,
                     aiwc_oob_stats* out);
+/* Grid cells in one launch (tables below 65,536 rows): ncells forests of num_trees trees
+ * each, forest c grown exactly as aiwc_fit(ctx, num_trees, mtry[c], min_node_size[c],
+ * seed, 0, num_trees, ...) would (tree t of every forest keyed by (seed, t)); the trees of
+ * forest c are [c*num_trees, (c+1)*num_trees) of the returned handle.  OOB statistics
+ * are not computed here: aiwc_oob_prefix_cells gives them for every tree prefix. */
+int aiwc_fit_cells(aiwc_ctx* ctx, uint32_t ncells, const uint32_t* mtry,
+                   const uint32_t* min_node_size, uint32_t num_trees, uint64_t seed,
+                   aiwc_forest** out);
+/* aiwc_oob_prefix for each forest of an aiwc_fit_cells handle: out[c*k + i] */
+int aiwc_oob_prefix_cells(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts,
+                          uint32_t k, aiwc_oob_stats* out);
 /* finalize OOB stats from per-row sum/count (forest.hpp:396-453) */
 int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
                       const uint32_t* row_count, aiwc_oob_stats* out);

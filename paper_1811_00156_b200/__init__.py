@@ -108,6 +108,8 @@ def lib():
         L.aiwc_evaluate_folds.argtypes = [P(f64), P(f64), u64, u32, P(u32), u32, u32, u32,
                                           u32, u32, u32, u64, C.c_int, P(f64)]
         L.aiwc_oob_prefix.argtypes = [vp, vp, P(u32), u32, P(OobStatsC)]
+        L.aiwc_fit_cells.argtypes = [vp, u32, P(u32), P(u32), u32, u64, P(vp)]
+        L.aiwc_oob_prefix_cells.argtypes = [vp, vp, P(u32), u32, P(OobStatsC)]
         L.aiwc_forest_profile.argtypes = [vp, P(f64), P(f64), P(u64), P(u32)]
         L.aiwc_launch_count.restype = u64
         L.aiwc_make_queries.argtypes = [vp, u64, u32, u64, u64, C.c_int, vp]
@@ -396,16 +398,34 @@ def oob_prefix(forest: Forest, prepared: PreparedDataset, tree_counts) -> list:
 
 
 def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
-             workers: int = 1) -> np.ndarray:
+             workers: int = 1, cell_batch: int = 64) -> np.ndarray:
     """C2 grid objective (tuner.hpp:247-253 / experiments.hpp:79-108): error_pct for
     every (mtry, min_node_size) cell x num.trees value, one fit of max(tree_counts)
-    trees per cell.  Returns an array [len(cells), len(tree_counts)].  `workers` host
-    threads, each with its own device copy of the dataset (a context serialises its
-    fits), keep several cells' fits in flight on the GPU at once."""
+    trees per cell.  Returns an array [len(cells), len(tree_counts)].  Tables below
+    65,536 rows grow `cell_batch` cells' forests per launch (aiwc_fit_cells); larger ones
+    fit cell by cell from `workers` host threads, each with its own device copy of the
+    dataset (a context serialises its fits)."""
     import threading
 
     cps = sorted(int(t) for t in tree_counts)
     out = np.zeros((len(cells), len(cps)))
+    if prepared.n < 65536:  # batched: many cells' forests in one launch (aiwc_fit_cells)
+        cpa = np.ascontiguousarray(cps, np.uint32)
+        for i0 in range(0, len(cells), cell_batch):
+            cs = cells[i0:i0 + cell_batch]
+            mt = np.ascontiguousarray([c[0] for c in cs], np.uint32)
+            mn = np.ascontiguousarray([c[1] for c in cs], np.uint32)
+            h = vp()
+            _check(lib().aiwc_fit_cells(prepared._h, len(cs), _p(mt, u32), _p(mn, u32), cps[-1],
+                                        seed, C.byref(h)))
+            try:
+                st = (OobStatsC * (len(cs) * len(cps)))()
+                _check(lib().aiwc_oob_prefix_cells(prepared._h, h, _p(cpa, u32), len(cps), st))
+                for j in range(len(cs)):
+                    out[i0 + j] = [st[j * len(cps) + i].error_pct for i in range(len(cps))]
+            finally:
+                lib().aiwc_forest_free(h)
+        return out
     workers = max(1, min(workers, len(cells)))
     preps = [prepared] + [PreparedDataset(prepared.col, prepared.y, prepared.n, prepared.p,
                                           prepared.device) for _ in range(workers - 1)]

@@ -293,6 +293,7 @@ struct aiwc_ctx {
 // ---------------------------------------------------------------------------------
 struct aiwc_forest {
   int device = 0;
+  uint32_t cells = 1;  // forests held (aiwc_fit_cells): trees of forest c are [c*T, (c+1)*T)
   uint64_t n = 0;  // training rows (inbag / oob arrays)
   uint32_t trees = 0, tree_begin = 0;
   uint32_t num_trees = 0, mtry = 0, mns = 0;
@@ -517,6 +518,375 @@ int pick_threads(uint64_t n) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+// One fit: trees [tree_begin, tree_end) of a num_trees forest, or, with `cells`, the
+// cells->n forests of cells->trees trees each (grid cells: per-tree mtry / mns, one
+// launch for all of them; trees of cell c are [c*trees, (c+1)*trees)).
+struct CellSpec {
+  uint32_t n;
+  const uint32_t* mtry;
+  const uint32_t* mns;
+  uint32_t trees;
+};
+
+void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
+              uint64_t seed, uint32_t tree_begin, uint32_t tree_end, int compute_oob,
+              const CellSpec* cells, aiwc_forest** out) {
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const auto t_start = std::chrono::steady_clock::now();
+  DeviceGuard dg(ctx->device);
+  struct {
+    cudaStream_t s;
+  } st{ctx->stream};
+  const uint64_t n = ctx->n;
+  const uint32_t p = ctx->p;
+  const uint32_t T = tree_end - tree_begin;
+  const int nt = pick_threads(n);
+
+  int dev = ctx->device, sms = 0, max_optin = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  SlotLayout L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, false);
+  const size_t bits_smem = (grow_bits_words(n, L.stride) + grow_pref_words(n, L.stride)) * 4;
+  // static shared memory of grow_kernel: scans + per-warp FP64 stages (< 12 KB)
+  const bool smem_bits = bits_smem + 12288 <= static_cast<size_t>(max_optin) &&
+                         std::getenv("AIWC_GROW_GBITS") == nullptr;
+  const size_t dyn = smem_bits ? bits_smem : 0;
+  if (!smem_bits) L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
+
+  GrowArgs a{};
+  a.d = ctx->view();
+  a.mtry = mtry;
+  a.mns = min_node_size;
+  a.seed = seed;
+  a.tag_tree = host_fnv1a64("tree", 4);
+  a.tree_begin = tree_begin;
+  a.tree_end = tree_end;
+  a.L = L;
+  a.bits_in_smem = smem_bits ? 1 : 0;
+  DevBuf<uint32_t> cell_m, cell_n;
+  if (cells) {
+    cell_m.alloc(cells->n);
+    cell_n.alloc(cells->n);
+    CK(cudaMemcpy(cell_m.p, cells->mtry, cells->n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cell_n.p, cells->mns, cells->n * 4, cudaMemcpyHostToDevice));
+    a.cell_mtry = cell_m.p;
+    a.cell_mns = cell_n.p;
+    a.cell_trees = cells->trees;
+  }
+
+  // large tables grow batches of trees level-synchronously with one grid-wide kernel
+  // per phase (grow_wide.cuh); small ones keep one persistent CTA per tree
+  bool wide = !cells && n >= 65536;
+  if (const char* e = std::getenv("AIWC_GROW_WIDE"); e && !cells) wide = std::atoi(e) != 0;
+  if (wide) {
+    L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
+    a.L = L;
+    a.bits_in_smem = 0;
+  }
+  int per_sm = 0;
+  if (wide) {
+    per_sm = 4;  // batch up to 4 trees per SM (bounded by memory below)
+    if (const char* e = std::getenv("AIWC_WIDE_PER_SM")) per_sm = std::max(1, std::atoi(e));
+  }
+  else
+    CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
+  if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
+  const bool tprof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
+  auto tmark = [&](const char* what) {
+    if (!tprof) return;
+    static thread_local auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[aiwc setup] %s %.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  };
+  tmark("start");
+  // outputs first: in-bag draws, OOB leaf values, node pool
+  auto f = std::make_unique<aiwc_forest>();
+  f->device = dev;
+  f->n = n;
+  f->trees = T;
+  f->tree_begin = tree_begin;
+  f->num_trees = num_trees;
+  f->mtry = mtry;
+  f->mns = min_node_size;
+  f->seed = seed;
+  f->inbag.alloc(size_t{T} * n);
+  f->oobval.alloc(size_t{T} * n);
+  CK(cudaMemsetAsync(f->oobval.p, 0xff, size_t{T} * n * 8, st.s));
+  tmark("inbag+oobval");
+  a.inbag = f->inbag.p;
+  a.oobval = f->oobval.p;
+
+  uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
+  int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
+  // node pool (28 B/node) plus the compacted forest built from it after growth
+  // (feature, left, thr, value, PredNode: 40 B/node) stay outside the slot scratch
+  const size_t pool_bytes = cap * (28 + 40);
+  // cudaMemGetInfo can stall for tens of milliseconds: small fits (a grid search's
+  // thousands of C1-size fits) skip the free-memory budget when they need under 1/16
+  // of the device
+  static size_t total_mem[64] = {};
+  size_t free_b = 0, total_b = 0;
+  if (dev < 64 && total_mem[dev] == 0) {
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    total_mem[dev] = total_b;
+  }
+  const size_t dev_total = dev < 64 ? total_mem[dev] : 0;
+  const bool small = dev_total && pool_bytes + size_t(slots) * L.bytes < dev_total / 16;
+  if (small) {
+    free_b = dev_total;  // ample: the budget below keeps every slot
+  } else {
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    // memory parked in the stream-ordered pool (and this ctx's scratch, which is
+    // reused or replaced) is available too; cudaMemGetInfo does not count it
+    cudaMemPool_t mp;
+    uint64_t reserved = 0, used_now = 0;
+    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess &&
+        cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+        cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used_now) == cudaSuccess &&
+        reserved > used_now)
+      free_b += reserved - used_now;
+    free_b += ctx->scratch.count;
+  }
+  const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
+  slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
+  if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
+  const size_t need = size_t(slots) * L.bytes;
+  tmark("budget");
+  if (ctx->scratch.count < need) ctx->scratch.alloc(need);
+  tmark("scratch");
+  a.scratch = ctx->scratch.p;
+  // hand the slots back to the stream-ordered pool when the fit ends (the pool keeps
+  // them reserved, so the next fit -- on this or another dataset -- reuses them)
+  struct ScratchRelease {
+    DevBuf<char>& b;
+    ~ScratchRelease() { b.release(); }
+  } scratch_release{ctx->scratch};
+  int nlanes = 1;
+  if (wide) {
+    nlanes = 4;  // concurrent batches (streams + host threads); 2 -> 4 measured +3 %
+    if (const char* e = std::getenv("AIWC_WIDE_LANES")) nlanes = std::max(1, std::atoi(e));
+    nlanes = std::max(1, std::min(nlanes, slots));
+  }
+  const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
+  DevBuf<TreeState> wts(wide ? slots : 0);
+  DevBuf<uint32_t> woff(wide ? 5 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
+      wctr(wide ? 4 * nlanes : 0);
+  // per-lane "trees still splitting" flags read back every level: a pinned buffer per
+  // fit, taken from a process-wide pool (cudaMallocHost / cudaFreeHost synchronise
+  // and cost milliseconds -- too much for the many small fits of a grid search)
+  PinnedFlags h_active;
+  std::vector<cudaStream_t> lane_streams;
+  struct StreamsGuard {
+    std::vector<cudaStream_t>& v;
+    ~StreamsGuard() {
+      for (auto s : v) cudaStreamDestroy(s);
+    }
+  } lsg{lane_streams};
+  for (int k = 1; k < nlanes; ++k) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    lane_streams.push_back(s);
+  }
+
+  DevBuf<uint32_t> queue(1), tree_cnt(T);
+  DevBuf<int> err(1);
+  DevBuf<uint64_t> tree_off(T);
+  a.queue = queue.p;
+  a.tree_off = tree_off.p;
+  a.tree_cnt = tree_cnt.p;
+  a.err = err.p;
+  DevBuf<int32_t> pf, pl;
+  DevBuf<double> pt, pv;
+  DevBuf<uint32_t> pr;
+  DevBuf<unsigned long long> used(1), split_rows(1), prof;
+  a.split_rows = split_rows.p;
+  const bool want_prof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
+  if (want_prof) {
+    prof.alloc(16);
+    CK(cudaMemset(prof.p, 0, 16 * 8));
+    a.prof = prof.p;
+  }
+  std::vector<uint32_t> cnt(T);
+  cudaEvent_t ev0, ev1, evf0, evf1;
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventCreate(&evf0));
+  CK(cudaEventCreate(&evf1));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
+    }
+  };
+  cudaEvent_t evs[4] = {ev0, ev1, evf0, evf1};
+  EvGuard eg{evs};
+  CK(cudaEventRecord(evf0, st.s));
+      tmark("streams+events+pool");
+  const auto t_grow0 = std::chrono::steady_clock::now();
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    pf.alloc(cap);
+    pl.alloc(cap);
+    pt.alloc(cap);
+    pv.alloc(cap);
+    pr.alloc(cap);
+    a.pool_feature = pf.p;
+    a.pool_left = pl.p;
+    a.pool_thr = pt.p;
+    a.pool_value = pv.p;
+    a.pool_rank = pr.p;
+    a.pool_used = used.p;
+    a.pool_cap = cap;
+    CK(cudaMemsetAsync(queue.p, 0, 4, st.s));
+    CK(cudaMemsetAsync(err.p, 0, 4, st.s));
+    CK(cudaMemsetAsync(used.p, 0, 8, st.s));
+    CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
+    CK(cudaEventRecord(ev0, st.s));
+    if (wide) {
+      // batched multi-kernel grower: K concurrent lanes (stream + host thread), each
+      // growing batches of `per` trees level-synchronously.  While one batch sits in
+      // the sequential tail of a level (a few long chains on huge nodes), the other
+      // lanes' kernels fill the SMs.
+      const int K = nlanes;
+      const uint32_t per = static_cast<uint32_t>(slots / K);
+      uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
+      if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
+      // CTA-per-chain / CTA-per-route for nodes >= coop_min rows: shorter critical
+      // paths, more warps per node -- a win only when a lane's batch is too small to
+      // keep the GPU busy (measured at C4: 64 trees +5 %, 200 trees -6 %, 1000 -7 %)
+      // lanes per chain for big nodes: 32 (a warp each) or 16 / 8 (lane groups)
+      uint32_t lane_max = 16;  // rows below which a node's chains run one lane each (measured)
+      if (const char* e = std::getenv("AIWC_LANE_MAX")) lane_max = static_cast<uint32_t>(std::atoi(e));
+      uint32_t big_lanes = 16;
+      if (const char* e = std::getenv("AIWC_BIG_LANES")) big_lanes = static_cast<uint32_t>(std::atoi(e));
+      if (big_lanes != 8 && big_lanes != 16) big_lanes = 32;
+      uint32_t coop_min = per <= 48 ? 32768u : 0xffffffffu;
+      if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
+      coop_min = std::max(coop_min, big_min);
+      std::vector<cudaError_t> lane_err(K, cudaSuccess);
+      std::vector<std::thread> lanes;
+      for (int k = 0; k < K; ++k) {
+        lanes.emplace_back([&, k] {
+          cudaSetDevice(dev);
+          const cudaStream_t ls = k == 0 ? st.s : lane_streams[k - 1];
+          for (uint32_t t0 = k * per; t0 < T; t0 += K * per) {
+            WideArgs w{};
+            w.g = a;
+            w.g.scratch = a.scratch + size_t{k} * per * L.bytes;
+            w.ts = wts.p + size_t{k} * per;
+            w.B = std::min<uint32_t>(per, T - t0);
+            w.big_min = big_min;
+            w.coop_min = coop_min;
+            w.pair_big = big_lanes;
+            w.lane_max = lane_max;
+            w.t0 = t0;
+            for (int i = 0; i < 5; ++i)
+              w.off[i] = woff.p + (size_t{k} * 5 + i) * (per + 1);
+            w.active = wactive.p + k;
+            w.task_ctr = wctr.p + 4 * k;
+            uint64_t nl = 0;
+            cudaError_t e = run_wide(ctx->rank_bytes, w, ls, sms, h_active.get() + k, &nl);
+            g_launches += nl;
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
+            if (e != cudaSuccess) {
+              lane_err[k] = e;
+              return;
+            }
+          }
+        });
+      }
+      for (auto& th : lanes) th.join();
+      for (cudaError_t e : lane_err)
+        if (e != cudaSuccess) throw Status(AIWC_ECUDA, std::string("wide grower: ") + cudaGetErrorString(e));
+    } else {
+      CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
+      g_launches += 1;
+    }
+    CK(cudaEventRecord(ev1, st.s));
+    f->grow_launches += 1;
+    int herr = 0;
+    unsigned long long hused = 0;
+    CK(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaMemcpyAsync(&hused, used.p, 8, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaStreamSynchronize(st.s));
+    {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      f->grow_ms += ms;
+    }
+    if (herr == 1 && attempt == 0) {  // pool overflow: exact size is now known
+      cap = hused;
+      continue;
+    }
+    if (herr == 2) throw Status(AIWC_EEXEC, "in-bag row count exceeded the slot bound");
+    if (herr == 3) throw Status(AIWC_EEXEC, "frontier/node capacity exceeded");
+    if (herr) throw Status(AIWC_EEXEC, "grow kernel error " + std::to_string(herr));
+    break;
+  }
+  CK(cudaMemcpy(cnt.data(), tree_cnt.p, size_t{T} * 4, cudaMemcpyDeviceToHost));
+  if (want_prof) {
+    unsigned long long h[16];
+    CK(cudaMemcpy(h, prof.p, 16 * 8, cudaMemcpyDeviceToHost));
+    static const char* names[14] = {"bootstrap", "bitmap", "payload0", "lists0+root",
+                                    "-", "elig", "sample", "chains", "decide", "route",
+                                    "segtab", "paypass", "listpass", "emit+oob"};
+    double tot = 0;
+    for (int i = 0; i < 14; ++i) tot += static_cast<double>(h[i]);
+    std::fprintf(stderr, "[aiwc grow phases] slots=%d trees=%u total=%.3g cycles:", slots, T, tot);
+    for (int i = 0; i < 14; ++i)
+      if (h[i]) std::fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * h[i] / tot);
+    std::fprintf(stderr, "\n");
+  }
+  f->off.assign(T + 1, 0);
+  for (uint32_t t = 0; t < T; ++t) f->off[t + 1] = f->off[t] + cnt[t];
+  const uint64_t N = f->off[T];
+  f->feature.alloc(N);
+  f->left.alloc(N);
+  f->thr.alloc(N);
+  f->value.alloc(N);
+  f->packed.alloc(N);
+  f->d_off.alloc(T + 1);
+  CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, st.s));
+  compact_kernel<<<T, 256, 0, st.s>>>(pf.p, pt.p, pl.p, pv.p, tree_off.p, f->d_off.p,
+                                      f->feature.p, f->thr.p, f->left.p, f->value.p,
+                                      f->packed.p);
+  CK(cudaGetLastError());
+  g_launches += 1;
+  CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
+  CK(cudaStreamSynchronize(st.s));
+  const auto t_compact = std::chrono::steady_clock::now();
+  if (compute_oob && tree_begin == 0 && tree_end == num_trees) {
+    std::vector<double> sum(n, 0.0);
+    std::vector<uint32_t> count(n, 0);
+    oob_accumulate_device(f.get(), sum.data(), count.data(), st.s);
+    f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
+    f->has_oob = true;
+  }
+  if (want_prof) {
+    const auto now = std::chrono::steady_clock::now();
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[aiwc fit host] setup %.1f ms, grow+compact %.1f ms, oob %.1f ms\n",
+                 ms(t_start, t_grow0), ms(t_grow0, t_compact), ms(t_compact, now));
+  }
+  CK(cudaEventRecord(evf1, st.s));
+  CK(cudaEventSynchronize(evf1));
+  {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, evf0, evf1));
+    f->fit_ms = ms;
+  }
+  *out = f.release();
+}
+
+}  // namespace
+
+extern "C" {
+
 int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
              uint64_t seed, uint32_t tree_begin, uint32_t tree_end, int compute_oob,
              aiwc_forest** out) {
@@ -531,342 +901,32 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
                                    std::to_string(mtry));
     if (tree_begin >= tree_end || tree_end > num_trees)
       throw Status(AIWC_EARG, "bad tree range");
-    std::lock_guard<std::mutex> lock(ctx->mu);
-    const auto t_start = std::chrono::steady_clock::now();
-    DeviceGuard dg(ctx->device);
-    struct {
-      cudaStream_t s;
-    } st{ctx->stream};
-    const uint64_t n = ctx->n;
-    const uint32_t p = ctx->p;
-    const uint32_t T = tree_end - tree_begin;
-    const int nt = pick_threads(n);
+    fit_body(ctx, num_trees, mtry, min_node_size, seed, tree_begin, tree_end, compute_oob,
+             nullptr, out);
+  });
+}
 
-    int dev = ctx->device, sms = 0, max_optin = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    SlotLayout L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, false);
-    const size_t bits_smem = (grow_bits_words(n, L.stride) + grow_pref_words(n, L.stride)) * 4;
-    // static shared memory of grow_kernel: scans + per-warp FP64 stages (< 12 KB)
-    const bool smem_bits = bits_smem + 12288 <= static_cast<size_t>(max_optin) &&
-                           std::getenv("AIWC_GROW_GBITS") == nullptr;
-    const size_t dyn = smem_bits ? bits_smem : 0;
-    if (!smem_bits) L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
-
-    GrowArgs a{};
-    a.d = ctx->view();
-    a.mtry = mtry;
-    a.mns = min_node_size;
-    a.seed = seed;
-    a.tag_tree = host_fnv1a64("tree", 4);
-    a.tree_begin = tree_begin;
-    a.tree_end = tree_end;
-    a.L = L;
-    a.bits_in_smem = smem_bits ? 1 : 0;
-
-    // large tables grow batches of trees level-synchronously with one grid-wide kernel
-    // per phase (grow_wide.cuh); small ones keep one persistent CTA per tree
-    bool wide = n >= 65536;
-    if (const char* e = std::getenv("AIWC_GROW_WIDE")) wide = std::atoi(e) != 0;
-    if (wide) {
-      L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
-      a.L = L;
-      a.bits_in_smem = 0;
+int aiwc_fit_cells(aiwc_ctx* ctx, uint32_t ncells, const uint32_t* mtry,
+                   const uint32_t* min_node_size, uint32_t num_trees, uint64_t seed,
+                   aiwc_forest** out) {
+  return guard([&] {
+    if (!ctx || !out || !mtry || !min_node_size || ncells == 0) throw Status(AIWC_EARG, "bad argument");
+    if (ctx->n < 2) throw Status(AIWC_EEXEC, "dataset must have at least 2 rows");
+    if (num_trees < 1) throw Status(AIWC_EEXEC, "num_trees must be >= 1");
+    if (ctx->n >= 65536) throw Status(AIWC_EARG, "grid cells batch tables below 65,536 rows");
+    if (uint64_t{ncells} * num_trees >= (uint64_t{1} << 31)) throw Status(AIWC_EARG, "too many trees");
+    uint32_t mmax = 0, nmin = UINT32_MAX;
+    for (uint32_t c = 0; c < ncells; ++c) {  // the checks of forest.hpp:482-490 per cell
+      if (min_node_size[c] < 1) throw Status(AIWC_EEXEC, "min_node_size must be >= 1");
+      if (mtry[c] < 1 || mtry[c] > ctx->p)
+        throw Status(AIWC_EEXEC, "mtry must be in [1, " + std::to_string(ctx->p) + "], got " +
+                                     std::to_string(mtry[c]));
+      mmax = std::max(mmax, mtry[c]);
+      nmin = std::min(nmin, min_node_size[c]);
     }
-    int per_sm = 0;
-    if (wide) {
-      per_sm = 4;  // batch up to 4 trees per SM (bounded by memory below)
-      if (const char* e = std::getenv("AIWC_WIDE_PER_SM")) per_sm = std::max(1, std::atoi(e));
-    }
-    else
-      CK(launch_grow(nt, ctx->rank_bytes, a, 0, dyn, st.s, &per_sm));
-    if (per_sm < 1) throw Status(AIWC_ECUDA, "grow kernel does not fit on an SM");
-    const bool tprof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
-    auto tmark = [&](const char* what) {
-      if (!tprof) return;
-      static thread_local auto last = std::chrono::steady_clock::now();
-      const auto now = std::chrono::steady_clock::now();
-      std::fprintf(stderr, "[aiwc setup] %s %.2f ms\n", what,
-                   std::chrono::duration<double, std::milli>(now - last).count());
-      last = now;
-    };
-    tmark("start");
-    // outputs first: in-bag draws, OOB leaf values, node pool
-    auto f = std::make_unique<aiwc_forest>();
-    f->device = dev;
-    f->n = n;
-    f->trees = T;
-    f->tree_begin = tree_begin;
-    f->num_trees = num_trees;
-    f->mtry = mtry;
-    f->mns = min_node_size;
-    f->seed = seed;
-    f->inbag.alloc(size_t{T} * n);
-    f->oobval.alloc(size_t{T} * n);
-    CK(cudaMemsetAsync(f->oobval.p, 0xff, size_t{T} * n * 8, st.s));
-    tmark("inbag+oobval");
-    a.inbag = f->inbag.p;
-    a.oobval = f->oobval.p;
-
-    uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
-    int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
-    // node pool (28 B/node) plus the compacted forest built from it after growth
-    // (feature, left, thr, value, PredNode: 40 B/node) stay outside the slot scratch
-    const size_t pool_bytes = cap * (28 + 40);
-    // cudaMemGetInfo can stall for tens of milliseconds: small fits (a grid search's
-    // thousands of C1-size fits) skip the free-memory budget when they need under 1/16
-    // of the device
-    static size_t total_mem[64] = {};
-    size_t free_b = 0, total_b = 0;
-    if (dev < 64 && total_mem[dev] == 0) {
-      CK(cudaMemGetInfo(&free_b, &total_b));
-      total_mem[dev] = total_b;
-    }
-    const size_t dev_total = dev < 64 ? total_mem[dev] : 0;
-    const bool small = dev_total && pool_bytes + size_t(slots) * L.bytes < dev_total / 16;
-    if (small) {
-      free_b = dev_total;  // ample: the budget below keeps every slot
-    } else {
-      CK(cudaMemGetInfo(&free_b, &total_b));
-      // memory parked in the stream-ordered pool (and this ctx's scratch, which is
-      // reused or replaced) is available too; cudaMemGetInfo does not count it
-      cudaMemPool_t mp;
-      uint64_t reserved = 0, used_now = 0;
-      if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess &&
-          cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
-          cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used_now) == cudaSuccess &&
-          reserved > used_now)
-        free_b += reserved - used_now;
-      free_b += ctx->scratch.count;
-    }
-    const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
-    slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
-    if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
-    const size_t need = size_t(slots) * L.bytes;
-    tmark("budget");
-    if (ctx->scratch.count < need) ctx->scratch.alloc(need);
-    tmark("scratch");
-    a.scratch = ctx->scratch.p;
-    // hand the slots back to the stream-ordered pool when the fit ends (the pool keeps
-    // them reserved, so the next fit -- on this or another dataset -- reuses them)
-    struct ScratchRelease {
-      DevBuf<char>& b;
-      ~ScratchRelease() { b.release(); }
-    } scratch_release{ctx->scratch};
-    int nlanes = 1;
-    if (wide) {
-      nlanes = 4;  // concurrent batches (streams + host threads); 2 -> 4 measured +3 %
-      if (const char* e = std::getenv("AIWC_WIDE_LANES")) nlanes = std::max(1, std::atoi(e));
-      nlanes = std::max(1, std::min(nlanes, slots));
-    }
-    const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
-    DevBuf<TreeState> wts(wide ? slots : 0);
-    DevBuf<uint32_t> woff(wide ? 5 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
-        wctr(wide ? 4 * nlanes : 0);
-    // per-lane "trees still splitting" flags read back every level: a pinned buffer per
-    // fit, taken from a process-wide pool (cudaMallocHost / cudaFreeHost synchronise
-    // and cost milliseconds -- too much for the many small fits of a grid search)
-    PinnedFlags h_active;
-    std::vector<cudaStream_t> lane_streams;
-    struct StreamsGuard {
-      std::vector<cudaStream_t>& v;
-      ~StreamsGuard() {
-        for (auto s : v) cudaStreamDestroy(s);
-      }
-    } lsg{lane_streams};
-    for (int k = 1; k < nlanes; ++k) {
-      cudaStream_t s;
-      CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-      lane_streams.push_back(s);
-    }
-
-    DevBuf<uint32_t> queue(1), tree_cnt(T);
-    DevBuf<int> err(1);
-    DevBuf<uint64_t> tree_off(T);
-    a.queue = queue.p;
-    a.tree_off = tree_off.p;
-    a.tree_cnt = tree_cnt.p;
-    a.err = err.p;
-    DevBuf<int32_t> pf, pl;
-    DevBuf<double> pt, pv;
-    DevBuf<uint32_t> pr;
-    DevBuf<unsigned long long> used(1), split_rows(1), prof;
-    a.split_rows = split_rows.p;
-    const bool want_prof = std::getenv("AIWC_PROFILE_PHASES") != nullptr;
-    if (want_prof) {
-      prof.alloc(16);
-      CK(cudaMemset(prof.p, 0, 16 * 8));
-      a.prof = prof.p;
-    }
-    std::vector<uint32_t> cnt(T);
-    cudaEvent_t ev0, ev1, evf0, evf1;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-    CK(cudaEventCreate(&evf0));
-    CK(cudaEventCreate(&evf1));
-    struct EvGuard {
-      cudaEvent_t* e;
-      ~EvGuard() {
-        for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]);
-      }
-    };
-    cudaEvent_t evs[4] = {ev0, ev1, evf0, evf1};
-    EvGuard eg{evs};
-    CK(cudaEventRecord(evf0, st.s));
-        tmark("streams+events+pool");
-    const auto t_grow0 = std::chrono::steady_clock::now();
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      pf.alloc(cap);
-      pl.alloc(cap);
-      pt.alloc(cap);
-      pv.alloc(cap);
-      pr.alloc(cap);
-      a.pool_feature = pf.p;
-      a.pool_left = pl.p;
-      a.pool_thr = pt.p;
-      a.pool_value = pv.p;
-      a.pool_rank = pr.p;
-      a.pool_used = used.p;
-      a.pool_cap = cap;
-      CK(cudaMemsetAsync(queue.p, 0, 4, st.s));
-      CK(cudaMemsetAsync(err.p, 0, 4, st.s));
-      CK(cudaMemsetAsync(used.p, 0, 8, st.s));
-      CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
-      CK(cudaEventRecord(ev0, st.s));
-      if (wide) {
-        // batched multi-kernel grower: K concurrent lanes (stream + host thread), each
-        // growing batches of `per` trees level-synchronously.  While one batch sits in
-        // the sequential tail of a level (a few long chains on huge nodes), the other
-        // lanes' kernels fill the SMs.
-        const int K = nlanes;
-        const uint32_t per = static_cast<uint32_t>(slots / K);
-        uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
-        if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
-        // CTA-per-chain / CTA-per-route for nodes >= coop_min rows: shorter critical
-        // paths, more warps per node -- a win only when a lane's batch is too small to
-        // keep the GPU busy (measured at C4: 64 trees +5 %, 200 trees -6 %, 1000 -7 %)
-        // lanes per chain for big nodes: 32 (a warp each) or 16 / 8 (lane groups)
-        uint32_t lane_max = 16;  // rows below which a node's chains run one lane each (measured)
-        if (const char* e = std::getenv("AIWC_LANE_MAX")) lane_max = static_cast<uint32_t>(std::atoi(e));
-        uint32_t big_lanes = 16;
-        if (const char* e = std::getenv("AIWC_BIG_LANES")) big_lanes = static_cast<uint32_t>(std::atoi(e));
-        if (big_lanes != 8 && big_lanes != 16) big_lanes = 32;
-        uint32_t coop_min = per <= 48 ? 32768u : 0xffffffffu;
-        if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
-        coop_min = std::max(coop_min, big_min);
-        std::vector<cudaError_t> lane_err(K, cudaSuccess);
-        std::vector<std::thread> lanes;
-        for (int k = 0; k < K; ++k) {
-          lanes.emplace_back([&, k] {
-            cudaSetDevice(dev);
-            const cudaStream_t ls = k == 0 ? st.s : lane_streams[k - 1];
-            for (uint32_t t0 = k * per; t0 < T; t0 += K * per) {
-              WideArgs w{};
-              w.g = a;
-              w.g.scratch = a.scratch + size_t{k} * per * L.bytes;
-              w.ts = wts.p + size_t{k} * per;
-              w.B = std::min<uint32_t>(per, T - t0);
-              w.big_min = big_min;
-              w.coop_min = coop_min;
-              w.pair_big = big_lanes;
-              w.lane_max = lane_max;
-              w.t0 = t0;
-              for (int i = 0; i < 5; ++i)
-                w.off[i] = woff.p + (size_t{k} * 5 + i) * (per + 1);
-              w.active = wactive.p + k;
-              w.task_ctr = wctr.p + 4 * k;
-              uint64_t nl = 0;
-              cudaError_t e = run_wide(ctx->rank_bytes, w, ls, sms, h_active.get() + k, &nl);
-              g_launches += nl;
-              if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
-              if (e != cudaSuccess) {
-                lane_err[k] = e;
-                return;
-              }
-            }
-          });
-        }
-        for (auto& th : lanes) th.join();
-        for (cudaError_t e : lane_err)
-          if (e != cudaSuccess) throw Status(AIWC_ECUDA, std::string("wide grower: ") + cudaGetErrorString(e));
-      } else {
-        CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
-        g_launches += 1;
-      }
-      CK(cudaEventRecord(ev1, st.s));
-      f->grow_launches += 1;
-      int herr = 0;
-      unsigned long long hused = 0;
-      CK(cudaMemcpyAsync(&herr, err.p, 4, cudaMemcpyDeviceToHost, st.s));
-      CK(cudaMemcpyAsync(&hused, used.p, 8, cudaMemcpyDeviceToHost, st.s));
-      CK(cudaStreamSynchronize(st.s));
-      {
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev0, ev1));
-        f->grow_ms += ms;
-      }
-      if (herr == 1 && attempt == 0) {  // pool overflow: exact size is now known
-        cap = hused;
-        continue;
-      }
-      if (herr == 2) throw Status(AIWC_EEXEC, "in-bag row count exceeded the slot bound");
-      if (herr == 3) throw Status(AIWC_EEXEC, "frontier/node capacity exceeded");
-      if (herr) throw Status(AIWC_EEXEC, "grow kernel error " + std::to_string(herr));
-      break;
-    }
-    CK(cudaMemcpy(cnt.data(), tree_cnt.p, size_t{T} * 4, cudaMemcpyDeviceToHost));
-    if (want_prof) {
-      unsigned long long h[16];
-      CK(cudaMemcpy(h, prof.p, 16 * 8, cudaMemcpyDeviceToHost));
-      static const char* names[14] = {"bootstrap", "bitmap", "payload0", "lists0+root",
-                                      "-", "elig", "sample", "chains", "decide", "route",
-                                      "segtab", "paypass", "listpass", "emit+oob"};
-      double tot = 0;
-      for (int i = 0; i < 14; ++i) tot += static_cast<double>(h[i]);
-      std::fprintf(stderr, "[aiwc grow phases] slots=%d trees=%u total=%.3g cycles:", slots, T, tot);
-      for (int i = 0; i < 14; ++i)
-        if (h[i]) std::fprintf(stderr, " %s=%.1f%%", names[i], 100.0 * h[i] / tot);
-      std::fprintf(stderr, "\n");
-    }
-    f->off.assign(T + 1, 0);
-    for (uint32_t t = 0; t < T; ++t) f->off[t + 1] = f->off[t] + cnt[t];
-    const uint64_t N = f->off[T];
-    f->feature.alloc(N);
-    f->left.alloc(N);
-    f->thr.alloc(N);
-    f->value.alloc(N);
-    f->packed.alloc(N);
-    f->d_off.alloc(T + 1);
-    CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, st.s));
-    compact_kernel<<<T, 256, 0, st.s>>>(pf.p, pt.p, pl.p, pv.p, tree_off.p, f->d_off.p,
-                                        f->feature.p, f->thr.p, f->left.p, f->value.p,
-                                        f->packed.p);
-    CK(cudaGetLastError());
-    g_launches += 1;
-    CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
-    CK(cudaStreamSynchronize(st.s));
-    const auto t_compact = std::chrono::steady_clock::now();
-    if (compute_oob && tree_begin == 0 && tree_end == num_trees) {
-      std::vector<double> sum(n, 0.0);
-      std::vector<uint32_t> count(n, 0);
-      oob_accumulate_device(f.get(), sum.data(), count.data(), st.s);
-      f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
-      f->has_oob = true;
-    }
-    if (want_prof) {
-      const auto now = std::chrono::steady_clock::now();
-      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-      std::fprintf(stderr, "[aiwc fit host] setup %.1f ms, grow+compact %.1f ms, oob %.1f ms\n",
-                   ms(t_start, t_grow0), ms(t_grow0, t_compact), ms(t_compact, now));
-    }
-    CK(cudaEventRecord(evf1, st.s));
-    CK(cudaEventSynchronize(evf1));
-    {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, evf0, evf1));
-      f->fit_ms = ms;
-    }
-    *out = f.release();
+    const CellSpec cs{ncells, mtry, min_node_size, num_trees};
+    fit_body(ctx, num_trees, mmax, nmin, seed, 0, ncells * num_trees, 0, &cs, out);
+    (*out)->cells = ncells;
   });
 }
 
@@ -1057,6 +1117,41 @@ int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, 
     CK(cudaStreamSynchronize(st.s));
     for (uint32_t i = 0; i < k; ++i)
       out[i] = finalize_oob(ctx->y.data(), n, hs.data() + size_t{i} * n, hc.data() + size_t{i} * n);
+  });
+}
+
+int aiwc_oob_prefix_cells(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts,
+                          uint32_t k, aiwc_oob_stats* out) {
+  return guard([&] {
+    if (!ctx || !f || !tree_counts || !out) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    const uint32_t T = f->trees / f->cells;
+    for (uint32_t i = 0; i < k; ++i)
+      if (tree_counts[i] < 1 || tree_counts[i] > T || (i && tree_counts[i] < tree_counts[i - 1]))
+        throw Status(AIWC_EARG, "tree counts must ascend within [1, trees per forest]");
+    if (k == 0) return;
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    const uint64_t n = f->n;
+    DevBuf<uint32_t> cps(k);
+    DevBuf<double> sums(size_t{k} * n);
+    DevBuf<uint32_t> counts(size_t{k} * n);
+    CK(cudaMemcpyAsync(cps.p, tree_counts, k * 4, cudaMemcpyHostToDevice, st.s));
+    std::vector<double> hs(size_t{k} * n);
+    std::vector<uint32_t> hc(size_t{k} * n);
+    for (uint32_t c = 0; c < f->cells; ++c) {  // forest c: trees [c*T, (c+1)*T)
+      oob_prefix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st.s>>>(
+          f->oobval.p + size_t{c} * T * n, cps.p, k, n, sums.p, counts.p);
+      CK(cudaGetLastError());
+      g_launches += 1;
+      CK(cudaMemcpyAsync(hs.data(), sums.p, hs.size() * 8, cudaMemcpyDeviceToHost, st.s));
+      CK(cudaMemcpyAsync(hc.data(), counts.p, hc.size() * 4, cudaMemcpyDeviceToHost, st.s));
+      CK(cudaStreamSynchronize(st.s));
+      for (uint32_t i = 0; i < k; ++i)
+        out[size_t{c} * k + i] = finalize_oob(ctx->y.data(), n, hs.data() + size_t{i} * n,
+                                              hc.data() + size_t{i} * n);
+    }
   });
 }
 

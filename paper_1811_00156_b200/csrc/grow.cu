@@ -1021,7 +1021,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   const DevData& d = a.d;
   const uint32_t n = static_cast<uint32_t>(d.n);
   const uint32_t p = d.p;
-  const uint32_t m = a.mtry;
   const uint32_t tid = threadIdx.x;
   const unsigned lane = lane_id();
   const unsigned wid = warp_id();
@@ -1087,7 +1086,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     __syncthreads();
     const uint32_t tl = s_tree;
     if (tl >= a.tree_end - a.tree_begin) break;
-    const uint64_t t = a.tree_begin + tl;
+    // this tree's parameters and its index in its forest (grid cells: forest tl / cell_trees)
+    const uint32_t cell = a.cell_trees ? tl / a.cell_trees : 0u;
+    const uint32_t m = a.cell_trees ? a.cell_mtry[cell] : a.mtry;
+    const uint32_t mns = a.cell_trees ? a.cell_mns[cell] : a.mns;
+    const uint64_t t = a.cell_trees ? tl - cell * a.cell_trees : a.tree_begin + tl;
     const uint64_t key = dmix64(a.seed ^ a.tag_tree ^ dmix64(t));
 
     // ---- bootstrap (forest.hpp:184-195) ----
@@ -1223,7 +1226,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
           if (f < F) {
             const NodeWork nw = fr[f];
             const double sse = __dsub_rn(nw.q, __ddiv_rn(__dmul_rn(nw.s, nw.s), nw.w));
-            const bool too_small = nw.w < 2.0 * static_cast<double>(a.mns);
+            const bool too_small = nw.w < 2.0 * static_cast<double>(mns);
             const bool pure = sse <= __dmul_rn(1e-12, nw.q > 1.0 ? nw.q : 1.0);
             if (too_small || pure)
               nval[nw.id] = __ddiv_rn(nw.s, nw.w);

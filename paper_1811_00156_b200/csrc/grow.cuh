@@ -80,6 +80,11 @@ struct SlotLayout {
 struct GrowArgs {
   DevData d;
   uint32_t mtry, mns;
+  // grid cells (CTA-per-tree grower only): tree tl belongs to cell tl / cell_trees, grows
+  // with that cell's mtry / min.node.size, and is tree tl % cell_trees of its forest
+  const uint32_t* cell_mtry;
+  const uint32_t* cell_mns;
+  uint32_t cell_trees;  // 0: one forest
   uint64_t seed;
   uint64_t tag_tree;  // fnv1a64("tree")
   uint32_t tree_begin, tree_end;

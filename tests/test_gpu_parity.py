@@ -321,3 +321,16 @@ def test_wide_grower_u32_ranks(seed):
     assert forests_equal(o, soa_of(f)) is None
     stats, _, _ = Oracle.oob(col, y, n, p, o)
     assert [f.oob.mse, f.oob.error_pct] == [stats[1], stats[3]]
+
+
+def test_grid_cells_batched_equal_separate_fits(c1, seed):
+    """aiwc_fit_cells (per-tree mtry / min.node.size, one launch) == one fit per cell:
+    every prefix OOB statistic bit-for-bit, over cells with different tree shapes."""
+    t, prep = c1
+    cells = [(1, 1), (6, 5), (42, 50), (17, 3), (30, 9)]
+    counts = [1, 13, 40]
+    got = pkg.grid_oob(prep, cells, counts, seed, cell_batch=3)
+    for i, (m, mns) in enumerate(cells):
+        f = pkg.fit(prep, pkg.ForestParams(counts[-1], m, mns, seed), compute_oob_stats=False)
+        want = [s.error_pct for s in pkg.oob_prefix(f, prep, counts)]
+        assert list(got[i]) == want, (m, mns)
