@@ -121,7 +121,7 @@ int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum,
  * 79-108) over the num.trees axis. */
 int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, uint32_t k,
                     aiwc_oob_stats* out);
-/* Grid cells in one launch (tables below 65,536 rows): ncells forests of num_trees trees
+/* Grid cells in one launch: ncells forests of num_trees trees
  * each, forest c grown exactly as aiwc_fit(ctx, num_trees, mtry[c], min_node_size[c],
  * seed, 0, num_trees, ...) would (tree t of every forest keyed by (seed, t)); the trees of
  * forest c are [c*num_trees, (c+1)*num_trees) of the returned handle.  OOB statistics

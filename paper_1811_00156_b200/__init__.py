@@ -398,7 +398,7 @@ def oob_prefix(forest: Forest, prepared: PreparedDataset, tree_counts) -> list:
 
 
 def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
-             workers: int = 1, cell_batch: int = 64) -> np.ndarray:
+             workers: int = 1, cell_batch: int = 34) -> np.ndarray:
     """C2 grid objective (tuner.hpp:247-253 / experiments.hpp:79-108): error_pct for
     every (mtry, min_node_size) cell x num.trees value, one fit of max(tree_counts)
     trees per cell.  Returns an array [len(cells), len(tree_counts)].  Tables below
@@ -409,7 +409,7 @@ def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
 
     cps = sorted(int(t) for t in tree_counts)
     out = np.zeros((len(cells), len(cps)))
-    if prepared.n < 65536:  # batched: many cells' forests in one launch (aiwc_fit_cells)
+    if prepared.n < 65536 and cell_batch > 0:  # many cells' forests per launch
         cpa = np.ascontiguousarray(cps, np.uint32)
         for i0 in range(0, len(cells), cell_batch):
             cs = cells[i0:i0 + cell_batch]

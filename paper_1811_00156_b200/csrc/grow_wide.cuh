@@ -92,14 +92,25 @@ __host__ __device__ inline uint32_t grp_width(uint32_t m) {
   while (c < m && c < 32) c <<= 1;
   return 32u / c;
 }
-__host__ __device__ inline uint32_t grp_tasks_per_node(uint32_t m) {
-  const uint32_t ng = 32u / grp_width(m);  // chains per warp
-  return (m + ng - 1) / ng;
-}
 
-__device__ __forceinline__ uint64_t tree_key(const GrowArgs& g, uint32_t tl) {
-  const uint64_t t = uint64_t{g.tree_begin} + tl;
-  return dmix64(g.seed ^ g.tag_tree ^ dmix64(t));
+// Per-tree parameters: with grid cells (GrowArgs::cell_trees > 0) the batch's tree b is
+// tree (t0+b) % cell_trees of cell (t0+b) / cell_trees, which has its own mtry / mns.
+__device__ __forceinline__ uint32_t tree_m(const WideArgs& a, uint32_t b) {
+  return a.g.cell_trees ? a.g.cell_mtry[(a.t0 + b) / a.g.cell_trees] : a.g.mtry;
+}
+__device__ __forceinline__ uint32_t tree_mns(const WideArgs& a, uint32_t b) {
+  return a.g.cell_trees ? a.g.cell_mns[(a.t0 + b) / a.g.cell_trees] : a.g.mns;
+}
+__device__ __forceinline__ uint64_t tree_key(const WideArgs& a, uint32_t b) {
+  const uint32_t tl = a.t0 + b;
+  const uint64_t t = a.g.cell_trees ? tl % a.g.cell_trees : uint64_t{a.g.tree_begin} + tl;
+  return dmix64(a.g.seed ^ a.g.tag_tree ^ dmix64(t));
+}
+// lane-group tasks of a node with m sampled columns when the group kernel was launched
+// for the batch's widest mtry (lane groups of grp_width(mmax))
+__host__ __device__ inline uint32_t grp_tpn(uint32_t m, uint32_t mmax) {
+  const uint32_t ng = 32u / grp_width(mmax);
+  return (m + ng - 1) / ng;
 }
 
 __device__ __forceinline__ uint32_t nchunks_of(uint32_t A, uint32_t nl) {
@@ -134,7 +145,7 @@ __global__ void w_boot(const WideArgs a) {
   const uint32_t b = blockIdx.y, tl = a.t0 + b;
   const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
-  const uint64_t key = tree_key(a.g, tl);
+  const uint64_t key = tree_key(a, b);
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t r = static_cast<uint32_t>(draw_bounded(key, uint64_t{j} + 1u, n));
     if (a.g.inbag) a.g.inbag[static_cast<size_t>(tl) * n + j] = r;
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   if (s.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
   const NodeWork* fr = P.front;
-  const uint32_t F = s.F, A = s.A, m = a.g.mtry, p = a.g.d.p;
+  const uint32_t F = s.F, A = s.A, m = tree_m(a, b), p = a.g.d.p;
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   uint32_t carry = 0;
   for (uint32_t base = 0; base < F; base += NT) {
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     if (f < F) {
       const NodeWork nw = fr[f];
       const double sse = __dsub_rn(nw.q, __ddiv_rn(__dmul_rn(nw.s, nw.s), nw.w));
-      const bool too_small = nw.w < 2.0 * static_cast<double>(a.g.mns);
+      const bool too_small = nw.w < 2.0 * static_cast<double>(tree_mns(a, b));
       const bool pure = sse <= __dmul_rn(1e-12, nw.q > 1.0 ? nw.q : 1.0);
       if (too_small || pure)
         P.nval[nw.id] = __ddiv_rn(nw.s, nw.w);
@@ -344,7 +355,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     carry += tot;
   }
   const uint32_t E = carry;
-  const uint64_t key = tree_key(a.g, a.t0 + b);
+  const uint64_t key = tree_key(a, b);
   for (uint32_t e = threadIdx.x; e < E; e += NT) {
     uint16_t pool[kMaxP];
     for (uint32_t c = 0; c < p; ++c) pool[c] = static_cast<uint16_t>(c);
@@ -410,9 +421,10 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
-        v0 = s.E0 * a.g.mtry;
-        v1 = s.E1 * grp_tasks_per_node(a.g.mtry);
-        v2 = s.E2 * a.g.mtry;
+        const uint32_t m = tree_m(a, b);
+        v0 = s.E0 * m;
+        v1 = s.E1 * grp_tpn(m, a.g.mtry);
+        v2 = s.E2 * m;
       } else {
         v0 = s.Sbig;
         v1 = s.S;
@@ -462,7 +474,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
   constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
   __shared__ double stage[8][GB == 32 ? 64 : 32 * UB];
   const uint32_t total = a.off[2][a.B];
-  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   // tasks are claimed dynamically (chains differ in length by orders of magnitude)
   for (;;) {
@@ -471,6 +483,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     t = __shfl_sync(kFull, t, 0);
     if (t >= total) break;
     const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
+    const uint32_t m = tree_m(a, b);
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
     const uint32_t e = P.ecls[st.E0 + st.E1 + k / m];  // class 2
@@ -538,7 +551,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
   __shared__ uint32_t s_w0;
   __shared__ uint32_t s_bp[kCoopW];
   const uint32_t total = a.off[2][a.B];
-  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   const unsigned lane = lane_id(), wid = warp_id();
   const uint32_t pt = threadIdx.x - 32;  // producer thread index (wid > 0)
@@ -549,6 +562,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
     __syncthreads();
     if (t >= total) break;
     const uint32_t b = owner(a.off[2], a.B, t), k = t - a.off[2][b];
+    const uint32_t m = tree_m(a, b);
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& ts = a.ts[b];
     const uint32_t e = P.ecls[ts.E0 + ts.E1 + k / m];
@@ -753,8 +767,8 @@ template <typename RankT, int G, int U>
 __global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
   __shared__ double stage[8][32 * U];
   const uint32_t total = a.off[1][a.B];
-  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
-  const uint32_t tpn = grp_tasks_per_node(m), grp = lane_id() / G;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const uint32_t grp = lane_id() / G;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   for (;;) {  // tasks claimed dynamically
     uint32_t t = 0;
@@ -762,6 +776,7 @@ __global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
     t = __shfl_sync(kFull, t, 0);
     if (t >= total) break;
     const uint32_t b = owner(a.off[1], a.B, t), k = t - a.off[1][b];
+    const uint32_t m = tree_m(a, b), tpn = grp_tpn(m, a.g.mtry);
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
     const uint32_t e = P.ecls[st.E0 + k / tpn];
@@ -784,10 +799,11 @@ __global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
 template <typename RankT>
 __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
   const uint32_t total = a.off[0][a.B];
-  const uint32_t m = a.g.mtry, n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
+  const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const uint32_t b = owner(a.off[0], a.B, t), k = t - a.off[0][b];
+    const uint32_t m = tree_m(a, b);
     const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t e = P.ecls[k / m];
     const uint32_t slot = e * m + k % m;
@@ -816,7 +832,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   if (st.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
   const DevData& d = a.g.d;
-  const uint32_t n = static_cast<uint32_t>(d.n), m = a.g.mtry, stride = a.g.L.stride;
+  const uint32_t n = static_cast<uint32_t>(d.n), m = tree_m(a, b), stride = a.g.L.stride;
   const RankT* rank = static_cast<const RankT*>(d.rank);
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;

@@ -329,7 +329,14 @@ def test_grid_cells_batched_equal_separate_fits(c1, seed):
     t, prep = c1
     cells = [(1, 1), (6, 5), (42, 50), (17, 3), (30, 9)]
     counts = [1, 13, 40]
-    got = pkg.grid_oob(prep, cells, counts, seed, cell_batch=3)
+    got = pkg.grid_oob(prep, cells, counts, seed, cell_batch=3)  # 120 trees: wide grower
+    # the CTA-per-tree grower takes the same cells (few trees per launch)
+    os.environ["AIWC_GROW_WIDE"] = "0"
+    try:
+        got0 = pkg.grid_oob(prep, cells, counts, seed, cell_batch=5)
+    finally:
+        del os.environ["AIWC_GROW_WIDE"]
+    assert np.array_equal(got, got0)
     for i, (m, mns) in enumerate(cells):
         f = pkg.fit(prep, pkg.ForestParams(counts[-1], m, mns, seed), compute_oob_stats=False)
         want = [s.error_pct for s in pkg.oob_prefix(f, prep, counts)]
