@@ -480,7 +480,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     ncell = max(1, ARGS.grid_cells)
     cells = [(m, 1 + (7 * m) % 50) for m in range(1, 35)][:ncell]
     allreduce = shard.torch_allreduce_sum(torch.device("cuda", local)) if world > 1 else (lambda a: a)
-    _ = pkg.grid_oob(prep, cells[:1], counts[:2], seed)  # warm-up
+    _ = pkg.grid_oob(prep, cells, counts, seed)  # warm-up (same batch sizes)
     barrier()
     s = time.perf_counter()
     err = shard.grid_sharded(cells, counts, rank, world,
