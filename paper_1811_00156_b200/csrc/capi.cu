@@ -1409,31 +1409,56 @@ int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t
     if (!col || !y || !kernel_of_row || !predicted_seconds)
       throw Status(AIWC_EARG, "NULL argument");
     if (fold_begin > fold_end || fold_end > K) throw Status(AIWC_EARG, "fold range out of [0, K]");
-    for (uint32_t k = fold_begin; k < fold_end; ++k) {
-      std::vector<uint64_t> train, test;
-      for (uint64_t i = 0; i < n; ++i) (kernel_of_row[i] == k ? test : train).push_back(i);
-      if (test.empty()) continue;
-      const uint64_t m = train.size();
-      std::vector<double> tc(m * p), ty(m), rows(test.size() * p), resp(test.size());
-      for (uint32_t c = 0; c < p; ++c)
-        for (uint64_t i = 0; i < m; ++i) tc[c * m + i] = col[c * n + train[i]];
-      for (uint64_t i = 0; i < m; ++i) ty[i] = y[train[i]];
-      for (uint64_t j = 0; j < test.size(); ++j)
-        for (uint32_t c = 0; c < p; ++c) rows[j * p + c] = col[c * n + test[j]];
-      aiwc_ctx* ctx = nullptr;
-      int rc = aiwc_ctx_create(tc.data(), ty.data(), m, p, device, &ctx);
-      if (rc) throw Status(rc, g_last_error);
-      std::unique_ptr<aiwc_ctx, int (*)(aiwc_ctx*)> cg(ctx, aiwc_ctx_free);
-      aiwc_forest* f = nullptr;
-      rc = aiwc_fit(ctx, num_trees, mtry, min_node_size, host_derive_seed(seed, "holdout", k),
-                    0, num_trees, 0, &f);
-      if (rc) throw Status(rc, g_last_error);
-      std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> fg(f, aiwc_forest_free);
-      rc = aiwc_predict(f, rows.data(), test.size(), p, resp.data());
-      if (rc) throw Status(rc, g_last_error);
-      for (uint64_t j = 0; j < test.size(); ++j)
-        predicted_seconds[test[j]] = std::pow(10.0, resp[j]);  // from_response, dataset.hpp:89-91
-    }
+    // folds are independent (own dataset copy, stream and forest): a few host threads
+    // keep several folds' fits in flight; each writes only its own held-out rows
+    std::atomic<uint32_t> next{fold_begin};
+    std::mutex emu;
+    int err_rc = 0;
+    std::string err_msg;
+    auto work = [&] {
+      for (;;) {
+        const uint32_t k = next.fetch_add(1);
+        if (k >= fold_end) return;
+        {
+          std::lock_guard<std::mutex> g(emu);
+          if (err_rc) return;
+        }
+        std::vector<uint64_t> train, test;
+        for (uint64_t i = 0; i < n; ++i) (kernel_of_row[i] == k ? test : train).push_back(i);
+        if (test.empty()) continue;
+        const uint64_t m = train.size();
+        std::vector<double> tc(m * p), ty(m), rows(test.size() * p), resp(test.size());
+        for (uint32_t c = 0; c < p; ++c)
+          for (uint64_t i = 0; i < m; ++i) tc[c * m + i] = col[c * n + train[i]];
+        for (uint64_t i = 0; i < m; ++i) ty[i] = y[train[i]];
+        for (uint64_t j = 0; j < test.size(); ++j)
+          for (uint32_t c = 0; c < p; ++c) rows[j * p + c] = col[c * n + test[j]];
+        aiwc_ctx* ctx = nullptr;
+        aiwc_forest* f = nullptr;
+        int rc = aiwc_ctx_create(tc.data(), ty.data(), m, p, device, &ctx);
+        if (!rc)
+          rc = aiwc_fit(ctx, num_trees, mtry, min_node_size, host_derive_seed(seed, "holdout", k),
+                        0, num_trees, 0, &f);
+        if (!rc) rc = aiwc_predict(f, rows.data(), test.size(), p, resp.data());
+        if (f) aiwc_forest_free(f);
+        if (ctx) aiwc_ctx_free(ctx);
+        if (rc) {
+          std::lock_guard<std::mutex> g(emu);
+          if (!err_rc) {
+            err_rc = rc;
+            err_msg = g_last_error;
+          }
+          return;
+        }
+        for (uint64_t j = 0; j < test.size(); ++j)  // from_response, dataset.hpp:89-91
+          predicted_seconds[test[j]] = std::pow(10.0, resp[j]);
+      }
+    };
+    const uint32_t nth = std::min<uint32_t>(4u, fold_end - fold_begin);
+    std::vector<std::thread> th;
+    for (uint32_t i = 0; i < nth; ++i) th.emplace_back(work);
+    for (auto& t : th) t.join();
+    if (err_rc) throw Status(err_rc, err_msg);
   });
 }
 
