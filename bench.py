@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--skip-predict", action="store_true")
     ap.add_argument("--skip-grid", action="store_true")
+    ap.add_argument("--gather-trees", type=int, default=100,
+                    help="trees per rank of the forest all-gathered over NCCL (N > 1)")
     ap.add_argument("--grid-cells", type=int, default=34)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-worker", action="store_true")
@@ -353,6 +355,12 @@ def main():
     e2e_s = max_over_ranks(float(np.median(e2e_times)))
     e2e_value = total_trees / e2e_s
 
+    # ---------------- forest gather over NCCL (N > 1) ----------------
+    forest_gather = None
+    if world > 1 and args.gather_trees > 0:
+        forest_gather = bench_forest_gather(pkg, torch, shard, prep, args, rank, world, local,
+                                            barrier, max_over_ranks, sum_over_ranks)
+
     del prep
     torch.cuda.empty_cache()
 
@@ -409,6 +417,7 @@ def main():
                                                             "extra_error") if k in cpu_res}
                                if cpu_res else None),
         "predict": predict,
+        "forest_gather": forest_gather,
         "c1": c1,
         "grid": grid,
         "loko": loko,
@@ -418,6 +427,39 @@ def main():
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_forest_gather(pkg, torch, shard, prep, args, rank, world, local, barrier,
+                        max_over_ranks, sum_over_ranks):
+    """Every rank fits its tree range of a (gather_trees x N)-tree C4 forest, then the node
+    SoA is all-gathered device to device over NCCL (shard.allgather_forest) so that every
+    rank holds the whole forest.  Bounded tree count: the full 1000-tree-per-GPU C4 forest
+    is 8.9 GB of nodes per rank, too large to replicate 8 times on every GPU."""
+    per = args.gather_trees
+    params = pkg.ForestParams(per * world, C4_MTRY, C4_MNS, pkg.derive_seed(1, "forest"))
+    f = pkg.fit(prep, params, rank * per, (rank + 1) * per, compute_oob_stats=False)
+    total_nodes = int(sum_over_ranks(float(f.total_nodes)))
+    need = total_nodes * 80 + (1 << 30)  # parts + concatenation + imported SoA + packed
+    free = torch.cuda.mem_get_info(local)[0]
+    ok = -max_over_ranks(-float(free >= need))
+    if ok < 1:
+        return {"skipped": f"needs ~{need / 1e9:.1f} GB free per GPU"}
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    g = shard.allgather_forest(f, world, local)
+    ev1.record(stream)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ok = g.num_trees == per * world and g.total_nodes == total_nodes
+    gathered = total_nodes * 24  # feature + left (i32) + threshold + value (f64) per node
+    del g, f
+    torch.cuda.empty_cache()
+    return {"trees_per_rank": per, "trees": per * world, "nodes": total_nodes, "ms": ms,
+            "bytes_gathered_per_rank": gathered, "GB_per_s_per_rank": gathered / ms / 1e6,
+            "complete": bool(ok),
+            "path": "aiwc_forest_export_device -> NCCL all_gather -> aiwc_forest_import_device"}
 
 
 def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak):

@@ -104,6 +104,17 @@ int aiwc_forest_import(uint32_t trees, const uint64_t* offsets, const int32_t* f
                        const double* value, const uint32_t* inbag, uint64_t n, int device,
                        aiwc_forest** out);
 
+/* Device-to-device forms of export / import, for gathering the tree-seed shards of a
+ * multi-GPU fit over NCCL: the SoA arrays (and inbag, trees x n) are DEVICE
+ * pointers on the forest's device; offsets stay on the host.  import_device checks the
+ * canonical BFS layout on the device (same AIWC_EPARSE as aiwc_forest_import). */
+int aiwc_forest_export_device(const aiwc_forest* f, int32_t* d_feature, double* d_threshold,
+                              int32_t* d_left, double* d_value, uint32_t* d_inbag);
+int aiwc_forest_import_device(uint32_t trees, const uint64_t* offsets, const int32_t* d_feature,
+                              const double* d_threshold, const int32_t* d_left,
+                              const double* d_value, const uint32_t* d_inbag, uint64_t n,
+                              int device, aiwc_forest** out);
+
 /* ---- OOB ---------------------------------------------------------------------
  * compute_oob over (forest, ctx): stats + optional per-row tree-ordered sum/count. */
 int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum,

@@ -98,6 +98,9 @@ def lib():
         L.aiwc_forest_oob_stats.argtypes = [vp, P(OobStatsC)]
         L.aiwc_forest_import.argtypes = [u32, P(u64), P(i32), P(f64), P(i32), P(i32), P(f64),
                                          P(u32), u64, C.c_int, P(vp)]
+        L.aiwc_forest_export_device.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.aiwc_forest_import_device.argtypes = [u32, P(u64), vp, vp, vp, vp, vp, u64, C.c_int,
+                                                P(vp)]
         L.aiwc_oob.argtypes = [vp, vp, P(OobStatsC), P(f64), P(u32)]
         L.aiwc_oob_accumulate.argtypes = [vp, vp, P(f64), P(u32)]
         L.aiwc_oob_finalize.argtypes = [P(f64), u64, P(f64), P(u32), P(OobStatsC)]
@@ -255,6 +258,29 @@ class Forest:
         _check(lib().aiwc_forest_export(self._h, _p(off, u64), _p(f, i32), _p(th, f64),
                                         _p(le, i32), _p(ri, i32), _p(va, f64)))
         return off, f, th, le, ri, va
+
+    def offsets(self) -> np.ndarray:
+        off = np.zeros(self.num_trees + 1, np.uint64)
+        _check(lib().aiwc_forest_export(self._h, _p(off, u64), None, None, None, None, None))
+        return off
+
+    def export_device(self, d_feature: int, d_threshold: int, d_left: int, d_value: int,
+                      d_inbag: int | None = None):
+        """Device-to-device copy of the node SoA (and in-bag draws) into caller buffers on
+        the forest's device (aiwc_forest_export_device)."""
+        _check(lib().aiwc_forest_export_device(self._h, d_feature, d_threshold, d_left,
+                                               d_value, d_inbag))
+
+    @classmethod
+    def from_device(cls, offsets, d_feature: int, d_threshold: int, d_left: int, d_value: int,
+                    d_inbag: int | None = None, n: int = 0, device: int = 0) -> "Forest":
+        """Forest from device SoA buffers (a forest gathered over NCCL); offsets on host."""
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        h = vp()
+        _check(lib().aiwc_forest_import_device(len(offsets) - 1, _p(offsets, u64), d_feature,
+                                               d_threshold, d_left, d_value, d_inbag, n,
+                                               device, C.byref(h)))
+        return cls(h, None, n)
 
     # --- Forest::inbag ---
     def inbag(self) -> np.ndarray:

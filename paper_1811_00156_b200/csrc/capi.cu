@@ -1054,6 +1054,73 @@ int aiwc_forest_import(uint32_t trees, const uint64_t* offsets, const int32_t* f
   });
 }
 
+int aiwc_forest_export_device(const aiwc_forest* f, int32_t* d_feature, double* d_threshold,
+                              int32_t* d_left, double* d_value, uint32_t* d_inbag) {
+  return guard([&] {
+    if (!f) throw Status(AIWC_EARG, "forest is NULL");
+    if (d_inbag && !f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
+    DeviceGuard dg(f->device);
+    const uint64_t N = f->off.back();
+    Stream st;
+    if (d_feature) CK(cudaMemcpyAsync(d_feature, f->feature.p, N * 4, cudaMemcpyDeviceToDevice, st.s));
+    if (d_threshold) CK(cudaMemcpyAsync(d_threshold, f->thr.p, N * 8, cudaMemcpyDeviceToDevice, st.s));
+    if (d_left) CK(cudaMemcpyAsync(d_left, f->left.p, N * 4, cudaMemcpyDeviceToDevice, st.s));
+    if (d_value) CK(cudaMemcpyAsync(d_value, f->value.p, N * 8, cudaMemcpyDeviceToDevice, st.s));
+    if (d_inbag)
+      CK(cudaMemcpyAsync(d_inbag, f->inbag.p, size_t{f->trees} * f->n * 4,
+                         cudaMemcpyDeviceToDevice, st.s));
+    CK(cudaStreamSynchronize(st.s));
+  });
+}
+
+int aiwc_forest_import_device(uint32_t trees, const uint64_t* offsets, const int32_t* d_feature,
+                              const double* d_threshold, const int32_t* d_left,
+                              const double* d_value, const uint32_t* d_inbag, uint64_t n,
+                              int device, aiwc_forest** out) {
+  return guard([&] {
+    if (!offsets || !d_feature || !d_threshold || !d_left || !d_value || !out || trees < 1)
+      throw Status(AIWC_EARG, "NULL argument or zero trees");
+    DeviceGuard dg(device);
+    auto f = std::make_unique<aiwc_forest>();
+    f->device = device;
+    f->n = n;
+    f->trees = trees;
+    f->num_trees = trees;
+    f->off.assign(offsets, offsets + trees + 1);
+    for (uint32_t t = 0; t < trees; ++t)
+      if (f->off[t + 1] <= f->off[t]) throw Status(AIWC_EPARSE, "empty tree in model");
+    const uint64_t N = f->off[trees];
+    f->feature.alloc(N);
+    f->left.alloc(N);
+    f->thr.alloc(N);
+    f->value.alloc(N);
+    f->packed.alloc(N);
+    f->d_off.alloc(trees + 1);
+    Stream st;
+    CK(cudaMemcpyAsync(f->feature.p, d_feature, N * 4, cudaMemcpyDeviceToDevice, st.s));
+    CK(cudaMemcpyAsync(f->left.p, d_left, N * 4, cudaMemcpyDeviceToDevice, st.s));
+    CK(cudaMemcpyAsync(f->thr.p, d_threshold, N * 8, cudaMemcpyDeviceToDevice, st.s));
+    CK(cudaMemcpyAsync(f->value.p, d_value, N * 8, cudaMemcpyDeviceToDevice, st.s));
+    CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (trees + 1) * 8, cudaMemcpyHostToDevice, st.s));
+    DevBuf<uint32_t> bad(1);
+    CK(cudaMemsetAsync(bad.p, 0, 4, st.s));
+    pack_check_kernel<<<std::min<uint32_t>(trees, 148u * 16u), 256, 0, st.s>>>(
+        f->d_off.p, trees, f->feature.p, f->thr.p, f->left.p, f->value.p, f->packed.p, bad.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    if (d_inbag && n) {
+      f->inbag.alloc(size_t{trees} * n);
+      CK(cudaMemcpyAsync(f->inbag.p, d_inbag, size_t{trees} * n * 4, cudaMemcpyDeviceToDevice,
+                         st.s));
+    }
+    uint32_t h_bad = 0;
+    CK(cudaMemcpyAsync(&h_bad, bad.p, 4, cudaMemcpyDeviceToHost, st.s));
+    CK(cudaStreamSynchronize(st.s));
+    if (h_bad) throw Status(AIWC_EPARSE, "model tree is not in canonical BFS layout");
+    *out = f.release();
+  });
+}
+
 int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum,
              uint32_t* row_count) {
   return guard([&] {

@@ -81,6 +81,30 @@ __global__ void right_child_kernel(const int32_t* __restrict__ left, uint64_t N,
   }
 }
 
+// Forest built from device SoA (a gathered forest, aiwc_forest_import_device): CTA per
+// tree packs the predict nodes and checks the canonical BFS layout the host import checks
+// (split nodes' children inside the tree, forest.hpp:310-311); *bad = 1 + tree on failure
+__global__ void pack_check_kernel(const uint64_t* __restrict__ off, uint32_t T,
+                                  const int32_t* __restrict__ feature,
+                                  const double* __restrict__ thr,
+                                  const int32_t* __restrict__ left,
+                                  const double* __restrict__ val, PredNode* __restrict__ packed,
+                                  uint32_t* __restrict__ bad) {
+  for (uint32_t t = blockIdx.x; t < T; t += gridDim.x) {
+    const uint64_t b = off[t], e = off[t + 1];
+    if (e <= b) {
+      if (threadIdx.x == 0) atomicCAS(bad, 0u, t + 1u);
+      continue;
+    }
+    const int64_t cnt = static_cast<int64_t>(e - b);
+    for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
+      const int32_t f = feature[i], l = left[i];
+      if (f >= 0 && (l < 1 || l + 1 >= cnt)) atomicCAS(bad, 0u, t + 1u);
+      packed[i] = PredNode{f >= 0 ? thr[i] : val[i], f, l};
+    }
+  }
+}
+
 // OOB leaf values of an imported forest: in-bag flags from the draws, then a walk
 // over the column store with the stored f64 thresholds (Tree::predict semantics)
 __global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t T, uint64_t n,

@@ -9,7 +9,9 @@ union equals a one-GPU fit.  Two exchanges exist:
   rank r receives the per-row (sum, count) of trees [0, t0_r) from rank r-1, continues
   it with its own trees (aiwc_oob_accumulate), and passes it on; the last rank
   finalises.  Result: bit-identical to the one-GPU / reference value.
-* the forest gather (node SoA + in-bag lists) concatenates rank parts in rank order.
+* the forest gather (node SoA + in-bag lists) concatenates rank parts in rank order
+  (`gather_forest`; `allgather_forest` keeps it on the devices: NCCL all-gather of
+  device buffers exported and re-imported through the C-ABI).
 
 The grid search (C2) and hold-one-kernel-out evaluate (C3) shard by cell / fold: each
 cell or fold is computed by exactly one rank into a zero-filled array, so a SUM
@@ -89,6 +91,82 @@ def concat_forests(parts):
         inb.append(ib)
     return (np.concatenate(offs), *[np.concatenate(c) for c in cols],
             np.concatenate(inb) if inb and inb[0] is not None else None)
+
+
+def gather_forest(off_local, arrays, world: int, all_gather, n: int = 0):
+    """All-gather of the tree-seed shards of a forest: every rank ends with the
+    whole forest in global tree order (rank order = tree order, `tree_range`).
+
+    off_local: this rank's host offsets (trees_local + 1).  arrays: this rank's flat
+    tensors [feature i32, threshold f64, left i32, value f64], plus the in-bag draws
+    (trees_local x n, int32 view of u32) when n > 0, all on the collective's device.
+    all_gather(list_of_tensors, tensor) is torch.distributed.all_gather (NCCL over NVLink
+    on the GPUs, gloo in the CPU tests).  Ragged shards are padded to the largest.
+    Returns (offsets u64 host, [gathered tensors in the same order])."""
+    import torch
+
+    dev = arrays[0].device
+    off_local = np.asarray(off_local, np.uint64)
+    counts = np.diff(off_local).astype(np.int64)
+    meta = torch.tensor([len(counts), int(off_local[-1])], dtype=torch.int64, device=dev)
+    metas = [torch.empty_like(meta) for _ in range(world)]
+    all_gather(metas, meta)
+    metas = [(int(m[0]), int(m[1])) for m in (x.cpu().numpy() for x in metas)]
+    tmax = max(m[0] for m in metas)
+    nmax = max(m[1] for m in metas)
+    ct = torch.zeros(max(1, tmax), dtype=torch.int64, device=dev)
+    ct[:len(counts)] = torch.from_numpy(counts).to(dev)
+    cts = [torch.empty_like(ct) for _ in range(world)]
+    all_gather(cts, ct)
+    all_counts = np.concatenate([c.cpu().numpy()[:m[0]] for c, m in zip(cts, metas)])
+    offsets = np.zeros(len(all_counts) + 1, np.uint64)
+    offsets[1:] = np.cumsum(all_counts).astype(np.uint64)
+    out = []
+    for k, a in enumerate(arrays):
+        node_array = k < 4  # nodes: N_r entries; in-bag: T_r x n
+        size = max(1, nmax if node_array else tmax * n)
+        buf = torch.zeros(size, dtype=a.dtype, device=dev)
+        buf[:a.numel()] = a
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        all_gather(parts, buf)
+        out.append(torch.cat([q[:(m[1] if node_array else m[0] * n)]
+                              for q, m in zip(parts, metas)]))
+        del parts, buf
+    return offsets, out
+
+
+def allgather_forest(forest, world: int, device: int, all_gather=None, with_inbag=False):
+    """Device path of `gather_forest`: the local shard is copied device-to-device out of
+    the fitted forest (aiwc_forest_export_device), all-gathered over NCCL, and the whole
+    forest is rebuilt on the device (aiwc_forest_import_device) — no host round trip."""
+    import torch
+
+    from . import Forest
+
+    if all_gather is None:
+        import torch.distributed as dist
+
+        all_gather = dist.all_gather
+    dev = torch.device("cuda", device)
+    N, T, n = forest.total_nodes, forest.num_trees, forest.n
+    fe = torch.empty(N, dtype=torch.int32, device=dev)
+    th = torch.empty(N, dtype=torch.float64, device=dev)
+    le = torch.empty(N, dtype=torch.int32, device=dev)
+    va = torch.empty(N, dtype=torch.float64, device=dev)
+    arrays = [fe, th, le, va]
+    ib = None
+    if with_inbag:
+        ib = torch.empty(T * n, dtype=torch.int32, device=dev)
+        arrays.append(ib)
+    torch.cuda.synchronize(dev)
+    forest.export_device(fe.data_ptr(), th.data_ptr(), le.data_ptr(), va.data_ptr(),
+                         ib.data_ptr() if ib is not None else None)
+    off, out = gather_forest(forest.offsets(), arrays, world, all_gather,
+                             n if with_inbag else 0)
+    torch.cuda.synchronize(dev)
+    return Forest.from_device(off, *(t.data_ptr() for t in out[:4]),
+                              out[4].data_ptr() if with_inbag else None,
+                              n if with_inbag else 0, device)
 
 
 def cells_for_rank(cells, rank: int, world: int):

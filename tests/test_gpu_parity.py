@@ -144,6 +144,78 @@ def test_tree_ranges_and_chained_oob(c1, seed):
     assert oob_list(pkg.oob_finalize(t.y, rs, rc)) == oob_list(full.oob)
 
 
+def _thread_all_gather(world):
+    """In-process all_gather for `world` threads on one GPU (copies only; stands in for
+    NCCL's all-gather of the multi-GPU path)."""
+    import threading
+
+    slots, bar = [None] * world, threading.Barrier(world)
+
+    def for_rank(r):
+        def ag(lst, t):
+            slots[r] = t.clone()
+            bar.wait()
+            for i in range(world):
+                lst[i].copy_(slots[i])
+            bar.wait()
+        return ag
+    return for_rank
+
+
+@pytest.mark.parametrize("with_inbag", [True, False])
+def test_device_forest_gather(c1, seed, with_inbag):
+    """allgather_forest (device export -> all-gather -> device import) of two ragged
+    tree-range shards gives the one-shot forest on every rank: same SoA, in-bag draws,
+    OOB and predictions."""
+    import threading
+
+    import torch
+    from paper_1811_00156_b200 import shard
+
+    t, prep = c1
+    params = pkg.ForestParams(70, 6, 5, seed)
+    full = pkg.fit(prep, params)
+    parts = [pkg.fit(prep, params, 0, 31, compute_oob_stats=False),
+             pkg.fit(prep, params, 31, 70, compute_oob_stats=False)]
+    ag = _thread_all_gather(2)
+    got, errs = [None, None], []
+
+    def run(r):
+        try:
+            torch.cuda.set_device(0)
+            got[r] = shard.allgather_forest(parts[r], 2, 0, ag(r), with_inbag=with_inbag)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=120)
+    assert not errs, errs
+    rows = t.predictor_rows()
+    want = soa_of(full)
+    for g in got:
+        assert forests_equal(want, soa_of(g, with_inbag), check_inbag=with_inbag) is None
+        assert np.array_equal(g.predict_response(rows), full.predict_response(rows))
+        if with_inbag:
+            assert oob_list(pkg.compute_oob(g, prep)) == oob_list(full.oob)
+
+
+def test_device_import_rejects_bad_layout(c1, seed):
+    import torch
+
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(3, 6, 5, seed))
+    s = soa_of(f, False)
+    le = s.left.copy()
+    le[0] = 10 ** 6  # root's children outside the tree
+    d = [torch.from_numpy(np.ascontiguousarray(a)).cuda()
+         for a in (s.feature, s.threshold, le, s.value)]
+    with pytest.raises(pkg.ParseError):
+        pkg.Forest.from_device(s.offsets, *(x.data_ptr() for x in d))
+
+
 def test_import_predict_and_oob(c1, seed):
     t, prep = c1
     f = pkg.fit(prep, pkg.ForestParams(40, 6, 5, seed))

@@ -72,9 +72,15 @@ def _worker(rank, world, port, T, m, mns, seed, q):
         part = Oracle.fit(col, y, n, p, T, m, mns, seed, trees=range(t0, t1))
         send, recv = shard.torch_transport()
         res = shard.chained_oob(n, rank, world, _oracle_accumulate(part, col), send, recv)
-        parts = [None] * world
-        dist.all_gather_object(parts, (part.offsets, part.feature, part.threshold, part.left,
-                                       part.right, part.value, part.inbag))
+        import torch
+
+        arrays = [torch.from_numpy(np.ascontiguousarray(a)) for a in
+                  (part.feature, part.threshold, part.left, part.value,
+                   part.inbag.reshape(-1).view(np.int32))]
+        off, g = shard.gather_forest(part.offsets, arrays, world, dist.all_gather, n)
+        fe, th, le, va, ib = (t.numpy() for t in g)
+        ri = np.where(le < 0, -1, le + 1).astype(np.int32)
+        gathered = (off, fe, th, le, ri, va, ib.view(np.uint32).reshape(-1, n))
         if rank == world - 1:
             from paper_1811_00156_b200 import oob_finalize  # host-only C-ABI function
 
@@ -82,7 +88,7 @@ def _worker(rank, world, port, T, m, mns, seed, q):
             q.put(("stats", [float(st.degenerate), st.mse, st.response_variance, st.error_pct,
                              st.r_squared, float(st.rows_evaluated)], res[0], res[1]))
         if rank == 0:
-            q.put(("forest", shard.concat_forests(parts)))
+            q.put(("forest", gathered))
     finally:
         dist.destroy_process_group()
 
