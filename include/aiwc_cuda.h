@@ -115,6 +115,15 @@ int aiwc_forest_import_device(uint32_t trees, const uint64_t* offsets, const int
                               const double* d_value, const uint32_t* d_inbag, uint64_t n,
                               int device, aiwc_forest** out);
 
+/* Device selection (cmd_rank, tools/main.cpp:338-349): for each of q feature rows
+ * (row-major q x nfeat, host) predict the response on every device, i.e. on
+ * Forest::make_row(features, device) (forest.hpp:98-115: the nfeat features, then a
+ * one-hot over ndev device columns; nfeat + ndev = the forest's column count), expanded
+ * on the device in chunks and scored by the predict kernels.  out_best[i] = the first-ranked device column offset (smallest
+ * predict_time, lowest device name on ties).  out_response (q x ndev) may be NULL. */
+int aiwc_rank(aiwc_forest* f, const double* features, uint64_t q, uint32_t nfeat,
+              uint32_t ndev, double* out_response, uint32_t* out_best);
+
 /* ---- OOB ---------------------------------------------------------------------
  * compute_oob over (forest, ctx): stats + optional per-row tree-ordered sum/count. */
 int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum,

@@ -101,6 +101,7 @@ def lib():
         L.aiwc_forest_export_device.argtypes = [vp, vp, vp, vp, vp, vp]
         L.aiwc_forest_import_device.argtypes = [u32, P(u64), vp, vp, vp, vp, vp, u64, C.c_int,
                                                 P(vp)]
+        L.aiwc_rank.argtypes = [vp, P(f64), u64, u32, u32, P(f64), P(u32)]
         L.aiwc_oob.argtypes = [vp, vp, P(OobStatsC), P(f64), P(u32)]
         L.aiwc_oob_accumulate.argtypes = [vp, vp, P(f64), P(u32)]
         L.aiwc_oob_finalize.argtypes = [P(f64), u64, P(f64), P(u32), P(OobStatsC)]
@@ -316,6 +317,17 @@ class Forest:
     def predict_time(self, rows: np.ndarray):
         """forest.hpp:84-86: from_response(Log10) = 10**r (dataset.hpp:89-91)"""
         return np.power(10.0, self.predict_response(rows))
+
+    def rank(self, features: np.ndarray, ndev: int):
+        """cmd_rank (tools/main.cpp:338-349) for each row of a q x nfeat feature array:
+        (responses q x ndev on make_row(features, device d), best device offset q)."""
+        feats = np.ascontiguousarray(features, np.float64)
+        q, nfeat = feats.shape
+        resp = np.zeros((q, ndev))
+        best = np.zeros(q, np.uint32)
+        _check(lib().aiwc_rank(self._h, _p(feats, f64), q, nfeat, ndev, _p(resp, f64),
+                               _p(best, u32)))
+        return resp, best
 
     def predict_device(self, d_rows_ptr: int, q: int, p: int, d_out_ptr: int):
         _check(lib().aiwc_predict_device(self._h, d_rows_ptr, q, p, d_out_ptr))

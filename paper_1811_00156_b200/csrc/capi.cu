@@ -1459,6 +1459,68 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
   });
 }
 
+int aiwc_rank(aiwc_forest* f, const double* features, uint64_t q, uint32_t nfeat,
+              uint32_t ndev, double* out_response, uint32_t* out_best) {
+  return guard([&] {
+    if (!f || (q && (!features || !out_best))) throw Status(AIWC_EARG, "NULL argument");
+    if (nfeat < 1 || ndev < 1) throw Status(AIWC_EARG, "nfeat and ndev must be >= 1");
+    if (q == 0) return;
+    DeviceGuard dg(f->device);
+    Stream st;
+    DevBuf<double> dfeat(q * nfeat), dresp(q * ndev);
+    DevBuf<uint32_t> dbest(q);
+    DevBuf<uint8_t> dtie(q);
+    h2d(dfeat.p, features, q * nfeat * 8, st.s);
+    // chunks of <= 2M device rows: expand make_row in HBM, score with the predict path
+    const uint32_t p = nfeat + ndev;
+    const uint64_t cq = std::max<uint64_t>(1, (uint64_t{1} << 21) / ndev);
+    DevBuf<double> drows(std::min(q, cq) * ndev * p);
+    PredScratch sc;
+    build_binned_once(f, p);
+    for (uint64_t i0 = 0; i0 < q; i0 += cq) {
+      const uint64_t nq = std::min(cq, q - i0);
+      expand_rows_kernel<<<static_cast<unsigned>(
+                               std::min<uint64_t>((nq * ndev * p + 255) / 256, 148u * 32u)),
+                           256, 0, st.s>>>(dfeat.p + i0 * nfeat, nq, nfeat, ndev, drows.p);
+      CK(cudaGetLastError());
+      g_launches += 1;
+      predict_dispatch(f, drows.p, nq * ndev, p, dresp.p + i0 * ndev, st.s, sc);
+    }
+    rank_best_kernel<<<static_cast<unsigned>(std::min<uint64_t>((q + 255) / 256, 148u * 64u)),
+                       256, 0, st.s>>>(dresp.p, q, ndev, dbest.p, dtie.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    std::vector<uint8_t> tie(q);
+    d2h(out_best, dbest.p, q * 4, st.s);
+    d2h(tie.data(), dtie.p, q, st.s);
+    std::vector<double> resp_buf;
+    double* resp = out_response;
+    if (!resp) {
+      resp_buf.resize(q * ndev);
+      resp = resp_buf.data();
+      bool any = false;
+      for (uint64_t i = 0; i < q && !any; ++i) any = tie[i];
+      if (!any) return;
+    }
+    d2h(resp, dresp.p, q * ndev * 8, st.s);
+    // exact tie-break of flagged queries: min (10^r, device column), tools/main.cpp:340-345
+    for (uint64_t i = 0; i < q; ++i) {
+      if (!tie[i]) continue;
+      const double* r = resp + i * ndev;
+      uint32_t b = 0;
+      double sb = std::pow(10.0, r[0]);
+      for (uint32_t d = 1; d < ndev; ++d) {
+        const double sd = std::pow(10.0, r[d]);
+        if (sd < sb) {
+          sb = sd;
+          b = d;
+        }
+      }
+      out_best[i] = b;
+    }
+  });
+}
+
 int aiwc_evaluate(const double* col, const double* y, uint64_t n, uint32_t p,
                   const uint32_t* kernel_of_row, uint32_t K, uint32_t num_trees,
                   uint32_t mtry, uint32_t min_node_size, uint64_t seed, int device,

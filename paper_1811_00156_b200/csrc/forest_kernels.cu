@@ -193,6 +193,50 @@ __global__ void __launch_bounds__(256) predict_small_kernel(const PredNode* __re
   if (lane == 0) out[i] = __ddiv_rn(s, static_cast<double>(T));
 }
 
+// ---- device ranking (cmd_rank, tools/main.cpp:338-349) ------------------------------
+// Rows of nq queries x ndev devices, each Forest::make_row(features_i, device d)
+// (forest.hpp:98-115): the nfeat feature values, then a one-hot over the device columns.
+// Expanded chunk-wise in HBM so the binned predict path scores them.
+__global__ void expand_rows_kernel(const double* __restrict__ feats, uint64_t nq,
+                                   uint32_t nfeat, uint32_t ndev, double* __restrict__ rows) {
+  const uint32_t p = nfeat + ndev;
+  const uint64_t total = nq * ndev * p;
+  for (uint64_t g = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; g < total;
+       g += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t r = g / p;
+    const uint32_t c = static_cast<uint32_t>(g - r * p);
+    const uint64_t i = r / ndev;
+    const uint32_t d = static_cast<uint32_t>(r - i * ndev);
+    rows[g] = c < nfeat ? feats[i * nfeat + c] : (c - nfeat == d ? 1.0 : 0.0);
+  }
+}
+
+// Thread per query: the first-ranked device = smallest response, lowest device column on
+// ties (ranking sorts (seconds, device name) and device columns are in name order,
+// dataset.hpp:121-126).  seconds = 10^r is monotone but may merge distinct responses a few
+// ulps apart, so a runner-up within 1e-12 relative flags the query for the exact host
+// tie-break (std::pow, as Forest::predict_time, forest.hpp:84-86).
+__global__ void rank_best_kernel(const double* __restrict__ resp, uint64_t q, uint32_t ndev,
+                                 uint32_t* __restrict__ best, uint8_t* __restrict__ near_tie) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < q;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const double* r = resp + i * ndev;
+    uint32_t b = 0;
+    double rb = r[0];
+    for (uint32_t d = 1; d < ndev; ++d)
+      if (r[d] < rb) {
+        rb = r[d];
+        b = d;
+      }
+    uint8_t tie = 0;
+    const double tol = 1e-12 * fmax(1.0, fabs(rb));
+    for (uint32_t d = 0; d < ndev; ++d)
+      if (d != b && r[d] - rb <= tol) tie = 1;
+    best[i] = b;
+    near_tie[i] = tie;
+  }
+}
+
 // ---- shared-memory predict over binned queries ------------------------------------
 // Threshold binning: with T_c the sorted distinct thresholds the forest uses on column
 // c and thr = T_c[j],  x <= thr  <=>  #{t in T_c : t < x} <= j.  NaN goes to the

@@ -216,6 +216,33 @@ def test_device_import_rejects_bad_layout(c1, seed):
         pkg.Forest.from_device(s.offsets, *(x.data_ptr() for x in d))
 
 
+def test_rank_devices_matches_make_row_predict(c1, seed):
+    """aiwc_rank (cmd_rank, tools/main.cpp:338-349): responses on the virtual
+    make_row(features, device) rows equal predict on the materialised rows bit for bit, and
+    the first-ranked device is the reference's (min 10^r, then device name = column)."""
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(60, 6, 5, seed))
+    nfeat, ndev = 27, t.p - 27
+    rows = t.predictor_rows()
+    rng = np.random.default_rng(5)
+    feats = np.concatenate([rows[::ndev, :nfeat],
+                            rows[:40, :nfeat] * rng.uniform(0.5, 1.5, size=(40, nfeat))])
+    resp, best = f.rank(feats, ndev)
+    q = len(feats)
+    full = np.zeros((q * ndev, t.p))
+    full[:, :nfeat] = np.repeat(feats, ndev, axis=0)
+    full[np.arange(q * ndev), nfeat + np.tile(np.arange(ndev), q)] = 1.0
+    want = f.predict_response(full).reshape(q, ndev)
+    assert np.array_equal(resp.view(np.uint64), want.view(np.uint64))
+    secs = np.power(10.0, want)
+    ref_best = [int(np.lexsort((np.arange(ndev), secs[i]))[0]) for i in range(q)]
+    assert best.tolist() == ref_best
+    # exact response ties resolve to the lowest device column
+    one = pkg.fit(prep, pkg.ForestParams(1, 1, 2000, seed))  # a single leaf: all tie
+    _, b1 = one.rank(feats[:4], ndev)
+    assert b1.tolist() == [0, 0, 0, 0]
+
+
 def test_import_predict_and_oob(c1, seed):
     t, prep = c1
     f = pkg.fit(prep, pkg.ForestParams(40, 6, 5, seed))
