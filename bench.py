@@ -496,6 +496,17 @@ def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
         _ = forest.predict_response(host)
         ts.append(time.perf_counter() - s)
     e2e = qe / float(np.median(ts))
+    # device selection (cmd_rank, tools/main.cpp:338-349): 1M feature rows x every device
+    nfeat = 27
+    ndev = t.p - nfeat
+    feats = np.ascontiguousarray(host[:1_000_000, :nfeat])
+    forest.rank(feats[:1000], ndev)
+    ts = []
+    for _ in range(3):
+        s = time.perf_counter()
+        _ = forest.rank(feats, ndev)
+        ts.append(time.perf_counter() - s)
+    rank_s = float(np.median(ts))
     del qbuf, out
     torch.cuda.empty_cache()
     return {"workload": "C5: 1000-tree C1 forest (m=6, mns=5), 100M device-selection queries "
@@ -505,7 +516,11 @@ def bench_predict(pkg, torch, args, local, barrier, max_over_ranks, world, peak)
                          "unit": "GB/s", "frac": alg / (ms / 1e3) / 1e9 / peak,
                          "note": "B_row = 8p+8 = 344 B; node visits (~12K/row) bind on-chip"},
             "e2e": {"value": e2e, "unit": "rows/s", "rows": qe,
-                    "h2d_bytes": qe * t.p * 8, "d2h_bytes": qe * 8}}
+                    "h2d_bytes": qe * t.p * 8, "d2h_bytes": qe * 8},
+            "rank": {"workload": f"cmd_rank over {len(feats)} feature rows x {ndev} devices "
+                                 "(aiwc_rank, host buffers, best device + responses)",
+                     "queries_per_s": len(feats) / rank_s,
+                     "device_rows_per_s": len(feats) * ndev / rank_s}}
 
 
 def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
@@ -523,12 +538,15 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     cells = [(m, 1 + (7 * m) % 50) for m in range(1, 35)][:ncell]
     allreduce = shard.torch_allreduce_sum(torch.device("cuda", local)) if world > 1 else (lambda a: a)
     _ = pkg.grid_oob(prep, cells, counts, seed)  # warm-up (same batch sizes)
-    barrier()
-    s = time.perf_counter()
-    err = shard.grid_sharded(cells, counts, rank, world,
-                             lambda cs: pkg.grid_oob(prep, cs, counts, seed), allreduce)
-    barrier()
-    gs = max_over_ranks(time.perf_counter() - s)
+    grid_runs = []
+    for _ in range(3):  # median of 3 (single runs see occasional host-side stalls)
+        barrier()
+        s = time.perf_counter()
+        err = shard.grid_sharded(cells, counts, rank, world,
+                                 lambda cs: pkg.grid_oob(prep, cs, counts, seed), allreduce)
+        barrier()
+        grid_runs.append(max_over_ranks(time.perf_counter() - s))
+    gs = float(np.median(grid_runs))
     # C1: the paper-shaped table itself -- 500-tree fit (OOB included) + predict of its
     # 2220 rows, the reference's configs[0]
     c1p = pkg.ForestParams(500, 6, 5, seed)
@@ -548,7 +566,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     grid = {"workload": f"C2 sample: {len(cells)} (mtry, min.node.size) cells x 20 num.trees "
                         "values (50..1000) on the C1 table, one 1000-tree fit per cell",
             "cells_per_s": len(cells) / gs, "grid_points_per_s": len(cells) * len(counts) / gs,
-            "s": gs, "full_grid_est_s": 1700 / (len(cells) / gs),
+            "s": gs, "runs_s": grid_runs, "full_grid_est_s": 1700 / (len(cells) / gs),
             "best": {"error_pct": float(err.min()),
                      "cell": cells[int(err.argmin() // len(counts))],
                      "num_trees": counts[int(err.argmin() % len(counts))]}}
