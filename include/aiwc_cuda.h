@@ -158,7 +158,9 @@ int aiwc_oob_finalize(const double* y, uint64_t n, const double* row_sum,
 
 /* ---- predict -----------------------------------------------------------------
  * rows: q x p row-major HOST array; out: q responses (mean over trees in tree
- * order, forest.hpp:77-81).  predict_time is the host-side pow(10, r). */
+ * order, forest.hpp:77-81).  predict_time is the host-side pow(10, r).  Rows narrower
+ * than the forest's largest split column fail with AIWC_ESCHEMA (predict, predict_device,
+ * rank). */
 int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
                  double* out_response);
 /* same with DEVICE pointers (inputs already resident in HBM) on the forest's device */

@@ -312,6 +312,9 @@ struct aiwc_forest {
   double grow_ms = 0, fit_ms = 0;
   uint64_t split_rows = 0;
   uint32_t grow_launches = 0;
+  // largest split column (-2 = not yet computed), for the schema-width check of predict
+  std::mutex mf_mu;
+  int32_t max_feature = -2;
   // binned, chunked copy for the shared-memory predict path (built on first predict)
   struct Chunk {
     uint64_t node0, leaf0, root0;
@@ -1393,8 +1396,33 @@ void build_binned_once(aiwc_forest* f, uint32_t p) { build_binned(f, p); }
 
 // device rows -> device responses; binned shared-memory path when the forest fits,
 // else the L2 walk (predict_kernel)
+// Query rows must hold every column the forest splits on (the reference guarantees it
+// through Forest::check_schema / make_row, forest.hpp:88-115); narrower rows are a
+// schema error instead of out-of-bounds reads.
+void check_row_width(aiwc_forest* f, uint32_t p, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(f->mf_mu);
+  if (f->max_feature == -2) {
+    const uint64_t N = f->off.back();
+    DevBuf<int32_t> d(1);
+    CK(cudaMemsetAsync(d.p, 0xff, 4, s));  // -1
+    max_feature_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 148u * 16u)),
+                         256, 0, s>>>(f->feature.p, N, d.p);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    int32_t h = -1;
+    CK(cudaMemcpyAsync(&h, d.p, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    f->max_feature = h;
+  }
+  if (f->max_feature >= 0 && static_cast<uint32_t>(f->max_feature) >= p)
+    throw Status(AIWC_ESCHEMA, "query rows have " + std::to_string(p) +
+                                   " columns but the forest splits on column " +
+                                   std::to_string(f->max_feature));
+}
+
 void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p,
                       double* d_out, cudaStream_t s, PredScratch& sc) {
+  check_row_width(f, p, s);
   if (q <= kSmallQ && !f->bin_ready) {  // a handful of rows: no binned copy
     predict_small_kernel<<<static_cast<unsigned>((q + 7) / 8), 256, 0, s>>>(
         f->packed.p, f->d_off.p, f->trees, d_rows, q, p, d_out);

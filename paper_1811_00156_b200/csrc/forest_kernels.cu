@@ -193,6 +193,17 @@ __global__ void __launch_bounds__(256) predict_small_kernel(const PredNode* __re
   if (lane == 0) out[i] = __ddiv_rn(s, static_cast<double>(T));
 }
 
+// Largest split column of a forest (-1 if all leaves): the schema-width check of predict
+__global__ void max_feature_kernel(const int32_t* __restrict__ feature, uint64_t N,
+                                   int32_t* __restrict__ out) {
+  int32_t m = -1;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < N;
+       i += uint64_t{gridDim.x} * blockDim.x)
+    m = max(m, feature[i]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31u) == 0) atomicMax(out, m);
+}
+
 // ---- device ranking (cmd_rank, tools/main.cpp:338-349) ------------------------------
 // Rows of nq queries x ndev devices, each Forest::make_row(features_i, device d)
 // (forest.hpp:98-115): the nfeat feature values, then a one-hot over the device columns.

@@ -66,6 +66,7 @@ __global__ void oob_reduce_kernel(const double* oobval, uint32_t T, uint64_t n, 
 __global__ void oob_prefix_kernel(const double* oobval, const uint32_t* cps, uint32_t k,
                                   uint64_t n, double* sums, uint32_t* counts);
 __global__ void right_child_kernel(const int32_t* left, uint64_t N, int32_t* right);
+__global__ void max_feature_kernel(const int32_t* feature, uint64_t N, int32_t* out);
 __global__ void expand_rows_kernel(const double* feats, uint64_t nq, uint32_t nfeat,
                                    uint32_t ndev, double* rows);
 __global__ void rank_best_kernel(const double* resp, uint64_t q, uint32_t ndev, uint32_t* best,

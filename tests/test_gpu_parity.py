@@ -243,6 +243,19 @@ def test_rank_devices_matches_make_row_predict(c1, seed):
     assert b1.tolist() == [0, 0, 0, 0]
 
 
+def test_predict_rejects_narrow_rows(c1, seed):
+    """Rows narrower than the forest's split columns are a SchemaError (status 5), on the
+    host-row, device-row and rank paths."""
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(30, 42, 5, seed))  # mtry = p: every column in play
+    rows = t.predictor_rows()
+    with pytest.raises(pkg.SchemaError):
+        f.predict_response(np.ascontiguousarray(rows[:8, :20]))
+    with pytest.raises(pkg.SchemaError):
+        f.rank(rows[:4, :27], 3)
+    assert np.array_equal(f.predict_response(rows[:8]), Oracle.predict(rows[:8], soa_of(f, False)))
+
+
 def test_import_predict_and_oob(c1, seed):
     t, prep = c1
     f = pkg.fit(prep, pkg.ForestParams(40, 6, 5, seed))
