@@ -301,7 +301,8 @@ struct aiwc_forest {
   std::vector<uint64_t> off;  // trees+1, tree order
   DevBuf<int32_t> feature, left;
   DevBuf<double> thr, value;
-  DevBuf<PredNode> packed;
+  DevBuf<PredNode> packed;  // 16-byte predict nodes: built on first use (ensure_packed)
+  std::mutex pk_mu;
   DevBuf<uint64_t> d_off;
   DevBuf<uint32_t> inbag;  // trees x n (may be empty)
   DevBuf<double> oobval;   // trees x n NaN = in bag (may be empty)
@@ -330,6 +331,25 @@ struct aiwc_forest {
   DevBuf<double> bleaves, bthr;
   DevBuf<uint32_t> broots, bthr_off;
 };
+
+namespace {
+// 16-byte predict nodes of a fitted forest, built on first use (OOB walks of imported
+// forests, the L2 predict paths): a fit does not pay their 16 B/node of allocation and
+// writes (6 GB per 1000 C4 trees) unless something walks them.
+void ensure_packed(aiwc_forest* f, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(f->pk_mu);
+  if (f->packed.p) return;
+  const uint64_t N = f->off.back();
+  f->packed.alloc(N);
+  DevBuf<uint32_t> bad(1);
+  CK(cudaMemsetAsync(bad.p, 0, 4, s));
+  pack_check_kernel<<<std::min<uint32_t>(f->trees, 148u * 16u), 256, 0, s>>>(
+      f->d_off.p, f->trees, f->feature.p, f->thr.p, f->left.p, f->value.p, f->packed.p, bad.p);
+  CK(cudaGetLastError());
+  g_launches += 1;
+  CK(cudaStreamSynchronize(s));
+}
+}  // namespace
 
 extern "C" {
 
@@ -860,12 +880,10 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   f->left.alloc(N);
   f->thr.alloc(N);
   f->value.alloc(N);
-  f->packed.alloc(N);
   f->d_off.alloc(T + 1);
   CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, st.s));
   compact_kernel<<<T, 256, 0, st.s>>>(pf.p, pt.p, pl.p, pv.p, tree_off.p, f->d_off.p,
-                                      f->feature.p, f->thr.p, f->left.p, f->value.p,
-                                      f->packed.p);
+                                      f->feature.p, f->thr.p, f->left.p, f->value.p, nullptr);
   CK(cudaGetLastError());
   g_launches += 1;
   CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
@@ -1139,6 +1157,7 @@ int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum
       CK(cudaMemsetAsync(flags.p, 0, size_t{f->trees} * n, st.s));
       const dim3 grid(static_cast<unsigned>((n + 255) / 256), f->trees);
       inbag_flags_kernel<<<grid, 256, 0, st.s>>>(f->inbag.p, f->trees, n, flags.p);
+      ensure_packed(f, st.s);
       oob_walk_kernel<<<grid, 256, 0, st.s>>>(f->packed.p, f->d_off.p, flags.p, ctx->col.p, n,
                                               f->oobval.p);
       CK(cudaGetLastError());
@@ -1424,6 +1443,7 @@ void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t
                       double* d_out, cudaStream_t s, PredScratch& sc) {
   check_row_width(f, p, s);
   if (q <= kSmallQ && !f->bin_ready) {  // a handful of rows: no binned copy
+    ensure_packed(f, s);
     predict_small_kernel<<<static_cast<unsigned>((q + 7) / 8), 256, 0, s>>>(
         f->packed.p, f->d_off.p, f->trees, d_rows, q, p, d_out);
     CK(cudaGetLastError());
@@ -1435,6 +1455,7 @@ void predict_dispatch(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t
     predict_binned(f, d_rows, q, p, d_out, s, sc);
     return;
   }
+  ensure_packed(f, s);
   predict_kernel<<<static_cast<unsigned>((q + 255) / 256), 256, 0, s>>>(f->packed.p, f->d_off.p,
                                                                         f->trees, d_rows, q, p, d_out);
   CK(cudaGetLastError());

@@ -7,7 +7,8 @@
 
 namespace aiwc_b200 {
 
-// one CTA per tree: pool (completion order) -> forest arrays (tree order)
+// one CTA per tree: pool (completion order) -> forest arrays (tree order); packed
+// predict nodes only when asked for (a fitted forest builds them lazily, ensure_packed)
 __global__ void compact_kernel(const int32_t* __restrict__ pf, const double* __restrict__ pt,
                                const int32_t* __restrict__ pl, const double* __restrict__ pv,
                                const uint64_t* __restrict__ src_off,
@@ -25,7 +26,7 @@ __global__ void compact_kernel(const int32_t* __restrict__ pf, const double* __r
     thr[o + i] = th;
     left[o + i] = le;
     val[o + i] = v;
-    packed[o + i] = PredNode{fi >= 0 ? th : v, fi, le};
+    if (packed) packed[o + i] = PredNode{fi >= 0 ? th : v, fi, le};
   }
 }
 
