@@ -186,3 +186,58 @@ def test_cells_and_folds_cover_once():
         fr = [shard.fold_range(r, world, 37) for r in range(world)]
         assert fr[0][0] == 0 and fr[-1][1] == 37
         assert all(a[1] == b[0] for a, b in zip(fr, fr[1:]))
+
+
+@pytest.mark.parametrize("T,world", [(7, 3), (2, 3)])
+def test_gather_forest_ragged_and_empty_shards(T, world):
+    """gather_forest over `world` threads (an in-process all_gather on CPU tensors): ragged
+    tree ranges, including a rank holding no trees, reassemble the one-shot forest."""
+    import threading
+
+    import torch
+    from paper_1811_00156_b200 import shard
+
+    col, y = _table()
+    p, n = col.shape
+    m, mns, seed = 3, 2, 777
+    full = Oracle.fit(col, y, n, p, T, m, mns, seed)
+    slots, bar = [None] * world, threading.Barrier(world)
+
+    def ag_for(r):
+        def ag(lst, t):
+            slots[r] = t.clone()
+            bar.wait()
+            for i in range(world):
+                lst[i].copy_(slots[i])
+            bar.wait()
+        return ag
+
+    got, errs = [None] * world, []
+
+    def run(r):
+        try:
+            t0, t1 = shard.tree_range(r, world, T)
+            if t1 > t0:
+                part = Oracle.fit(col, y, n, p, T, m, mns, seed, trees=range(t0, t1))
+                off, arrs = part.offsets, (part.feature, part.threshold, part.left, part.value,
+                                           part.inbag.reshape(-1).view(np.int32))
+            else:
+                off = np.zeros(1, np.uint64)
+                arrs = (np.zeros(0, np.int32), np.zeros(0), np.zeros(0, np.int32), np.zeros(0),
+                        np.zeros(0, np.int32))
+            tens = [torch.from_numpy(np.ascontiguousarray(a)) for a in arrs]
+            got[r] = shard.gather_forest(off, tens, world, ag_for(r), n)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=120)
+    assert not errs, errs
+    for off, g in got:
+        fe, thr, le, va, ib = (t.numpy() for t in g)
+        ri = np.where(le < 0, -1, le + 1).astype(np.int32)
+        s = ForestSoA(off, fe, thr, le, ri, va, inbag=ib.view(np.uint32).reshape(-1, n))
+        assert forests_equal(full, s) is None
