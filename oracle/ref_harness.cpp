@@ -19,10 +19,68 @@
 
 #include <cstdint>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
 using namespace aiwc;
+
+#ifdef AIWC_REF_QUARANTINE
+// Golden-generation build only (oracle/_ref/libaiwc_ref_q.so, linked -Bsymbolic so these
+// bind for the reference code inside this library alone): freed blocks are held in a
+// FIFO quarantine (like AddressSanitizer's) before they go back to malloc, so the
+// reference's dangling read of node.left/right after tree.nodes reallocates
+// (forest.hpp:245, 312-318 -- REFERENCE_DEFECT.md) always sees the values it just wrote,
+// i.e. the reference's intended semantics, whatever the heap state.
+#include <malloc.h>
+#include <cstdlib>
+#include <mutex>
+#include <new>
+namespace {
+struct Quarantine {  // a malloc'd ring of pending frees (no allocation through delete)
+  std::mutex mu;
+  void** ring = nullptr;
+  std::size_t cap = 0, head = 0, len = 0, bytes = 0;
+  static constexpr std::size_t kBudget = std::size_t{1} << 29;  // 512 MB
+  void put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu);
+    if (len == cap) {  // grow the ring (malloc / free only)
+      const std::size_t nc = cap ? 2 * cap : 1024;
+      void** nr = static_cast<void**>(std::malloc(nc * sizeof(void*)));
+      for (std::size_t i = 0; i < len; ++i) nr[i] = ring[(head + i) % cap];
+      std::free(ring);
+      ring = nr;
+      cap = nc;
+      head = 0;
+    }
+    ring[(head + len) % cap] = p;
+    ++len;
+    bytes += malloc_usable_size(p);
+    while (bytes > kBudget && len) {
+      void* o = ring[head];
+      head = (head + 1) % cap;
+      --len;
+      bytes -= malloc_usable_size(o);
+      std::free(o);
+    }
+  }
+};
+Quarantine& quarantine() {
+  static Quarantine* z = new Quarantine;
+  return *z;
+}
+}  // namespace
+void* operator new(std::size_t n) {
+  if (void* p = std::malloc(n ? n : 1)) return p;
+  throw std::bad_alloc();
+}
+void* operator new[](std::size_t n) { return ::operator new(n); }
+void operator delete(void* p) noexcept { quarantine().put(p); }
+void operator delete[](void* p) noexcept { quarantine().put(p); }
+void operator delete(void* p, std::size_t) noexcept { quarantine().put(p); }
+void operator delete[](void* p, std::size_t) noexcept { quarantine().put(p); }
+#endif
 
 namespace {
 thread_local std::string g_err;
@@ -192,6 +250,49 @@ int ref_grow_range(void* prep, uint32_t num_trees, uint32_t mtry, uint32_t mns,
     uint64_t s = 0;
     for (auto v : nodes) s += v;
     if (total_nodes) *total_nodes = s;
+  });
+}
+
+// Grow tree t alone (single thread, the intended semantics -- REFERENCE_DEFECT.md) and
+// walk its out-of-bag rows exactly as compute_oob does (forest.hpp:418-433): oob[i] =
+// the leaf value tree t gives row i, NaN for in-bag rows.  Node arrays go to the caller
+// when `cap` holds them (returns the node count in *nodes either way).  Used to pin the
+// 1000-tree C4 forest, one process per tree range (tests/golden/make_c4_forest.py).
+int ref_grow_tree_oob(void* prep, uint32_t num_trees, uint32_t mtry, uint32_t mns,
+                      uint64_t seed, uint32_t t, double* oob, uint64_t cap, uint64_t* nodes,
+                      int32_t* feature, double* threshold, int32_t* left, int32_t* right,
+                      double* value, uint32_t* inbag_out) {
+  return guarded([&] {
+    const auto& ctx = static_cast<PreparedDataset*>(prep)->context();
+    detail::TreeGrower g(ctx, ForestParams{num_trees, mtry, mns, seed});
+    std::vector<std::uint32_t> draws;
+    const Tree tree = g.grow(t, draws);
+    const std::size_t n = ctx.n;
+    std::vector<char> inbag(n, 0);
+    for (std::uint32_t r : draws) inbag[r] = 1;
+    for (std::size_t i = 0; i < n; ++i) {
+      if (inbag[i]) {
+        oob[i] = std::numeric_limits<double>::quiet_NaN();
+        continue;
+      }
+      std::int32_t node = 0;
+      while (tree.nodes[static_cast<std::size_t>(node)].feature >= 0) {
+        const TreeNode& nd = tree.nodes[static_cast<std::size_t>(node)];
+        node = ctx.col[static_cast<std::size_t>(nd.feature)][i] <= nd.threshold ? nd.left
+                                                                                 : nd.right;
+      }
+      oob[i] = tree.nodes[static_cast<std::size_t>(node)].value;
+    }
+    *nodes = tree.nodes.size();
+    if (cap >= tree.nodes.size())
+      for (std::size_t i = 0; i < tree.nodes.size(); ++i) {
+        feature[i] = tree.nodes[i].feature;
+        threshold[i] = tree.nodes[i].threshold;
+        left[i] = tree.nodes[i].left;
+        right[i] = tree.nodes[i].right;
+        value[i] = tree.nodes[i].value;
+      }
+    if (inbag_out) std::memcpy(inbag_out, draws.data(), draws.size() * sizeof(std::uint32_t));
   });
 }
 

@@ -263,6 +263,7 @@ using namespace aiwc_b200;
 // PreparedDataset on the device
 // ---------------------------------------------------------------------------------
 struct aiwc_ctx {
+  uint64_t uid = 0;  // process-unique id (a forest's cached OOB leaves name their dataset)
   int device = 0;
   uint64_t n = 0;
   uint32_t p = 0;
@@ -304,8 +305,9 @@ struct aiwc_forest {
   DevBuf<PredNode> packed;  // 16-byte predict nodes: built on first use (ensure_packed)
   std::mutex pk_mu;
   DevBuf<uint64_t> d_off;
-  DevBuf<uint32_t> inbag;  // trees x n (may be empty)
-  DevBuf<double> oobval;   // trees x n NaN = in bag (may be empty)
+  DevBuf<uint32_t> inbag;    // trees x n (may be empty)
+  DevBuf<uint32_t> oobleaf;  // trees x n tree-local OOB leaf index, kInBag = in bag
+  uint64_t oob_ctx = 0;      // uid of the aiwc_ctx whose rows oobleaf walks (0: none)
   bool has_oob = false;
   aiwc_oob_stats oob{};
   // measurement: grow-kernel device time (CUDA events on its stream), whole fit time,
@@ -333,6 +335,8 @@ struct aiwc_forest {
 };
 
 namespace {
+void check_row_width(aiwc_forest* f, uint32_t p, cudaStream_t s);  // below, with predict
+
 // 16-byte predict nodes of a fitted forest, built on first use (OOB walks of imported
 // forests, the L2 predict paths): a fit does not pay their 16 B/node of allocation and
 // writes (6 GB per 1000 C4 trees) unless something walks them.
@@ -379,6 +383,8 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
     if (n >= (uint64_t{1} << 31)) throw Status(AIWC_EARG, "too many rows (max 2^31-1)");
     DeviceGuard dg(device);
     auto ctx = std::make_unique<aiwc_ctx>();
+    static std::atomic<uint64_t> next_uid{1};
+    ctx->uid = next_uid.fetch_add(1);
     ctx->device = device;
     ctx->n = n;
     ctx->p = p;
@@ -523,8 +529,8 @@ void oob_accumulate_device(aiwc_forest* f, double* row_sum, uint32_t* row_count,
   DevBuf<uint32_t> dc(n);
   CK(cudaMemcpyAsync(ds.p, row_sum, n * 8, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dc.p, row_count, n * 4, cudaMemcpyHostToDevice, s));
-  oob_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(f->oobval.p, f->trees,
-                                                                            n, ds.p, dc.p);
+  oob_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      f->oobleaf.p, f->d_off.p, f->value.p, f->trees, n, ds.p, dc.p);
   CK(cudaGetLastError());
   g_launches += 1;
   CK(cudaMemcpyAsync(row_sum, ds.p, n * 8, cudaMemcpyDeviceToHost, s));
@@ -644,12 +650,13 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   f->mtry = mtry;
   f->mns = min_node_size;
   f->seed = seed;
+  // every (tree, row) entry of both is written by the grower (no fill needed)
   f->inbag.alloc(size_t{T} * n);
-  f->oobval.alloc(size_t{T} * n);
-  CK(cudaMemsetAsync(f->oobval.p, 0xff, size_t{T} * n * 8, st.s));
-  tmark("inbag+oobval");
+  f->oobleaf.alloc(size_t{T} * n);
+  f->oob_ctx = ctx->uid;
+  tmark("inbag+oobleaf");
   a.inbag = f->inbag.p;
-  a.oobval = f->oobval.p;
+  a.oobleaf = f->oobleaf.p;
 
   uint64_t cap = uint64_t{T} * std::min<uint64_t>(L.nodes_cap, std::max<uint64_t>(1024, L.stride));
   int slots = static_cast<int>(std::min<uint64_t>(T, uint64_t(per_sm) * sms));
@@ -778,13 +785,16 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
     CK(cudaMemsetAsync(used.p, 0, 8, st.s));
     CK(cudaMemsetAsync(split_rows.p, 0, 8, st.s));
     CK(cudaEventRecord(ev0, st.s));
+    // lane streams start after these resets (and the counters' earlier uses) on st.s
+    for (cudaStream_t ls : lane_streams) CK(cudaStreamWaitEvent(ls, ev0, 0));
     if (wide) {
       // batched multi-kernel grower: K concurrent lanes (stream + host thread), each
       // growing batches of `per` trees level-synchronously.  While one batch sits in
       // the sequential tail of a level (a few long chains on huge nodes), the other
       // lanes' kernels fill the SMs.
       const int K = nlanes;
-      const uint32_t per = static_cast<uint32_t>(slots / K);
+      // a batch's trees are gridDim.y of the per-row kernels: at most 65,535
+      const uint32_t per = std::min<uint32_t>(static_cast<uint32_t>(slots / K), 65535u);
       uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
       if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
       // CTA-per-chain / CTA-per-route for nodes >= coop_min rows: shorter critical
@@ -1048,8 +1058,10 @@ int aiwc_forest_import(uint32_t trees, const uint64_t* offsets, const int32_t* f
       for (uint64_t i = b; i < e; ++i) {
         const int64_t cnt = static_cast<int64_t>(e - b);
         if (feature[i] >= 0) {
-          // BFS layout: right == left + 1, children inside the tree
-          if (left[i] < 1 || left[i] + 1 >= cnt || (right && right[i] != left[i] + 1))
+          // BFS layout: right == left + 1, children after their parent and inside the
+          // tree (a back edge would make every walk of the tree loop forever)
+          if (left[i] <= static_cast<int64_t>(i - b) || left[i] + 1 >= cnt ||
+              (right && right[i] != left[i] + 1))
             throw Status(AIWC_EPARSE, "model tree is not in canonical BFS layout");
         }
         pk[i] = PredNode{feature[i] >= 0 ? threshold[i] : value[i], feature[i], left[i]};
@@ -1147,21 +1159,28 @@ int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum
   return guard([&] {
     if (!ctx || !f || !out) throw Status(AIWC_EARG, "NULL argument");
     if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    if (f->device != ctx->device) throw Status(AIWC_EARG, "forest and dataset live on different devices");
     if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
     DeviceGuard dg(ctx->device);
     Stream st;
     const uint64_t n = ctx->n;
-    if (!f->oobval.p) {
-      f->oobval.alloc(size_t{f->trees} * n);
+    check_row_width(f, ctx->p, st.s);  // split columns must exist in this dataset
+    // the leaves cached by the fit walked its training context; any other dataset (same
+    // row count) is walked afresh, as oob_error(forest, data) does (forest.hpp:518-522)
+    if (!f->oobleaf.p || f->oob_ctx != ctx->uid) {
+      f->oobleaf.alloc(size_t{f->trees} * n);
+      f->oob_ctx = ctx->uid;
       DevBuf<uint8_t> flags(size_t{f->trees} * n);
       CK(cudaMemsetAsync(flags.p, 0, size_t{f->trees} * n, st.s));
-      const dim3 grid(static_cast<unsigned>((n + 255) / 256), f->trees);
-      inbag_flags_kernel<<<grid, 256, 0, st.s>>>(f->inbag.p, f->trees, n, flags.p);
       ensure_packed(f, st.s);
-      oob_walk_kernel<<<grid, 256, 0, st.s>>>(f->packed.p, f->d_off.p, flags.p, ctx->col.p, n,
-                                              f->oobval.p);
-      CK(cudaGetLastError());
-      g_launches += 2;
+      for (uint32_t t0 = 0; t0 < f->trees; t0 += 65535u) {  // gridDim.y <= 65,535
+        const dim3 grid(static_cast<unsigned>((n + 255) / 256), std::min(65535u, f->trees - t0));
+        inbag_flags_kernel<<<grid, 256, 0, st.s>>>(f->inbag.p, t0, n, flags.p);
+        oob_walk_kernel<<<grid, 256, 0, st.s>>>(f->packed.p, f->d_off.p, flags.p, ctx->col.p, n,
+                                                t0, f->oobleaf.p);
+        CK(cudaGetLastError());
+        g_launches += 2;
+      }
       CK(cudaStreamSynchronize(st.s));
     }
     std::vector<double> sum(n, 0.0);
@@ -1176,7 +1195,7 @@ int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum
 int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum, uint32_t* row_count) {
   return guard([&] {
     if (!ctx || !f || !row_sum || !row_count) throw Status(AIWC_EARG, "NULL argument");
-    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (!f->oobleaf.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
     if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
     DeviceGuard dg(ctx->device);
     Stream st;
@@ -1188,7 +1207,7 @@ int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, 
                     aiwc_oob_stats* out) {
   return guard([&] {
     if (!ctx || !f || !tree_counts || !out) throw Status(AIWC_EARG, "NULL argument");
-    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (!f->oobleaf.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
     if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
     if (f->tree_begin != 0) throw Status(AIWC_EARG, "tree prefixes need a forest from tree 0");
     for (uint32_t i = 0; i < k; ++i)
@@ -1203,7 +1222,7 @@ int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, 
     DevBuf<uint32_t> counts(size_t{k} * n);
     CK(cudaMemcpyAsync(cps.p, tree_counts, k * 4, cudaMemcpyHostToDevice, st.s));
     oob_prefix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st.s>>>(
-        f->oobval.p, cps.p, k, n, sums.p, counts.p);
+        f->oobleaf.p, f->d_off.p, f->value.p, cps.p, k, n, sums.p, counts.p);
     CK(cudaGetLastError());
     g_launches += 1;
     std::vector<double> hs(size_t{k} * n);
@@ -1220,7 +1239,7 @@ int aiwc_oob_prefix_cells(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_co
                           uint32_t k, aiwc_oob_stats* out) {
   return guard([&] {
     if (!ctx || !f || !tree_counts || !out) throw Status(AIWC_EARG, "NULL argument");
-    if (!f->oobval.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (!f->oobleaf.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
     if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
     const uint32_t T = f->trees / f->cells;
     for (uint32_t i = 0; i < k; ++i)
@@ -1238,7 +1257,8 @@ int aiwc_oob_prefix_cells(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_co
     std::vector<uint32_t> hc(size_t{k} * n);
     for (uint32_t c = 0; c < f->cells; ++c) {  // forest c: trees [c*T, (c+1)*T)
       oob_prefix_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st.s>>>(
-          f->oobval.p + size_t{c} * T * n, cps.p, k, n, sums.p, counts.p);
+          f->oobleaf.p + size_t{c} * T * n, f->d_off.p + size_t{c} * T, f->value.p, cps.p, k, n,
+          sums.p, counts.p);
       CK(cudaGetLastError());
       g_launches += 1;
       CK(cudaMemcpyAsync(hs.data(), sums.p, hs.size() * 8, cudaMemcpyDeviceToHost, st.s));
@@ -1493,7 +1513,7 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
     DevBuf<double> dr[2], dout(q);
     dr[0].alloc(std::min(q, chunk) * p);
     if (q > chunk) dr[1].alloc(chunk * p);
-    build_binned_once(f, p);
+    if (q > kSmallQ) build_binned_once(f, p);  // a handful of rows: predict_small_kernel
     uint64_t i = 0;
     for (uint64_t r0 = 0; r0 < q; r0 += chunk, ++i) {
       const uint64_t rn = std::min(chunk, q - r0);
@@ -1525,7 +1545,7 @@ int aiwc_rank(aiwc_forest* f, const double* features, uint64_t q, uint32_t nfeat
     const uint64_t cq = std::max<uint64_t>(1, (uint64_t{1} << 21) / ndev);
     DevBuf<double> drows(std::min(q, cq) * ndev * p);
     PredScratch sc;
-    build_binned_once(f, p);
+    if (q * ndev > kSmallQ) build_binned_once(f, p);
     for (uint64_t i0 = 0; i0 < q; i0 += cq) {
       const uint64_t nq = std::min(cq, q - i0);
       expand_rows_kernel<<<static_cast<unsigned>(

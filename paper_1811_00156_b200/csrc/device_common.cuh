@@ -8,6 +8,7 @@ namespace aiwc_b200 {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
 constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kInBag = 0xffffffffu;  // OOB leaf index of an in-bag row
 
 // splitmix64 finaliser (rng.hpp:13-18)
 __device__ __forceinline__ uint64_t dmix64(uint64_t x) {

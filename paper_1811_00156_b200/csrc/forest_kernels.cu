@@ -30,18 +30,22 @@ __global__ void compact_kernel(const int32_t* __restrict__ pf, const double* __r
   }
 }
 
-// per row, tree-ordered sum of OOB leaf values (forest.hpp:418-435); NaN marks in-bag.
+// per row, tree-ordered sum of OOB leaf values (forest.hpp:418-435).  oobleaf[t*n + i]
+// is the tree-local index of the leaf tree t sends OOB row i to (0xffffffff = in bag);
+// the value is read from the forest's node arrays (off = per-tree node offsets).
 // Continues from (sum, count) so chained partial forests reproduce the order.
-__global__ void oob_reduce_kernel(const double* __restrict__ oobval, uint32_t T, uint64_t n,
+__global__ void oob_reduce_kernel(const uint32_t* __restrict__ oobleaf,
+                                  const uint64_t* __restrict__ off,
+                                  const double* __restrict__ value, uint32_t T, uint64_t n,
                                   double* __restrict__ sum, uint32_t* __restrict__ count) {
   const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
   if (i >= n) return;
   double s = sum[i];
   uint32_t c = count[i];
   for (uint32_t t = 0; t < T; ++t) {
-    const double v = __ldg(oobval + t * n + i);
-    if (v == v) {
-      s = __dadd_rn(s, v);
+    const uint32_t l = __ldg(oobleaf + t * n + i);
+    if (l != kInBag) {
+      s = __dadd_rn(s, __ldg(value + __ldg(off + t) + l));
       ++c;
     }
   }
@@ -52,7 +56,9 @@ __global__ void oob_reduce_kernel(const double* __restrict__ oobval, uint32_t T,
 // Per-row OOB (sum, count) after each of k ascending tree-count checkpoints, summed in
 // tree order: the OOB statistics of every tree prefix of one fit at once (a T-tree fit is
 // the first T trees of a longer fit with the same seed, forest.hpp:182, 477-479).
-__global__ void oob_prefix_kernel(const double* __restrict__ oobval,
+__global__ void oob_prefix_kernel(const uint32_t* __restrict__ oobleaf,
+                                  const uint64_t* __restrict__ off,
+                                  const double* __restrict__ value,
                                   const uint32_t* __restrict__ cps, uint32_t k, uint64_t n,
                                   double* __restrict__ sums, uint32_t* __restrict__ counts) {
   const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
@@ -61,9 +67,9 @@ __global__ void oob_prefix_kernel(const double* __restrict__ oobval,
   uint32_t c = 0, t = 0;
   for (uint32_t j = 0; j < k; ++j) {
     for (const uint32_t te = cps[j]; t < te; ++t) {
-      const double v = __ldg(oobval + t * n + i);
-      if (v == v) {
-        s = __dadd_rn(s, v);
+      const uint32_t l = __ldg(oobleaf + t * n + i);
+      if (l != kInBag) {
+        s = __dadd_rn(s, __ldg(value + __ldg(off + t) + l));
         ++c;
       }
     }
@@ -84,7 +90,7 @@ __global__ void right_child_kernel(const int32_t* __restrict__ left, uint64_t N,
 
 // Forest built from device SoA (a gathered forest, aiwc_forest_import_device): CTA per
 // tree packs the predict nodes and checks the canonical BFS layout the host import checks
-// (split nodes' children inside the tree, forest.hpp:310-311); *bad = 1 + tree on failure
+// (split nodes' children after them and inside the tree, forest.hpp:310-311); *bad = 1 + tree on failure
 __global__ void pack_check_kernel(const uint64_t* __restrict__ off, uint32_t T,
                                   const int32_t* __restrict__ feature,
                                   const double* __restrict__ thr,
@@ -100,29 +106,31 @@ __global__ void pack_check_kernel(const uint64_t* __restrict__ off, uint32_t T,
     const int64_t cnt = static_cast<int64_t>(e - b);
     for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
       const int32_t f = feature[i], l = left[i];
-      if (f >= 0 && (l < 1 || l + 1 >= cnt)) atomicCAS(bad, 0u, t + 1u);
+      // children after their parent (no back edges: walks terminate) and inside the tree
+      if (f >= 0 && (l <= static_cast<int64_t>(i - b) || l + 1 >= cnt)) atomicCAS(bad, 0u, t + 1u);
       packed[i] = PredNode{f >= 0 ? thr[i] : val[i], f, l};
     }
   }
 }
 
-// OOB leaf values of an imported forest: in-bag flags from the draws, then a walk
-// over the column store with the stored f64 thresholds (Tree::predict semantics)
-__global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t T, uint64_t n,
+// OOB leaves of an imported forest: in-bag flags from the draws, then a walk over the
+// column store with the stored f64 thresholds (Tree::predict semantics).  Trees
+// [t0, t0 + gridDim.y) -- the host loops over chunks of <= 65,535 trees.
+__global__ void inbag_flags_kernel(const uint32_t* __restrict__ inbag, uint32_t t0, uint64_t n,
                                    uint8_t* __restrict__ flags) {
   const uint64_t j = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
-  const uint32_t t = blockIdx.y;
+  const uint64_t t = t0 + blockIdx.y;
   if (j < n) flags[t * n + inbag[t * n + j]] = 1;
 }
 
 __global__ void oob_walk_kernel(const PredNode* __restrict__ nodes,
                                 const uint64_t* __restrict__ off, const uint8_t* __restrict__ flags,
-                                const double* __restrict__ col, uint64_t n,
-                                double* __restrict__ oobval) {
+                                const double* __restrict__ col, uint64_t n, uint32_t t0,
+                                uint32_t* __restrict__ oobleaf) {
   const uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x;
-  const uint32_t t = blockIdx.y;
+  const uint64_t t = t0 + blockIdx.y;
   if (i >= n) return;
-  double v = __longlong_as_double(-1ll);  // NaN
+  uint32_t leaf = kInBag;
   if (!flags[t * n + i]) {
     const PredNode* nd = nodes + off[t];
     int32_t k = 0;
@@ -131,9 +139,9 @@ __global__ void oob_walk_kernel(const PredNode* __restrict__ nodes,
       k = col[static_cast<uint64_t>(x.feature) * n + i] <= x.thr ? x.left : x.left + 1;
       x = nd[k];
     }
-    v = x.thr;
+    leaf = static_cast<uint32_t>(k);
   }
-  oobval[t * n + i] = v;
+  oobleaf[t * n + i] = leaf;
 }
 
 // predict_response for q row-major rows: mean over trees, summed in tree order

@@ -61,9 +61,11 @@ __global__ void compact_kernel(const int32_t* pf, const double* pt, const int32_
                                const double* pv, const uint64_t* src_off,
                                const uint64_t* dst_off, int32_t* f, double* thr,
                                int32_t* left, double* val, PredNode* packed);
-__global__ void oob_reduce_kernel(const double* oobval, uint32_t T, uint64_t n, double* sum,
+__global__ void oob_reduce_kernel(const uint32_t* oobleaf, const uint64_t* off,
+                                  const double* value, uint32_t T, uint64_t n, double* sum,
                                   uint32_t* count);
-__global__ void oob_prefix_kernel(const double* oobval, const uint32_t* cps, uint32_t k,
+__global__ void oob_prefix_kernel(const uint32_t* oobleaf, const uint64_t* off,
+                                  const double* value, const uint32_t* cps, uint32_t k,
                                   uint64_t n, double* sums, uint32_t* counts);
 __global__ void right_child_kernel(const int32_t* left, uint64_t N, int32_t* right);
 __global__ void max_feature_kernel(const int32_t* feature, uint64_t N, int32_t* out);
@@ -74,11 +76,11 @@ __global__ void rank_best_kernel(const double* resp, uint64_t q, uint32_t ndev, 
 __global__ void pack_check_kernel(const uint64_t* off, uint32_t T, const int32_t* feature,
                                   const double* thr, const int32_t* left, const double* val,
                                   PredNode* packed, uint32_t* bad);
-__global__ void inbag_flags_kernel(const uint32_t* inbag, uint32_t T, uint64_t n,
+__global__ void inbag_flags_kernel(const uint32_t* inbag, uint32_t t0, uint64_t n,
                                    uint8_t* flags);
 __global__ void oob_walk_kernel(const PredNode* nodes, const uint64_t* off,
-                                const uint8_t* flags, const double* col, uint64_t n,
-                                double* oobval);
+                                const uint8_t* flags, const double* col, uint64_t n, uint32_t t0,
+                                uint32_t* oobleaf);
 __global__ void make_queries_kernel(const double* rows, uint64_t n, uint32_t p, uint64_t q,
                                     uint64_t seed, uint64_t tag, double* out);
 __global__ void predict_small_kernel(const PredNode* nodes, const uint64_t* off, uint32_t T,

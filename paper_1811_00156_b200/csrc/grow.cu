@@ -1593,11 +1593,14 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         a.pool_rank[off + i] = nrank[i];
       }
     }
-    // ---- out-of-bag leaf values (walk per OOB row, forest.hpp:418-435) ----
-    if (a.oobval) {
-      double* ov = a.oobval + static_cast<size_t>(tl) * n;
+    // ---- out-of-bag leaves (walk per OOB row, forest.hpp:418-435) ----
+    if (a.oobleaf) {
+      uint32_t* ol = a.oobleaf + static_cast<size_t>(tl) * n;
       for (uint32_t r = tid; r < n; r += NT) {
-        if (mult_g[r]) continue;
+        if (mult_g[r]) {
+          ol[r] = kInBag;
+          continue;
+        }
         int32_t i = 0;
         int32_t fi = nf[0];
         while (fi >= 0) {
@@ -1605,7 +1608,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
           i = nleft[i] + (left ? 0 : 1);
           fi = nf[i];
         }
-        ov[r] = nval[i];
+        ol[r] = static_cast<uint32_t>(i);
       }
     }
   }

@@ -94,7 +94,7 @@ struct GrowArgs {
   int bits_in_smem;
   // outputs (indexed by local tree t - tree_begin)
   uint32_t* inbag;    // T x n, may be null
-  double* oobval;     // T x n (NaN = in bag), may be null
+  uint32_t* oobleaf;  // T x n tree-local OOB leaf index (kInBag = in bag), may be null
   int32_t* pool_feature;
   double* pool_thr;
   int32_t* pool_left;

@@ -1371,9 +1371,12 @@ __global__ void w_oob(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const RankT* rank = static_cast<const RankT*>(a.g.d.rank);
-  double* ov = a.g.oobval + static_cast<size_t>(tl) * n;
+  uint32_t* ol = a.g.oobleaf + static_cast<size_t>(tl) * n;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
-    if (P.mult[r]) continue;
+    if (P.mult[r]) {
+      ol[r] = kInBag;
+      continue;
+    }
     int32_t i = 0;
     int32_t fi = P.nf[0];
     while (fi >= 0) {
@@ -1381,7 +1384,7 @@ __global__ void w_oob(const WideArgs a) {
       i = P.nleft[i] + (left ? 0 : 1);
       fi = P.nf[i];
     }
-    ov[r] = P.nval[i];
+    ol[r] = static_cast<uint32_t>(i);
   }
 }
 
@@ -1466,7 +1469,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
   }
   WCK((w_emit<<<a.B, 256, 0, st>>>(a)));
-  if (a.g.oobval) WCK((w_oob<RankT><<<rowsgrid, 256, 0, st>>>(a)));
+  if (a.g.oobleaf) WCK((w_oob<RankT><<<rowsgrid, 256, 0, st>>>(a)));
 #undef WCK
   return cudaSuccess;
 }

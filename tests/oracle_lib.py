@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-REF_SO = os.path.join(ROOT, "oracle", "_ref", "libaiwc_ref.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libaiwc_ref_q.so" if os.environ.get("AIWC_REF_QUARANTINE") else "libaiwc_ref.so")
 ORACLE_SO = os.path.join(ROOT, "oracle", "build", "liboracle.so")
 
 u64, u32, i32, f64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_double, C.c_void_p
