@@ -1682,6 +1682,7 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_e2f = take(emax * 4);
   L.off_ecls = take(emax * 4);
   L.off_wsplit = take(emax * 4);
+  L.off_lsplit = take(emax * 4);
   L.off_samp = take(emax * mtry * 2);
   L.off_res = take(emax * mtry * sizeof(ChainRes));
   L.off_split = take(emax * sizeof(SplitInfo));

@@ -26,6 +26,7 @@ struct SlotPtrs {
   uint32_t* e2f;
   uint32_t* ecls;
   uint32_t* wsplit;
+  uint32_t* lsplit;
   uint16_t* samp;
   ChainRes* res;
   SplitInfo* spl;
@@ -60,6 +61,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.e2f = reinterpret_cast<uint32_t*>(s + L.off_e2f);
   p.ecls = reinterpret_cast<uint32_t*>(s + L.off_ecls);
   p.wsplit = reinterpret_cast<uint32_t*>(s + L.off_wsplit);
+  p.lsplit = reinterpret_cast<uint32_t*>(s + L.off_lsplit);
   p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
   p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
   p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       else
         el = 1;
       P.segtab[f].offL = INT_MIN;
+      P.segtab[f].loffL = INT_MIN;
     }
     uint32_t tot;
     const uint32_t ex = block_excl_scan<NT>(el, sh, &tot);
@@ -374,10 +377,11 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       }
     for (uint32_t i = 0; i < m; ++i) P.samp[static_cast<size_t>(e) * m + i] = pool[i];
   }
-  // eligible nodes by size class, BFS order inside each: [0, E0) small (< kLaneMax
-  // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain)
-  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0;
-  for (uint32_t cls = 0; cls < 3; ++cls) {
+  // eligible nodes by size class, BFS order inside each: [0, E0) small (< lane_max
+  // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain), then
+  // local (< local_max rows: no lists, w_local)
+  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0, E3 = 0;
+  for (uint32_t cls = 0; cls < 4; ++cls) {
     carry = 0;
     for (uint32_t b0 = 0; b0 < E; b0 += NT) {
       const uint32_t e = b0 + threadIdx.x;
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       if (e < E) {
         const NodeWork& nw = fr[P.e2f[e]];
         const uint32_t R = nw.e - nw.b;
-        const uint32_t c = R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u);
+        const uint32_t c = R < a.local_max ? 3u : (R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u));
         in = c == cls;
       }
       uint32_t tot;
@@ -396,6 +400,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     if (cls == 0) E0 = carry;
     if (cls == 1) E1 = carry;
     if (cls == 2) E2 = carry;
+    if (cls == 3) E3 = carry;
     base += carry;
   }
   for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
@@ -404,6 +409,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     s.E0 = E0;
     s.E1 = E1;
     s.E2 = E2;
+    s.E3 = E3;
   }
 }
 
@@ -414,10 +420,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
   for (uint32_t base = 0; base < a.B; base += NT) {
     const uint32_t b = base + threadIdx.x;
-    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0;
+    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
@@ -425,12 +431,14 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
         v0 = s.E0 * m;
         v1 = s.E1 * grp_tpn(m, a.g.mtry);
         v2 = s.E2 * m;
+        v5 = s.E3;
       } else {
         v0 = s.Sbig;
         v1 = s.S;
         v2 = s.A;
         v3 = nchunks_of(s.A, a.g.d.nlisted);
         v4 = s.Swarp;
+        v5 = s.Slocal;
       }
     }
     uint32_t t0, t1, t2, t3;
@@ -438,27 +446,31 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
     const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
     const uint32_t e3 = block_excl_scan<NT>(v3, sh, &t3);
-    uint32_t t4;
+    uint32_t t4, t5;
     const uint32_t e4 = block_excl_scan<NT>(v4, sh, &t4);
+    const uint32_t e5 = block_excl_scan<NT>(v5, sh, &t5);
     if (b < a.B) {
       a.off[0][b] = c0 + e0;
       a.off[1][b] = c1 + e1;
       a.off[2][b] = c2 + e2;
       a.off[3][b] = c3 + e3;
       if (which == 1) a.off[4][b] = c4 + e4;
+      a.off[5][b] = c5 + e5;
     }
     c0 += t0;
     c1 += t1;
     c2 += t2;
     c3 += t3;
     c4 += t4;
+    c5 += t5;
   }
   if (threadIdx.x == 0) {
     if (which == 1) {
       a.off[4][a.B] = c4;
-      a.task_ctr[2] = 0u;
+      a.task_ctr[2] = a.task_ctr[5] = 0u;
     }
-    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = 0u;
+    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = a.task_ctr[4] = 0u;
+    a.off[5][a.B] = c5;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
     a.off[2][a.B] = c2;
@@ -837,7 +849,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
   const bool coop_route = d.list_of[0] >= 0;
-  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0;
+  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0, lcarry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
     const uint32_t e = base + threadIdx.x;
     uint32_t sp = 0, c = 0, thr_rank = 0;
@@ -846,13 +858,14 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     if (e < E) {
       nw = fr[P.e2f[e]];
       double bg = -INFINITY;
-      uint32_t bi = 0, bp = 0;
+      uint32_t bi = 0, bp = 0, bx = 0;
       for (uint32_t i = 0; i < m; ++i) {
         const ChainRes r = P.res[static_cast<size_t>(e) * m + i];
         if (r.gain > bg) {
           bg = r.gain;
           bi = i;
           bp = r.pos;
+          bx = r.pad;
         }
       }
       if (bg == -INFINITY) {
@@ -865,9 +878,16 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
         double prev, v;
         uint32_t lo, hi;
         if (li >= 0) {
-          const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
-          const uint32_t r1 = P.pay[lc[bp - 1]].row;
-          const uint32_t r0 = P.pay[lc[bp]].row;
+          // rows either side of the boundary: from the list, or (local node) given
+          uint32_t r1, r0;
+          if (bx & 0x80000000u) {
+            r1 = bx & 0x7fffffffu;
+            r0 = bp;
+          } else {
+            const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
+            r1 = P.pay[lc[bp - 1]].row;
+            r0 = P.pay[lc[bp]].row;
+          }
           prev = d.col[static_cast<size_t>(c) * n + r1];
           v = d.col[static_cast<size_t>(c) * n + r0];
           lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
@@ -894,12 +914,17 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     const uint32_t cex = block_excl_scan<NT>(cnt, sh, &ctot);
     // splits routed by a whole CTA (w_route_coop), compacted into ecls (free after the
     // chain kernels)
-    const uint32_t big = sp && coop_route && cnt >= a.coop_min ? 1u : 0u;
+    const uint32_t loc = sp && cnt < a.local_max ? 1u : 0u;  // w_local_route
+    uint32_t ltot;
+    const uint32_t lex = block_excl_scan<NT>(loc, sh, &ltot);
+    if (loc) P.lsplit[lcarry + lex] = carry + ex;
+    lcarry += ltot;
+    const uint32_t big = sp && !loc && coop_route && cnt >= a.coop_min ? 1u : 0u;
     uint32_t btot;
     const uint32_t bex = block_excl_scan<NT>(big, sh, &btot);
     if (big) P.ecls[bcarry + bex] = carry + ex;
     bcarry += btot;
-    const uint32_t wsp = sp && !big && cnt >= kLaneMax ? 1u : 0u;  // warp-routed splits
+    const uint32_t wsp = sp && !big && !loc && cnt >= kLaneMax ? 1u : 0u;  // warp-routed splits
     uint32_t wtot;
     const uint32_t wex = block_excl_scan<NT>(wsp, sh, &wtot);
     if (wsp) P.wsplit[wcarry + wex] = carry + ex;
@@ -929,6 +954,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     st.S = carry;
     st.Sbig = bcarry;
     st.Swarp = wcarry;
+    st.Slocal = lcarry;
     st.A_next = ccarry;
     st.split_rows += ccarry;
     st.elig_base += E;
@@ -974,7 +1000,7 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     }
     const SlotPtrs P = slot_ptrs(a, b);
     const SplitInfo si = P.spl[s];
-    if (!kWarp && si.cnt >= kLaneMax) continue;
+    if (!kWarp && (si.cnt >= kLaneMax || si.cnt < a.local_max)) continue;
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
@@ -1122,22 +1148,33 @@ __global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a, b);
   const NodeWork* fr = P.front;
   const uint32_t S = st.S, A = st.A;
-  uint32_t carry = 0;
+  // payload offsets count every split's left rows; list offsets only those of splits
+  // whose lists are read (local splits keep none)
+  uint32_t carry = 0, kcarry = 0;
   for (uint32_t base = 0; base < S; base += NT) {
     const uint32_t s = base + threadIdx.x;
-    const uint32_t nl = s < S ? P.spl[s].nl : 0u;
-    uint32_t tot;
+    SplitInfo si{};
+    if (s < S) si = P.spl[s];
+    const uint32_t nl = s < S ? si.nl : 0u;
+    const bool skip = s < S && si.cnt < a.local_max;
+    uint32_t tot, ktot;
     const uint32_t ex = block_excl_scan<NT>(nl, sh, &tot);
+    const uint32_t kex = block_excl_scan<NT>(skip ? 0u : nl, sh, &ktot);
     if (s < S) {
-      const SplitInfo si = P.spl[s];
-      const uint32_t bL = carry + ex;
-      const uint32_t bb = fr[si.f].b;
-      P.segtab[si.f] = SegTab{static_cast<int32_t>(si.base) - static_cast<int32_t>(bL),
-                              static_cast<int32_t>(si.base + nl) - static_cast<int32_t>(bb) +
-                                  static_cast<int32_t>(bL),
-                              2 * s, 0u};
+      const int32_t bL = static_cast<int32_t>(carry + ex), bK = static_cast<int32_t>(kcarry + kex);
+      const int32_t bb = static_cast<int32_t>(fr[si.f].b), bs = static_cast<int32_t>(si.base);
+      const int32_t nli = static_cast<int32_t>(nl);
+      SegTab tb{bs - bL, bs + nli - bb + bL, 2 * s, 0u, bs - bK, bs + nli - bb + bK, 0u, 0u};
+      if (skip) {
+        tb.loffL = INT_MIN;
+      } else {
+        if (nl < a.local_max) tb.loffL = kNoWrite;            // left child is local
+        if (si.cnt - nl < a.local_max) tb.loffR = kNoWrite;   // right child is local
+      }
+      P.segtab[si.f] = tb;
     }
     carry += tot;
+    kcarry += ktot;
   }
   if (threadIdx.x == 0) st.totL = carry;
   const uint32_t aw = (A + 31u) / 32u;
@@ -1160,7 +1197,7 @@ __global__ void w_pay(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t f = P.seg[k];
     const SegTab tb = P.segtab[f];
-    P.off2[k] = make_int2(tb.offL, tb.offR);
+    if (a.write_off2) P.off2[k] = make_int2(tb.offL, tb.offR);
     if (tb.offL == INT_MIN) continue;
     const bool l = get_bit(P.bits, k);
     const int32_t lp = static_cast<int32_t>(bits_before(P.bits, P.pref, k));
@@ -1173,94 +1210,105 @@ __global__ void w_pay(const WideArgs a) {
 }
 
 // List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
-// staged in shared memory and one warp per sorted list.  A warp walks its list in
-// position order, 256 positions per step as 8 sub-rows of 32 consecutive positions
-// (lane i holds position k0 + 32j + i of sub-row j), so the count of left-going entries
-// before each entry is the warp's running carry plus ballot counts -- no count pass --
-// and each sub-row's left (right) entries land on consecutive destinations: every
-// store instruction writes at most two contiguous runs.  The next step's entries and
-// segment offsets are loaded before this step is scattered.
+// staged in shared memory and one warp per sorted list.  The CTA walks the positions in
+// steps of kLwStep; each step's per-position segment offsets (list destinations, payload
+// offsets) are staged once in shared memory for all lists, one step ahead.  A warp
+// covers a step of its list as 8 sub-rows of 32 consecutive positions (lane i holds
+// position k0 + 32j + i), so the count of left-going entries before an entry is the
+// list's running carry plus ballot counts -- no count pass -- and each store instruction
+// writes at most two contiguous runs.  Entries of leaf segments and of local split nodes
+// (no lists) are neither read nor counted; entries whose child is local are counted but
+// not written.
 constexpr uint32_t kLwStep = 256;
-constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
-struct LwStage {
-  uint32_t q[8];
-  int2 t[8];
-};
+constexpr int kLwWarps = 28;  // warps per list-pass CTA
 
-__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
-                                        const int2* off2) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t k = k0 + 32u * j + lane_id();
-    if (k < A) {
-      v.q[j] = list[k];
-      v.t[j] = off2[k];
-    } else {
-      v.t[j] = make_int2(INT_MIN, 0);
-    }
-  }
+__host__ __device__ inline size_t lw_smem_bytes(uint32_t stride, uint32_t nlisted) {
+  const size_t aw4 = ((stride + 31) / 32 + 3) / 4 * 4;
+  return aw4 * 8 + 2 * kLwStep * 16 + size_t{nlisted} * 4 + 16;
 }
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
-  extern __shared__ uint32_t sm[];
+  extern __shared__ __align__(16) uint32_t sm[];
   const uint32_t b = blockIdx.x;
   const TreeState& st = a.ts[b];
   if (st.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t A = st.A, aw = (A + 31u) / 32u;
   const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
+  const uint32_t aw4 = ((stride + 31u) / 32u + 3u) / 4u * 4u;
   uint32_t* sbits = sm;
-  uint32_t* spref = sm + (aw + 3u) / 4u * 4u;
+  uint32_t* spref = sm + aw4;
+  int4* s_t = reinterpret_cast<int4*>(sm + 2 * aw4);
+  uint32_t* s_carry = reinterpret_cast<uint32_t*>(s_t + 2 * kLwStep);
   {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
-    const uint32_t aw4 = (aw + 3u) / 4u;
+    const uint32_t n4 = (aw + 3u) / 4u;
     const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
     const uint4* gp = reinterpret_cast<const uint4*>(P.pref);
-    for (uint32_t w = threadIdx.x; w < aw4; w += blockDim.x) {
-      const uint4 x = gb[w], y = gp[w];
-      sbits[4 * w] = x.x; sbits[4 * w + 1] = x.y; sbits[4 * w + 2] = x.z; sbits[4 * w + 3] = x.w;
-      spref[4 * w] = y.x; spref[4 * w + 1] = y.y; spref[4 * w + 2] = y.z; spref[4 * w + 3] = y.w;
+    for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) {
+      reinterpret_cast<uint4*>(sbits)[w] = gb[w];
+      reinterpret_cast<uint4*>(spref)[w] = gp[w];
     }
+    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) s_carry[li] = 0u;
   }
+  auto stage = [&](uint32_t k0, int4* dst) {
+    const uint32_t ke = min(A, k0 + kLwStep);
+    for (uint32_t k = k0 + threadIdx.x; k < ke; k += blockDim.x) {
+      const SegTab tb = P.segtab[P.seg[k]];
+      dst[k - k0] = make_int4(tb.loffL, tb.loffR, tb.offL, tb.offR);
+    }
+  };
+  stage(0, s_t);
   __syncthreads();
   const unsigned lane = lane_id(), lt = lanemask_lt();
-  for (uint32_t li = warp_id(); li < nl; li += blockDim.x >> 5) {
-    const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
-    uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
-    uint32_t carry = 0;  // left-going entries of this list before the sub-row
-    LwStage cur, nxt;
-    lw_load(cur, 0, A, src, P.off2);
-    for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
-      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
-      // all 16 shared-memory lookups of the lane first (branch-free), then the scatter
+  const uint32_t nwarps = blockDim.x >> 5;
+  uint32_t it = 0;
+  for (uint32_t k0 = 0; k0 < A; k0 += kLwStep, ++it) {
+    const int4* cur = s_t + (it & 1u) * kLwStep;
+    bool staged = false;
+    for (uint32_t li = warp_id(); li < nl; li += nwarps) {
+      const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
+      uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
+      uint32_t q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // entries of read segments only
+        const uint32_t k = k0 + 32u * j + lane;
+        q[j] = (k < A && cur[32u * j + lane].x != INT_MIN) ? src[k] : 0u;
+      }
+      if (!staged) {  // the next step's offsets, while the entries are in flight
+        if (k0 + kLwStep < A) stage(k0 + kLwStep, s_t + ((it + 1u) & 1u) * kLwStep);
+        staged = true;
+      }
+      uint32_t carry = s_carry[li];  // left-going entries of this list before the step
       uint32_t wv[8], pv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t wi = cur.t[j].x != INT_MIN ? cur.q[j] >> 5 : 0u;
-        wv[j] = sbits[wi];
-        pv[j] = spref[wi];
+        wv[j] = sbits[q[j] >> 5];
+        pv[j] = spref[q[j] >> 5];
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int2 t = cur.t[j];
+        const uint32_t k = k0 + 32u * j + lane;
+        const int4 t = k < A ? cur[32u * j + lane] : make_int4(INT_MIN, 0, 0, 0);
         const bool keep = t.x != INT_MIN;
-        const uint32_t qq = cur.q[j];
+        const uint32_t qq = q[j];
         const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
         const bool l = keep && bit;
         const unsigned bl = __ballot_sync(kFull, l);
         const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
-        if (keep) {
+        const int32_t off = l ? t.x : t.y;
+        if (keep && off != kNoWrite) {
           const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
-          const uint32_t k = k0 + 32u * j + lane;
-          const uint32_t nq = static_cast<uint32_t>(l ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
-          const uint32_t dst =
-              static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
+          const uint32_t nq = static_cast<uint32_t>(l ? t.z + lq : t.w + static_cast<int32_t>(qq) - lq);
+          const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(k) - pl);
           dstl[dst] = nq;
         }
         carry += __popc(bl);
       }
-      cur = nxt;
+      if (lane == 0) s_carry[li] = carry;
     }
+    if (!staged && k0 + kLwStep < A) stage(k0 + kLwStep, s_t + ((it + 1u) & 1u) * kLwStep);
+    __syncthreads();
   }
 }
 
@@ -1388,6 +1436,8 @@ __global__ void w_oob(const WideArgs a) {
   }
 }
 
+#include "grow_local.cuh"
+
 // ---- host driver for one batch of trees [t0, t0+B) (local indices) ----------------
 template <typename RankT>
 cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
@@ -1396,7 +1446,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const dim3 rowsgrid((n + 1023) / 1024, a.B);
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
   // per-tree list pass with the bitmap + prefix in shared memory when they fit
-  size_t lw_smem = ((a.g.L.stride + 31) / 32 + 3) / 4 * 4 * 8;
+  size_t lw_smem = lw_smem_bytes(a.g.L.stride, a.g.d.nlisted);
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -1408,6 +1458,24 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     cudaGetLastError();
   }
   const int lw_warps = static_cast<int>(std::min<uint32_t>(kLwWarps, std::max<uint32_t>(1u, a.g.d.nlisted)));
+  // local (list-free) small nodes: need the row records and the shared-memory list pass
+  using LayA = LocalLayout<64, int(kLocalSmall), false>;
+  using LayB = LocalLayout<256, int(kLocalMaxRows), false>;
+  using RLayA = LocalLayout<64, int(kLocalSmall), true>;
+  using RLayB = LocalLayout<256, int(kLocalMaxRows), true>;
+  if (!lw_smem || a.g.d.rec_stride == 0 || sizeof(RankT) != 2) a.local_max = 0;
+  a.local_max = std::min(a.local_max, kLocalMaxRows);
+  a.write_off2 = lw_smem ? 0u : 1u;
+  if (a.local_max > kLocalSmall &&
+      (cudaFuncSetAttribute(w_local<256, int(kLocalMaxRows)>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(LayB::bytes)) != cudaSuccess ||
+       cudaFuncSetAttribute(w_local_route<256, int(kLocalMaxRows)>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(RLayB::bytes)) != cudaSuccess)) {
+    cudaGetLastError();
+    a.local_max = std::min(a.local_max, kLocalSmall);
+  }
+  // every node of every tree is local: no sorted lists at all
+  const bool lists = a.g.d.nlisted && a.g.L.stride >= a.local_max;
 #define WCK(x)                              \
   do {                                      \
     x;                                      \
@@ -1419,7 +1487,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   WCK((w_boot<<<rowsgrid, 256, 0, st>>>(a)));
   WCK((w_bits<1024><<<a.B, 1024, 0, st>>>(a)));
   WCK((w_payload<<<rowsgrid, 256, 0, st>>>(a)));
-  if (a.g.d.nlisted) {
+  if (lists) {
     WCK((w_l0count<<<wgrid, 256, 0, st>>>(a)));
     WCK((w_chunkscan<1024><<<a.B, 1024, 0, st>>>(a, 0)));
     WCK((w_l0scatter<<<wgrid, 256, 0, st>>>(a)));
@@ -1445,6 +1513,12 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       default: WCK((w_chains_grp<RankT, 1, 4><<<wgrid, 256, 0, st>>>(a))); break;
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
+    if (a.local_max) {
+      WCK((w_local<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, LayA::bytes, st>>>(a, 0u)));
+      if (a.local_max > kLocalSmall)
+        WCK((w_local<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, LayB::bytes, st>>>(
+            a, kLocalSmall)));
+    }
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
     cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
@@ -1455,9 +1529,16 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
+    if (a.local_max) {
+      WCK((w_local_route<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, RLayA::bytes, st>>>(
+          a, 0u)));
+      if (a.local_max > kLocalSmall)
+        WCK((w_local_route<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, RLayB::bytes,
+                                                       st>>>(a, kLocalSmall)));
+    }
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
-    if (a.g.d.nlisted) {
+    if (lists) {
       if (lw_smem) {
         WCK((w_lwarp<kLwWarps><<<a.B, lw_warps * 32, lw_smem, st>>>(a)));
       } else {
