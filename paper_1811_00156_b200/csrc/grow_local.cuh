@@ -187,7 +187,7 @@ __device__ __forceinline__ void local_chain(bool listed, const uint16_t* perm, c
 
 // split chains of the local nodes with rmin < rows <= SMAX (forest.hpp:255-297)
 template <int NT, int SMAX>
-__global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin) {
+__global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin, uint32_t ctr) {
   using Lay = LocalLayout<NT, SMAX, false>;
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char lsm[];
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin) {
   const uint32_t total = a.off[5][a.B];
   const unsigned tid = threadIdx.x, w = warp_id();
   for (;;) {
-    if (tid == 0) s_task = atomicAdd(a.task_ctr + 4, 1u);
+    if (tid == 0) s_task = atomicAdd(a.task_ctr + ctr, 1u);  // one counter per size class
     __syncthreads();
     const uint32_t t = s_task;
     __syncthreads();
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin) {
 // (a stable sort by the column-0 rank), child (weight, sum, sumsq) as sequential FP64
 // sums in that order (forest.hpp:323-352), goes-left bits for the payload pass
 template <int NT, int SMAX>
-__global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t rmin) {
+__global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t rmin, uint32_t ctr) {
   using Lay = LocalLayout<NT, SMAX, true>;
   extern __shared__ __align__(16) unsigned char lsm[];
   double* s_wy = reinterpret_cast<double*>(lsm + Lay::wy);
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t r
   const int32_t slot0 = rec_slot(d, 0);
   const bool two0 = (d.vals_off[1] - d.vals_off[0]) > 256u;
   for (;;) {
-    if (tid == 0) s_task = atomicAdd(a.task_ctr + 5, 1u);
+    if (tid == 0) s_task = atomicAdd(a.task_ctr + ctr, 1u);  // one counter per size class
     __syncthreads();
     const uint32_t t = s_task;
     __syncthreads();

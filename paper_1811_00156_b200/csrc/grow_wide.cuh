@@ -467,9 +467,9 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   if (threadIdx.x == 0) {
     if (which == 1) {
       a.off[4][a.B] = c4;
-      a.task_ctr[2] = a.task_ctr[5] = 0u;
+      a.task_ctr[2] = a.task_ctr[5] = a.task_ctr[7] = 0u;
     }
-    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = a.task_ctr[4] = 0u;
+    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = a.task_ctr[4] = a.task_ctr[6] = 0u;
     a.off[5][a.B] = c5;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
@@ -1212,19 +1212,20 @@ __global__ void w_pay(const WideArgs a) {
 // List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
 // staged in shared memory and one warp per sorted list.  The CTA walks the positions in
 // steps of kLwStep; each step's per-position segment offsets (list destinations, payload
-// offsets) are staged once in shared memory for all lists, one step ahead.  A warp
-// covers a step of its list as 8 sub-rows of 32 consecutive positions (lane i holds
-// position k0 + 32j + i), so the count of left-going entries before an entry is the
-// list's running carry plus ballot counts -- no count pass -- and each store instruction
-// writes at most two contiguous runs.  Entries of leaf segments and of local split nodes
-// (no lists) are neither read nor counted; entries whose child is local are counted but
-// not written.
+// offsets) are staged once in shared memory for all lists, two steps ahead, and a warp
+// loads its list's entries of the next step while it scatters this one.  A warp covers
+// a step of its list as 8 sub-rows of 32 consecutive positions (lane i holds position
+// k0 + 32j + i), so the count of left-going entries before an entry is the list's
+// running carry plus ballot counts -- no count pass -- and each store instruction writes
+// at most two contiguous runs.  Entries of leaf segments and of local split nodes (no
+// lists) are neither read nor counted; entries whose child is local are counted but not
+// written.
 constexpr uint32_t kLwStep = 256;
 constexpr int kLwWarps = 28;  // warps per list-pass CTA
 
 __host__ __device__ inline size_t lw_smem_bytes(uint32_t stride, uint32_t nlisted) {
   const size_t aw4 = ((stride + 31) / 32 + 3) / 4 * 4;
-  return aw4 * 8 + 2 * kLwStep * 16 + size_t{nlisted} * 4 + 16;
+  return aw4 * 8 + 3 * kLwStep * 16 + size_t{nlisted} * 4 + 16;
 }
 
 template <int NW>
@@ -1239,8 +1240,8 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   const uint32_t aw4 = ((stride + 31u) / 32u + 3u) / 4u * 4u;
   uint32_t* sbits = sm;
   uint32_t* spref = sm + aw4;
-  int4* s_t = reinterpret_cast<int4*>(sm + 2 * aw4);
-  uint32_t* s_carry = reinterpret_cast<uint32_t*>(s_t + 2 * kLwStep);
+  int4* s_t = reinterpret_cast<int4*>(sm + 2 * aw4);  // [3][kLwStep]
+  uint32_t* s_carry = reinterpret_cast<uint32_t*>(s_t + 3 * kLwStep);
   {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
     const uint32_t n4 = (aw + 3u) / 4u;
     const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
@@ -1258,56 +1259,73 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
       dst[k - k0] = make_int4(tb.loffL, tb.loffR, tb.offL, tb.offR);
     }
   };
-  stage(0, s_t);
-  __syncthreads();
   const unsigned lane = lane_id(), lt = lanemask_lt();
-  const uint32_t nwarps = blockDim.x >> 5;
+  // entries of read segments only
+  auto load8 = [&](uint32_t k0, const int4* tb, const uint32_t* src, uint32_t (&q)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t k = k0 + 32u * j + lane;
+      q[j] = (k < A && tb[32u * j + lane].x != INT_MIN) ? src[k] : 0u;
+    }
+  };
+  auto scatter = [&](uint32_t k0, const int4* tb, const uint32_t (&q)[8], uint32_t* dstl,
+                     uint32_t& carry) {
+    uint32_t wv[8], pv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      wv[j] = sbits[q[j] >> 5];
+      pv[j] = spref[q[j] >> 5];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t k = k0 + 32u * j + lane;
+      const int4 t = k < A ? tb[32u * j + lane] : make_int4(INT_MIN, 0, 0, 0);
+      const bool keep = t.x != INT_MIN;
+      const uint32_t qq = q[j];
+      const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
+      const bool l = keep && bit;
+      const unsigned bl = __ballot_sync(kFull, l);
+      const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
+      const int32_t off = l ? t.x : t.y;
+      if (keep && off != kNoWrite) {
+        const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
+        const uint32_t nq = static_cast<uint32_t>(l ? t.z + lq : t.w + static_cast<int32_t>(qq) - lq);
+        const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(k) - pl);
+        dstl[dst] = nq;
+      }
+      carry += __popc(bl);
+    }
+  };
+  stage(0, s_t);
+  if (kLwStep < A) stage(kLwStep, s_t + kLwStep);
+  __syncthreads();
+  const uint32_t nwarps = blockDim.x >> 5, w0 = warp_id();
+  const bool single = nl <= nwarps;  // one list per warp: pipelined entry loads
+  const uint32_t* src0 = P.lists + static_cast<size_t>(w0) * stride;
+  uint32_t* dst0 = P.lists_n + static_cast<size_t>(w0) * stride;
+  uint32_t qc[8], carry0 = 0;
+  if (single && w0 < nl) load8(0, s_t, src0, qc);
   uint32_t it = 0;
   for (uint32_t k0 = 0; k0 < A; k0 += kLwStep, ++it) {
-    const int4* cur = s_t + (it & 1u) * kLwStep;
-    bool staged = false;
-    for (uint32_t li = warp_id(); li < nl; li += nwarps) {
-      const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
-      uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
-      uint32_t q[8];
+    const int4* cur = s_t + (it % 3u) * kLwStep;
+    const int4* nxt = s_t + ((it + 1u) % 3u) * kLwStep;
+    if (single) {
+      uint32_t qn[8];
+      if (w0 < nl && k0 + kLwStep < A) load8(k0 + kLwStep, nxt, src0, qn);
+      if (k0 + 2 * kLwStep < A) stage(k0 + 2 * kLwStep, s_t + ((it + 2u) % 3u) * kLwStep);
+      if (w0 < nl) scatter(k0, cur, qc, dst0, carry0);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {  // entries of read segments only
-        const uint32_t k = k0 + 32u * j + lane;
-        q[j] = (k < A && cur[32u * j + lane].x != INT_MIN) ? src[k] : 0u;
+      for (int j = 0; j < 8; ++j) qc[j] = qn[j];
+    } else {
+      if (k0 + 2 * kLwStep < A) stage(k0 + 2 * kLwStep, s_t + ((it + 2u) % 3u) * kLwStep);
+      for (uint32_t li = w0; li < nl; li += nwarps) {
+        uint32_t q[8];
+        load8(k0, cur, P.lists + static_cast<size_t>(li) * stride, q);
+        uint32_t carry = s_carry[li];  // left-going entries of this list before the step
+        scatter(k0, cur, q, P.lists_n + static_cast<size_t>(li) * stride, carry);
+        if (lane == 0) s_carry[li] = carry;
       }
-      if (!staged) {  // the next step's offsets, while the entries are in flight
-        if (k0 + kLwStep < A) stage(k0 + kLwStep, s_t + ((it + 1u) & 1u) * kLwStep);
-        staged = true;
-      }
-      uint32_t carry = s_carry[li];  // left-going entries of this list before the step
-      uint32_t wv[8], pv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        wv[j] = sbits[q[j] >> 5];
-        pv[j] = spref[q[j] >> 5];
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t k = k0 + 32u * j + lane;
-        const int4 t = k < A ? cur[32u * j + lane] : make_int4(INT_MIN, 0, 0, 0);
-        const bool keep = t.x != INT_MIN;
-        const uint32_t qq = q[j];
-        const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
-        const bool l = keep && bit;
-        const unsigned bl = __ballot_sync(kFull, l);
-        const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
-        const int32_t off = l ? t.x : t.y;
-        if (keep && off != kNoWrite) {
-          const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
-          const uint32_t nq = static_cast<uint32_t>(l ? t.z + lq : t.w + static_cast<int32_t>(qq) - lq);
-          const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(k) - pl);
-          dstl[dst] = nq;
-        }
-        carry += __popc(bl);
-      }
-      if (lane == 0) s_carry[li] = carry;
     }
-    if (!staged && k0 + kLwStep < A) stage(k0 + kLwStep, s_t + ((it + 1u) & 1u) * kLwStep);
     __syncthreads();
   }
 }
@@ -1514,10 +1532,10 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
     if (a.local_max) {
-      WCK((w_local<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, LayA::bytes, st>>>(a, 0u)));
+      WCK((w_local<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, LayA::bytes, st>>>(a, 0u, 4u)));
       if (a.local_max > kLocalSmall)
         WCK((w_local<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, LayB::bytes, st>>>(
-            a, kLocalSmall)));
+            a, kLocalSmall, 6u)));
     }
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
@@ -1531,10 +1549,10 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
     if (a.local_max) {
       WCK((w_local_route<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, RLayA::bytes, st>>>(
-          a, 0u)));
+          a, 0u, 5u)));
       if (a.local_max > kLocalSmall)
         WCK((w_local_route<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, RLayB::bytes,
-                                                       st>>>(a, kLocalSmall)));
+                                                       st>>>(a, kLocalSmall, 7u)));
     }
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
