@@ -745,7 +745,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   }
   const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
   DevBuf<TreeState> wts(wide ? slots : 0);
-  DevBuf<uint32_t> woff(wide ? 6 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
+  DevBuf<uint32_t> woff(wide ? 7 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
       wctr(wide ? 8 * nlanes : 0);
   // per-lane "trees still splitting" flags read back every level: a pinned buffer per
   // fit, taken from a process-wide pool (cudaMallocHost / cudaFreeHost synchronise
@@ -863,8 +863,8 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
             w.lane_max = lane_max;
             w.local_max = local_max;
             w.t0 = t0;
-            for (int i = 0; i < 6; ++i)
-              w.off[i] = woff.p + (size_t{k} * 6 + i) * (per + 1);
+            for (int i = 0; i < 7; ++i)
+              w.off[i] = woff.p + (size_t{k} * 7 + i) * (per + 1);
             w.active = wactive.p + k;
             w.task_ctr = wctr.p + 8 * k;
             uint64_t nl = 0;

@@ -40,6 +40,7 @@ namespace aiwc_b200 {
 namespace {
 
 constexpr uint32_t kLaneMax = 48;  // nodes below this size use one lane per chain
+constexpr uint32_t kLocalSmallRows = 64;  // wide grower: local nodes of the 64-thread class
 constexpr uint32_t kMaxP = 1024;
 constexpr int kPhases = 14;
 constexpr int kE = 16;  // elements per thread in the flat partition passes
@@ -1683,6 +1684,7 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_ecls = take(emax * 4);
   L.off_wsplit = take(emax * 4);
   L.off_lsplit = take(emax * 4);
+  L.off_lsplit2 = take(emax * 4);
   L.off_samp = take(emax * mtry * 2);
   L.off_res = take(emax * mtry * sizeof(ChainRes));
   L.off_split = take(emax * sizeof(SplitInfo));

@@ -85,7 +85,7 @@ struct SlotLayout {
   size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
       off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
-      off_ecls, off_wsplit, off_lsplit;
+      off_ecls, off_wsplit, off_lsplit, off_lsplit2;
   size_t bytes;
 };
 
@@ -127,8 +127,9 @@ struct TreeState {
   uint32_t nodes, done, totL, A_next;
   uint32_t E0, E1, E2;  // eligible nodes by size class: small (lane chains), mid (lane
                         // groups), big (warp per chain)
-  uint32_t E3;          // eligible local nodes (< local_max rows: no lists, w_local)
-  uint32_t Slocal;      // split nodes routed by w_local_route
+  uint32_t E3, E4;      // eligible local nodes (< local_max rows: no lists, w_local):
+                        // up to kLocalSmall rows / larger
+  uint32_t Slocal, SlocalB;  // split nodes routed by w_local_route (same two classes)
   uint32_t Sbig;        // split nodes routed by a CTA (column 0 listed, >= coop_min rows)
   uint32_t Swarp;       // split nodes routed by a warp (the rest of those >= kLaneMax rows)
   unsigned long long elig_base, split_rows;
@@ -146,8 +147,8 @@ struct WideArgs {
   uint32_t lane_max; // nodes below this many rows run one lane per chain
   uint32_t local_max;  // nodes below this many rows keep no lists (0: off)
   uint32_t write_off2; // w_pay expands per-position offsets (the global-bitmap list pass)
-  uint32_t* off[6];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp
-                     // routes, local nodes (level) / local splits (route)
+  uint32_t* off[7];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp
+                     // routes, small / large local nodes (level) or local splits (route)
   uint32_t* active;  // trees still splitting after this level's decide
   uint32_t* task_ctr;  // dynamic task counters of this level's chain kernels (zeroed by w_prefix)
 };

@@ -15,7 +15,8 @@
 // (included inside namespace aiwc_b200 by grow_wide.cuh)
 
 constexpr int kLocMB = 8;                 // sampled columns staged per batch
-constexpr uint32_t kLocalSmall = 64;      // nodes up to this size: counting sort, 64 threads
+constexpr uint32_t kLocalSmall = kLocalSmallRows;  // nodes up to this size: counting sort,
+                                                   // 64-thread CTAs (their own task list)
 constexpr uint32_t kLocalMaxRows = 2048;  // largest local node (shared-memory bound)
 
 // listed column slot (>= 0) or -(1 + bit) of a two-level column, for the record lookups
@@ -187,7 +188,7 @@ __device__ __forceinline__ void local_chain(bool listed, const uint16_t* perm, c
 
 // split chains of the local nodes with rmin < rows <= SMAX (forest.hpp:255-297)
 template <int NT, int SMAX>
-__global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin, uint32_t ctr) {
+__global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t cls, uint32_t ctr) {
   using Lay = LocalLayout<NT, SMAX, false>;
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char lsm[];
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin, u
   __shared__ int32_t s_slot[kLocMB];
   __shared__ uint32_t s_two[kLocMB];
   const DevData& d = a.g.d;
-  const uint32_t total = a.off[5][a.B];
+  const uint32_t* off = a.off[5 + cls];  // cls 0: <= kLocalSmall rows, 1: larger
+  const uint32_t total = off[a.B];
   const unsigned tid = threadIdx.x, w = warp_id();
   for (;;) {
     if (tid == 0) s_task = atomicAdd(a.task_ctr + ctr, 1u);  // one counter per size class
@@ -211,13 +213,12 @@ __global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin, u
     const uint32_t t = s_task;
     __syncthreads();
     if (t >= total) break;
-    const uint32_t b = owner(a.off[5], a.B, t), k = t - a.off[5][b];
+    const uint32_t b = owner(off, a.B, t), k = t - off[b];
     const SlotPtrs P = slot_ptrs(a, b);
     const TreeState& st = a.ts[b];
-    const uint32_t e = P.ecls[st.E0 + st.E1 + st.E2 + k];
+    const uint32_t e = P.ecls[st.E0 + st.E1 + st.E2 + (cls ? st.E3 : 0u) + k];
     const NodeWork nw = P.front[P.e2f[e]];
     const uint32_t R = nw.e - nw.b;
-    if (R > static_cast<uint32_t>(SMAX) || R <= rmin) continue;  // another size class
     const uint32_t m = tree_m(a, b);
     for (uint32_t i = tid; i < R; i += NT) {
       const Payload pv = P.pay[nw.b + i];
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(NT) w_local(const WideArgs a, uint32_t rmin, u
 // (a stable sort by the column-0 rank), child (weight, sum, sumsq) as sequential FP64
 // sums in that order (forest.hpp:323-352), goes-left bits for the payload pass
 template <int NT, int SMAX>
-__global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t rmin, uint32_t ctr) {
+__global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t cls, uint32_t ctr) {
   using Lay = LocalLayout<NT, SMAX, true>;
   extern __shared__ __align__(16) unsigned char lsm[];
   double* s_wy = reinterpret_cast<double*>(lsm + Lay::wy);
@@ -270,7 +271,8 @@ __global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t r
   __shared__ uint32_t s_task, s_cnts[3];
   __shared__ double s_sum[4];
   const DevData& d = a.g.d;
-  const uint32_t total = a.off[5][a.B];
+  const uint32_t* off = a.off[5 + cls];
+  const uint32_t total = off[a.B];
   const unsigned tid = threadIdx.x, lane = lane_id(), w = warp_id();
   const int32_t slot0 = rec_slot(d, 0);
   const bool two0 = (d.vals_off[1] - d.vals_off[0]) > 256u;
@@ -280,13 +282,12 @@ __global__ void __launch_bounds__(NT) w_local_route(const WideArgs a, uint32_t r
     const uint32_t t = s_task;
     __syncthreads();
     if (t >= total) break;
-    const uint32_t b = owner(a.off[5], a.B, t), k = t - a.off[5][b];
+    const uint32_t b = owner(off, a.B, t), k = t - off[b];
     const SlotPtrs P = slot_ptrs(a, b);
-    const uint32_t s = P.lsplit[k];
+    const uint32_t s = (cls ? P.lsplit2 : P.lsplit)[k];
     const SplitInfo si = P.spl[s];
     const NodeWork nw = P.front[si.f];
     const uint32_t R = nw.e - nw.b;
-    if (R > static_cast<uint32_t>(SMAX) || R <= rmin) continue;
     const int32_t slotc = rec_slot(d, si.c);
     if (tid < 3) s_cnts[tid] = 0u;
     uint32_t c_nl = 0, c_wl = 0, c_wr = 0;

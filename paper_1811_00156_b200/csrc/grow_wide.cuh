@@ -26,7 +26,8 @@ struct SlotPtrs {
   uint32_t* e2f;
   uint32_t* ecls;
   uint32_t* wsplit;
-  uint32_t* lsplit;
+  uint32_t* lsplit;   // local splits up to kLocalSmall rows
+  uint32_t* lsplit2;  // larger local splits
   uint16_t* samp;
   ChainRes* res;
   SplitInfo* spl;
@@ -62,6 +63,7 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.ecls = reinterpret_cast<uint32_t*>(s + L.off_ecls);
   p.wsplit = reinterpret_cast<uint32_t*>(s + L.off_wsplit);
   p.lsplit = reinterpret_cast<uint32_t*>(s + L.off_lsplit);
+  p.lsplit2 = reinterpret_cast<uint32_t*>(s + L.off_lsplit2);
   p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
   p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
   p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
@@ -380,8 +382,8 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   // eligible nodes by size class, BFS order inside each: [0, E0) small (< lane_max
   // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain), then
   // local (< local_max rows: no lists, w_local)
-  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0, E3 = 0;
-  for (uint32_t cls = 0; cls < 4; ++cls) {
+  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0, E3 = 0, E4 = 0;
+  for (uint32_t cls = 0; cls < 5; ++cls) {
     carry = 0;
     for (uint32_t b0 = 0; b0 < E; b0 += NT) {
       const uint32_t e = b0 + threadIdx.x;
@@ -389,7 +391,8 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       if (e < E) {
         const NodeWork& nw = fr[P.e2f[e]];
         const uint32_t R = nw.e - nw.b;
-        const uint32_t c = R < a.local_max ? 3u : (R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u));
+        const uint32_t c = R < a.local_max ? (R <= kLocalSmallRows ? 3u : 4u)
+                                           : (R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u));
         in = c == cls;
       }
       uint32_t tot;
@@ -401,6 +404,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     if (cls == 1) E1 = carry;
     if (cls == 2) E2 = carry;
     if (cls == 3) E3 = carry;
+    if (cls == 4) E4 = carry;
     base += carry;
   }
   for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     s.E1 = E1;
     s.E2 = E2;
     s.E3 = E3;
+    s.E4 = E4;
   }
 }
 
@@ -420,10 +425,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0;
   for (uint32_t base = 0; base < a.B; base += NT) {
     const uint32_t b = base + threadIdx.x;
-    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
+    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0, v6 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
         v1 = s.E1 * grp_tpn(m, a.g.mtry);
         v2 = s.E2 * m;
         v5 = s.E3;
+        v6 = s.E4;
       } else {
         v0 = s.Sbig;
         v1 = s.S;
@@ -439,6 +445,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
         v3 = nchunks_of(s.A, a.g.d.nlisted);
         v4 = s.Swarp;
         v5 = s.Slocal;
+        v6 = s.SlocalB;
       }
     }
     uint32_t t0, t1, t2, t3;
@@ -446,9 +453,10 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
     const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
     const uint32_t e3 = block_excl_scan<NT>(v3, sh, &t3);
-    uint32_t t4, t5;
+    uint32_t t4, t5, t6;
     const uint32_t e4 = block_excl_scan<NT>(v4, sh, &t4);
     const uint32_t e5 = block_excl_scan<NT>(v5, sh, &t5);
+    const uint32_t e6 = block_excl_scan<NT>(v6, sh, &t6);
     if (b < a.B) {
       a.off[0][b] = c0 + e0;
       a.off[1][b] = c1 + e1;
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
       a.off[3][b] = c3 + e3;
       if (which == 1) a.off[4][b] = c4 + e4;
       a.off[5][b] = c5 + e5;
+      a.off[6][b] = c6 + e6;
     }
     c0 += t0;
     c1 += t1;
@@ -463,6 +472,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     c3 += t3;
     c4 += t4;
     c5 += t5;
+    c6 += t6;
   }
   if (threadIdx.x == 0) {
     if (which == 1) {
@@ -471,6 +481,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     }
     if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = a.task_ctr[4] = a.task_ctr[6] = 0u;
     a.off[5][a.B] = c5;
+    a.off[6][a.B] = c6;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
     a.off[2][a.B] = c2;
@@ -849,7 +860,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
   const bool coop_route = d.list_of[0] >= 0;
-  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0, lcarry = 0;
+  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0, lcarry = 0, l2carry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
     const uint32_t e = base + threadIdx.x;
     uint32_t sp = 0, c = 0, thr_rank = 0;
@@ -915,10 +926,14 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     // splits routed by a whole CTA (w_route_coop), compacted into ecls (free after the
     // chain kernels)
     const uint32_t loc = sp && cnt < a.local_max ? 1u : 0u;  // w_local_route
-    uint32_t ltot;
-    const uint32_t lex = block_excl_scan<NT>(loc, sh, &ltot);
-    if (loc) P.lsplit[lcarry + lex] = carry + ex;
+    const uint32_t locA = loc && cnt <= kLocalSmallRows ? 1u : 0u, locB = loc - locA;
+    uint32_t ltot, l2tot;
+    const uint32_t lex = block_excl_scan<NT>(locA, sh, &ltot);
+    const uint32_t l2ex = block_excl_scan<NT>(locB, sh, &l2tot);
+    if (locA) P.lsplit[lcarry + lex] = carry + ex;
+    if (locB) P.lsplit2[l2carry + l2ex] = carry + ex;
     lcarry += ltot;
+    l2carry += l2tot;
     const uint32_t big = sp && !loc && coop_route && cnt >= a.coop_min ? 1u : 0u;
     uint32_t btot;
     const uint32_t bex = block_excl_scan<NT>(big, sh, &btot);
@@ -955,6 +970,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     st.Sbig = bcarry;
     st.Swarp = wcarry;
     st.Slocal = lcarry;
+    st.SlocalB = l2carry;
     st.A_next = ccarry;
     st.split_rows += ccarry;
     st.elig_base += E;
@@ -1535,7 +1551,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       WCK((w_local<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, LayA::bytes, st>>>(a, 0u, 4u)));
       if (a.local_max > kLocalSmall)
         WCK((w_local<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, LayB::bytes, st>>>(
-            a, kLocalSmall, 6u)));
+            a, 1u, 6u)));
     }
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
@@ -1552,7 +1568,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
           a, 0u, 5u)));
       if (a.local_max > kLocalSmall)
         WCK((w_local_route<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, RLayB::bytes,
-                                                       st>>>(a, kLocalSmall, 7u)));
+                                                       st>>>(a, 1u, 7u)));
     }
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
