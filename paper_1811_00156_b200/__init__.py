@@ -30,7 +30,8 @@ __all__ = [
     "evaluate", "derive_seed", "synthesize", "lib", "device_count", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libaiwc_cuda.so")
+LIB_PATH = os.environ.get("AIWC_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "libaiwc_cuda.so")
 
 u64, u32, i32, f64, vp = C.c_uint64, C.c_uint32, C.c_int32, C.c_double, C.c_void_p
 P = C.POINTER

@@ -842,7 +842,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
       if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
       coop_min = std::max(coop_min, big_min);
       // nodes below local_max rows keep no sorted lists (grow_local.cuh)
-      uint32_t local_max = 2048;
+      uint32_t local_max = 0;  // opt-in (AIWC_LOCAL_MAX): measured slower at C4
       if (const char* e = std::getenv("AIWC_LOCAL_MAX")) local_max = static_cast<uint32_t>(std::atoll(e));
       if (!ctx->rec_stride) local_max = 0;
       std::vector<cudaError_t> lane_err(K, cudaSuccess);

@@ -10,6 +10,18 @@
 // longer idles the rest of its CTA: other trees' tasks fill the SMs.
 #pragma once
 
+// resident 256-thread CTAs per SM the chain / route kernels are compiled for (register
+// budget 64K / (256 * minb)); measured in tools/prof_minb.sh
+#ifndef AIWC_CHAIN_MINB
+#define AIWC_CHAIN_MINB 1
+#endif
+#ifndef AIWC_GRP_MINB
+#define AIWC_GRP_MINB 1
+#endif
+#ifndef AIWC_ROUTE_MINB
+#define AIWC_ROUTE_MINB 1
+#endif
+
 namespace aiwc_b200 {
 
 // Pointers of slot b for the current level (cur) and the next one (suffix _n).  The
@@ -493,7 +505,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 // big nodes (>= big_min rows) run one warp per (node, column) ...
 constexpr int kBigU = 4;
 template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
-__global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
+__global__ void __launch_bounds__(256, AIWC_CHAIN_MINB) w_chains_warp(const WideArgs a) {
   constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
   __shared__ double stage[8][GB == 32 ? 64 : 32 * UB];
   const uint32_t total = a.off[2][a.B];
@@ -787,7 +799,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
 // ... mid nodes run one warp per node (or per group of 32/G of its columns), G lanes
 // per column (chain_grp) ...
 template <typename RankT, int G, int U>
-__global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
+__global__ void __launch_bounds__(256, AIWC_GRP_MINB) w_chains_grp(const WideArgs a) {
   __shared__ double stage[8][32 * U];
   const uint32_t total = a.off[1][a.B];
   const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
@@ -988,7 +1000,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
 
 // route in column-0 order (forest.hpp:323-352): warps take split nodes >= kLaneMax
 template <typename RankT, bool kWarp>
-__global__ void __launch_bounds__(256) w_route(const WideArgs a) {
+__global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a) {
   __shared__ double stage[8][128];
   const uint32_t total = a.off[1][a.B];
   const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
@@ -1225,7 +1237,7 @@ __global__ void w_pay(const WideArgs a) {
   }
 }
 
-// List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
+// List pass with local nodes: one CTA per tree with the tree's goes-left bitmap + prefix
 // staged in shared memory and one warp per sorted list.  The CTA walks the positions in
 // steps of kLwStep; each step's per-position segment offsets (list destinations, payload
 // offsets) are staged once in shared memory for all lists, two steps ahead, and a warp
@@ -1343,6 +1355,96 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
       }
     }
     __syncthreads();
+  }
+}
+
+// List pass without local nodes (the default): single read, one CTA per tree with the tree's goes-left bitmap + prefix
+// staged in shared memory and one warp per sorted list.  A warp walks its list in
+// position order, 256 positions per step as 8 sub-rows of 32 consecutive positions
+// (lane i holds position k0 + 32j + i of sub-row j), so the count of left-going entries
+// before each entry is the warp's running carry plus ballot counts -- no count pass --
+// and each sub-row's left (right) entries land on consecutive destinations: every
+// store instruction writes at most two contiguous runs.  The next step's entries and
+// segment offsets are loaded before this step is scattered.
+struct LwStage {  // one warp step: 8 sub-rows' entries + offsets
+  uint32_t q[8];
+  int2 t[8];
+};
+
+__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
+                                        const int2* off2) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t k = k0 + 32u * j + lane_id();
+    if (k < A) {
+      v.q[j] = list[k];
+      v.t[j] = off2[k];
+    } else {
+      v.t[j] = make_int2(INT_MIN, 0);
+    }
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) w_lwarp_off2(const WideArgs a) {
+  extern __shared__ uint32_t sm[];
+  const uint32_t b = blockIdx.x;
+  const TreeState& st = a.ts[b];
+  if (st.done) return;
+  const SlotPtrs P = slot_ptrs(a, b);
+  const uint32_t A = st.A, aw = (A + 31u) / 32u;
+  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
+  uint32_t* sbits = sm;
+  uint32_t* spref = sm + (aw + 3u) / 4u * 4u;
+  {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
+    const uint32_t aw4 = (aw + 3u) / 4u;
+    const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
+    const uint4* gp = reinterpret_cast<const uint4*>(P.pref);
+    for (uint32_t w = threadIdx.x; w < aw4; w += blockDim.x) {
+      const uint4 x = gb[w], y = gp[w];
+      sbits[4 * w] = x.x; sbits[4 * w + 1] = x.y; sbits[4 * w + 2] = x.z; sbits[4 * w + 3] = x.w;
+      spref[4 * w] = y.x; spref[4 * w + 1] = y.y; spref[4 * w + 2] = y.z; spref[4 * w + 3] = y.w;
+    }
+  }
+  __syncthreads();
+  const unsigned lane = lane_id(), lt = lanemask_lt();
+  for (uint32_t li = warp_id(); li < nl; li += blockDim.x >> 5) {
+    const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
+    uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
+    uint32_t carry = 0;  // left-going entries of this list before the sub-row
+    LwStage cur, nxt;
+    lw_load(cur, 0, A, src, P.off2);
+    for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
+      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
+      // all 16 shared-memory lookups of the lane first (branch-free), then the scatter
+      uint32_t wv[8], pv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t wi = cur.t[j].x != INT_MIN ? cur.q[j] >> 5 : 0u;
+        wv[j] = sbits[wi];
+        pv[j] = spref[wi];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int2 t = cur.t[j];
+        const bool keep = t.x != INT_MIN;
+        const uint32_t qq = cur.q[j];
+        const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
+        const bool l = keep && bit;
+        const unsigned bl = __ballot_sync(kFull, l);
+        const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
+        if (keep) {
+          const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
+          const uint32_t k = k0 + 32u * j + lane;
+          const uint32_t nq = static_cast<uint32_t>(l ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
+          const uint32_t dst =
+              static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
+          dstl[dst] = nq;
+        }
+        carry += __popc(bl);
+      }
+      cur = nxt;
+    }
   }
 }
 
@@ -1481,13 +1583,16 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
   // per-tree list pass with the bitmap + prefix in shared memory when they fit
   size_t lw_smem = lw_smem_bytes(a.g.L.stride, a.g.d.nlisted);
+  const size_t lw_smem_off2 = ((a.g.L.stride + 31) / 32 + 3) / 4 * 4 * 8;
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (lw_smem + 1024 > static_cast<size_t>(optin) || std::getenv("AIWC_LW_GLOBAL") ||
         cudaFuncSetAttribute(w_lwarp<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(lw_smem)) != cudaSuccess)
+                             static_cast<int>(lw_smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(w_lwarp_off2<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(lw_smem_off2)) != cudaSuccess)
       lw_smem = 0;
     cudaGetLastError();
   }
@@ -1499,7 +1604,9 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   using RLayB = LocalLayout<256, int(kLocalMaxRows), true>;
   if (!lw_smem || a.g.d.rec_stride == 0 || sizeof(RankT) != 2) a.local_max = 0;
   a.local_max = std::min(a.local_max, kLocalMaxRows);
-  a.write_off2 = lw_smem ? 0u : 1u;
+  // per-position offsets for the list passes without local nodes (w_lwarp_off2 and the
+  // global-bitmap fallback); with local nodes w_lwarp stages per-segment offsets itself
+  a.write_off2 = a.local_max ? 0u : 1u;
   if (a.local_max > kLocalSmall &&
       (cudaFuncSetAttribute(w_local<256, int(kLocalMaxRows)>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(LayB::bytes)) != cudaSuccess ||
@@ -1573,8 +1680,10 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
     if (lists) {
-      if (lw_smem) {
+      if (lw_smem && a.local_max) {
         WCK((w_lwarp<kLwWarps><<<a.B, lw_warps * 32, lw_smem, st>>>(a)));
+      } else if (lw_smem) {
+        WCK((w_lwarp_off2<kLwWarps><<<a.B, lw_warps * 32, lw_smem_off2, st>>>(a)));
       } else {
         WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
         WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));
