@@ -279,6 +279,8 @@ struct aiwc_ctx {
   DevBuf<uint8_t> rec;
   DevBuf<int32_t> bin_of;
   uint32_t rec_stride = 0, rec_bits = 0;
+  DevBuf<uint32_t> bitcols;  // two-level columns, 1 bit per row
+  uint32_t bitcol_words = 0;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
   DevBuf<char> scratch;
@@ -290,7 +292,7 @@ struct aiwc_ctx {
   DevData view() const {
     return DevData{n, p, rank_bytes, nlisted, order_stride, col.p, dy.p, order.p, rank.p,
                    vals.p, vals_off.p, list_of.p, listed.p, rec.p, rec_stride, rec_bits,
-                   bin_of.p};
+                   bin_of.p, bitcols.p, bitcol_words};
   }
 };
 
@@ -473,21 +475,30 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
         }
       const uint32_t bits_byte = (2 * ctx->nlisted + 3) & ~3u;
       const uint32_t stride = (bits_byte + 4 * ((static_cast<uint32_t>(bincols.size()) + 31) / 32) + 15) & ~15u;
-      if (ctx->rank_bytes == 2 && stride <= 128) {
+      ctx->bin_of.alloc(p);
+      CK(cudaMemcpyAsync(ctx->bin_of.p, bin_of.data(), p * 4, cudaMemcpyHostToDevice, s));
+      DevBuf<uint32_t> dbin(std::max<size_t>(bincols.size(), 1));
+      if (!bincols.empty()) {
+        CK(cudaMemcpyAsync(dbin.p, bincols.data(), bincols.size() * 4, cudaMemcpyHostToDevice, s));
+        ctx->bitcol_words = static_cast<uint32_t>((n + 31) / 32);
+        ctx->bitcols.alloc(bincols.size() * size_t{ctx->bitcol_words});
+        CK(build_bitcols(ctx->rank.p, static_cast<int>(ctx->rank_bytes), n,
+                         static_cast<uint32_t>(bincols.size()), dbin.p, ctx->bitcol_words,
+                         ctx->bitcols.p, s));
+        g_launches += 1;
+      }
+      // records serve only the opt-in local mode (AIWC_LOCAL_MAX set when the dataset is
+      // prepared): 64 B per row otherwise left to the grower's tree slots
+      if (ctx->rank_bytes == 2 && stride <= 128 && std::getenv("AIWC_LOCAL_MAX")) {
         ctx->rec_stride = stride;
         ctx->rec_bits = bits_byte;
         ctx->rec.alloc(size_t{stride} * n);
-        ctx->bin_of.alloc(p);
-        CK(cudaMemcpyAsync(ctx->bin_of.p, bin_of.data(), p * 4, cudaMemcpyHostToDevice, s));
-        DevBuf<uint32_t> dbin(std::max<size_t>(bincols.size(), 1));
-        if (!bincols.empty())
-          CK(cudaMemcpyAsync(dbin.p, bincols.data(), bincols.size() * 4, cudaMemcpyHostToDevice, s));
         CK(build_records(reinterpret_cast<const uint16_t*>(ctx->rank.p), n, ctx->nlisted,
                          ctx->listed.p, static_cast<uint32_t>(bincols.size()), dbin.p, stride,
                          bits_byte, ctx->rec.p, s));
         g_launches += 1;
-        CK(cudaStreamSynchronize(s));
       }
+      CK(cudaStreamSynchronize(s));  // dbin is freed on scope exit
     }
     CK(cudaStreamSynchronize(s));  // the temporaries above are freed on return
     *out = ctx.release();
@@ -845,6 +856,9 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
       uint32_t local_max = 0;  // opt-in (AIWC_LOCAL_MAX): measured slower at C4
       if (const char* e = std::getenv("AIWC_LOCAL_MAX")) local_max = static_cast<uint32_t>(std::atoll(e));
       if (!ctx->rec_stride) local_max = 0;
+      if (std::getenv("AIWC_VERBOSE"))
+        std::fprintf(stderr, "[aiwc wide] trees=%u slots=%d lanes=%d per=%u slot_bytes=%zu\n", T, slots,
+                     K, per, L.bytes);
       std::vector<cudaError_t> lane_err(K, cudaSuccess);
       std::vector<std::thread> lanes;
       for (int k = 0; k < K; ++k) {

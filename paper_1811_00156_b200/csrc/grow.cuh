@@ -74,7 +74,19 @@ struct DevData {
   // columns' 0/1 ranks at byte rec_bits; rec_stride == 0: no records (u32 ranks)
   const uint8_t* rec;
   uint32_t rec_stride, rec_bits;
-  const int32_t* bin_of;    // p: bit of a two-level column in the record bitmask, or -1
+  const int32_t* bin_of;    // p: index of a two-level column (record bit, bit column), or -1
+  // two-level columns' 0/1 ranks as bit columns (1 bit per row, bitcol_words per
+  // column): a chain over such a column reads 32 rows per word from L2 instead of one
+  // 2-byte rank per 32-byte sector
+  const uint32_t* bitcols;
+  uint32_t bitcol_words;
+};
+
+// rank source of one column: dense ranks, or (two-level column) its bit column
+template <typename RankT>
+struct RankSrc {
+  const RankT* rk;
+  const uint32_t* bits;  // null: use rk
 };
 
 struct SlotLayout {

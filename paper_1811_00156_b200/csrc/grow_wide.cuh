@@ -537,14 +537,14 @@ __global__ void __launch_bounds__(256, AIWC_CHAIN_MINB) w_chains_warp(const Wide
       uint32_t bp;
       chain_grp<RankT, (GB < 32 ? GB : 16), UB>(
           act, li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride, nw_.b,
-          nw_.e, P.pay, rank + static_cast<size_t>(c) * n, nw_.w, nw_.s, bg, bp,
+          nw_.e, P.pay, rank_src<RankT>(a.g.d, c, true), nw_.w, nw_.s, bg, bp,
           stage[warp_id()] + grp * UB * GB);
       if (act && (lane_id() % GB) == 0) P.res[e * m + jj] = ChainRes{bg, bp, 0u};
       continue;
     }
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
-    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
     double bg;
     uint32_t bp;
     chain_warp_p<RankT, 2>(li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride,
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
     const int32_t li = a.g.d.list_of[c];
     const bool listed = li >= 0;
     const uint32_t* list = P.lists + static_cast<size_t>(listed ? li : 0) * stride;
-    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
     const uint32_t R = nw.e - nw.b, nblk = (R + kCB - 1) / kCB;
     // producers: a register pipeline over blocks -- at step i a producer lane writes
     // block i+1 (ranks gathered at step i-1) into its stage, gathers the ranks of block
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(256, AIWC_GRP_MINB) w_chains_grp(const WideArg
     const NodeWork nw_ = P.front[P.e2f[e]];
     const uint32_t c = act ? P.samp[e * m + j] : 0u;
     const int32_t li = a.g.d.list_of[c];
-    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
     const uint32_t* list = P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride;
     double bg;
     uint32_t bp;
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
     const NodeWork nw_ = P.front[P.e2f[e]];
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
-    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
+    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
     double bg;
     uint32_t bp;
     if (li >= 0)
@@ -1030,7 +1030,7 @@ __global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a
     const SplitInfo si = P.spl[s];
     if (!kWarp && (si.cnt >= kLaneMax || si.cnt < a.local_max)) continue;
     const NodeWork nw = P.front[si.f];
-    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+    const RankSrc<RankT> rk_f = rank_src<RankT>(a.g.d, si.c, true);
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
@@ -1038,14 +1038,14 @@ __global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a
         route_warp_p<RankT, 2>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
                                P.bits, o, stage[warp_id()]);
       else
-        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels,
+        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank_src<RankT>(a.g.d, 0, true), k0levels,
                                     rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
       if (lane_id() != 0) continue;
     } else {
       if (l0)
         route_lane<RankT>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank, P.bits, o);
       else
-        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels, rk_f,
+        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank_src<RankT>(a.g.d, 0, true), k0levels, rk_f,
                                  si.thr_rank, P.bits, o);
     }
     P.spl[s].nl = o.nl;
@@ -1076,7 +1076,7 @@ __global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
     const uint32_t s = P.ecls[k];
     const SplitInfo si = P.spl[s];
     const NodeWork nw = P.front[si.f];
-    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
+    const RankSrc<RankT> rk_f = rank_src<RankT>(a.g.d, si.c, true);
     const uint32_t* l0 = P.lists + static_cast<size_t>(list0) * stride;
     const uint32_t nblk = (nw.e - nw.b + kCoopBlock - 1) / kCoopBlock;
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;

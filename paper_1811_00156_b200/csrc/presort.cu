@@ -99,6 +99,37 @@ __global__ void record_kernel(const uint16_t* __restrict__ rank, uint64_t n, uin
   }
 }
 
+// Bit columns of the two-level columns (DevData::bitcols): word w of column bi holds
+// rows [32w, 32w+32), bit k set when row 32w+k has rank 1.
+__global__ void bitcol_kernel(const void* __restrict__ rank, int rank_bytes, uint64_t n,
+                              uint32_t nbin, const uint32_t* __restrict__ bincols,
+                              uint32_t words, uint32_t* __restrict__ out) {
+  const uint64_t total = uint64_t{nbin} * words;
+  for (uint64_t x = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; x < total;
+       x += uint64_t{gridDim.x} * blockDim.x) {
+    const uint32_t bi = static_cast<uint32_t>(x / words), w = static_cast<uint32_t>(x % words);
+    const size_t base = size_t{bincols[bi]} * n;
+    uint32_t v = 0;
+    for (uint32_t k = 0; k < 32; ++k) {
+      const uint64_t r = uint64_t{w} * 32 + k;
+      if (r >= n) break;
+      const uint32_t rk = rank_bytes == 2 ? static_cast<const uint16_t*>(rank)[base + r]
+                                          : static_cast<const uint32_t*>(rank)[base + r];
+      v |= (rk != 0 ? 1u : 0u) << k;
+    }
+    out[x] = v;
+  }
+}
+
+cudaError_t build_bitcols(const void* d_rank, int rank_bytes, uint64_t n, uint32_t nbin,
+                          const uint32_t* d_bincols, uint32_t words, uint32_t* d_out,
+                          cudaStream_t s) {
+  const uint64_t total = uint64_t{nbin} * words;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148u * 64u));
+  if (total) bitcol_kernel<<<blocks, 256, 0, s>>>(d_rank, rank_bytes, n, nbin, d_bincols, words, d_out);
+  return cudaGetLastError();
+}
+
 cudaError_t build_records(const uint16_t* d_rank, uint64_t n, uint32_t nlisted,
                           const uint32_t* d_listed, uint32_t nbin, const uint32_t* d_bincols,
                           uint32_t stride_bytes, uint32_t bits_byte, uint8_t* d_rec,

@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for r in 1 2; do
+  for v in base head; do
+    if [ $v = base ]; then L=build/variants/c_f0bb2f7/libaiwc_cuda.so; else L=paper_1811_00156_b200/libaiwc_cuda.so; fi
+    AIWC_VERBOSE=1 AIWC_LIB=$L timeout 600 python tools/fit_once.py c4 1000 2 >> gpurun_out/bis2_$v.log 2>&1
+  done
+done
