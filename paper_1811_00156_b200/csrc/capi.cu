@@ -275,12 +275,6 @@ struct aiwc_ctx {
   DevBuf<int32_t> list_of;
   DevBuf<uint8_t> rank;
   DevBuf<uint64_t> vals_off;
-  // row records of the wide grower's local kernels (DevData::rec); empty with u32 ranks
-  DevBuf<uint8_t> rec;
-  DevBuf<int32_t> bin_of;
-  uint32_t rec_stride = 0, rec_bits = 0;
-  DevBuf<uint32_t> bitcols;  // two-level columns, 1 bit per row
-  uint32_t bitcol_words = 0;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
   DevBuf<char> scratch;
@@ -291,8 +285,7 @@ struct aiwc_ctx {
 
   DevData view() const {
     return DevData{n, p, rank_bytes, nlisted, order_stride, col.p, dy.p, order.p, rank.p,
-                   vals.p, vals_off.p, list_of.p, listed.p, rec.p, rec_stride, rec_bits,
-                   bin_of.p, bitcols.p, bitcol_words};
+                   vals.p, vals_off.p, list_of.p, listed.p};
   }
 };
 
@@ -464,42 +457,6 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
     if (!listed.empty())
       CK(cudaMemcpyAsync(ctx->listed.p, listed.data(), listed.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->vals_off.p, voff.data(), voff.size() * 8, cudaMemcpyHostToDevice, s));
-    // row records (u16 ranks only): listed ranks, then the two-level columns' bits
-    {
-      std::vector<int32_t> bin_of(p, -1);
-      std::vector<uint32_t> bincols;
-      for (uint32_t c = 0; c < p; ++c)
-        if (cnt[c] < 3) {
-          bin_of[c] = static_cast<int32_t>(bincols.size());
-          bincols.push_back(c);
-        }
-      const uint32_t bits_byte = (2 * ctx->nlisted + 3) & ~3u;
-      const uint32_t stride = (bits_byte + 4 * ((static_cast<uint32_t>(bincols.size()) + 31) / 32) + 15) & ~15u;
-      ctx->bin_of.alloc(p);
-      CK(cudaMemcpyAsync(ctx->bin_of.p, bin_of.data(), p * 4, cudaMemcpyHostToDevice, s));
-      DevBuf<uint32_t> dbin(std::max<size_t>(bincols.size(), 1));
-      if (!bincols.empty()) {
-        CK(cudaMemcpyAsync(dbin.p, bincols.data(), bincols.size() * 4, cudaMemcpyHostToDevice, s));
-        ctx->bitcol_words = static_cast<uint32_t>((n + 31) / 32);
-        ctx->bitcols.alloc(bincols.size() * size_t{ctx->bitcol_words});
-        CK(build_bitcols(ctx->rank.p, static_cast<int>(ctx->rank_bytes), n,
-                         static_cast<uint32_t>(bincols.size()), dbin.p, ctx->bitcol_words,
-                         ctx->bitcols.p, s));
-        g_launches += 1;
-      }
-      // records serve only the opt-in local mode (AIWC_LOCAL_MAX set when the dataset is
-      // prepared): 64 B per row otherwise left to the grower's tree slots
-      if (ctx->rank_bytes == 2 && stride <= 128 && std::getenv("AIWC_LOCAL_MAX")) {
-        ctx->rec_stride = stride;
-        ctx->rec_bits = bits_byte;
-        ctx->rec.alloc(size_t{stride} * n);
-        CK(build_records(reinterpret_cast<const uint16_t*>(ctx->rank.p), n, ctx->nlisted,
-                         ctx->listed.p, static_cast<uint32_t>(bincols.size()), dbin.p, stride,
-                         bits_byte, ctx->rec.p, s));
-        g_launches += 1;
-      }
-      CK(cudaStreamSynchronize(s));  // dbin is freed on scope exit
-    }
     CK(cudaStreamSynchronize(s));  // the temporaries above are freed on return
     *out = ctx.release();
   });
@@ -756,8 +713,8 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   }
   const size_t per_lane = wide ? size_t(slots) / nlanes : 0;
   DevBuf<TreeState> wts(wide ? slots : 0);
-  DevBuf<uint32_t> woff(wide ? 7 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
-      wctr(wide ? 8 * nlanes : 0);
+  DevBuf<uint32_t> woff(wide ? 5 * nlanes * (per_lane + 1) : 0), wactive(wide ? nlanes : 0),
+      wctr(wide ? 4 * nlanes : 0);
   // per-lane "trees still splitting" flags read back every level: a pinned buffer per
   // fit, taken from a process-wide pool (cudaMallocHost / cudaFreeHost synchronise
   // and cost milliseconds -- too much for the many small fits of a grid search)
@@ -852,10 +809,6 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
       uint32_t coop_min = per <= 48 ? 32768u : 0xffffffffu;
       if (const char* e = std::getenv("AIWC_COOP_MIN")) coop_min = static_cast<uint32_t>(std::atoll(e));
       coop_min = std::max(coop_min, big_min);
-      // nodes below local_max rows keep no sorted lists (grow_local.cuh)
-      uint32_t local_max = 0;  // opt-in (AIWC_LOCAL_MAX): measured slower at C4
-      if (const char* e = std::getenv("AIWC_LOCAL_MAX")) local_max = static_cast<uint32_t>(std::atoll(e));
-      if (!ctx->rec_stride) local_max = 0;
       if (std::getenv("AIWC_VERBOSE"))
         std::fprintf(stderr, "[aiwc wide] trees=%u slots=%d lanes=%d per=%u slot_bytes=%zu\n", T, slots,
                      K, per, L.bytes);
@@ -875,12 +828,11 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
             w.coop_min = coop_min;
             w.pair_big = big_lanes;
             w.lane_max = lane_max;
-            w.local_max = local_max;
             w.t0 = t0;
-            for (int i = 0; i < 7; ++i)
-              w.off[i] = woff.p + (size_t{k} * 7 + i) * (per + 1);
+            for (int i = 0; i < 5; ++i)
+              w.off[i] = woff.p + (size_t{k} * 5 + i) * (per + 1);
             w.active = wactive.p + k;
-            w.task_ctr = wctr.p + 8 * k;
+            w.task_ctr = wctr.p + 4 * k;
             uint64_t nl = 0;
             cudaError_t e = run_wide(ctx->rank_bytes, w, ls, sms, h_active.get() + k, &nl);
             g_launches += nl;

@@ -46,13 +46,6 @@ cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* node
 cudaError_t gpu_presort(const double* d_col, uint64_t n, uint32_t p, cudaStream_t s,
                         uint32_t* d_sorted, uint32_t* d_rank, double* d_vals,
                         uint32_t* d_counts, uint64_t* launches);
-cudaError_t build_bitcols(const void* d_rank, int rank_bytes, uint64_t n, uint32_t nbin,
-                          const uint32_t* d_bincols, uint32_t words, uint32_t* d_out,
-                          cudaStream_t s);
-cudaError_t build_records(const uint16_t* d_rank, uint64_t n, uint32_t nlisted,
-                          const uint32_t* d_listed, uint32_t nbin, const uint32_t* d_bincols,
-                          uint32_t stride_bytes, uint32_t bits_byte, uint8_t* d_rec,
-                          cudaStream_t s);
 cudaError_t narrow_ranks(const uint32_t* d_in, uint64_t count, uint16_t* d_out, cudaStream_t s);
 cudaError_t count_nonfinite(const double* d_v, uint64_t count, unsigned long long* d_bad,
                             cudaStream_t s);

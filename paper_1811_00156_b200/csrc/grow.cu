@@ -40,7 +40,6 @@ namespace aiwc_b200 {
 namespace {
 
 constexpr uint32_t kLaneMax = 48;  // nodes below this size use one lane per chain
-constexpr uint32_t kLocalSmallRows = 64;  // wide grower: local nodes of the 64-thread class
 constexpr uint32_t kMaxP = 1024;
 constexpr int kPhases = 14;
 constexpr int kE = 16;  // elements per thread in the flat partition passes
@@ -70,18 +69,6 @@ __device__ __forceinline__ uint32_t inbag_pos(const uint32_t* bits, const uint32
 template <typename RankT>
 __device__ __forceinline__ uint32_t rank_of(const RankT* rank_c, uint32_t row) {
   return static_cast<uint32_t>(__ldg(rank_c + row));
-}
-template <typename RankT>
-__device__ __forceinline__ uint32_t rank_of(const RankSrc<RankT>& s, uint32_t row) {
-  return s.bits ? (__ldg(s.bits + (row >> 5)) >> (row & 31u)) & 1u
-                : static_cast<uint32_t>(__ldg(s.rk + row));
-}
-// rank source of column c (the wide grower reads two-level columns' bit columns)
-template <typename RankT>
-__device__ __forceinline__ RankSrc<RankT> rank_src(const DevData& d, uint32_t c, bool use_bits) {
-  const RankT* rk = static_cast<const RankT*>(d.rank) + static_cast<size_t>(c) * d.n;
-  const int32_t bi = (use_bits && d.bitcols) ? d.bin_of[c] : -1;
-  return RankSrc<RankT>{rk, bi >= 0 ? d.bitcols + static_cast<size_t>(bi) * d.bitcol_words : nullptr};
 }
 
 __device__ __forceinline__ double gain_at(double sl, double wl, double W, double S) {
@@ -241,7 +228,7 @@ __device__ __forceinline__ void warp_best(double& bg, uint32_t& bp) {
 // ---- split chain over a sorted list, warp-cooperative (large nodes) ---------------
 template <typename RankT, int G>
 __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
-                           const Payload* pay, const RankSrc<RankT> rk_c,
+                           const Payload* pay, const RankT* __restrict__ rk_c,
                            double W, double S, double& best_gain, uint32_t& best_pos,
                            double* st) {
   const unsigned lane = lane_id();
@@ -309,7 +296,7 @@ __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
 // flight.  Same arithmetic (and order) as chain_warp / chain_bin_warp.
 template <typename RankT, int G>
 __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint32_t e,
-                             const Payload* pay, const RankSrc<RankT> rk_c, double W,
+                             const Payload* pay, const RankT* __restrict__ rk_c, double W,
                              double S, double& best_gain, uint32_t& best_pos, double* st) {
   const unsigned lane = lane_id();
   double sl = 0.0, bg = -INFINITY;
@@ -423,7 +410,7 @@ __device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint
 // ---- split chain over a sorted list, one lane (small nodes) -----------------------
 template <typename RankT>
 __device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
-                           const Payload* pay, const RankSrc<RankT> rk_c,
+                           const Payload* pay, const RankT* __restrict__ rk_c,
                            double W, double S, double& best_gain, uint32_t& best_pos) {
   double sl = 0.0, bg = -INFINITY;
   uint32_t wl = 0, prev = 0, bp = 0xffffffffu;
@@ -470,7 +457,7 @@ __device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
 // rows, and sl there is their sequential sum in row (= payload) order --------------
 template <typename RankT, int G>
 __device__ void chain_bin_warp(const Payload* pay, uint32_t b, uint32_t e,
-                               const RankSrc<RankT> rk_c, double W, double S,
+                               const RankT* __restrict__ rk_c, double W, double S,
                                double& best_gain, uint32_t& best_pos, double* st) {
   const unsigned lane = lane_id();
   double s0 = 0.0;
@@ -517,7 +504,7 @@ __device__ void chain_bin_warp(const Payload* pay, uint32_t b, uint32_t e,
 
 template <typename RankT>
 __device__ void chain_bin_lane(const Payload* pay, uint32_t b, uint32_t e,
-                               const RankSrc<RankT> rk_c, double W, double S,
+                               const RankT* __restrict__ rk_c, double W, double S,
                                double& best_gain, uint32_t& best_pos) {
   double s0 = 0.0;
   uint32_t w0 = 0, n0 = 0;
@@ -561,7 +548,7 @@ __device__ void chain_bin_lane(const Payload* pay, uint32_t b, uint32_t e,
 template <typename RankT, int G, int U>
 __device__ __forceinline__ void chain_grp(bool active, bool listed, const uint32_t* list,
                                           uint32_t b, uint32_t e, const Payload* pay,
-                                          const RankSrc<RankT> rk_c, double W, double S,
+                                          const RankT* __restrict__ rk_c, double W, double S,
                                           double& best_gain, uint32_t& best_pos, double* st) {
   static_assert(U % 4 == 0, "U must be a multiple of 4 (uint4 list loads)");
   constexpr uint32_t R = G * U;  // positions per round
@@ -737,7 +724,7 @@ struct RouteOut {
 template <typename RankT, int G>
 __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
                            const Payload* pay, const double* wyy,
-                           const RankSrc<RankT> rk_f, uint32_t thr_rank, uint32_t* bits,
+                           const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                            RouteOut& o, double* st) {
   const unsigned lane = lane_id();
   for (uint32_t k0 = b; k0 < e; k0 += 32 * G) {
@@ -795,7 +782,7 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
 template <typename RankT, int G>
 __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
                              const Payload* pay, const double* wyy,
-                             const RankSrc<RankT> rk_f, uint32_t thr_rank, uint32_t* bits,
+                             const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                              RouteOut& o, double* st /* 4*32 doubles */) {
   const unsigned lane = lane_id(), grp = lane >> 3;
   double acc = 0.0;  // this lane's group chain: 0 sl, 1 ql, 2 sr, 3 qr
@@ -897,7 +884,7 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
 template <typename RankT>
 __device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
                            const Payload* pay, const double* wyy,
-                           const RankSrc<RankT> rk_f, uint32_t thr_rank, uint32_t* bits,
+                           const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                            RouteOut& o) {
   for (uint32_t k = b; k < e; k += 4) {
     uint32_t q[4], row[4], mu[4];
@@ -938,8 +925,8 @@ __device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
 template <typename RankT, int G>
 __device__ void route_groups_warp(const Payload* pay,
                                   const double* wyy, uint32_t b, uint32_t e,
-                                  const RankSrc<RankT> rk0, uint32_t k0levels,
-                                  const RankSrc<RankT> rk_f, uint32_t thr_rank,
+                                  const RankT* __restrict__ rk0, uint32_t k0levels,
+                                  const RankT* __restrict__ rk_f, uint32_t thr_rank,
                                   uint32_t* bits, RouteOut& o, double* st) {
   const unsigned lane = lane_id();
   for (uint32_t grp = 0; grp < k0levels; ++grp) {
@@ -969,8 +956,8 @@ __device__ void route_groups_warp(const Payload* pay,
 template <typename RankT>
 __device__ void route_groups_lane(const Payload* pay,
                                   const double* wyy, uint32_t b, uint32_t e,
-                                  const RankSrc<RankT> rk0, uint32_t k0levels,
-                                  const RankSrc<RankT> rk_f, uint32_t thr_rank,
+                                  const RankT* __restrict__ rk0, uint32_t k0levels,
+                                  const RankT* __restrict__ rk_f, uint32_t thr_rank,
                                   uint32_t* bits, RouteOut& o) {
   for (uint32_t grp = 0; grp < k0levels; ++grp) {
     for (uint32_t k = b; k < e; ++k) {
@@ -1287,7 +1274,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         if (nw.e - nw.b < kLaneMax) continue;
         const uint32_t c = samp[k];
         const int32_t li = d.list_of[c];
-        const RankSrc<RankT> rk_c{rank + static_cast<size_t>(c) * n, nullptr};
+        const RankT* rk_c = rank + static_cast<size_t>(c) * n;
         double bg;
         uint32_t bp;
         if (li >= 0)
@@ -1303,7 +1290,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         if (nw.e - nw.b >= kLaneMax) continue;
         const uint32_t c = samp[k];
         const int32_t li = d.list_of[c];
-        const RankSrc<RankT> rk_c{rank + static_cast<size_t>(c) * n, nullptr};
+        const RankT* rk_c = rank + static_cast<size_t>(c) * n;
         double bg;
         uint32_t bp;
         if (li >= 0)
@@ -1417,7 +1404,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       {
         const uint32_t* l0 = list0 >= 0 ? lists[cur] + static_cast<size_t>(list0) * stride
                                         : nullptr;
-        const RankSrc<RankT> rk0{rank, nullptr};  // column 0
+        const RankT* rk0 = rank;  // column 0
         for (int pass = 0; pass < 2; ++pass) {
           // pass 0: warps take large nodes; pass 1: lanes take small ones
           const uint32_t step = pass == 0 ? NW : NT;
@@ -1425,7 +1412,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
             const SplitInfo si = spl[s];
             if ((pass == 0) != (si.cnt >= kLaneMax)) continue;
             const NodeWork nw = fr[si.f];
-            const RankSrc<RankT> rk_f{rank + static_cast<size_t>(si.c) * n, nullptr};
+            const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
             RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
             if (pass == 0) {
               if (l0)
@@ -1695,8 +1682,6 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_e2f = take(emax * 4);
   L.off_ecls = take(emax * 4);
   L.off_wsplit = take(emax * 4);
-  L.off_lsplit = take(emax * 4);
-  L.off_lsplit2 = take(emax * 4);
   L.off_samp = take(emax * mtry * 2);
   L.off_res = take(emax * mtry * sizeof(ChainRes));
   L.off_split = take(emax * sizeof(SplitInfo));

@@ -36,18 +36,12 @@ struct SplitInfo {
   uint32_t pad0, pad1;
 };
 
-// per segment (frontier node) partition offsets; offL == INT32_MIN => leaf (drop).
-// (loffL, loffR): the sorted lists' destinations (wide grower) -- they differ from the
-// payload's when some segments keep no lists (local nodes): loffL == INT32_MIN => the
-// segment's list entries are not read at all, kNoWrite => that child keeps no lists.
+// per segment (frontier node) partition offsets; offL == INT32_MIN => leaf (drop)
 struct SegTab {
   int32_t offL, offR;
   uint32_t child;  // next-frontier index of the left child
   uint32_t pad;
-  int32_t loffL, loffR;
-  uint32_t pad1, pad2;
 };
-constexpr int32_t kNoWrite = INT32_MIN + 1;
 
 // Device view of a PreparedDataset (forest.hpp:134-161): column store, responses,
 // per-column (value,row) argsort, dense value ranks and the distinct values.
@@ -69,24 +63,6 @@ struct DevData {
   const uint64_t* vals_off; // p+1
   const int32_t* list_of;   // p: list slot of column c, or -1
   const uint32_t* listed;   // nlisted: column of list slot i
-  // row-major row records for the wide grower's local (small-node) kernels: per row the
-  // u16 rank of every listed column (slot order), then a bitmask of the two-level
-  // columns' 0/1 ranks at byte rec_bits; rec_stride == 0: no records (u32 ranks)
-  const uint8_t* rec;
-  uint32_t rec_stride, rec_bits;
-  const int32_t* bin_of;    // p: index of a two-level column (record bit, bit column), or -1
-  // two-level columns' 0/1 ranks as bit columns (1 bit per row, bitcol_words per
-  // column): a chain over such a column reads 32 rows per word from L2 instead of one
-  // 2-byte rank per 32-byte sector
-  const uint32_t* bitcols;
-  uint32_t bitcol_words;
-};
-
-// rank source of one column: dense ranks, or (two-level column) its bit column
-template <typename RankT>
-struct RankSrc {
-  const RankT* rk;
-  const uint32_t* bits;  // null: use rk
 };
 
 struct SlotLayout {
@@ -97,7 +73,7 @@ struct SlotLayout {
   size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
       off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
-      off_ecls, off_wsplit, off_lsplit, off_lsplit2;
+      off_ecls, off_wsplit;
   size_t bytes;
 };
 
@@ -139,9 +115,6 @@ struct TreeState {
   uint32_t nodes, done, totL, A_next;
   uint32_t E0, E1, E2;  // eligible nodes by size class: small (lane chains), mid (lane
                         // groups), big (warp per chain)
-  uint32_t E3, E4;      // eligible local nodes (< local_max rows: no lists, w_local):
-                        // up to kLocalSmall rows / larger
-  uint32_t Slocal, SlocalB;  // split nodes routed by w_local_route (same two classes)
   uint32_t Sbig;        // split nodes routed by a CTA (column 0 listed, >= coop_min rows)
   uint32_t Swarp;       // split nodes routed by a warp (the rest of those >= kLaneMax rows)
   unsigned long long elig_base, split_rows;
@@ -157,10 +130,7 @@ struct WideArgs {
   uint32_t coop_min; // split nodes with >= coop_min rows are routed by one CTA each
   uint32_t pair_big; // lanes per chain for big nodes: 32 (warp), 16 or 8 (lane groups)
   uint32_t lane_max; // nodes below this many rows run one lane per chain
-  uint32_t local_max;  // nodes below this many rows keep no lists (0: off)
-  uint32_t write_off2; // w_pay expands per-position offsets (the global-bitmap list pass)
-  uint32_t* off[7];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp
-                     // routes, small / large local nodes (level) or local splits (route)
+  uint32_t* off[5];  // [B+1] prefixes: chain tasks, splits, positions, list chunks, warp routes
   uint32_t* active;  // trees still splitting after this level's decide
   uint32_t* task_ctr;  // dynamic task counters of this level's chain kernels (zeroed by w_prefix)
 };

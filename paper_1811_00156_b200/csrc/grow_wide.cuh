@@ -10,18 +10,6 @@
 // longer idles the rest of its CTA: other trees' tasks fill the SMs.
 #pragma once
 
-// resident 256-thread CTAs per SM the chain / route kernels are compiled for (register
-// budget 64K / (256 * minb)); measured in tools/prof_minb.sh
-#ifndef AIWC_CHAIN_MINB
-#define AIWC_CHAIN_MINB 1
-#endif
-#ifndef AIWC_GRP_MINB
-#define AIWC_GRP_MINB 1
-#endif
-#ifndef AIWC_ROUTE_MINB
-#define AIWC_ROUTE_MINB 1
-#endif
-
 namespace aiwc_b200 {
 
 // Pointers of slot b for the current level (cur) and the next one (suffix _n).  The
@@ -38,8 +26,6 @@ struct SlotPtrs {
   uint32_t* e2f;
   uint32_t* ecls;
   uint32_t* wsplit;
-  uint32_t* lsplit;   // local splits up to kLocalSmall rows
-  uint32_t* lsplit2;  // larger local splits
   uint16_t* samp;
   ChainRes* res;
   SplitInfo* spl;
@@ -74,8 +60,6 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.e2f = reinterpret_cast<uint32_t*>(s + L.off_e2f);
   p.ecls = reinterpret_cast<uint32_t*>(s + L.off_ecls);
   p.wsplit = reinterpret_cast<uint32_t*>(s + L.off_wsplit);
-  p.lsplit = reinterpret_cast<uint32_t*>(s + L.off_lsplit);
-  p.lsplit2 = reinterpret_cast<uint32_t*>(s + L.off_lsplit2);
   p.samp = reinterpret_cast<uint16_t*>(s + L.off_samp);
   p.res = reinterpret_cast<ChainRes*>(s + L.off_res);
   p.spl = reinterpret_cast<SplitInfo*>(s + L.off_split);
@@ -364,7 +348,6 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       else
         el = 1;
       P.segtab[f].offL = INT_MIN;
-      P.segtab[f].loffL = INT_MIN;
     }
     uint32_t tot;
     const uint32_t ex = block_excl_scan<NT>(el, sh, &tot);
@@ -391,11 +374,10 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       }
     for (uint32_t i = 0; i < m; ++i) P.samp[static_cast<size_t>(e) * m + i] = pool[i];
   }
-  // eligible nodes by size class, BFS order inside each: [0, E0) small (< lane_max
-  // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain), then
-  // local (< local_max rows: no lists, w_local)
-  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0, E3 = 0, E4 = 0;
-  for (uint32_t cls = 0; cls < 5; ++cls) {
+  // eligible nodes by size class, BFS order inside each: [0, E0) small (< kLaneMax
+  // rows: lane per chain), [E0, E0+E1) mid (lane groups), then big (warp per chain)
+  uint32_t base = 0, E0 = 0, E1 = 0, E2 = 0;
+  for (uint32_t cls = 0; cls < 3; ++cls) {
     carry = 0;
     for (uint32_t b0 = 0; b0 < E; b0 += NT) {
       const uint32_t e = b0 + threadIdx.x;
@@ -403,8 +385,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
       if (e < E) {
         const NodeWork& nw = fr[P.e2f[e]];
         const uint32_t R = nw.e - nw.b;
-        const uint32_t c = R < a.local_max ? (R <= kLocalSmallRows ? 3u : 4u)
-                                           : (R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u));
+        const uint32_t c = R < a.lane_max ? 0u : (R < a.big_min ? 1u : 2u);
         in = c == cls;
       }
       uint32_t tot;
@@ -415,8 +396,6 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     if (cls == 0) E0 = carry;
     if (cls == 1) E1 = carry;
     if (cls == 2) E2 = carry;
-    if (cls == 3) E3 = carry;
-    if (cls == 4) E4 = carry;
     base += carry;
   }
   for (uint32_t w = threadIdx.x; w < (A + 31u) / 32u; w += NT) P.bits[w] = 0u;
@@ -425,8 +404,6 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
     s.E0 = E0;
     s.E1 = E1;
     s.E2 = E2;
-    s.E3 = E3;
-    s.E4 = E4;
   }
 }
 
@@ -437,10 +414,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
-  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0, c6 = 0;
+  uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0;
   for (uint32_t base = 0; base < a.B; base += NT) {
     const uint32_t b = base + threadIdx.x;
-    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0, v6 = 0;
+    uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0;
     if (b < a.B && !a.ts[b].done) {
       const TreeState& s = a.ts[b];
       if (which == 0) {  // chain tasks: lane (small), group (mid), warp (big)
@@ -448,16 +425,12 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
         v0 = s.E0 * m;
         v1 = s.E1 * grp_tpn(m, a.g.mtry);
         v2 = s.E2 * m;
-        v5 = s.E3;
-        v6 = s.E4;
       } else {
         v0 = s.Sbig;
         v1 = s.S;
         v2 = s.A;
         v3 = nchunks_of(s.A, a.g.d.nlisted);
         v4 = s.Swarp;
-        v5 = s.Slocal;
-        v6 = s.SlocalB;
       }
     }
     uint32_t t0, t1, t2, t3;
@@ -465,35 +438,27 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
     const uint32_t e1 = block_excl_scan<NT>(v1, sh, &t1);
     const uint32_t e2 = block_excl_scan<NT>(v2, sh, &t2);
     const uint32_t e3 = block_excl_scan<NT>(v3, sh, &t3);
-    uint32_t t4, t5, t6;
+    uint32_t t4;
     const uint32_t e4 = block_excl_scan<NT>(v4, sh, &t4);
-    const uint32_t e5 = block_excl_scan<NT>(v5, sh, &t5);
-    const uint32_t e6 = block_excl_scan<NT>(v6, sh, &t6);
     if (b < a.B) {
       a.off[0][b] = c0 + e0;
       a.off[1][b] = c1 + e1;
       a.off[2][b] = c2 + e2;
       a.off[3][b] = c3 + e3;
       if (which == 1) a.off[4][b] = c4 + e4;
-      a.off[5][b] = c5 + e5;
-      a.off[6][b] = c6 + e6;
     }
     c0 += t0;
     c1 += t1;
     c2 += t2;
     c3 += t3;
     c4 += t4;
-    c5 += t5;
-    c6 += t6;
   }
   if (threadIdx.x == 0) {
     if (which == 1) {
       a.off[4][a.B] = c4;
-      a.task_ctr[2] = a.task_ctr[5] = a.task_ctr[7] = 0u;
+      a.task_ctr[2] = 0u;
     }
-    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = a.task_ctr[4] = a.task_ctr[6] = 0u;
-    a.off[5][a.B] = c5;
-    a.off[6][a.B] = c6;
+    if (which == 0) a.task_ctr[0] = a.task_ctr[1] = a.task_ctr[3] = 0u;
     a.off[0][a.B] = c0;
     a.off[1][a.B] = c1;
     a.off[2][a.B] = c2;
@@ -505,7 +470,7 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 // big nodes (>= big_min rows) run one warp per (node, column) ...
 constexpr int kBigU = 4;
 template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
-__global__ void __launch_bounds__(256, AIWC_CHAIN_MINB) w_chains_warp(const WideArgs a) {
+__global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
   constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
   __shared__ double stage[8][GB == 32 ? 64 : 32 * UB];
   const uint32_t total = a.off[2][a.B];
@@ -537,14 +502,14 @@ __global__ void __launch_bounds__(256, AIWC_CHAIN_MINB) w_chains_warp(const Wide
       uint32_t bp;
       chain_grp<RankT, (GB < 32 ? GB : 16), UB>(
           act, li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride, nw_.b,
-          nw_.e, P.pay, rank_src<RankT>(a.g.d, c, true), nw_.w, nw_.s, bg, bp,
+          nw_.e, P.pay, rank + static_cast<size_t>(c) * n, nw_.w, nw_.s, bg, bp,
           stage[warp_id()] + grp * UB * GB);
       if (act && (lane_id() % GB) == 0) P.res[e * m + jj] = ChainRes{bg, bp, 0u};
       continue;
     }
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
-    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     double bg;
     uint32_t bp;
     chain_warp_p<RankT, 2>(li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride,
@@ -608,7 +573,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
     const int32_t li = a.g.d.list_of[c];
     const bool listed = li >= 0;
     const uint32_t* list = P.lists + static_cast<size_t>(listed ? li : 0) * stride;
-    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     const uint32_t R = nw.e - nw.b, nblk = (R + kCB - 1) / kCB;
     // producers: a register pipeline over blocks -- at step i a producer lane writes
     // block i+1 (ranks gathered at step i-1) into its stage, gathers the ranks of block
@@ -799,7 +764,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
 // ... mid nodes run one warp per node (or per group of 32/G of its columns), G lanes
 // per column (chain_grp) ...
 template <typename RankT, int G, int U>
-__global__ void __launch_bounds__(256, AIWC_GRP_MINB) w_chains_grp(const WideArgs a) {
+__global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
   __shared__ double stage[8][32 * U];
   const uint32_t total = a.off[1][a.B];
   const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
@@ -820,7 +785,7 @@ __global__ void __launch_bounds__(256, AIWC_GRP_MINB) w_chains_grp(const WideArg
     const NodeWork nw_ = P.front[P.e2f[e]];
     const uint32_t c = act ? P.samp[e * m + j] : 0u;
     const int32_t li = a.g.d.list_of[c];
-    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     const uint32_t* list = P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride;
     double bg;
     uint32_t bp;
@@ -845,7 +810,7 @@ __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
     const NodeWork nw_ = P.front[P.e2f[e]];
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
-    const RankSrc<RankT> rk_c = rank_src<RankT>(a.g.d, c, true);
+    const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     double bg;
     uint32_t bp;
     if (li >= 0)
@@ -872,7 +837,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
   const NodeWork* fr = P.front;
   const uint32_t E = st.E, nodes0 = st.nodes;
   const bool coop_route = d.list_of[0] >= 0;
-  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0, lcarry = 0, l2carry = 0;
+  uint32_t carry = 0, ccarry = 0, bcarry = 0, wcarry = 0;
   for (uint32_t base = 0; base < E; base += NT) {
     const uint32_t e = base + threadIdx.x;
     uint32_t sp = 0, c = 0, thr_rank = 0;
@@ -881,14 +846,13 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     if (e < E) {
       nw = fr[P.e2f[e]];
       double bg = -INFINITY;
-      uint32_t bi = 0, bp = 0, bx = 0;
+      uint32_t bi = 0, bp = 0;
       for (uint32_t i = 0; i < m; ++i) {
         const ChainRes r = P.res[static_cast<size_t>(e) * m + i];
         if (r.gain > bg) {
           bg = r.gain;
           bi = i;
           bp = r.pos;
-          bx = r.pad;
         }
       }
       if (bg == -INFINITY) {
@@ -901,16 +865,9 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
         double prev, v;
         uint32_t lo, hi;
         if (li >= 0) {
-          // rows either side of the boundary: from the list, or (local node) given
-          uint32_t r1, r0;
-          if (bx & 0x80000000u) {
-            r1 = bx & 0x7fffffffu;
-            r0 = bp;
-          } else {
-            const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
-            r1 = P.pay[lc[bp - 1]].row;
-            r0 = P.pay[lc[bp]].row;
-          }
+          const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
+          const uint32_t r1 = P.pay[lc[bp - 1]].row;
+          const uint32_t r0 = P.pay[lc[bp]].row;
           prev = d.col[static_cast<size_t>(c) * n + r1];
           v = d.col[static_cast<size_t>(c) * n + r0];
           lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
@@ -937,21 +894,12 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     const uint32_t cex = block_excl_scan<NT>(cnt, sh, &ctot);
     // splits routed by a whole CTA (w_route_coop), compacted into ecls (free after the
     // chain kernels)
-    const uint32_t loc = sp && cnt < a.local_max ? 1u : 0u;  // w_local_route
-    const uint32_t locA = loc && cnt <= kLocalSmallRows ? 1u : 0u, locB = loc - locA;
-    uint32_t ltot, l2tot;
-    const uint32_t lex = block_excl_scan<NT>(locA, sh, &ltot);
-    const uint32_t l2ex = block_excl_scan<NT>(locB, sh, &l2tot);
-    if (locA) P.lsplit[lcarry + lex] = carry + ex;
-    if (locB) P.lsplit2[l2carry + l2ex] = carry + ex;
-    lcarry += ltot;
-    l2carry += l2tot;
-    const uint32_t big = sp && !loc && coop_route && cnt >= a.coop_min ? 1u : 0u;
+    const uint32_t big = sp && coop_route && cnt >= a.coop_min ? 1u : 0u;
     uint32_t btot;
     const uint32_t bex = block_excl_scan<NT>(big, sh, &btot);
     if (big) P.ecls[bcarry + bex] = carry + ex;
     bcarry += btot;
-    const uint32_t wsp = sp && !big && !loc && cnt >= kLaneMax ? 1u : 0u;  // warp-routed splits
+    const uint32_t wsp = sp && !big && cnt >= kLaneMax ? 1u : 0u;  // warp-routed splits
     uint32_t wtot;
     const uint32_t wex = block_excl_scan<NT>(wsp, sh, &wtot);
     if (wsp) P.wsplit[wcarry + wex] = carry + ex;
@@ -981,8 +929,6 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
     st.S = carry;
     st.Sbig = bcarry;
     st.Swarp = wcarry;
-    st.Slocal = lcarry;
-    st.SlocalB = l2carry;
     st.A_next = ccarry;
     st.split_rows += ccarry;
     st.elig_base += E;
@@ -1000,7 +946,7 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
 
 // route in column-0 order (forest.hpp:323-352): warps take split nodes >= kLaneMax
 template <typename RankT, bool kWarp>
-__global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a) {
+__global__ void __launch_bounds__(256) w_route(const WideArgs a) {
   __shared__ double stage[8][128];
   const uint32_t total = a.off[1][a.B];
   const uint32_t n = static_cast<uint32_t>(a.g.d.n), stride = a.g.L.stride;
@@ -1028,9 +974,9 @@ __global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a
     }
     const SlotPtrs P = slot_ptrs(a, b);
     const SplitInfo si = P.spl[s];
-    if (!kWarp && (si.cnt >= kLaneMax || si.cnt < a.local_max)) continue;
+    if (!kWarp && si.cnt >= kLaneMax) continue;
     const NodeWork nw = P.front[si.f];
-    const RankSrc<RankT> rk_f = rank_src<RankT>(a.g.d, si.c, true);
+    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
     const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
@@ -1038,14 +984,14 @@ __global__ void __launch_bounds__(256, AIWC_ROUTE_MINB) w_route(const WideArgs a
         route_warp_p<RankT, 2>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
                                P.bits, o, stage[warp_id()]);
       else
-        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank_src<RankT>(a.g.d, 0, true), k0levels,
+        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels,
                                     rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
       if (lane_id() != 0) continue;
     } else {
       if (l0)
         route_lane<RankT>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank, P.bits, o);
       else
-        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank_src<RankT>(a.g.d, 0, true), k0levels, rk_f,
+        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels, rk_f,
                                  si.thr_rank, P.bits, o);
     }
     P.spl[s].nl = o.nl;
@@ -1076,7 +1022,7 @@ __global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
     const uint32_t s = P.ecls[k];
     const SplitInfo si = P.spl[s];
     const NodeWork nw = P.front[si.f];
-    const RankSrc<RankT> rk_f = rank_src<RankT>(a.g.d, si.c, true);
+    const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
     const uint32_t* l0 = P.lists + static_cast<size_t>(list0) * stride;
     const uint32_t nblk = (nw.e - nw.b + kCoopBlock - 1) / kCoopBlock;
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;
@@ -1176,33 +1122,22 @@ __global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a, b);
   const NodeWork* fr = P.front;
   const uint32_t S = st.S, A = st.A;
-  // payload offsets count every split's left rows; list offsets only those of splits
-  // whose lists are read (local splits keep none)
-  uint32_t carry = 0, kcarry = 0;
+  uint32_t carry = 0;
   for (uint32_t base = 0; base < S; base += NT) {
     const uint32_t s = base + threadIdx.x;
-    SplitInfo si{};
-    if (s < S) si = P.spl[s];
-    const uint32_t nl = s < S ? si.nl : 0u;
-    const bool skip = s < S && si.cnt < a.local_max;
-    uint32_t tot, ktot;
+    const uint32_t nl = s < S ? P.spl[s].nl : 0u;
+    uint32_t tot;
     const uint32_t ex = block_excl_scan<NT>(nl, sh, &tot);
-    const uint32_t kex = block_excl_scan<NT>(skip ? 0u : nl, sh, &ktot);
     if (s < S) {
-      const int32_t bL = static_cast<int32_t>(carry + ex), bK = static_cast<int32_t>(kcarry + kex);
-      const int32_t bb = static_cast<int32_t>(fr[si.f].b), bs = static_cast<int32_t>(si.base);
-      const int32_t nli = static_cast<int32_t>(nl);
-      SegTab tb{bs - bL, bs + nli - bb + bL, 2 * s, 0u, bs - bK, bs + nli - bb + bK, 0u, 0u};
-      if (skip) {
-        tb.loffL = INT_MIN;
-      } else {
-        if (nl < a.local_max) tb.loffL = kNoWrite;            // left child is local
-        if (si.cnt - nl < a.local_max) tb.loffR = kNoWrite;   // right child is local
-      }
-      P.segtab[si.f] = tb;
+      const SplitInfo si = P.spl[s];
+      const uint32_t bL = carry + ex;
+      const uint32_t bb = fr[si.f].b;
+      P.segtab[si.f] = SegTab{static_cast<int32_t>(si.base) - static_cast<int32_t>(bL),
+                              static_cast<int32_t>(si.base + nl) - static_cast<int32_t>(bb) +
+                                  static_cast<int32_t>(bL),
+                              2 * s, 0u};
     }
     carry += tot;
-    kcarry += ktot;
   }
   if (threadIdx.x == 0) st.totL = carry;
   const uint32_t aw = (A + 31u) / 32u;
@@ -1225,7 +1160,7 @@ __global__ void w_pay(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t f = P.seg[k];
     const SegTab tb = P.segtab[f];
-    if (a.write_off2) P.off2[k] = make_int2(tb.offL, tb.offR);
+    P.off2[k] = make_int2(tb.offL, tb.offR);
     if (tb.offL == INT_MIN) continue;
     const bool l = get_bit(P.bits, k);
     const int32_t lp = static_cast<int32_t>(bits_before(P.bits, P.pref, k));
@@ -1237,128 +1172,7 @@ __global__ void w_pay(const WideArgs a) {
   }
 }
 
-// List pass with local nodes: one CTA per tree with the tree's goes-left bitmap + prefix
-// staged in shared memory and one warp per sorted list.  The CTA walks the positions in
-// steps of kLwStep; each step's per-position segment offsets (list destinations, payload
-// offsets) are staged once in shared memory for all lists, two steps ahead, and a warp
-// loads its list's entries of the next step while it scatters this one.  A warp covers
-// a step of its list as 8 sub-rows of 32 consecutive positions (lane i holds position
-// k0 + 32j + i), so the count of left-going entries before an entry is the list's
-// running carry plus ballot counts -- no count pass -- and each store instruction writes
-// at most two contiguous runs.  Entries of leaf segments and of local split nodes (no
-// lists) are neither read nor counted; entries whose child is local are counted but not
-// written.
-constexpr uint32_t kLwStep = 256;
-constexpr int kLwWarps = 28;  // warps per list-pass CTA
-
-__host__ __device__ inline size_t lw_smem_bytes(uint32_t stride, uint32_t nlisted) {
-  const size_t aw4 = ((stride + 31) / 32 + 3) / 4 * 4;
-  return aw4 * 8 + 3 * kLwStep * 16 + size_t{nlisted} * 4 + 16;
-}
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
-  extern __shared__ __align__(16) uint32_t sm[];
-  const uint32_t b = blockIdx.x;
-  const TreeState& st = a.ts[b];
-  if (st.done) return;
-  const SlotPtrs P = slot_ptrs(a, b);
-  const uint32_t A = st.A, aw = (A + 31u) / 32u;
-  const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
-  const uint32_t aw4 = ((stride + 31u) / 32u + 3u) / 4u * 4u;
-  uint32_t* sbits = sm;
-  uint32_t* spref = sm + aw4;
-  int4* s_t = reinterpret_cast<int4*>(sm + 2 * aw4);  // [3][kLwStep]
-  uint32_t* s_carry = reinterpret_cast<uint32_t*>(s_t + 3 * kLwStep);
-  {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
-    const uint32_t n4 = (aw + 3u) / 4u;
-    const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
-    const uint4* gp = reinterpret_cast<const uint4*>(P.pref);
-    for (uint32_t w = threadIdx.x; w < n4; w += blockDim.x) {
-      reinterpret_cast<uint4*>(sbits)[w] = gb[w];
-      reinterpret_cast<uint4*>(spref)[w] = gp[w];
-    }
-    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) s_carry[li] = 0u;
-  }
-  auto stage = [&](uint32_t k0, int4* dst) {
-    const uint32_t ke = min(A, k0 + kLwStep);
-    for (uint32_t k = k0 + threadIdx.x; k < ke; k += blockDim.x) {
-      const SegTab tb = P.segtab[P.seg[k]];
-      dst[k - k0] = make_int4(tb.loffL, tb.loffR, tb.offL, tb.offR);
-    }
-  };
-  const unsigned lane = lane_id(), lt = lanemask_lt();
-  // entries of read segments only
-  auto load8 = [&](uint32_t k0, const int4* tb, const uint32_t* src, uint32_t (&q)[8]) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t k = k0 + 32u * j + lane;
-      q[j] = (k < A && tb[32u * j + lane].x != INT_MIN) ? src[k] : 0u;
-    }
-  };
-  auto scatter = [&](uint32_t k0, const int4* tb, const uint32_t (&q)[8], uint32_t* dstl,
-                     uint32_t& carry) {
-    uint32_t wv[8], pv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      wv[j] = sbits[q[j] >> 5];
-      pv[j] = spref[q[j] >> 5];
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t k = k0 + 32u * j + lane;
-      const int4 t = k < A ? tb[32u * j + lane] : make_int4(INT_MIN, 0, 0, 0);
-      const bool keep = t.x != INT_MIN;
-      const uint32_t qq = q[j];
-      const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
-      const bool l = keep && bit;
-      const unsigned bl = __ballot_sync(kFull, l);
-      const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
-      const int32_t off = l ? t.x : t.y;
-      if (keep && off != kNoWrite) {
-        const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
-        const uint32_t nq = static_cast<uint32_t>(l ? t.z + lq : t.w + static_cast<int32_t>(qq) - lq);
-        const uint32_t dst = static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(k) - pl);
-        dstl[dst] = nq;
-      }
-      carry += __popc(bl);
-    }
-  };
-  stage(0, s_t);
-  if (kLwStep < A) stage(kLwStep, s_t + kLwStep);
-  __syncthreads();
-  const uint32_t nwarps = blockDim.x >> 5, w0 = warp_id();
-  const bool single = nl <= nwarps;  // one list per warp: pipelined entry loads
-  const uint32_t* src0 = P.lists + static_cast<size_t>(w0) * stride;
-  uint32_t* dst0 = P.lists_n + static_cast<size_t>(w0) * stride;
-  uint32_t qc[8], carry0 = 0;
-  if (single && w0 < nl) load8(0, s_t, src0, qc);
-  uint32_t it = 0;
-  for (uint32_t k0 = 0; k0 < A; k0 += kLwStep, ++it) {
-    const int4* cur = s_t + (it % 3u) * kLwStep;
-    const int4* nxt = s_t + ((it + 1u) % 3u) * kLwStep;
-    if (single) {
-      uint32_t qn[8];
-      if (w0 < nl && k0 + kLwStep < A) load8(k0 + kLwStep, nxt, src0, qn);
-      if (k0 + 2 * kLwStep < A) stage(k0 + 2 * kLwStep, s_t + ((it + 2u) % 3u) * kLwStep);
-      if (w0 < nl) scatter(k0, cur, qc, dst0, carry0);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) qc[j] = qn[j];
-    } else {
-      if (k0 + 2 * kLwStep < A) stage(k0 + 2 * kLwStep, s_t + ((it + 2u) % 3u) * kLwStep);
-      for (uint32_t li = w0; li < nl; li += nwarps) {
-        uint32_t q[8];
-        load8(k0, cur, P.lists + static_cast<size_t>(li) * stride, q);
-        uint32_t carry = s_carry[li];  // left-going entries of this list before the step
-        scatter(k0, cur, q, P.lists_n + static_cast<size_t>(li) * stride, carry);
-        if (lane == 0) s_carry[li] = carry;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// List pass without local nodes (the default): single read, one CTA per tree with the tree's goes-left bitmap + prefix
+// List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
 // staged in shared memory and one warp per sorted list.  A warp walks its list in
 // position order, 256 positions per step as 8 sub-rows of 32 consecutive positions
 // (lane i holds position k0 + 32j + i of sub-row j), so the count of left-going entries
@@ -1366,7 +1180,9 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
 // and each sub-row's left (right) entries land on consecutive destinations: every
 // store instruction writes at most two contiguous runs.  The next step's entries and
 // segment offsets are loaded before this step is scattered.
-struct LwStage {  // one warp step: 8 sub-rows' entries + offsets
+constexpr uint32_t kLwStep = 256;
+constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
+struct LwStage {
   uint32_t q[8];
   int2 t[8];
 };
@@ -1386,7 +1202,7 @@ __device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, con
 }
 
 template <int NW>
-__global__ void __launch_bounds__(NW * 32) w_lwarp_off2(const WideArgs a) {
+__global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   extern __shared__ uint32_t sm[];
   const uint32_t b = blockIdx.x;
   const TreeState& st = a.ts[b];
@@ -1572,8 +1388,6 @@ __global__ void w_oob(const WideArgs a) {
   }
 }
 
-#include "grow_local.cuh"
-
 // ---- host driver for one batch of trees [t0, t0+B) (local indices) ----------------
 template <typename RankT>
 cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
@@ -1582,41 +1396,18 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   const dim3 rowsgrid((n + 1023) / 1024, a.B);
   const unsigned wgrid = static_cast<unsigned>(sms) * 8;  // persistent grid-stride kernels
   // per-tree list pass with the bitmap + prefix in shared memory when they fit
-  size_t lw_smem = lw_smem_bytes(a.g.L.stride, a.g.d.nlisted);
-  const size_t lw_smem_off2 = ((a.g.L.stride + 31) / 32 + 3) / 4 * 4 * 8;
+  size_t lw_smem = ((a.g.L.stride + 31) / 32 + 3) / 4 * 4 * 8;
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (lw_smem + 1024 > static_cast<size_t>(optin) || std::getenv("AIWC_LW_GLOBAL") ||
         cudaFuncSetAttribute(w_lwarp<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(lw_smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(w_lwarp_off2<kLwWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(lw_smem_off2)) != cudaSuccess)
+                             static_cast<int>(lw_smem)) != cudaSuccess)
       lw_smem = 0;
     cudaGetLastError();
   }
   const int lw_warps = static_cast<int>(std::min<uint32_t>(kLwWarps, std::max<uint32_t>(1u, a.g.d.nlisted)));
-  // local (list-free) small nodes: need the row records and the shared-memory list pass
-  using LayA = LocalLayout<64, int(kLocalSmall), false>;
-  using LayB = LocalLayout<256, int(kLocalMaxRows), false>;
-  using RLayA = LocalLayout<64, int(kLocalSmall), true>;
-  using RLayB = LocalLayout<256, int(kLocalMaxRows), true>;
-  if (!lw_smem || a.g.d.rec_stride == 0 || sizeof(RankT) != 2) a.local_max = 0;
-  a.local_max = std::min(a.local_max, kLocalMaxRows);
-  // per-position offsets for the list passes without local nodes (w_lwarp_off2 and the
-  // global-bitmap fallback); with local nodes w_lwarp stages per-segment offsets itself
-  a.write_off2 = a.local_max ? 0u : 1u;
-  if (a.local_max > kLocalSmall &&
-      (cudaFuncSetAttribute(w_local<256, int(kLocalMaxRows)>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(LayB::bytes)) != cudaSuccess ||
-       cudaFuncSetAttribute(w_local_route<256, int(kLocalMaxRows)>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(RLayB::bytes)) != cudaSuccess)) {
-    cudaGetLastError();
-    a.local_max = std::min(a.local_max, kLocalSmall);
-  }
-  // every node of every tree is local: no sorted lists at all
-  const bool lists = a.g.d.nlisted && a.g.L.stride >= a.local_max;
 #define WCK(x)                              \
   do {                                      \
     x;                                      \
@@ -1628,7 +1419,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   WCK((w_boot<<<rowsgrid, 256, 0, st>>>(a)));
   WCK((w_bits<1024><<<a.B, 1024, 0, st>>>(a)));
   WCK((w_payload<<<rowsgrid, 256, 0, st>>>(a)));
-  if (lists) {
+  if (a.g.d.nlisted) {
     WCK((w_l0count<<<wgrid, 256, 0, st>>>(a)));
     WCK((w_chunkscan<1024><<<a.B, 1024, 0, st>>>(a, 0)));
     WCK((w_l0scatter<<<wgrid, 256, 0, st>>>(a)));
@@ -1654,12 +1445,6 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       default: WCK((w_chains_grp<RankT, 1, 4><<<wgrid, 256, 0, st>>>(a))); break;
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
-    if (a.local_max) {
-      WCK((w_local<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, LayA::bytes, st>>>(a, 0u, 4u)));
-      if (a.local_max > kLocalSmall)
-        WCK((w_local<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, LayB::bytes, st>>>(
-            a, 1u, 6u)));
-    }
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
     cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
@@ -1670,20 +1455,11 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
-    if (a.local_max) {
-      WCK((w_local_route<64, int(kLocalSmall)><<<static_cast<unsigned>(sms) * 32, 64, RLayA::bytes, st>>>(
-          a, 0u, 5u)));
-      if (a.local_max > kLocalSmall)
-        WCK((w_local_route<256, int(kLocalMaxRows)><<<static_cast<unsigned>(sms) * 2, 256, RLayB::bytes,
-                                                       st>>>(a, 1u, 7u)));
-    }
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
-    if (lists) {
-      if (lw_smem && a.local_max) {
+    if (a.g.d.nlisted) {
+      if (lw_smem) {
         WCK((w_lwarp<kLwWarps><<<a.B, lw_warps * 32, lw_smem, st>>>(a)));
-      } else if (lw_smem) {
-        WCK((w_lwarp_off2<kLwWarps><<<a.B, lw_warps * 32, lw_smem_off2, st>>>(a)));
       } else {
         WCK((w_lcount<<<wgrid, 256, 0, st>>>(a)));
         WCK((w_chunkscan<512><<<a.B, 512, 0, st>>>(a, 1)));

@@ -5,8 +5,6 @@
 // cuBLAS).  -0.0 and +0.0 compare equal in the reference, so both map to one key; a
 // distinct value is stored as the first row's original value in sorted order, exactly
 // as the reference's `distinct.push_back(v[o[k]])`.
-#include <algorithm>
-
 #include <cub/cub.cuh>
 
 #include "forest_kernels.cuh"
@@ -70,76 +68,6 @@ __global__ void narrow_kernel(const uint32_t* __restrict__ in, uint64_t count,
   for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < count;
        i += uint64_t{gridDim.x} * blockDim.x)
     out[i] = static_cast<uint16_t>(in[i]);
-}
-
-// Row records of the wide grower's local kernels (DevData::rec): per row the u16 rank of
-// every listed column, then the 0/1 ranks of the two-level columns as a bitmask.  One
-// thread per (row, 32-bit record word): coalesced writes, column-major rank reads.
-__global__ void record_kernel(const uint16_t* __restrict__ rank, uint64_t n, uint32_t nlisted,
-                              const uint32_t* __restrict__ listed, uint32_t nbin,
-                              const uint32_t* __restrict__ bincols, uint32_t words,
-                              uint32_t bits_word, uint32_t* __restrict__ rec) {
-  const uint64_t total = n * words;
-  for (uint64_t x = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; x < total;
-       x += uint64_t{gridDim.x} * blockDim.x) {
-    const uint64_t r = x / words;
-    const uint32_t w = static_cast<uint32_t>(x - r * words);
-    uint32_t v = 0;
-    if (w < bits_word) {  // two u16 ranks
-      for (uint32_t h = 0; h < 2; ++h) {
-        const uint32_t li = 2 * w + h;
-        if (li < nlisted) v |= static_cast<uint32_t>(rank[size_t{listed[li]} * n + r]) << (16 * h);
-      }
-    } else {  // 32 two-level columns' bits
-      const uint32_t b0 = (w - bits_word) * 32;
-      for (uint32_t k = 0; k < 32 && b0 + k < nbin; ++k)
-        v |= (rank[size_t{bincols[b0 + k]} * n + r] != 0 ? 1u : 0u) << k;
-    }
-    rec[x] = v;
-  }
-}
-
-// Bit columns of the two-level columns (DevData::bitcols): word w of column bi holds
-// rows [32w, 32w+32), bit k set when row 32w+k has rank 1.
-__global__ void bitcol_kernel(const void* __restrict__ rank, int rank_bytes, uint64_t n,
-                              uint32_t nbin, const uint32_t* __restrict__ bincols,
-                              uint32_t words, uint32_t* __restrict__ out) {
-  const uint64_t total = uint64_t{nbin} * words;
-  for (uint64_t x = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; x < total;
-       x += uint64_t{gridDim.x} * blockDim.x) {
-    const uint32_t bi = static_cast<uint32_t>(x / words), w = static_cast<uint32_t>(x % words);
-    const size_t base = size_t{bincols[bi]} * n;
-    uint32_t v = 0;
-    for (uint32_t k = 0; k < 32; ++k) {
-      const uint64_t r = uint64_t{w} * 32 + k;
-      if (r >= n) break;
-      const uint32_t rk = rank_bytes == 2 ? static_cast<const uint16_t*>(rank)[base + r]
-                                          : static_cast<const uint32_t*>(rank)[base + r];
-      v |= (rk != 0 ? 1u : 0u) << k;
-    }
-    out[x] = v;
-  }
-}
-
-cudaError_t build_bitcols(const void* d_rank, int rank_bytes, uint64_t n, uint32_t nbin,
-                          const uint32_t* d_bincols, uint32_t words, uint32_t* d_out,
-                          cudaStream_t s) {
-  const uint64_t total = uint64_t{nbin} * words;
-  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148u * 64u));
-  if (total) bitcol_kernel<<<blocks, 256, 0, s>>>(d_rank, rank_bytes, n, nbin, d_bincols, words, d_out);
-  return cudaGetLastError();
-}
-
-cudaError_t build_records(const uint16_t* d_rank, uint64_t n, uint32_t nlisted,
-                          const uint32_t* d_listed, uint32_t nbin, const uint32_t* d_bincols,
-                          uint32_t stride_bytes, uint32_t bits_byte, uint8_t* d_rec,
-                          cudaStream_t s) {
-  const uint32_t words = stride_bytes / 4, bits_word = bits_byte / 4;
-  const uint64_t total = n * words;
-  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148u * 64u));
-  record_kernel<<<blocks, 256, 0, s>>>(d_rank, n, nlisted, d_listed, nbin, d_bincols, words,
-                                       bits_word, reinterpret_cast<uint32_t*>(d_rec));
-  return cudaGetLastError();
 }
 
 cudaError_t narrow_ranks(const uint32_t* d_in, uint64_t count, uint16_t* d_out, cudaStream_t s) {

@@ -453,44 +453,3 @@ def test_grid_cells_batched_equal_separate_fits(c1, seed):
         f = pkg.fit(prep, pkg.ForestParams(counts[-1], m, mns, seed), compute_oob_stats=False)
         want = [s.error_pct for s in pkg.oob_prefix(f, prep, counts)]
         assert list(got[i]) == want, (m, mns)
-
-
-@pytest.mark.parametrize("local_max", ["64", "300", "2048"])
-def test_wide_grower_local_mode(local_max, seed, golden, monkeypatch):
-    """The wide grower's opt-in local mode (AIWC_LOCAL_MAX: nodes below it keep no sorted
-    lists; shared-memory stable sorts by value rank rebuild the (value,row) order) stays
-    bit-exact: random tables mixing continuous / tied / two-level columns, the edge
-    tables, and C1."""
-    monkeypatch.setenv("AIWC_GROW_WIDE", "1")
-    monkeypatch.setenv("AIWC_LOCAL_MAX", local_max)
-    rng = np.random.default_rng(int(local_max))
-    for case, (p, m) in enumerate([(5, 3), (12, 8), (40, 33), (7, 7)]):
-        n = int(rng.integers(300, 3000))
-        kinds = rng.integers(0, 3, size=p)
-        col = np.empty((p, n))
-        for c in range(p):
-            col[c] = (rng.normal(size=n) if kinds[c] == 0 else
-                      rng.integers(0, 7 if kinds[c] == 1 else 2, size=n).astype(float))
-        col[0] = rng.integers(0, 400, size=n)  # > 256 distinct ranks: two radix passes
-        y = rng.normal(size=n)
-        prep = pkg.PreparedDataset(col, y, n, p)
-        f = pkg.fit(prep, pkg.ForestParams(6, m, int(rng.integers(1, 6)), seed))
-        mns = f.params.min_node_size
-        o = Oracle.fit(col, y, n, p, 6, m, mns, seed)
-        assert forests_equal(o, soa_of(f)) is None, (case, n, p, m, local_max)
-    for name in ("ties", "constcol", "wide", "step"):
-        z = np.load(os.path.join(GOLD, f"edge_{name}.npz"))
-        col, y = z["col"], z["y"]
-        p, n = col.shape
-        prm = golden["edges"][name]
-        f = pkg.fit(pkg.PreparedDataset(col, y, n, p),
-                    pkg.ForestParams(prm["T"], prm["mtry"], prm["mns"], seed))
-        g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"],
-                      z["value"], inbag=z["inbag"])
-        assert forests_equal(g, soa_of(f)) is None, name
-    t = pkg.Table()
-    f = pkg.fit(pkg.PreparedDataset.from_table(t), pkg.ForestParams(20, 6, 5, seed))
-    z = np.load(os.path.join(GOLD, "c1_t20_m6_n5.npz"))
-    g = ForestSoA(z["offsets"], z["feature"], z["threshold"], z["left"], z["right"], z["value"])
-    assert forests_equal(g, soa_of(f), check_inbag=False) is None
-    assert oob_list(f.oob) == list(z["oob"])
