@@ -197,8 +197,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--skip-predict", action="store_true")
     ap.add_argument("--skip-grid", action="store_true")
-    ap.add_argument("--gather-trees", type=int, default=100,
-                    help="trees per rank of the forest all-gathered over NCCL (N > 1)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="headline: weak = --trees-per-gpu trees on every GPU; strong = "
+                         "--trees-per-gpu trees in total split by tree range (N > 1 also "
+                         "measures the other mode and gathers the strong-mode forest)")
+    ap.add_argument("--strong-steps", type=int, default=3,
+                    help="timed steps of the secondary (non-headline) scaling mode at N > 1")
     ap.add_argument("--grid-cells", type=int, default=34)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-worker", action="store_true")
@@ -241,8 +245,15 @@ def main():
     import paper_1811_00156_b200 as pkg
 
     torch.cuda.set_device(local)
+    # AIWC_BENCH_BACKEND=gloo: the N > 1 code path on ONE GPU (ranks share cuda:0, host-
+    # staged collectives) -- a functional check only, its timings mean nothing
+    backend = os.environ.get("AIWC_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    cdev = "cuda" if backend == "nccl" else "cpu"  # where the small reductions live
 
     def barrier():
         if world > 1:
@@ -252,14 +263,14 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
         dist.all_reduce(t)
         return float(t.item())
 
@@ -276,56 +287,87 @@ def main():
     table = pkg.Table(C4_KERNELS, C4_DEVICES)
     prep = pkg.PreparedDataset.from_table(table, device=local)
     setup_s = time.perf_counter() - t_setup
-    per = args.trees_per_gpu
-    total_trees = per * world
     seed = pkg.derive_seed(1, "forest")
-    params = pkg.ForestParams(total_trees, C4_MTRY, C4_MNS, seed)
-    tb, te = rank * per, (rank + 1) * per
-
     from paper_1811_00156_b200 import shard
 
-    send, recv = shard.torch_transport(device=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    dsend, drecv = shard.torch_device_transport(host_staging=backend != "nccl")
 
-    def chained_oob(forest):
-        """Exact tree-ordered OOB over ranks: rank r continues rank r-1's per-row sums."""
-        res = shard.chained_oob(table.n, rank, world,
-                                lambda rs, rc: pkg.oob_accumulate(forest, prep, rs, rc),
-                                send, recv)
-        return None if res is None else pkg.oob_finalize(table.y, *res)
+    def measure(mode: str, steps: int, warmup: int, keep_last: bool = False):
+        """Timed C4 fits.  weak: rank r grows trees [T r, T (r+1)) of a T*N-tree forest;
+        strong: the T-tree forest split by tree_range.  OOB (forest.hpp:393-454) is part of
+        every step: one GPU finalises its own; N GPUs chain the per-row sums in tree order
+        over NCCL on the devices (shard.chained_oob_device)."""
+        T = args.trees_per_gpu
+        total = T * world if mode == "weak" else T
+        tb, te = (rank * T, (rank + 1) * T) if mode == "weak" else shard.tree_range(rank, world, T)
+        params = pkg.ForestParams(total, C4_MTRY, C4_MNS, seed)
 
-    def fit_step():
-        if world == 1:
-            f = pkg.fit(prep, params)
-            return f, f.oob
-        f = pkg.fit(prep, params, tb, te, compute_oob_stats=False)
-        return f, chained_oob(f)
+        def step():
+            if world == 1:
+                f = pkg.fit(prep, params)
+                return f, f.oob
+            f = pkg.fit(prep, params, tb, te, compute_oob_stats=False)
+            res = shard.chained_oob_device(
+                table.n, rank, world, dev,
+                lambda ps, pc: pkg.oob_accumulate_device(f, prep, ps, pc), dsend, drecv)
+            if res is None:
+                return f, None
+            rs, rc = res
+            return f, pkg.oob_finalize(table.y, rs.cpu().numpy(),
+                                       rc.cpu().numpy().view(np.uint32))
 
-    for _ in range(args.warmup):
-        f, _ = fit_step()
-        del f
-    barrier()
-    launches0 = pkg.launch_count()
-    stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    grow_ms, split_rows, grow_launch = 0.0, 0, 0
-    oob = None
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            f, o = fit_step()
-            prof = f.profile()
-            grow_ms += prof["grow_ms"]
-            split_rows += prof["split_rows"]
-            grow_launch += prof["grow_launches"]
-            oob = o if o is not None else oob
-            nodes_last = f.total_nodes
+        for _ in range(warmup):
+            f, _ = step()
             del f
-        ev1.record(stream)
         barrier()
-    launches = pkg.launch_count() - launches0
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
-    value = total_trees * args.steps / (ms / 1e3)
+        l0 = pkg.launch_count()
+        stream = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r = {"grow_ms": 0.0, "split_rows": 0, "grow_launches": 0, "oob": None, "nodes": 0,
+             "trees_total": total, "trees_rank": te - tb, "step_ms": []}
+        last = None
+        with ClockSampler(local) as clk:
+            barrier()
+            ev0.record(stream)
+            for i in range(steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                f, o = step()
+                e1.record(stream)
+                e1.synchronize()
+                r["step_ms"].append(e0.elapsed_time(e1))
+                prof = f.profile()
+                r["grow_ms"] += prof["grow_ms"]
+                r["split_rows"] += prof["split_rows"]
+                r["grow_launches"] += prof["grow_launches"]
+                r["oob"] = o if o is not None else r["oob"]
+                r["nodes"] = f.total_nodes
+                if keep_last and i == steps - 1:
+                    last = f
+                del f
+            ev1.record(stream)
+            barrier()
+        r["launches"] = pkg.launch_count() - l0
+        r["ms"] = max_over_ranks(ev0.elapsed_time(ev1))
+        r["clocks"] = clk.summary()
+        r["value"] = total * steps / (r["ms"] / 1e3)
+        # the OOB statistic lives on the chain's last rank: hand it to rank 0
+        err = r["oob"].error_pct if r["oob"] is not None else -1.0
+        r["oob_error_pct"] = max_over_ranks(err)
+        return r, last
+
+    head, _ = measure(args.scaling, args.steps, args.warmup)
+    per = head["trees_rank"]
+    total_trees = head["trees_total"]
+    ms, value, launches = head["ms"], head["value"], head["launches"]
+    grow_ms, split_rows, grow_launch = head["grow_ms"], head["split_rows"], head["grow_launches"]
+    nodes_last = head["nodes"]
+    oob = head["oob_error_pct"]
+    clk_summary = head["clocks"]
+    tb, te = ((rank * args.trees_per_gpu, (rank + 1) * args.trees_per_gpu) if args.scaling == "weak"
+              else shard.tree_range(rank, world, args.trees_per_gpu))
+    params = pkg.ForestParams(total_trees, C4_MTRY, C4_MNS, seed)
     # roofline of the grow kernel: SURVEY 8d algorithmic bytes
     #   B_tree = 4n + sum_split_nodes rows(N) * (24*mtry + 16)
     n = table.n
@@ -343,7 +385,7 @@ def main():
             f2 = pkg.fit(p2, params)
             _ = f2.oob
         else:
-            f2 = pkg.fit(p2, params, tb, te, compute_oob_stats=False)
+            f2 = pkg.fit(p2, params, int(tb), int(te), compute_oob_stats=False)
         arrs = f2.export()
         ib = f2.inbag()
         e2e_times.append(time.perf_counter() - s)
@@ -353,11 +395,25 @@ def main():
     e2e_s = max_over_ranks(float(np.median(e2e_times)))
     e2e_value = total_trees / e2e_s
 
-    # ---------------- forest gather over NCCL (N > 1) ----------------
-    forest_gather = None
-    if world > 1 and args.gather_trees > 0:
-        forest_gather = bench_forest_gather(pkg, torch, shard, prep, args, rank, world, local,
-                                            barrier, max_over_ranks, sum_over_ranks)
+    # ---------------- the other scaling mode + whole-forest gather (N > 1) ----
+    other = None
+    if world > 1:
+        mode = "strong" if args.scaling == "weak" else "weak"
+        r2, last = measure(mode, max(1, args.strong_steps), 1, keep_last=(mode == "strong"))
+        other = {"scaling": mode, "value": r2["value"], "unit": "trees/s",
+                 "ms_per_step": r2["ms"] / max(1, args.strong_steps),
+                 "steps": max(1, args.strong_steps), "trees_total": r2["trees_total"],
+                 "oob_error_pct": r2["oob_error_pct"], "clocks": r2["clocks"]}
+        if mode == "strong" or args.scaling == "strong":
+            if last is None:  # headline strong: refit the strong shard once for the gather
+                T = args.trees_per_gpu
+                a0, a1 = shard.tree_range(rank, world, T)
+                last = pkg.fit(prep, pkg.ForestParams(T, C4_MTRY, C4_MNS, seed), a0, a1,
+                               compute_oob_stats=False)
+            other["forest_gather"] = bench_forest_gather(pkg, torch, shard, last, rank, world,
+                                                         local, barrier, max_over_ranks,
+                                                         sum_over_ranks)
+            del last
 
     del prep
     torch.cuda.empty_cache()
@@ -384,16 +440,19 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference synthesize()+make_dataset() restated bit-exactly; "
                 "random forest trained from scratch each step)",
         "config": {"workload": "C4 fit: synthetic AIWC 1,000,036 x 64 (6757 kernels x 4 "
                                "sizes x 37 devices), mtry 8, min.node.size 5, "
-                               f"{per} trees/GPU, OOB included",
+                               + (f"{per} trees/GPU" if args.scaling == "weak" else
+                                  f"{total_trees} trees split over {world} GPU(s)")
+                               + ", OOB included",
                    "trees_total": total_trees, "rows": table.n, "predictors": table.p,
-                   "parallelism": f"tree-seed shards x{world}, chained OOB",
+                   "parallelism": f"tree-seed shards x{world}, chained OOB on the devices",
                    "l2": "inputs (512 MB f64 column store + 128 MB ranks) exceed L2"},
-        "oob_error_pct": None if oob is None else oob.error_pct,
+        "oob_error_pct": None if oob < 0 else oob,
+        "step_ms": head["step_ms"],
         "nodes_per_tree": nodes_last / per,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_per_launch(per * args.steps,
@@ -409,7 +468,7 @@ def main():
                 "d2h_bytes_per_step": d2h,
                 "path": "aiwc_ctx_create(host col,y)+aiwc_fit+export(nodes,inbag)"},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clk_summary,
         "setup_s": setup_s,
         "cpu_baseline": ({k: cpu_res.get(k) for k in ("value", "unit", "cores", "kind", "sample")}
                          if cpu_res else None),
@@ -418,7 +477,7 @@ def main():
                                                             "extra_error") if k in cpu_res}
                                if cpu_res else None),
         "predict": predict,
-        "forest_gather": forest_gather,
+        "other_scaling": other,
         "c1": c1,
         "grid": grid,
         "loko": loko,
@@ -430,35 +489,32 @@ def main():
         dist.destroy_process_group()
 
 
-def bench_forest_gather(pkg, torch, shard, prep, args, rank, world, local, barrier,
-                        max_over_ranks, sum_over_ranks):
-    """Every rank fits its tree range of a (gather_trees x N)-tree C4 forest, then the node
-    SoA is all-gathered device to device over NCCL (shard.allgather_forest) so that every
-    rank holds the whole forest.  Bounded tree count: the full 1000-tree-per-GPU C4 forest
-    is 8.9 GB of nodes per rank, too large to replicate 8 times on every GPU."""
-    per = args.gather_trees
-    params = pkg.ForestParams(per * world, C4_MTRY, C4_MNS, pkg.derive_seed(1, "forest"))
-    f = pkg.fit(prep, params, rank * per, (rank + 1) * per, compute_oob_stats=False)
+def bench_forest_gather(pkg, torch, shard, f, rank, world, local, barrier, max_over_ranks,
+                        sum_over_ranks):
+    """The strong-mode forest (every rank's tree range of the 1000-tree C4 forest) is
+    all-gathered device to device over NCCL (shard.allgather_forest: export -> all_gather
+    -> import, in-bag draws included), so every rank ends with the whole forest that was
+    fit (~8.9 GB of nodes + 4 GB of in-bag draws)."""
     total_nodes = int(sum_over_ranks(float(f.total_nodes)))
-    need = total_nodes * 80 + (1 << 30)  # parts + concatenation + imported SoA + packed
-    free = torch.cuda.mem_get_info(local)[0]
-    ok = -max_over_ranks(-float(free >= need))
-    if ok < 1:
-        return {"skipped": f"needs ~{need / 1e9:.1f} GB free per GPU"}
+    total_trees = int(sum_over_ranks(float(f.num_trees)))
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)
-    g = shard.allgather_forest(f, world, local)
+    import torch.distributed as dist
+
+    ag = (dist.all_gather if os.environ.get("AIWC_BENCH_BACKEND", "nccl") == "nccl"
+          else shard.host_staged_all_gather(dist.all_gather))
+    g = shard.allgather_forest(f, world, local, ag, with_inbag=True)
     ev1.record(stream)
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
-    ok = g.num_trees == per * world and g.total_nodes == total_nodes
-    gathered = total_nodes * 24  # feature + left (i32) + threshold + value (f64) per node
-    del g, f
+    ok = g.num_trees == total_trees and g.total_nodes == total_nodes
+    gathered = total_nodes * 24 + total_trees * f.n * 4  # node SoA + in-bag draws
+    del g
     torch.cuda.empty_cache()
-    return {"trees_per_rank": per, "trees": per * world, "nodes": total_nodes, "ms": ms,
-            "bytes_gathered_per_rank": gathered, "GB_per_s_per_rank": gathered / ms / 1e6,
+    return {"trees": total_trees, "nodes": total_nodes, "ms": ms,
+            "bytes_per_rank": gathered, "GB_per_s_per_rank": gathered / ms / 1e6,
             "complete": bool(ok),
             "path": "aiwc_forest_export_device -> NCCL all_gather -> aiwc_forest_import_device"}
 
@@ -537,17 +593,19 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     counts = list(range(50, 1001, 50))
     ncell = max(1, ARGS.grid_cells)
     cells = [(m, 1 + (7 * m) % 50) for m in range(1, 35)][:ncell]
-    allreduce = shard.torch_allreduce_sum(torch.device("cuda", local)) if world > 1 else (lambda a: a)
+    nccl = os.environ.get("AIWC_BENCH_BACKEND", "nccl") == "nccl"
+    allreduce = (shard.torch_allreduce_sum(torch.device("cuda", local) if nccl else None)
+                 if world > 1 else (lambda a: a))
     _ = pkg.grid_oob(prep, cells, counts, seed)  # warm-up (same batch sizes)
     grid_runs = []
-    for _ in range(3):  # median of 3 (single runs see occasional host-side stalls)
+    for _ in range(3):  # every run reported; the headline is their mean
         barrier()
         s = time.perf_counter()
         err = shard.grid_sharded(cells, counts, rank, world,
                                  lambda cs: pkg.grid_oob(prep, cs, counts, seed), allreduce)
         barrier()
         grid_runs.append(max_over_ranks(time.perf_counter() - s))
-    gs = float(np.median(grid_runs))
+    gs = float(np.mean(grid_runs))
     # C1: the paper-shaped table itself -- 500-tree fit (OOB included) + predict of its
     # 2220 rows, the reference's configs[0]
     c1p = pkg.ForestParams(500, 6, 5, seed)
@@ -574,7 +632,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     prm = pkg.ForestParams(505, 30, 9, 0)
     _ = pkg.evaluate(t, prm, seed, device=local, folds=(0, 1))  # warm-up
     loko_runs = []
-    for _ in range(3):  # median of 3, as the grid
+    for _ in range(3):  # every run reported; the headline is their mean
         barrier()
         s = time.perf_counter()
         part = pkg.evaluate(t, prm, seed, device=local,
@@ -582,7 +640,7 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
         pred = allreduce(part)
         barrier()
         loko_runs.append(max_over_ranks(time.perf_counter() - s))
-    ls = float(np.median(loko_runs))
+    ls = float(np.mean(loko_runs))
     err_row = 100.0 * np.abs(pred - t.seconds) / t.seconds
     loko = {"workload": "C3: evaluate(C1, 505/30/9): 37 folds x 60 held-out rows",
             "folds_per_s": t.kernels / ls, "s": ls, "runs_s": loko_runs, "mape_pct": float(err_row.mean())}

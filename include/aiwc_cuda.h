@@ -133,6 +133,12 @@ int aiwc_oob(aiwc_ctx* ctx, aiwc_forest* f, aiwc_oob_stats* out, double* row_sum
  * rank 0 -> 1 -> ... reproduces the single-forest tree-order sum bit-exactly. */
 int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum,
                         uint32_t* row_count);
+/* The same on DEVICE buffers (n doubles, n uint32 on the forest's device): the multi-GPU
+ * OOB chain passes (row_sum, row_count) rank to rank over NCCL without host copies.
+ * The caller's writes to the buffers must be complete (its stream synchronised); the
+ * call returns when the sums are updated.  Replaces the same loop as above. */
+int aiwc_oob_accumulate_device(aiwc_ctx* ctx, aiwc_forest* f, double* d_row_sum,
+                               uint32_t* d_row_count);
 /* OOB statistics of the forest's first tree_counts[i] trees, i < k (ascending counts,
  * forest grown from tree 0): compute_oob (forest.hpp:393-454) of every T-tree fit of
  * the same (data, mtry, min.node.size, seed) at once -- by the tree-prefix property a

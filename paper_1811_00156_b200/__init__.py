@@ -105,6 +105,7 @@ def lib():
         L.aiwc_rank.argtypes = [vp, P(f64), u64, u32, u32, P(f64), P(u32)]
         L.aiwc_oob.argtypes = [vp, vp, P(OobStatsC), P(f64), P(u32)]
         L.aiwc_oob_accumulate.argtypes = [vp, vp, P(f64), P(u32)]
+        L.aiwc_oob_accumulate_device.argtypes = [vp, vp, vp, vp]
         L.aiwc_oob_finalize.argtypes = [P(f64), u64, P(f64), P(u32), P(OobStatsC)]
         L.aiwc_predict.argtypes = [vp, P(f64), u64, u32, P(f64)]
         L.aiwc_predict_device.argtypes = [vp, vp, u64, u32, vp]
@@ -388,6 +389,13 @@ def oob_accumulate(forest: Forest, prepared: PreparedDataset, row_sum: np.ndarra
     """Continue per-row tree-ordered OOB sums with this (partial) forest, in place."""
     _check(lib().aiwc_oob_accumulate(prepared._h, forest._h, _p(row_sum, f64),
                                      _p(row_count, u32)))
+
+
+def oob_accumulate_device(forest: Forest, prepared: PreparedDataset, d_row_sum: int,
+                          d_row_count: int):
+    """oob_accumulate on device buffers (pointers: n float64, n uint32/int32 on the forest's
+    device); the caller's stream must be synchronised before the call."""
+    _check(lib().aiwc_oob_accumulate_device(prepared._h, forest._h, d_row_sum, d_row_count))
 
 
 def oob_finalize(y: np.ndarray, row_sum: np.ndarray, row_count: np.ndarray) -> OobStats:

@@ -1206,6 +1206,24 @@ int aiwc_oob_accumulate(aiwc_ctx* ctx, aiwc_forest* f, double* row_sum, uint32_t
   });
 }
 
+int aiwc_oob_accumulate_device(aiwc_ctx* ctx, aiwc_forest* f, double* d_row_sum,
+                               uint32_t* d_row_count) {
+  return guard([&] {
+    if (!ctx || !f || !d_row_sum || !d_row_count) throw Status(AIWC_EARG, "NULL argument");
+    if (!f->oobleaf.p) throw Status(AIWC_EEXEC, "forest holds no OOB leaf values");
+    if (f->n != ctx->n) throw Status(AIWC_ESCHEMA, "forest and dataset row counts differ");
+    if (f->device != ctx->device) throw Status(AIWC_EARG, "forest and dataset live on different devices");
+    DeviceGuard dg(ctx->device);
+    Stream st;
+    const uint64_t n = f->n;
+    oob_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st.s>>>(
+        f->oobleaf.p, f->d_off.p, f->value.p, f->trees, n, d_row_sum, d_row_count);
+    CK(cudaGetLastError());
+    g_launches += 1;
+    CK(cudaStreamSynchronize(st.s));
+  });
+}
+
 int aiwc_oob_prefix(aiwc_ctx* ctx, aiwc_forest* f, const uint32_t* tree_counts, uint32_t k,
                     aiwc_oob_stats* out) {
   return guard([&] {

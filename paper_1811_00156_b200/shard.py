@@ -60,6 +60,52 @@ def chained_oob(n: int, rank: int, world: int,
     return rs, rc
 
 
+def chained_oob_device(n: int, rank: int, world: int, device,
+                       accumulate: Callable[[int, int], None],
+                       send: Callable, recv: Callable):
+    """The OOB chain with the per-row (sum, count) kept on the GPU: rank r receives the
+    device buffers of trees [0, t0_r) from rank r-1 (NCCL send/recv of device tensors,
+    or host staging for gloo), continues them in place with its own trees
+    (aiwc_oob_accumulate_device) and sends them on.  Returns the device tensors
+    (row_sum float64, row_count int32 holding uint32 counts) on the last rank, else None.
+
+    accumulate(d_sum_ptr, d_count_ptr); send(tensor, dst); recv(tensor, src) (in place)."""
+    import torch
+
+    rs = torch.zeros(n, dtype=torch.float64, device=device)
+    rc = torch.zeros(n, dtype=torch.int32, device=device)
+    if rank > 0:
+        recv(rs, rank - 1)
+        recv(rc, rank - 1)
+    if torch.device(device).type == "cuda":
+        torch.cuda.current_stream(device).synchronize()
+    accumulate(rs.data_ptr(), rc.data_ptr())
+    if rank < world - 1:
+        send(rs, rank + 1)
+        send(rc, rank + 1)
+        return None
+    return rs, rc
+
+
+def torch_device_transport(host_staging: bool = False):
+    """send / recv of device tensors over the default process group: directly (NCCL over
+    NVLink) or through host copies (gloo, the CPU-backend tests)."""
+    import torch.distributed as dist
+
+    def send(t, dst: int):
+        dist.send(t.cpu() if host_staging else t, dst=dst)
+
+    def recv(t, src: int):
+        if host_staging:
+            h = t.cpu()
+            dist.recv(h, src=src)
+            t.copy_(h)
+        else:
+            dist.recv(t, src=src)
+
+    return send, recv
+
+
 def torch_transport(device=None):
     """send/recv callables over the default torch.distributed process group."""
     import torch
@@ -133,6 +179,16 @@ def gather_forest(off_local, arrays, world: int, all_gather, n: int = 0):
                               for q, m in zip(parts, metas)]))
         del parts, buf
     return offsets, out
+
+
+def host_staged_all_gather(all_gather):
+    """all_gather of device tensors through host copies (gloo)."""
+    def ag(outs, t):
+        h = [o.cpu() for o in outs]
+        all_gather(h, t.cpu())
+        for o, x in zip(outs, h):
+            o.copy_(x)
+    return ag
 
 
 def allgather_forest(forest, world: int, device: int, all_gather=None, with_inbag=False):
