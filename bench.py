@@ -244,10 +244,12 @@ def main():
 
     import paper_1811_00156_b200 as pkg
 
+    backend = os.environ.get("AIWC_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())  # functional check: ranks share GPUs
     torch.cuda.set_device(local)
     # AIWC_BENCH_BACKEND=gloo: the N > 1 code path on ONE GPU (ranks share cuda:0, host-
     # staged collectives) -- a functional check only, its timings mean nothing
-    backend = os.environ.get("AIWC_BENCH_BACKEND", "nccl")
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
