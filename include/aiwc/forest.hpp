@@ -13,7 +13,11 @@
 //
 // Differences a caller can observe:
 //   * `jobs` is accepted and ignored (the forest grows on the GPU; results never
-//     depended on it in the reference's intended semantics, forest.hpp:477-479);
+//     depended on it in the reference's intended semantics, forest.hpp:477-479).
+//     Concurrent fits on one PreparedDataset (the heatmap / loko / tune threads) are
+//     merged by the library into one multi-forest launch per batch, and successive
+//     calls are spread round-robin over the visible GPUs (AIWC_DEVICES limits them);
+//   * Tree::predict walks its one tree on the host (the reference's loop, exact);
 //   * FitContext::order is left empty (the presort lives on the device);
 //   * predictions run on the GPU: the Forest lazily uploads its trees and caches the
 //     device copy (call invalidate_device_cache() after mutating `trees` by hand);
@@ -22,7 +26,9 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -53,7 +59,22 @@ inline void check(int rc) {
     default: throw ExecutionError(msg);
   }
 }
+// devices used by the drop-in (AIWC_DEVICES=k: the first k; default all visible)
+inline int device_count() {
+  static const int n = [] {
+    int c = 0;
+    if (aiwc_device_count(&c) != AIWC_OK || c < 1) c = 1;
+    if (const char* e = std::getenv("AIWC_DEVICES")) c = std::max(1, std::min(c, std::atoi(e)));
+    return c;
+  }();
+  return n;
+}
 inline int device() { return 0; }
+// round-robin device of the next fit
+inline int next_device() {
+  static std::atomic<unsigned> rr{0};
+  return static_cast<int>(rr.fetch_add(1) % static_cast<unsigned>(device_count()));
+}
 }  // namespace b200
 
 struct ForestParams {
@@ -114,18 +135,16 @@ struct ForestHandle {
 struct Tree {
   std::vector<TreeNode> nodes;
 
-  // Single-tree prediction on the GPU (a one-tree device forest); batched callers
-  // should use Forest::predict_response / predict_responses.
+  // One tree, one row (forest.hpp:42-50): a handful of node visits, walked here -- a
+  // device round trip per call would cost more than the walk.  Batched callers use
+  // Forest::predict_response / predict_responses (GPU).
   double predict(std::span<const double> row) const {
-    const std::vector<Tree> one{*this};
-    const b200::Soa s = b200::to_soa(one);
-    aiwc_forest* h = nullptr;
-    b200::check(aiwc_forest_import(1, s.off.data(), s.f.data(), s.thr.data(), s.l.data(),
-                                   s.r.data(), s.val.data(), nullptr, 0, b200::device(), &h));
-    b200::ForestHandle guard(h);
-    double out = 0;
-    b200::check(aiwc_predict(h, row.data(), 1, static_cast<std::uint32_t>(row.size()), &out));
-    return out;
+    std::int32_t node = 0;
+    while (nodes[static_cast<std::size_t>(node)].feature >= 0) {
+      const TreeNode& nd = nodes[static_cast<std::size_t>(node)];
+      node = row[static_cast<std::size_t>(nd.feature)] <= nd.threshold ? nd.left : nd.right;
+    }
+    return nodes[static_cast<std::size_t>(node)].value;
   }
 };
 
@@ -231,23 +250,40 @@ struct FitContext {
   std::vector<std::vector<double>> col;           // p columns of n values
   std::vector<double> y;                          // response
   std::vector<std::vector<std::uint32_t>> order;  // left empty: the presort is on the GPU
-  std::shared_ptr<aiwc_ctx> dev;
+  std::shared_ptr<aiwc_ctx> dev;                  // device 0's copy (created eagerly)
 
   FitContext(const Dataset& data, ResponseTransform t) {
     n = data.rows.size();
     p = data.predictor_count();
     col.assign(p, std::vector<double>(n));
-    std::vector<double> flat(p * n);
     for (std::size_t c = 0; c < p; ++c)
-      for (std::size_t i = 0; i < n; ++i) flat[c * n + i] = col[c][i] = data.predictor_value(i, c);
+      for (std::size_t i = 0; i < n; ++i) col[c][i] = data.predictor_value(i, c);
     y = data.responses(t);
-    if (n >= 2) {
-      aiwc_ctx* h = nullptr;
-      b200::check(aiwc_ctx_create(flat.data(), y.data(), n, static_cast<std::uint32_t>(p),
-                                  b200::device(), &h));
-      dev = std::shared_ptr<aiwc_ctx>(h, [](aiwc_ctx* x) { aiwc_ctx_free(x); });
-    }
+    devs_ = std::make_shared<Devs>();
+    devs_->ctx.resize(static_cast<std::size_t>(b200::device_count()));
+    if (n >= 2) dev = on_device(0);
   }
+
+  // the dataset's device copy on device d (uploaded and presorted on first use)
+  std::shared_ptr<aiwc_ctx> on_device(int d) const {
+    std::lock_guard<std::mutex> lock(devs_->mu);
+    auto& c = devs_->ctx[static_cast<std::size_t>(d)];
+    if (!c) {
+      std::vector<double> flat(p * n);
+      for (std::size_t k = 0; k < p; ++k) std::copy(col[k].begin(), col[k].end(), flat.begin() + k * n);
+      aiwc_ctx* h = nullptr;
+      b200::check(aiwc_ctx_create(flat.data(), y.data(), n, static_cast<std::uint32_t>(p), d, &h));
+      c = std::shared_ptr<aiwc_ctx>(h, [](aiwc_ctx* x) { aiwc_ctx_free(x); });
+    }
+    return c;
+  }
+
+ private:
+  struct Devs {
+    std::mutex mu;
+    std::vector<std::shared_ptr<aiwc_ctx>> ctx;
+  };
+  std::shared_ptr<Devs> devs_;
 };
 
 }  // namespace detail
@@ -304,8 +340,9 @@ inline Forest fit(const PreparedDataset& prepared, const ForestParams& params,
     throw ExecutionError("mtry must be in [1, " + std::to_string(prepared.predictor_count()) +
                          "], got " + std::to_string(params.mtry));
   aiwc_forest* h = nullptr;
-  b200::check(aiwc_fit(prepared.context().dev.get(), params.num_trees, params.mtry,
-                       params.min_node_size, params.seed, 0, params.num_trees, 1, &h));
+  const std::shared_ptr<aiwc_ctx> ctx = prepared.context().on_device(b200::next_device());
+  b200::check(aiwc_fit(ctx.get(), params.num_trees, params.mtry, params.min_node_size,
+                       params.seed, 0, params.num_trees, 1, &h));
   b200::ForestHandle guard(h);
   Forest forest;
   forest.params = params;

@@ -395,4 +395,34 @@ int ref_evaluate(void* h, uint32_t num_trees, uint32_t mtry, uint32_t mns,
   });
 }
 
+// heatmap_scan (experiments.hpp:79-123): the SA chains from the 4 corners + random
+// starts, every objective a reference fit (tuner.hpp:247-253).  Cells (num_trees, mtry,
+// mean error_pct) go to out (3 doubles each); *nevals = total objective evaluations.
+int ref_heatmap(void* prep, int64_t nt_lo, int64_t nt_hi, int64_t mt_lo, int64_t mt_hi,
+                int64_t mns, uint64_t max_evals, uint64_t random_starts, uint64_t forest_seed,
+                uint64_t sa_seed, unsigned jobs, double* out, uint64_t cap, uint64_t* ncells,
+                uint64_t* nevals) {
+  return guarded([&] {
+    HeatmapConfig cfg;
+    cfg.space.num_trees = {nt_lo, nt_hi};
+    cfg.space.mtry = {mt_lo, mt_hi};
+    cfg.fixed_min_node_size = mns;
+    cfg.schedule.max_evaluations = max_evals;
+    cfg.random_starts = random_starts;
+    cfg.forest_seed = forest_seed;
+    cfg.sa_seed = sa_seed;
+    cfg.jobs = jobs;
+    const HeatmapResult r = heatmap_scan(*static_cast<PreparedDataset*>(prep), cfg);
+    *ncells = r.cells.size();
+    uint64_t ev = 0;
+    for (const auto& c : r.chains) ev += c.entries.size();
+    *nevals = ev;
+    for (std::size_t i = 0; i < r.cells.size() && 3 * i + 2 < cap; ++i) {
+      out[3 * i] = static_cast<double>(r.cells[i].num_trees);
+      out[3 * i + 1] = static_cast<double>(r.cells[i].mtry);
+      out[3 * i + 2] = r.cells[i].error_pct;
+    }
+  });
+}
+
 }  // extern "C"

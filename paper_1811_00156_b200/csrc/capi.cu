@@ -12,6 +12,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -275,6 +276,17 @@ struct aiwc_ctx {
   DevBuf<int32_t> list_of;
   DevBuf<uint8_t> rank;
   DevBuf<uint64_t> vals_off;
+  // Concurrent aiwc_fit calls on this dataset (the reference's heatmap / loko / tune
+  // threads, experiments.hpp:104-110, 175-181) queue here; one caller at a time leads and
+  // grows every queued request's trees in ONE launch sequence (fit_batch).
+  struct FitRequest;
+  struct FitQueue {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<FitRequest*> pending;
+    bool leader = false;
+    size_t last_batch = 1;
+  } q;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
   DevBuf<char> scratch;
@@ -287,6 +299,16 @@ struct aiwc_ctx {
     return DevData{n, p, rank_bytes, nlisted, order_stride, col.p, dy.p, order.p, rank.p,
                    vals.p, vals_off.p, list_of.p, listed.p};
   }
+};
+
+struct aiwc_ctx::FitRequest {
+  uint32_t num_trees, mtry, mns, tb, te;
+  uint64_t seed;
+  int compute_oob;
+  aiwc_forest* out = nullptr;
+  int status = AIWC_OK;
+  std::string msg;
+  bool done = false;
 };
 
 // ---------------------------------------------------------------------------------
@@ -332,6 +354,17 @@ struct aiwc_forest {
   int node_bytes = 8;
   DevBuf<double> bleaves, bthr;
   DevBuf<uint32_t> broots, bthr_off;
+  // few-row predictions (the reference's per-row predict_response / predict_time loops,
+  // experiments.hpp:399-402): a stream, device buffers and pinned staging kept per forest
+  std::mutex sm_mu;
+  cudaStream_t sm_stream = nullptr;
+  DevBuf<double> sm_rows, sm_out;
+  double* sm_pin = nullptr;
+  size_t sm_pin_cap = 0;
+  ~aiwc_forest() {
+    if (sm_stream) cudaStreamDestroy(sm_stream);
+    if (sm_pin) cudaFreeHost(sm_pin);
+  }
 };
 
 namespace {
@@ -552,13 +585,16 @@ extern "C" {
 namespace {
 
 // One fit: trees [tree_begin, tree_end) of a num_trees forest, or, with `cells`, the
-// cells->n forests of cells->trees trees each (grid cells: per-tree mtry / mns, one
-// launch for all of them; trees of cell c are [c*trees, (c+1)*trees)).
+// cells->n forests (grid cells, batched concurrent fits): forest c grows its trees
+// [tb[c], te[c]) with its own mtry / mns / seed, all in one launch; its trees follow
+// those of forest c-1 in the result.
 struct CellSpec {
   uint32_t n;
   const uint32_t* mtry;
   const uint32_t* mns;
-  uint32_t trees;
+  const uint64_t* seed;
+  const uint32_t* tb;
+  const uint32_t* te;
 };
 
 void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
@@ -596,15 +632,31 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   a.tree_end = tree_end;
   a.L = L;
   a.bits_in_smem = smem_bits ? 1 : 0;
-  DevBuf<uint32_t> cell_m, cell_n;
+  DevBuf<uint32_t> cell_m, cell_n, tcell, tidx;
+  DevBuf<uint64_t> cell_s;
   if (cells) {
+    std::vector<uint32_t> hc, ht;
+    for (uint32_t c = 0; c < cells->n; ++c)
+      for (uint32_t t = cells->tb[c]; t < cells->te[c]; ++t) {
+        hc.push_back(c);
+        ht.push_back(t);
+      }
+    if (hc.size() != T) throw Status(AIWC_EARG, "cell tree ranges do not add up");
     cell_m.alloc(cells->n);
     cell_n.alloc(cells->n);
+    cell_s.alloc(cells->n);
+    tcell.alloc(T);
+    tidx.alloc(T);
     CK(cudaMemcpy(cell_m.p, cells->mtry, cells->n * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(cell_n.p, cells->mns, cells->n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(cell_s.p, cells->seed, cells->n * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(tcell.p, hc.data(), size_t{T} * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(tidx.p, ht.data(), size_t{T} * 4, cudaMemcpyHostToDevice));
     a.cell_mtry = cell_m.p;
     a.cell_mns = cell_n.p;
-    a.cell_trees = cells->trees;
+    a.cell_seed = cell_s.p;
+    a.tree_cell = tcell.p;
+    a.tree_t = tidx.p;
   }
 
   // large tables grow batches of trees level-synchronously with one grid-wide kernel
@@ -929,6 +981,160 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
 
 extern "C" {
 
+namespace {
+
+// Forest c of a multi-forest fit (trees [t0, t1) of F) as a forest of its own: node SoA,
+// in-bag draws and OOB leaves copied device to device; OOB statistics when asked for.
+aiwc_forest* split_cell(aiwc_ctx* ctx, const aiwc_forest* F, uint32_t t0, uint32_t t1,
+                        const aiwc_ctx::FitRequest& r, cudaStream_t s) {
+  auto f = std::make_unique<aiwc_forest>();
+  const uint64_t n = F->n, b = F->off[t0], N = F->off[t1] - b;
+  const uint32_t T = t1 - t0;
+  f->device = F->device;
+  f->n = n;
+  f->trees = T;
+  f->tree_begin = r.tb;
+  f->num_trees = r.num_trees;
+  f->mtry = r.mtry;
+  f->mns = r.mns;
+  f->seed = r.seed;
+  f->grow_ms = F->grow_ms;
+  f->fit_ms = F->fit_ms;
+  f->grow_launches = F->grow_launches;
+  f->off.resize(T + 1);
+  for (uint32_t t = 0; t <= T; ++t) f->off[t] = F->off[t0 + t] - b;
+  f->feature.alloc(N);
+  f->left.alloc(N);
+  f->thr.alloc(N);
+  f->value.alloc(N);
+  f->d_off.alloc(T + 1);
+  CK(cudaMemcpyAsync(f->feature.p, F->feature.p + b, N * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(f->left.p, F->left.p + b, N * 4, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(f->thr.p, F->thr.p + b, N * 8, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(f->value.p, F->value.p + b, N * 8, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, s));
+  f->inbag.alloc(size_t{T} * n);
+  f->oobleaf.alloc(size_t{T} * n);
+  f->oob_ctx = F->oob_ctx;
+  CK(cudaMemcpyAsync(f->inbag.p, F->inbag.p + size_t{t0} * n, size_t{T} * n * 4,
+                     cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(f->oobleaf.p, F->oobleaf.p + size_t{t0} * n, size_t{T} * n * 4,
+                     cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  if (r.compute_oob && r.tb == 0 && r.te == r.num_trees) {
+    std::vector<double> sum(n, 0.0);
+    std::vector<uint32_t> count(n, 0);
+    oob_accumulate_device(f.get(), sum.data(), count.data(), s);
+    f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
+    f->has_oob = true;
+  }
+  return f.release();
+}
+
+// One queued batch: a lone request is a plain fit; several grow as the forests of one
+// multi-forest launch (each tree keyed by its own forest's seed and index, so every
+// forest equals its standalone fit bit for bit) and are then split apart.
+void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
+  auto fail_all = [&](int rc, const std::string& m) {
+    for (auto* r : batch) {
+      if (r->out) {
+        aiwc_forest_free(r->out);
+        r->out = nullptr;
+      }
+      r->status = rc;
+      r->msg = m;
+    }
+  };
+  try {
+    if (batch.size() == 1) {
+      auto* r = batch[0];
+      fit_body(ctx, r->num_trees, r->mtry, r->mns, r->seed, r->tb, r->te, r->compute_oob,
+               nullptr, &r->out);
+      return;
+    }
+    const uint32_t k = static_cast<uint32_t>(batch.size());
+    std::vector<uint32_t> m(k), mn(k), tb(k), te(k);
+    std::vector<uint64_t> sd(k);
+    uint32_t mmax = 0, nmin = UINT32_MAX, total = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+      m[i] = batch[i]->mtry;
+      mn[i] = batch[i]->mns;
+      sd[i] = batch[i]->seed;
+      tb[i] = batch[i]->tb;
+      te[i] = batch[i]->te;
+      mmax = std::max(mmax, m[i]);
+      nmin = std::min(nmin, mn[i]);
+      total += te[i] - tb[i];
+    }
+    const CellSpec cs{k, m.data(), mn.data(), sd.data(), tb.data(), te.data()};
+    aiwc_forest* F = nullptr;
+    fit_body(ctx, total, mmax, nmin, sd[0], 0, total, 0, &cs, &F);
+    std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> hold(F, aiwc_forest_free);
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    uint32_t t0 = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t t1 = t0 + (te[i] - tb[i]);
+      try {
+        batch[i]->out = split_cell(ctx, F, t0, t1, *batch[i], ctx->stream);
+      } catch (const Status& e) {  // this forest alone (e.g. no out-of-bag rows)
+        batch[i]->status = e.code;
+        batch[i]->msg = e.msg;
+      }
+      t0 = t1;
+    }
+  } catch (const Status& e) {
+    fail_all(e.code, e.msg);
+  } catch (const std::exception& e) {
+    fail_all(AIWC_EEXEC, e.what());
+  }
+}
+
+// Queue a fit on ctx and return when it is grown.  The first caller to find no leader
+// leads: it takes every queued request (after waiting up to AIWC_BATCH_WINDOW_US, default
+// 3000, for as many as the previous batch held) and runs them as one batch; the others
+// sleep until their request is done.  AIWC_FIT_BATCH=0 runs every fit alone.
+void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
+  static const bool batching = [] {
+    const char* e = std::getenv("AIWC_FIT_BATCH");
+    return !(e && std::atoi(e) == 0);
+  }();
+  static const auto window = std::chrono::microseconds([] {
+    const char* e = std::getenv("AIWC_BATCH_WINDOW_US");
+    return e ? std::atoll(e) : 3000ll;
+  }());
+  auto& q = ctx->q;
+  std::unique_lock<std::mutex> lk(q.mu);
+  q.pending.push_back(&req);
+  q.cv.notify_all();
+  while (!req.done) {
+    if (q.leader) {
+      q.cv.wait(lk);
+      continue;
+    }
+    q.leader = true;
+    if (batching && q.last_batch > 1)
+      q.cv.wait_for(lk, window, [&] { return q.pending.size() >= q.last_batch; });
+    std::vector<aiwc_ctx::FitRequest*> batch;
+    if (batching) {
+      batch.swap(q.pending);
+    } else {  // one at a time, own request first
+      batch.push_back(&req);
+      q.pending.erase(std::find(q.pending.begin(), q.pending.end(), &req));
+    }
+    q.last_batch = batch.size();
+    lk.unlock();
+    fit_batch(ctx, batch);
+    lk.lock();
+    for (auto* r : batch) r->done = true;
+    q.leader = false;
+    q.cv.notify_all();
+  }
+  if (req.status != AIWC_OK) throw Status(req.status, req.msg);
+}
+
+}  // namespace
+
 int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
              uint64_t seed, uint32_t tree_begin, uint32_t tree_end, int compute_oob,
              aiwc_forest** out) {
@@ -943,8 +1149,10 @@ int aiwc_fit(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node
                                    std::to_string(mtry));
     if (tree_begin >= tree_end || tree_end > num_trees)
       throw Status(AIWC_EARG, "bad tree range");
-    fit_body(ctx, num_trees, mtry, min_node_size, seed, tree_begin, tree_end, compute_oob,
-             nullptr, out);
+    aiwc_ctx::FitRequest req{num_trees, mtry, min_node_size, tree_begin, tree_end, seed,
+                             compute_oob};
+    submit_fit(ctx, req);
+    *out = req.out;
   });
 }
 
@@ -965,7 +1173,9 @@ int aiwc_fit_cells(aiwc_ctx* ctx, uint32_t ncells, const uint32_t* mtry,
       mmax = std::max(mmax, mtry[c]);
       nmin = std::min(nmin, min_node_size[c]);
     }
-    const CellSpec cs{ncells, mtry, min_node_size, num_trees};
+    const std::vector<uint64_t> seeds(ncells, seed);
+    const std::vector<uint32_t> tb(ncells, 0u), te(ncells, num_trees);
+    const CellSpec cs{ncells, mtry, min_node_size, seeds.data(), tb.data(), te.data()};
     fit_body(ctx, num_trees, mmax, nmin, seed, 0, ncells * num_trees, 0, &cs, out);
     (*out)->cells = ncells;
   });
@@ -1526,6 +1736,28 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
     if (!f || (!rows && q) || (!out_response && q)) throw Status(AIWC_EARG, "NULL argument");
     if (q == 0) return;
     DeviceGuard dg(f->device);
+    if (q <= kSmallQ && !f->bin_ready) {  // a few rows: cached stream + buffers, no binning
+      std::lock_guard<std::mutex> lock(f->sm_mu);
+      if (!f->sm_stream) CK(cudaStreamCreateWithFlags(&f->sm_stream, cudaStreamNonBlocking));
+      const cudaStream_t s = f->sm_stream;
+      const size_t need = q * p + q;
+      if (f->sm_pin_cap < need) {
+        if (f->sm_pin) CK(cudaFreeHost(f->sm_pin));
+        f->sm_pin = nullptr;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&f->sm_pin), need * 8));
+        f->sm_pin_cap = need;
+      }
+      if (f->sm_rows.count < q * p) f->sm_rows.alloc(std::max<size_t>(q * p, 64 * size_t{p}));
+      if (f->sm_out.count < q) f->sm_out.alloc(std::max<uint64_t>(q, 64));
+      std::memcpy(f->sm_pin, rows, q * p * 8);
+      CK(cudaMemcpyAsync(f->sm_rows.p, f->sm_pin, q * p * 8, cudaMemcpyHostToDevice, s));
+      PredScratch none;
+      predict_dispatch(f, f->sm_rows.p, q, p, f->sm_out.p, s, none);
+      CK(cudaMemcpyAsync(f->sm_pin + q * p, f->sm_out.p, q * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::memcpy(out_response, f->sm_pin + q * p, q * 8);
+      return;
+    }
     // row chunks on two streams: the upload of chunk i+1 (host copy into pinned memory,
     // DMA) overlaps the predict kernels of chunk i
     Stream st[2];

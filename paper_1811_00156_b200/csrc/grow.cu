@@ -1086,12 +1086,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     __syncthreads();
     const uint32_t tl = s_tree;
     if (tl >= a.tree_end - a.tree_begin) break;
-    // this tree's parameters and its index in its forest (grid cells: forest tl / cell_trees)
-    const uint32_t cell = a.cell_trees ? tl / a.cell_trees : 0u;
-    const uint32_t m = a.cell_trees ? a.cell_mtry[cell] : a.mtry;
-    const uint32_t mns = a.cell_trees ? a.cell_mns[cell] : a.mns;
-    const uint64_t t = a.cell_trees ? tl - cell * a.cell_trees : a.tree_begin + tl;
-    const uint64_t key = dmix64(a.seed ^ a.tag_tree ^ dmix64(t));
+    // this tree's parameters and its index in its forest (several forests: tree_cell)
+    const uint32_t cell = a.tree_cell ? a.tree_cell[tl] : 0u;
+    const uint32_t m = a.tree_cell ? a.cell_mtry[cell] : a.mtry;
+    const uint32_t mns = a.tree_cell ? a.cell_mns[cell] : a.mns;
+    const uint64_t t = a.tree_cell ? uint64_t{a.tree_t[tl]} : uint64_t{a.tree_begin} + tl;
+    const uint64_t seed = a.tree_cell ? a.cell_seed[cell] : a.seed;
+    const uint64_t key = dmix64(seed ^ a.tag_tree ^ dmix64(t));
 
     // ---- bootstrap (forest.hpp:184-195) ----
     for (uint32_t i = tid; i < n; i += NT) mult_g[i] = 0u;

@@ -80,11 +80,14 @@ struct SlotLayout {
 struct GrowArgs {
   DevData d;
   uint32_t mtry, mns;
-  // grid cells (CTA-per-tree grower only): tree tl belongs to cell tl / cell_trees, grows
-  // with that cell's mtry / min.node.size, and is tree tl % cell_trees of its forest
+  // several forests in one launch (grid cells, batched concurrent fits): local tree tl
+  // belongs to forest tree_cell[tl], grows with that forest's mtry / min.node.size /
+  // seed, and is tree tree_t[tl] of its forest (its RNG key).  Null: one forest.
+  const uint32_t* tree_cell;
+  const uint32_t* tree_t;
   const uint32_t* cell_mtry;
   const uint32_t* cell_mns;
-  uint32_t cell_trees;  // 0: one forest
+  const uint64_t* cell_seed;
   uint64_t seed;
   uint64_t tag_tree;  // fnv1a64("tree")
   uint32_t tree_begin, tree_end;

@@ -93,18 +93,19 @@ __host__ __device__ inline uint32_t grp_width(uint32_t m) {
   return 32u / c;
 }
 
-// Per-tree parameters: with grid cells (GrowArgs::cell_trees > 0) the batch's tree b is
-// tree (t0+b) % cell_trees of cell (t0+b) / cell_trees, which has its own mtry / mns.
+// Per-tree parameters: with several forests (GrowArgs::tree_cell) the batch's tree b is
+// tree tree_t[t0+b] of forest tree_cell[t0+b], which has its own mtry / mns / seed.
 __device__ __forceinline__ uint32_t tree_m(const WideArgs& a, uint32_t b) {
-  return a.g.cell_trees ? a.g.cell_mtry[(a.t0 + b) / a.g.cell_trees] : a.g.mtry;
+  return a.g.tree_cell ? a.g.cell_mtry[a.g.tree_cell[a.t0 + b]] : a.g.mtry;
 }
 __device__ __forceinline__ uint32_t tree_mns(const WideArgs& a, uint32_t b) {
-  return a.g.cell_trees ? a.g.cell_mns[(a.t0 + b) / a.g.cell_trees] : a.g.mns;
+  return a.g.tree_cell ? a.g.cell_mns[a.g.tree_cell[a.t0 + b]] : a.g.mns;
 }
 __device__ __forceinline__ uint64_t tree_key(const WideArgs& a, uint32_t b) {
   const uint32_t tl = a.t0 + b;
-  const uint64_t t = a.g.cell_trees ? tl % a.g.cell_trees : uint64_t{a.g.tree_begin} + tl;
-  return dmix64(a.g.seed ^ a.g.tag_tree ^ dmix64(t));
+  if (a.g.tree_cell)
+    return dmix64(a.g.cell_seed[a.g.tree_cell[tl]] ^ a.g.tag_tree ^ dmix64(uint64_t{a.g.tree_t[tl]}));
+  return dmix64(a.g.seed ^ a.g.tag_tree ^ dmix64(uint64_t{a.g.tree_begin} + tl));
 }
 // lane-group tasks of a node with m sampled columns when the group kernel was launched
 // for the batch's widest mtry (lane groups of grp_width(mmax))

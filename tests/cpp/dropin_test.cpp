@@ -7,12 +7,51 @@
 #include <aiwc/synth.hpp>
 #include <aiwc/tuner.hpp>
 
+#include <chrono>
 #include <cstdio>
 #include <string>
 
 using namespace aiwc;
 
-int main() {
+// heatmap mode: the reference's heatmap_scan (experiments.hpp:79-123) with 12 SA chains on
+// 12 threads, every objective a drop-in fit (concurrent fits on one PreparedDataset: the
+// library batches them); configuration = tests/golden/make_heatmap_golden.py
+static int heatmap() {
+  const SynthResult s = synthesize(SynthConfig{});
+  const Dataset d = make_dataset(s.features, s.runtimes);
+  const PreparedDataset prep(d, ResponseTransform::Log10);
+  HeatmapConfig cfg;
+  cfg.space.num_trees = {10, 300};
+  cfg.space.mtry = {1, 34};
+  cfg.fixed_min_node_size = 9;
+  cfg.schedule.max_evaluations = 30;
+  cfg.random_starts = 8;
+  cfg.forest_seed = derive_seed(1, "forest");
+  cfg.sa_seed = 1;
+  cfg.jobs = 12;
+  (void)fit(prep, ForestParams{10, 6, 9, cfg.forest_seed});  // warm: contexts, pools
+  const auto t0 = std::chrono::steady_clock::now();
+  const HeatmapResult r = heatmap_scan(prep, cfg);
+  const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::size_t ev = 0;
+  for (const auto& c : r.chains) ev += c.entries.size();
+  std::printf("{\"seconds\": %.6f, \"evaluations\": %zu, \"cells\": [", sec, ev);
+  for (std::size_t i = 0; i < r.cells.size(); ++i)
+    std::printf("%s[%lld, %lld, %.17g]", i ? ", " : "", static_cast<long long>(r.cells[i].num_trees),
+                static_cast<long long>(r.cells[i].mtry), r.cells[i].error_pct);
+  std::printf("]}\n");
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "heatmap") {
+    try {
+      return heatmap();
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "dropin_test heatmap: %s\n", e.what());
+      return 3;
+    }
+  }
   try {
     const SynthResult s = synthesize(SynthConfig{});
     const Dataset d = make_dataset(s.features, s.runtimes);

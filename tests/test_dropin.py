@@ -41,3 +41,26 @@ def test_reference_callers_run_unchanged_on_gpu(golden):
     assert got["c3_50_mape"] == pytest.approx(c3["mape"], rel=1e-13)
     assert (got["pairs"], got["pairs_correct"]) == (c3["pairs"], c3["pairs_correct"])
     assert got["roundtrip"] is True
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_heatmap_scan_batches_concurrent_fits():
+    """The reference's heatmap_scan (experiments.hpp:79-123), 12 SA chains on 12 threads,
+    every objective a drop-in fit on ONE PreparedDataset: the library merges the chains'
+    concurrent fits into one multi-forest launch per round.  The cells equal the
+    reference's own run (tests/golden/heatmap_c1.json) bit for bit, and batching beats
+    the same scan with every fit run alone (AIWC_FIT_BATCH=0)."""
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "heatmap_c1.json")))
+    runs = {}
+    for mode, env in (("serial", {"AIWC_FIT_BATCH": "0"}), ("batched", {})):
+        r = subprocess.run([BIN, "heatmap"], capture_output=True, text=True, timeout=900,
+                           env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr
+        runs[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+        assert runs[mode]["evaluations"] == gold["evaluations"]
+        assert runs[mode]["cells"] == gold["cells"], mode
+    speedup = runs["serial"]["seconds"] / runs["batched"]["seconds"]
+    print(f"heatmap_scan: serial {runs['serial']['seconds']:.3f} s, batched "
+          f"{runs['batched']['seconds']:.3f} s, x{speedup:.2f}")
+    assert speedup > 3.0
