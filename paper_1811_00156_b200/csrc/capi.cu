@@ -285,7 +285,7 @@ struct aiwc_ctx {
     std::condition_variable cv;
     std::vector<FitRequest*> pending;
     bool leader = false;
-    size_t last_batch = 1;
+    size_t returning = 0;  // callers of the last batch that have not queued again yet
   } q;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
@@ -354,6 +354,12 @@ struct aiwc_forest {
   int node_bytes = 8;
   DevBuf<double> bleaves, bthr;
   DevBuf<uint32_t> broots, bthr_off;
+  // host copy of the node SoA + in-bag draws, made by a batched fit for each of its
+  // forests in one transfer (the batch's callers export them without device calls)
+  bool host_cached = false;
+  std::vector<int32_t> h_feature, h_left;
+  std::vector<double> h_thr, h_value;
+  std::vector<uint32_t> h_inbag;
   // few-row predictions (the reference's per-row predict_response / predict_time loops,
   // experiments.hpp:399-402): a stream, device buffers and pinned staging kept per forest
   std::mutex sm_mu;
@@ -1072,11 +1078,41 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
     std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> hold(F, aiwc_forest_free);
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dg(ctx->device);
+    // small batches (tuning loops on paper-sized tables): the whole batch's nodes and
+    // in-bag draws come to the host in one transfer each, so the callers' exports are
+    // plain copies
+    const uint64_t N = F->off.back();
+    const bool cache = N * 24 + uint64_t{total} * F->n * 4 < (uint64_t{256} << 20);
+    std::vector<int32_t> hf, hl;
+    std::vector<double> ht, hv;
+    std::vector<uint32_t> hi;
+    if (cache) {
+      hf.resize(N);
+      hl.resize(N);
+      ht.resize(N);
+      hv.resize(N);
+      hi.resize(size_t{total} * F->n);
+      d2h(hf.data(), F->feature.p, N * 4, ctx->stream);
+      d2h(hl.data(), F->left.p, N * 4, ctx->stream);
+      d2h(ht.data(), F->thr.p, N * 8, ctx->stream);
+      d2h(hv.data(), F->value.p, N * 8, ctx->stream);
+      d2h(hi.data(), F->inbag.p, hi.size() * 4, ctx->stream);
+    }
     uint32_t t0 = 0;
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t t1 = t0 + (te[i] - tb[i]);
       try {
-        batch[i]->out = split_cell(ctx, F, t0, t1, *batch[i], ctx->stream);
+        aiwc_forest* f = split_cell(ctx, F, t0, t1, *batch[i], ctx->stream);
+        batch[i]->out = f;
+        if (cache) {
+          const uint64_t b = F->off[t0], e = F->off[t1];
+          f->h_feature.assign(hf.begin() + b, hf.begin() + e);
+          f->h_left.assign(hl.begin() + b, hl.begin() + e);
+          f->h_thr.assign(ht.begin() + b, ht.begin() + e);
+          f->h_value.assign(hv.begin() + b, hv.begin() + e);
+          f->h_inbag.assign(hi.begin() + size_t{t0} * F->n, hi.begin() + size_t{t1} * F->n);
+          f->host_cached = true;
+        }
       } catch (const Status& e) {  // this forest alone (e.g. no out-of-bag rows)
         batch[i]->status = e.code;
         batch[i]->msg = e.msg;
@@ -1091,9 +1127,11 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
 }
 
 // Queue a fit on ctx and return when it is grown.  The first caller to find no leader
-// leads: it takes every queued request (after waiting up to AIWC_BATCH_WINDOW_US, default
-// 3000, for as many as the previous batch held) and runs them as one batch; the others
-// sleep until their request is done.  AIWC_FIT_BATCH=0 runs every fit alone.
+// leads: it takes every queued request and runs them as one batch -- after waiting (up to
+// AIWC_BATCH_WINDOW_US, default 20000) until every caller served by the previous batch has
+// queued again, so the threads of a tuning loop (one fit per step each) keep meeting in
+// one batch per step; a caller that stops costs one window.  The others sleep until their
+// request is done.  AIWC_FIT_BATCH=0 runs every fit alone.
 void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
   static const bool batching = [] {
     const char* e = std::getenv("AIWC_FIT_BATCH");
@@ -1101,11 +1139,12 @@ void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
   }();
   static const auto window = std::chrono::microseconds([] {
     const char* e = std::getenv("AIWC_BATCH_WINDOW_US");
-    return e ? std::atoll(e) : 3000ll;
+    return e ? std::atoll(e) : 20000ll;
   }());
   auto& q = ctx->q;
   std::unique_lock<std::mutex> lk(q.mu);
   q.pending.push_back(&req);
+  if (q.returning) --q.returning;
   q.cv.notify_all();
   while (!req.done) {
     if (q.leader) {
@@ -1113,8 +1152,9 @@ void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
       continue;
     }
     q.leader = true;
-    if (batching && q.last_batch > 1)
-      q.cv.wait_for(lk, window, [&] { return q.pending.size() >= q.last_batch; });
+    if (batching && q.returning &&
+        !q.cv.wait_for(lk, window, [&] { return q.returning == 0; }))
+      q.returning = 0;  // some caller stopped fitting
     std::vector<aiwc_ctx::FitRequest*> batch;
     if (batching) {
       batch.swap(q.pending);
@@ -1122,11 +1162,13 @@ void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
       batch.push_back(&req);
       q.pending.erase(std::find(q.pending.begin(), q.pending.end(), &req));
     }
-    q.last_batch = batch.size();
+
+    if (std::getenv("AIWC_VERBOSE")) std::fprintf(stderr, "[aiwc batch] %zu fits\n", batch.size());
     lk.unlock();
     fit_batch(ctx, batch);
     lk.lock();
     for (auto* r : batch) r->done = true;
+    if (batching) q.returning += batch.size();
     q.leader = false;
     q.cv.notify_all();
   }
@@ -1212,10 +1254,19 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
                        double* threshold, int32_t* left, int32_t* right, double* value) {
   return guard([&] {
     if (!f) throw Status(AIWC_EARG, "forest is NULL");
-    DeviceGuard dg(f->device);
     const uint64_t N = f->off.back();
-    Stream st;
     if (offsets) std::copy(f->off.begin(), f->off.end(), offsets);
+    if (f->host_cached) {  // a batched fit's forest: host copies made by the batch
+      if (feature) std::copy(f->h_feature.begin(), f->h_feature.end(), feature);
+      if (threshold) std::copy(f->h_thr.begin(), f->h_thr.end(), threshold);
+      if (left) std::copy(f->h_left.begin(), f->h_left.end(), left);
+      if (right)
+        for (uint64_t i = 0; i < N; ++i) right[i] = f->h_left[i] < 0 ? -1 : f->h_left[i] + 1;
+      if (value) std::copy(f->h_value.begin(), f->h_value.end(), value);
+      return;
+    }
+    DeviceGuard dg(f->device);
+    Stream st;
     if (feature) d2h(feature, f->feature.p, N * 4, st.s);
     if (threshold) d2h(threshold, f->thr.p, N * 8, st.s);
     if (left) d2h(left, f->left.p, N * 4, st.s);
@@ -1235,6 +1286,10 @@ int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag) {
   return guard([&] {
     if (!f || !inbag) throw Status(AIWC_EARG, "NULL argument");
     if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
+    if (f->host_cached) {
+      std::copy(f->h_inbag.begin(), f->h_inbag.end(), inbag);
+      return;
+    }
     DeviceGuard dg(f->device);
     Stream st;
     d2h(inbag, f->inbag.p, size_t{f->trees} * f->n * 4, st.s);
