@@ -46,8 +46,15 @@ template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
+  bool owned = true;  // false: a view into memory another object owns (never freed here)
   DevBuf() = default;
   explicit DevBuf(size_t c) { alloc(c); }
+  void view(T* q, size_t c) {
+    release();
+    p = q;
+    count = c;
+    owned = false;
+  }
   // stream-ordered allocation from the device's default pool (kept warm, see
   // warm_pool): fits in tuning loops allocate/free without device-wide syncs.  Every
   // API call synchronises its stream before returning, so a buffer is idle when freed.
@@ -57,23 +64,27 @@ struct DevBuf {
     count = c;
   }
   void release() {
-    if (p) cudaFreeAsync(p, 0);
+    if (p && owned) cudaFreeAsync(p, 0);
     p = nullptr;
     count = 0;
+    owned = true;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count), owned(o.owned) {
     o.p = nullptr;
     o.count = 0;
+    o.owned = true;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
     release();
     p = o.p;
     count = o.count;
+    owned = o.owned;
     o.p = nullptr;
     o.count = 0;
+    o.owned = true;
     return *this;
   }
 };
@@ -357,6 +368,9 @@ struct aiwc_forest {
   // host copy of the node SoA + in-bag draws, made by a batched fit for each of its
   // forests in one transfer (the batch's callers export them without device calls)
   bool host_cached = false;
+  // a forest split out of a batched fit views its parent's device arrays
+  std::shared_ptr<aiwc_forest> parent;
+  DevBuf<uint64_t> aux;  // (parent) the children's rebased per-tree node offsets
   std::vector<int32_t> h_feature, h_left;
   std::vector<double> h_thr, h_value;
   std::vector<uint32_t> h_inbag;
@@ -989,13 +1003,15 @@ extern "C" {
 
 namespace {
 
-// Forest c of a multi-forest fit (trees [t0, t1) of F) as a forest of its own: node SoA,
-// in-bag draws and OOB leaves copied device to device; OOB statistics when asked for.
-aiwc_forest* split_cell(aiwc_ctx* ctx, const aiwc_forest* F, uint32_t t0, uint32_t t1,
-                        const aiwc_ctx::FitRequest& r, cudaStream_t s) {
+// Forest c of a multi-forest fit (trees [t0, t1) of F) as a forest of its own: views of
+// F's node SoA, in-bag draws and OOB leaves (F stays alive while any child does);
+// d_off = the child's slice of F->aux (offsets rebased to the child's first node).
+aiwc_forest* split_cell(const std::shared_ptr<aiwc_forest>& F, uint32_t t0, uint32_t t1,
+                        uint64_t aux0, const aiwc_ctx::FitRequest& r) {
   auto f = std::make_unique<aiwc_forest>();
   const uint64_t n = F->n, b = F->off[t0], N = F->off[t1] - b;
   const uint32_t T = t1 - t0;
+  f->parent = F;
   f->device = F->device;
   f->n = n;
   f->trees = T;
@@ -1009,31 +1025,14 @@ aiwc_forest* split_cell(aiwc_ctx* ctx, const aiwc_forest* F, uint32_t t0, uint32
   f->grow_launches = F->grow_launches;
   f->off.resize(T + 1);
   for (uint32_t t = 0; t <= T; ++t) f->off[t] = F->off[t0 + t] - b;
-  f->feature.alloc(N);
-  f->left.alloc(N);
-  f->thr.alloc(N);
-  f->value.alloc(N);
-  f->d_off.alloc(T + 1);
-  CK(cudaMemcpyAsync(f->feature.p, F->feature.p + b, N * 4, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(f->left.p, F->left.p + b, N * 4, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(f->thr.p, F->thr.p + b, N * 8, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(f->value.p, F->value.p + b, N * 8, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, s));
-  f->inbag.alloc(size_t{T} * n);
-  f->oobleaf.alloc(size_t{T} * n);
+  f->feature.view(F->feature.p + b, N);
+  f->left.view(F->left.p + b, N);
+  f->thr.view(F->thr.p + b, N);
+  f->value.view(F->value.p + b, N);
+  f->d_off.view(F->aux.p + aux0, T + 1);
+  f->inbag.view(F->inbag.p + size_t{t0} * n, size_t{T} * n);
+  f->oobleaf.view(F->oobleaf.p + size_t{t0} * n, size_t{T} * n);
   f->oob_ctx = F->oob_ctx;
-  CK(cudaMemcpyAsync(f->inbag.p, F->inbag.p + size_t{t0} * n, size_t{T} * n * 4,
-                     cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(f->oobleaf.p, F->oobleaf.p + size_t{t0} * n, size_t{T} * n * 4,
-                     cudaMemcpyDeviceToDevice, s));
-  CK(cudaStreamSynchronize(s));
-  if (r.compute_oob && r.tb == 0 && r.te == r.num_trees) {
-    std::vector<double> sum(n, 0.0);
-    std::vector<uint32_t> count(n, 0);
-    oob_accumulate_device(f.get(), sum.data(), count.data(), s);
-    f->oob = finalize_oob(ctx->y.data(), n, sum.data(), count.data());
-    f->has_oob = true;
-  }
   return f.release();
 }
 
@@ -1075,14 +1074,24 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
     const CellSpec cs{k, m.data(), mn.data(), sd.data(), tb.data(), te.data()};
     aiwc_forest* F = nullptr;
     fit_body(ctx, total, mmax, nmin, sd[0], 0, total, 0, &cs, &F);
-    std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> hold(F, aiwc_forest_free);
+    const std::shared_ptr<aiwc_forest> Fs(F, [](aiwc_forest* x) { aiwc_forest_free(x); });
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dg(ctx->device);
+    const cudaStream_t st = ctx->stream;
+    const uint64_t n = F->n;
+    // children's rebased node offsets, one upload
+    std::vector<uint64_t> aux;
+    std::vector<uint32_t> t0s(k + 1, 0);
+    for (uint32_t i = 0; i < k; ++i) t0s[i + 1] = t0s[i] + (te[i] - tb[i]);
+    for (uint32_t i = 0; i < k; ++i)
+      for (uint32_t t = t0s[i]; t <= t0s[i + 1]; ++t) aux.push_back(F->off[t] - F->off[t0s[i]]);
+    F->aux.alloc(aux.size());
+    CK(cudaMemcpyAsync(F->aux.p, aux.data(), aux.size() * 8, cudaMemcpyHostToDevice, st));
     // small batches (tuning loops on paper-sized tables): the whole batch's nodes and
     // in-bag draws come to the host in one transfer each, so the callers' exports are
     // plain copies
     const uint64_t N = F->off.back();
-    const bool cache = N * 24 + uint64_t{total} * F->n * 4 < (uint64_t{256} << 20);
+    const bool cache = N * 24 + uint64_t{total} * n * 4 < (uint64_t{256} << 20);
     std::vector<int32_t> hf, hl;
     std::vector<double> ht, hv;
     std::vector<uint32_t> hi;
@@ -1091,34 +1100,70 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
       hl.resize(N);
       ht.resize(N);
       hv.resize(N);
-      hi.resize(size_t{total} * F->n);
-      d2h(hf.data(), F->feature.p, N * 4, ctx->stream);
-      d2h(hl.data(), F->left.p, N * 4, ctx->stream);
-      d2h(ht.data(), F->thr.p, N * 8, ctx->stream);
-      d2h(hv.data(), F->value.p, N * 8, ctx->stream);
-      d2h(hi.data(), F->inbag.p, hi.size() * 4, ctx->stream);
+      hi.resize(size_t{total} * n);
+      d2h(hf.data(), F->feature.p, N * 4, st);
+      d2h(hl.data(), F->left.p, N * 4, st);
+      d2h(ht.data(), F->thr.p, N * 8, st);
+      d2h(hv.data(), F->value.p, N * 8, st);
+      d2h(hi.data(), F->inbag.p, hi.size() * 4, st);
     }
-    uint32_t t0 = 0;
+    std::vector<aiwc_forest*> kids(k, nullptr);
+    uint64_t a0 = 0;
     for (uint32_t i = 0; i < k; ++i) {
-      const uint32_t t1 = t0 + (te[i] - tb[i]);
-      try {
-        aiwc_forest* f = split_cell(ctx, F, t0, t1, *batch[i], ctx->stream);
-        batch[i]->out = f;
-        if (cache) {
-          const uint64_t b = F->off[t0], e = F->off[t1];
-          f->h_feature.assign(hf.begin() + b, hf.begin() + e);
-          f->h_left.assign(hl.begin() + b, hl.begin() + e);
-          f->h_thr.assign(ht.begin() + b, ht.begin() + e);
-          f->h_value.assign(hv.begin() + b, hv.begin() + e);
-          f->h_inbag.assign(hi.begin() + size_t{t0} * F->n, hi.begin() + size_t{t1} * F->n);
-          f->host_cached = true;
-        }
-      } catch (const Status& e) {  // this forest alone (e.g. no out-of-bag rows)
-        batch[i]->status = e.code;
-        batch[i]->msg = e.msg;
+      const uint32_t t0 = t0s[i], t1 = t0s[i + 1];
+      aiwc_forest* f = split_cell(Fs, t0, t1, a0, *batch[i]);
+      a0 += t1 - t0 + 1;
+      kids[i] = f;
+      batch[i]->out = f;
+      if (cache) {
+        const uint64_t b = F->off[t0], e = F->off[t1];
+        f->h_feature.assign(hf.begin() + b, hf.begin() + e);
+        f->h_left.assign(hl.begin() + b, hl.begin() + e);
+        f->h_thr.assign(ht.begin() + b, ht.begin() + e);
+        f->h_value.assign(hv.begin() + b, hv.begin() + e);
+        f->h_inbag.assign(hi.begin() + size_t{t0} * n, hi.begin() + size_t{t1} * n);
+        f->host_cached = true;
       }
-      t0 = t1;
     }
+    // OOB statistics of every forest that asks for them: one tree-ordered reduction per
+    // forest into one buffer, one transfer, the reference's row-order finalisation each
+    DevBuf<double> sums(size_t{k} * n);
+    DevBuf<uint32_t> cnts(size_t{k} * n);
+    CK(cudaMemsetAsync(sums.p, 0, size_t{k} * n * 8, st));
+    CK(cudaMemsetAsync(cnts.p, 0, size_t{k} * n * 4, st));
+    bool any = false;
+    for (uint32_t i = 0; i < k; ++i) {
+      const auto& r = *batch[i];
+      if (!(r.compute_oob && r.tb == 0 && r.te == r.num_trees)) continue;
+      any = true;
+      oob_reduce_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+          kids[i]->oobleaf.p, kids[i]->d_off.p, kids[i]->value.p, kids[i]->trees, n,
+          sums.p + size_t{i} * n, cnts.p + size_t{i} * n);
+      CK(cudaGetLastError());
+      g_launches += 1;
+    }
+    if (any) {
+      std::vector<double> hs(size_t{k} * n);
+      std::vector<uint32_t> hc(size_t{k} * n);
+      CK(cudaMemcpyAsync(hs.data(), sums.p, hs.size() * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hc.data(), cnts.p, hc.size() * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (uint32_t i = 0; i < k; ++i) {
+        const auto& r = *batch[i];
+        if (!(r.compute_oob && r.tb == 0 && r.te == r.num_trees)) continue;
+        try {
+          kids[i]->oob = finalize_oob(ctx->y.data(), n, hs.data() + size_t{i} * n,
+                                      hc.data() + size_t{i} * n);
+          kids[i]->has_oob = true;
+        } catch (const Status& e) {  // this forest alone (no out-of-bag rows)
+          aiwc_forest_free(kids[i]);
+          batch[i]->out = nullptr;
+          batch[i]->status = e.code;
+          batch[i]->msg = e.msg;
+        }
+      }
+    }
+    CK(cudaStreamSynchronize(st));
   } catch (const Status& e) {
     fail_all(e.code, e.msg);
   } catch (const std::exception& e) {
