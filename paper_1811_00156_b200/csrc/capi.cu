@@ -155,6 +155,39 @@ struct PinnedFlags {
   uint32_t* get() const { return p; }
 };
 
+// pinned host buffers recycled process-wide (cudaMallocHost pins pages: milliseconds)
+struct PinnedPool {
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::vector<std::pair<char*, size_t>>& free_list() {
+    static std::vector<std::pair<char*, size_t>> v;
+    return v;
+  }
+  static std::pair<char*, size_t> take(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu());
+      auto& v = free_list();
+      for (size_t i = 0; i < v.size(); ++i)
+        if (v[i].second >= bytes) {
+          auto r = v[i];
+          v.erase(v.begin() + static_cast<long>(i));
+          return r;
+        }
+    }
+    char* p = nullptr;
+    const size_t cap = std::max<size_t>(bytes + bytes / 2, size_t{1} << 20);
+    CK(cudaMallocHost(reinterpret_cast<void**>(&p), cap));
+    return {p, cap};
+  }
+  static void give(std::pair<char*, size_t> b) {
+    if (!b.first) return;
+    std::lock_guard<std::mutex> g(mu());
+    free_list().push_back(b);
+  }
+};
+
 // host threads for the pinned <-> pageable copies (AIWC_COPY_THREADS, default 16)
 unsigned copy_threads() {
   static const unsigned n = [] {
@@ -368,12 +401,13 @@ struct aiwc_forest {
   // host copy of the node SoA + in-bag draws, made by a batched fit for each of its
   // forests in one transfer (the batch's callers export them without device calls)
   bool host_cached = false;
+  const int32_t *h_feature = nullptr, *h_left = nullptr;  // into the parent's pinned copy
+  const double *h_thr = nullptr, *h_value = nullptr;
+  const uint32_t* h_inbag = nullptr;
+  std::pair<char*, size_t> pinned{nullptr, 0};  // (parent) that copy, back to PinnedPool
   // a forest split out of a batched fit views its parent's device arrays
   std::shared_ptr<aiwc_forest> parent;
   DevBuf<uint64_t> aux;  // (parent) the children's rebased per-tree node offsets
-  std::vector<int32_t> h_feature, h_left;
-  std::vector<double> h_thr, h_value;
-  std::vector<uint32_t> h_inbag;
   // few-row predictions (the reference's per-row predict_response / predict_time loops,
   // experiments.hpp:399-402): a stream, device buffers and pinned staging kept per forest
   std::mutex sm_mu;
@@ -384,6 +418,7 @@ struct aiwc_forest {
   ~aiwc_forest() {
     if (sm_stream) cudaStreamDestroy(sm_stream);
     if (sm_pin) cudaFreeHost(sm_pin);
+    PinnedPool::give(pinned);
   }
 };
 
@@ -1073,7 +1108,10 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
     }
     const CellSpec cs{k, m.data(), mn.data(), sd.data(), tb.data(), te.data()};
     aiwc_forest* F = nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto c0 = clk::now();
     fit_body(ctx, total, mmax, nmin, sd[0], 0, total, 0, &cs, &F);
+    const auto c1 = clk::now();
     const std::shared_ptr<aiwc_forest> Fs(F, [](aiwc_forest* x) { aiwc_forest_free(x); });
     std::lock_guard<std::mutex> lock(ctx->mu);
     DeviceGuard dg(ctx->device);
@@ -1091,22 +1129,26 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
     // in-bag draws come to the host in one transfer each, so the callers' exports are
     // plain copies
     const uint64_t N = F->off.back();
-    const bool cache = N * 24 + uint64_t{total} * n * 4 < (uint64_t{256} << 20);
-    std::vector<int32_t> hf, hl;
-    std::vector<double> ht, hv;
-    std::vector<uint32_t> hi;
-    if (cache) {
-      hf.resize(N);
-      hl.resize(N);
-      ht.resize(N);
-      hv.resize(N);
-      hi.resize(size_t{total} * n);
-      d2h(hf.data(), F->feature.p, N * 4, st);
-      d2h(hl.data(), F->left.p, N * 4, st);
-      d2h(ht.data(), F->thr.p, N * 8, st);
-      d2h(hv.data(), F->value.p, N * 8, st);
-      d2h(hi.data(), F->inbag.p, hi.size() * 4, st);
+    const size_t cbytes = N * 24 + size_t{total} * n * 4;
+    const bool cache = cbytes < (size_t{256} << 20);
+    int32_t *hf = nullptr, *hl = nullptr;
+    double *ht = nullptr, *hv = nullptr;
+    uint32_t* hi = nullptr;
+    if (cache) {  // straight DMA into a pinned buffer the batch forest owns
+      F->pinned = PinnedPool::take(cbytes);
+      ht = reinterpret_cast<double*>(F->pinned.first);
+      hv = ht + N;
+      hf = reinterpret_cast<int32_t*>(hv + N);
+      hl = hf + N;
+      hi = reinterpret_cast<uint32_t*>(hl + N);
+      CK(cudaMemcpyAsync(ht, F->thr.p, N * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hv, F->value.p, N * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hf, F->feature.p, N * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hl, F->left.p, N * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hi, F->inbag.p, size_t{total} * n * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
     }
+    const auto c2 = clk::now();
     std::vector<aiwc_forest*> kids(k, nullptr);
     uint64_t a0 = 0;
     for (uint32_t i = 0; i < k; ++i) {
@@ -1117,14 +1159,15 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
       batch[i]->out = f;
       if (cache) {
         const uint64_t b = F->off[t0], e = F->off[t1];
-        f->h_feature.assign(hf.begin() + b, hf.begin() + e);
-        f->h_left.assign(hl.begin() + b, hl.begin() + e);
-        f->h_thr.assign(ht.begin() + b, ht.begin() + e);
-        f->h_value.assign(hv.begin() + b, hv.begin() + e);
-        f->h_inbag.assign(hi.begin() + size_t{t0} * n, hi.begin() + size_t{t1} * n);
+        f->h_feature = hf + b;
+        f->h_left = hl + b;
+        f->h_thr = ht + b;
+        f->h_value = hv + b;
+        f->h_inbag = hi + size_t{t0} * n;
         f->host_cached = true;
       }
     }
+    const auto c3 = clk::now();
     // OOB statistics of every forest that asks for them: one tree-ordered reduction per
     // forest into one buffer, one transfer, the reference's row-order finalisation each
     DevBuf<double> sums(size_t{k} * n);
@@ -1164,6 +1207,11 @@ void fit_batch(aiwc_ctx* ctx, const std::vector<aiwc_ctx::FitRequest*>& batch) {
       }
     }
     CK(cudaStreamSynchronize(st));
+    if (std::getenv("AIWC_VERBOSE")) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[aiwc batch split] fit_body %.2f, aux+host copy %.2f, children %.2f, oob %.2f ms\n",
+                   ms(c0, c1), ms(c1, c2), ms(c2, c3), ms(c3, clk::now()));
+    }
   } catch (const Status& e) {
     fail_all(e.code, e.msg);
   } catch (const std::exception& e) {
@@ -1197,9 +1245,11 @@ void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
       continue;
     }
     q.leader = true;
+    const auto tw = std::chrono::steady_clock::now();
     if (batching && q.returning &&
         !q.cv.wait_for(lk, window, [&] { return q.returning == 0; }))
       q.returning = 0;  // some caller stopped fitting
+    const auto tw1 = std::chrono::steady_clock::now();
     std::vector<aiwc_ctx::FitRequest*> batch;
     if (batching) {
       batch.swap(q.pending);
@@ -1208,9 +1258,12 @@ void submit_fit(aiwc_ctx* ctx, aiwc_ctx::FitRequest& req) {
       q.pending.erase(std::find(q.pending.begin(), q.pending.end(), &req));
     }
 
-    if (std::getenv("AIWC_VERBOSE")) std::fprintf(stderr, "[aiwc batch] %zu fits\n", batch.size());
     lk.unlock();
     fit_batch(ctx, batch);
+    if (std::getenv("AIWC_VERBOSE"))
+      std::fprintf(stderr, "[aiwc batch] %zu fits: waited %.2f ms, ran %.2f ms\n", batch.size(),
+                   std::chrono::duration<double, std::milli>(tw1 - tw).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tw1).count());
     lk.lock();
     for (auto* r : batch) r->done = true;
     if (batching) q.returning += batch.size();
@@ -1301,13 +1354,13 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
     if (!f) throw Status(AIWC_EARG, "forest is NULL");
     const uint64_t N = f->off.back();
     if (offsets) std::copy(f->off.begin(), f->off.end(), offsets);
-    if (f->host_cached) {  // a batched fit's forest: host copies made by the batch
-      if (feature) std::copy(f->h_feature.begin(), f->h_feature.end(), feature);
-      if (threshold) std::copy(f->h_thr.begin(), f->h_thr.end(), threshold);
-      if (left) std::copy(f->h_left.begin(), f->h_left.end(), left);
+    if (f->host_cached) {  // a batched fit's forest: the batch's pinned host copy
+      if (feature) std::memcpy(feature, f->h_feature, N * 4);
+      if (threshold) std::memcpy(threshold, f->h_thr, N * 8);
+      if (left) std::memcpy(left, f->h_left, N * 4);
       if (right)
         for (uint64_t i = 0; i < N; ++i) right[i] = f->h_left[i] < 0 ? -1 : f->h_left[i] + 1;
-      if (value) std::copy(f->h_value.begin(), f->h_value.end(), value);
+      if (value) std::memcpy(value, f->h_value, N * 8);
       return;
     }
     DeviceGuard dg(f->device);
@@ -1332,7 +1385,7 @@ int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag) {
     if (!f || !inbag) throw Status(AIWC_EARG, "NULL argument");
     if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
     if (f->host_cached) {
-      std::copy(f->h_inbag.begin(), f->h_inbag.end(), inbag);
+      std::memcpy(inbag, f->h_inbag, size_t{f->trees} * f->n * 4);
       return;
     }
     DeviceGuard dg(f->device);
