@@ -396,6 +396,7 @@ struct aiwc_forest {
   DevBuf<BinNode> bnodes;
   DevBuf<uint32_t> bnodes4;  // packed 4-byte nodes (node_bytes == 4)
   int node_bytes = 8;
+  PredFmt fmt{};  // their field layout
   DevBuf<double> bleaves, bthr;
   DevBuf<uint32_t> broots, bthr_off;
   // host copy of the node SoA + in-bag draws, made by a batched fit for each of its
@@ -1703,11 +1704,23 @@ void build_binned(aiwc_forest* f, uint32_t p) {
   }
   if (maxT >= 0xffff) return;
   f->bin_bytes = maxT < 0xff ? 1 : 2;
-  const size_t tile = size_t{kPredNT} * kPredictQ * p * f->bin_bytes;
+  // one tile of warp-transposed bins (whole 32-query groups)
+  const size_t tile = bin_words(uint64_t{kPredNT} * kPredictQ, p, f->bin_bytes) * 4;
   if (tile + 4096 > kPredSmem) return;
   const size_t budget = kPredSmem - tile - 64;
-  // packed 4-byte nodes: column < 127, bin < 256, chunk-relative indices < 2^17
-  const bool node4 = p < 127 && maxT <= 256 && std::getenv("AIWC_PRED_NODE8") == nullptr;
+  // packed 4-byte nodes: field widths fitted to the forest -- cb column bits (all ones
+  // marks a leaf, so p <= 2^cb - 1), bb bits for the largest threshold index, the rest
+  // for chunk-relative child / leaf indices
+  auto bits = [](uint64_t v) {
+    uint32_t b = 1;
+    while ((uint64_t{1} << b) <= v) ++b;
+    return b;
+  };
+  const uint32_t cb = bits(p), bbits = bits(maxT ? maxT - 1 : 0);
+  const uint32_t chbits = cb + bbits < 32 ? 32 - cb - bbits : 0;
+  const uint64_t chmax = chbits >= 32 ? UINT32_MAX : (uint64_t{1} << chbits);
+  const bool node4 = chbits >= 12 && std::getenv("AIWC_PRED_NODE8") == nullptr;
+  f->fmt = PredFmt{cb, bbits, cb + bbits, (1u << cb) - 1u, (1u << bbits) - 1u};
   const size_t nb = node4 ? 4 : sizeof(BinNode);
   std::vector<double> thr_all;
   for (auto& v : T) thr_all.insert(thr_all.end(), v.begin(), v.end());
@@ -1721,11 +1734,13 @@ void build_binned(aiwc_forest* f, uint32_t p) {
     uint32_t nl = 0;
     for (uint64_t i = b; i < e; ++i) nl += fe[i] < 0;
     const size_t need = (ch.nnodes + (e - b)) * nb + 32 + (ch.nleaves + nl) * 8;
-    if (ch.ntrees > 0 && need > budget) {
+    const bool idx_full = node4 && (ch.nnodes + (e - b) >= chmax || ch.nleaves + nl >= chmax);
+    if (ch.ntrees > 0 && (need > budget || idx_full)) {
       f->chunks.push_back(ch);
       ch = aiwc_forest::Chunk{nodes.size(), leaves.size(), roots.size(), 0, 0, 0};
     }
     if ((e - b) * nb + 16 + nl * 8 > budget) return;  // one tree too big
+    if (node4 && (e - b >= chmax || nl >= chmax)) return;
     roots.push_back(ch.nnodes);
     for (uint64_t i = b; i < e; ++i) {
       const uint32_t local = static_cast<uint32_t>(i - b) + ch.nnodes;
@@ -1749,11 +1764,12 @@ void build_binned(aiwc_forest* f, uint32_t p) {
   if (node4) {
     std::vector<uint32_t> n4(nodes.size());
     bool ok = true;
+    const PredFmt& fm = f->fmt;
     for (size_t i = 0; i < nodes.size(); ++i) {
       const BinNode& v = nodes[i];
-      if (v.child >= (1u << 17)) ok = false;
-      n4[i] = v.feat == 0xffff ? (127u | (v.child << 15))
-                               : (v.feat | (uint32_t{v.j} << 7) | (v.child << 15));
+      if (v.child >= chmax) ok = false;
+      n4[i] = v.feat == 0xffff ? (fm.cmask | (v.child << fm.sh))
+                               : (v.feat | (uint32_t{v.j} << fm.cb) | (v.child << fm.sh));
     }
     if (ok) {
       f->node_bytes = 4;
@@ -1780,19 +1796,19 @@ void build_binned(aiwc_forest* f, uint32_t p) {
 // scratch of the binned path for up to q rows (bins + running sums); kernels using it
 // must have finished before it is freed (DevBuf frees on the legacy stream)
 struct PredScratch {
-  DevBuf<uint8_t> bins;
+  DevBuf<uint32_t> bins;  // warp-transposed (bin_words)
   DevBuf<double> sum;
   void reserve(uint64_t q, uint32_t p) {
-    if (bins.count < q * p * 2) bins.alloc(q * p * 2);
+    const uint64_t w = bin_words(q, p, 2);
+    if (bins.count < w) bins.alloc(w);
     if (sum.count < q) sum.alloc(q);
   }
 };
 
 void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p, double* d_out,
                     cudaStream_t s, PredScratch& sc) {
-  const size_t bb = f->bin_bytes;
   sc.reserve(q, p);
-  uint8_t* const bins = sc.bins.p;
+  uint32_t* const bins = sc.bins.p;
   double* const sum = sc.sum.p;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, f->device));
@@ -1804,13 +1820,14 @@ void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p
     const auto& ch = f->chunks[k];
     const size_t smem = ((size_t{ch.nnodes} * f->node_bytes + 15) & ~size_t{15}) +
                         ((size_t{ch.nleaves} * 8 + 15) & ~size_t{15}) +
-                        size_t{kPredNT} * kPredictQ * p * bb;
+                        bin_words(uint64_t{kPredNT} * kPredictQ, p, f->bin_bytes) * 4;
     const void* nodes = f->node_bytes == 4 ? static_cast<const void*>(f->bnodes4.p + ch.node0)
                                            : static_cast<const void*>(f->bnodes.p + ch.node0);
     CK(launch_predict_chunk(f->bin_bytes, f->node_bytes, nodes, ch.nnodes,
                             f->bleaves.p + ch.leaf0, ch.nleaves, f->broots.p + ch.root0, ch.ntrees,
                             bins, q, p, sum, k == 0, k + 1 == f->chunks.size(),
-                            static_cast<double>(f->trees), d_out, grid, smem, kPredSmem, s));
+                            static_cast<double>(f->trees), d_out, grid, smem, kPredSmem, f->fmt,
+                            s));
     g_launches += 1;
   }
 }

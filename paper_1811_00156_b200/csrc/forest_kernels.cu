@@ -261,108 +261,121 @@ __global__ void rank_best_kernel(const double* __restrict__ resp, uint64_t q, ui
 // Threshold binning: with T_c the sorted distinct thresholds the forest uses on column
 // c and thr = T_c[j],  x <= thr  <=>  #{t in T_c : t < x} <= j.  NaN goes to the
 // largest bin (every comparison false -> right child, as in Tree::predict).
+//
+// Bins are stored warp-transposed: per group of 32 queries, word k of query l (bins
+// k*E .. k*E+E-1, E = 4 / sizeof(BinT)) at group*W*32 + k*32 + l.  A warp's 32 queries
+// then read their bins from 32 different banks whatever columns they test -- no shared-
+// memory bank conflicts in the tree walks (row-major bins cost 2.15 wavefronts/load).
 template <typename BinT>
 __global__ void bin_queries_kernel(const double* __restrict__ rows, uint64_t q, uint32_t p,
                                    const double* __restrict__ thr,
-                                   const uint32_t* __restrict__ thr_off, BinT* __restrict__ bins) {
-  const uint64_t total = q * p;
+                                   const uint32_t* __restrict__ thr_off,
+                                   uint32_t* __restrict__ bins) {
+  constexpr uint32_t E = 4 / sizeof(BinT);
+  const uint32_t W = (p + E - 1) / E;
+  const uint64_t groups = (q + 31) / 32, total = groups * W * 32;
   for (uint64_t g = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; g < total;
        g += uint64_t{gridDim.x} * blockDim.x) {
-    const uint32_t c = static_cast<uint32_t>(g % p);
-    const double x = rows[g];
-    const double* t = thr + thr_off[c];
-    uint32_t lo = 0, hi = thr_off[c + 1] - thr_off[c];
-    if (x != x) {
-      lo = sizeof(BinT) == 1 ? 0xffu : 0xffffu;
-    } else {
-      while (lo < hi) {  // first index with t >= x == count of thresholds < x
-        const uint32_t mid = (lo + hi) >> 1;
-        if (t[mid] < x) lo = mid + 1; else hi = mid;
+    const uint64_t grp = g / (uint64_t{W} * 32);
+    const uint32_t rem = static_cast<uint32_t>(g - grp * W * 32), k = rem / 32, l = rem % 32;
+    const uint64_t qi = grp * 32 + l;
+    uint32_t word = 0;
+    for (uint32_t e = 0; e < E; ++e) {
+      const uint32_t c = k * E + e;
+      if (c >= p || qi >= q) break;
+      const double x = rows[qi * p + c];
+      const double* t = thr + thr_off[c];
+      uint32_t lo = 0, hi = thr_off[c + 1] - thr_off[c];
+      if (x != x) {
+        lo = sizeof(BinT) == 1 ? 0xffu : 0xffffu;
+      } else {
+        while (lo < hi) {  // first index with t >= x == count of thresholds < x
+          const uint32_t mid = (lo + hi) >> 1;
+          if (t[mid] < x) lo = mid + 1; else hi = mid;
+        }
       }
+      word |= lo << (8 * sizeof(BinT) * e);
     }
-    bins[g] = static_cast<BinT>(lo);
+    bins[g] = word;
   }
 }
 
-// Node accessors: 8-byte BinNode, or the packed 4-byte form (bits 0-6 column, 127 =
-// leaf; bits 7-14 threshold bin; bits 15-31 chunk-relative left child / leaf index)
-// used when the schema and the chunk are small enough -- half the shared-memory
-// wavefronts per visit and twice the trees per chunk.
+// Node accessors: 8-byte BinNode, or the packed 4-byte form -- column in the low cb
+// bits (all ones = leaf), threshold bin in the next bb bits, chunk-relative left child
+// (right = left + 1) or leaf index in the rest; widths fit the forest (PredFmt) --
+// half the shared-memory wavefronts per visit and twice the trees per chunk.
 struct Node8 {
   using T = BinNode;
-  static __device__ __forceinline__ bool leaf(const BinNode& v) { return v.feat == 0xffffu; }
-  static __device__ __forceinline__ uint32_t feat(const BinNode& v) { return v.feat; }
-  static __device__ __forceinline__ uint32_t j(const BinNode& v) { return v.j; }
-  static __device__ __forceinline__ uint32_t child(const BinNode& v) { return v.child; }
+  static __device__ __forceinline__ bool leaf(const BinNode& v, PredFmt) { return v.feat == 0xffffu; }
+  static __device__ __forceinline__ uint32_t feat(const BinNode& v, PredFmt) { return v.feat; }
+  static __device__ __forceinline__ uint32_t j(const BinNode& v, PredFmt) { return v.j; }
+  static __device__ __forceinline__ uint32_t child(const BinNode& v, PredFmt) { return v.child; }
 };
 struct Node4 {
   using T = uint32_t;
-  static __device__ __forceinline__ bool leaf(uint32_t v) { return (v & 127u) == 127u; }
-  static __device__ __forceinline__ uint32_t feat(uint32_t v) { return v & 127u; }
-  static __device__ __forceinline__ uint32_t j(uint32_t v) { return (v >> 7) & 255u; }
-  static __device__ __forceinline__ uint32_t child(uint32_t v) { return v >> 15; }
+  static __device__ __forceinline__ bool leaf(uint32_t v, PredFmt f) {
+    return (v & f.cmask) == f.cmask;
+  }
+  static __device__ __forceinline__ uint32_t feat(uint32_t v, PredFmt f) { return v & f.cmask; }
+  static __device__ __forceinline__ uint32_t j(uint32_t v, PredFmt f) {
+    return (v >> f.cb) & f.bmask;
+  }
+  static __device__ __forceinline__ uint32_t child(uint32_t v, PredFmt f) { return v >> f.sh; }
 };
 
 // One launch per tree chunk: the chunk's nodes and leaf values sit in shared memory,
 // every query walks the chunk's trees in order, continuing its running sum from the
 // previous chunk (so the per-query sum keeps the reference's tree order exactly).
-// A tile holds Q*NT queries; thread t walks queries t, t+NT, ... of it as Q independent
-// node chains, so their shared-memory latencies overlap.
+// A tile holds Q*NT queries (whole 32-query groups of the transposed bins); thread t
+// walks queries t, t+NT, ... of it as Q independent node chains.
 template <typename BinT, typename NA, int NT, int Q>
 __global__ void __launch_bounds__(NT, 1)
     predict_chunk_kernel(const typename NA::T* __restrict__ nodes, uint32_t nnodes,
                          const double* __restrict__ leaves, uint32_t nleaves,
                          const uint32_t* __restrict__ roots, uint32_t ntrees,
-                         const BinT* __restrict__ bins, uint64_t q, uint32_t p,
+                         const uint32_t* __restrict__ bins, uint64_t q, uint32_t p,
                          double* __restrict__ sum, int first, int last, double total_trees,
-                         double* __restrict__ out) {
+                         double* __restrict__ out, PredFmt fmt) {
   using NodeT = typename NA::T;
   constexpr uint32_t TQ = NT * Q;
+  constexpr uint32_t E = 4 / sizeof(BinT);
+  const uint32_t W = (p + E - 1) / E;  // bin words per query
   extern __shared__ __align__(16) unsigned char smem[];
   NodeT* sn = reinterpret_cast<NodeT*>(smem);
   double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(NodeT) + 15) & ~size_t{15}));
-  BinT* sb = reinterpret_cast<BinT*>(reinterpret_cast<unsigned char*>(sl) +
-                                     ((size_t{nleaves} * 8 + 15) & ~size_t{15}));
+  uint32_t* sb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sl) +
+                                             ((size_t{nleaves} * 8 + 15) & ~size_t{15}));
   for (uint32_t i = threadIdx.x; i < nnodes; i += NT) sn[i] = nodes[i];
   for (uint32_t i = threadIdx.x; i < nleaves; i += NT) sl[i] = leaves[i];
+  const unsigned lane = threadIdx.x & 31u;
   for (uint64_t tile = uint64_t{blockIdx.x} * TQ; tile < q; tile += uint64_t{gridDim.x} * TQ) {
     __syncthreads();
     const uint64_t rem = q - tile;
     const uint32_t cnt = rem < TQ ? static_cast<uint32_t>(rem) : TQ;
-    {  // stage the tile's bins: 16-byte vector copies, all of a thread's loads in flight
-      const size_t bytes = size_t{cnt} * p * sizeof(BinT);
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(bins + tile * p);
-      unsigned char* dst = reinterpret_cast<unsigned char*>(sb);
-      const bool vec = (reinterpret_cast<uintptr_t>(src) & 15u) == 0 &&
-                       (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
-      size_t done16 = 0;
-      if (vec) {
-        const size_t n16 = bytes / 16;
-        const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        uint4* d4 = reinterpret_cast<uint4*>(dst);
-        size_t i = threadIdx.x;
-        for (; i + 3 * NT < n16; i += 4 * NT) {
-          const uint4 a0 = __ldg(s4 + i), a1 = __ldg(s4 + i + NT), a2 = __ldg(s4 + i + 2 * NT),
-                      a3 = __ldg(s4 + i + 3 * NT);
-          d4[i] = a0;
-          d4[i + NT] = a1;
-          d4[i + 2 * NT] = a2;
-          d4[i + 3 * NT] = a3;
-        }
-        for (; i < n16; i += NT) d4[i] = __ldg(s4 + i);
-        done16 = n16 * 16;
+    {  // stage the tile's groups of transposed bins: 16-byte copies, 4 in flight
+      const size_t n16 = size_t{(cnt + 31) / 32} * W * 32 / 4;
+      const uint4* s4 = reinterpret_cast<const uint4*>(bins + (tile / 32) * W * 32);
+      uint4* d4 = reinterpret_cast<uint4*>(sb);
+      size_t i = threadIdx.x;
+      for (; i + 3 * NT < n16; i += 4 * NT) {
+        const uint4 a0 = __ldg(s4 + i), a1 = __ldg(s4 + i + NT), a2 = __ldg(s4 + i + 2 * NT),
+                    a3 = __ldg(s4 + i + 3 * NT);
+        d4[i] = a0;
+        d4[i + NT] = a1;
+        d4[i + 2 * NT] = a2;
+        d4[i + 3 * NT] = a3;
       }
-      for (size_t i = done16 + threadIdx.x; i < bytes; i += NT) dst[i] = src[i];
+      for (; i < n16; i += NT) d4[i] = __ldg(s4 + i);
     }
     __syncthreads();
     if (threadIdx.x >= cnt) continue;
-    const BinT* bq[Q];
+    const uint32_t* bq[Q];
     double s[Q];
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
       // a query slot past the tile's end re-walks query threadIdx.x (result dropped)
       const uint32_t qi = threadIdx.x + u * NT < cnt ? threadIdx.x + u * NT : threadIdx.x;
-      bq[u] = sb + qi * p;
+      bq[u] = sb + (qi / 32) * W * 32 + lane;
       s[u] = first ? 0.0 : sum[tile + qi];
     }
     for (uint32_t t = 0; t < ntrees; ++t) {
@@ -374,24 +387,27 @@ __global__ void __launch_bounds__(NT, 1)
       for (int u = 0; u < Q; ++u) {
         idx[u] = r;
         v[u] = sn[r];
-        done = done && NA::leaf(v[u]);
+        done = done && NA::leaf(v[u], fmt);
       }
       while (!done) {
         done = true;
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
-          const bool lf = NA::leaf(v[u]);
-          const uint32_t bin = bq[u][lf ? 0u : NA::feat(v[u])];
-          idx[u] = lf ? idx[u] : NA::child(v[u]) + (bin <= NA::j(v[u]) ? 0u : 1u);
+          const bool lf = NA::leaf(v[u], fmt);
+          const uint32_t f = lf ? 0u : NA::feat(v[u], fmt);
+          const uint32_t w = bq[u][(f / E) * 32];
+          const uint32_t bin = sizeof(BinT) == 1 ? (w >> (8 * (f % E))) & 0xffu
+                                                 : (w >> (16 * (f % E))) & 0xffffu;
+          idx[u] = lf ? idx[u] : NA::child(v[u], fmt) + (bin <= NA::j(v[u], fmt) ? 0u : 1u);
         }
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
           v[u] = sn[idx[u]];
-          done = done && NA::leaf(v[u]);
+          done = done && NA::leaf(v[u], fmt);
         }
       }
 #pragma unroll
-      for (int u = 0; u < Q; ++u) s[u] = __dadd_rn(s[u], sl[NA::child(v[u])]);
+      for (int u = 0; u < Q; ++u) s[u] = __dadd_rn(s[u], sl[NA::child(v[u], fmt)]);
     }
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
@@ -410,24 +426,25 @@ namespace {
 template <typename BinT>
 cudaError_t bin_t(const double* rows, uint64_t q, uint32_t p, const double* thr,
                   const uint32_t* thr_off, void* bins, cudaStream_t s) {
-  const uint64_t blocks = (q * p + 255) / 256;
+  const uint64_t words = bin_words(q, p, sizeof(BinT));
+  const uint64_t blocks = (words + 255) / 256;
   bin_queries_kernel<BinT><<<static_cast<unsigned>(blocks < 524288 ? blocks : 524288), 256, 0,
-                             s>>>(rows, q, p, thr, thr_off, static_cast<BinT*>(bins));
+                             s>>>(rows, q, p, thr, thr_off, static_cast<uint32_t*>(bins));
   return cudaGetLastError();
 }
 template <typename BinT, typename NA>
 cudaError_t chunk_t(const void* nodes, uint32_t nnodes, const double* leaves, uint32_t nleaves,
                     const uint32_t* roots, uint32_t ntrees, const void* bins, uint64_t q,
                     uint32_t p, double* sum, int first, int last, double total_trees, double* out,
-                    unsigned grid, size_t smem, size_t smem_max, cudaStream_t s) {
+                    unsigned grid, size_t smem, size_t smem_max, PredFmt fmt, cudaStream_t s) {
   auto k = predict_chunk_kernel<BinT, NA, kPredictThreads, kPredictQ>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_max));
   if (e != cudaSuccess) return e;
   k<<<grid, kPredictThreads, smem, s>>>(static_cast<const typename NA::T*>(nodes), nnodes,
                                         leaves, nleaves, roots, ntrees,
-                                        static_cast<const BinT*>(bins), q, p, sum, first, last,
-                                        total_trees, out);
+                                        static_cast<const uint32_t*>(bins), q, p, sum, first,
+                                        last, total_trees, out, fmt);
   return cudaGetLastError();
 }
 }  // namespace
@@ -444,21 +461,22 @@ cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* node
                                  const uint32_t* roots, uint32_t ntrees, const void* bins,
                                  uint64_t q, uint32_t p, double* sum, int first, int last,
                                  double total_trees, double* out, unsigned grid, size_t smem,
-                                 size_t smem_max, cudaStream_t s) {
+                                 size_t smem_max, PredFmt fmt, cudaStream_t s) {
   if (node_bytes == 4)
     return bin_bytes == 1
                ? chunk_t<uint8_t, Node4>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q,
                                          p, sum, first, last, total_trees, out, grid, smem,
-                                         smem_max, s)
+                                         smem_max, fmt, s)
                : chunk_t<uint16_t, Node4>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q,
                                           p, sum, first, last, total_trees, out, grid, smem,
-                                          smem_max, s);
+                                          smem_max, fmt, s);
   return bin_bytes == 1
              ? chunk_t<uint8_t, Node8>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p,
-                                       sum, first, last, total_trees, out, grid, smem, smem_max, s)
+                                       sum, first, last, total_trees, out, grid, smem, smem_max,
+                                       fmt, s)
              : chunk_t<uint16_t, Node8>(nodes, nnodes, leaves, nleaves, roots, ntrees, bins, q, p,
                                         sum, first, last, total_trees, out, grid, smem, smem_max,
-                                        s);
+                                        fmt, s);
 }
 
 // C5 query generator: query i copies table row Rng(derive_seed(seed,"query",i)).bounded(n)

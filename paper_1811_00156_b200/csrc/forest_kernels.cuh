@@ -24,6 +24,17 @@ struct BinNode {
   uint32_t child;
 };
 
+// field layout of packed 4-byte predict nodes: column in bits [0, cb) (cmask = leaf),
+// threshold bin in [cb, cb+bb), chunk-relative child / leaf index from bit sh = cb+bb
+struct PredFmt {
+  uint32_t cb, bb, sh, cmask, bmask;
+};
+// 32-bit words of the warp-transposed bins of q queries x p columns
+inline uint64_t bin_words(uint64_t q, uint32_t p, uint32_t bin_bytes) {
+  const uint64_t e = 4 / bin_bytes;
+  return (q + 31) / 32 * ((p + e - 1) / e) * 32;
+}
+
 constexpr int kPredictThreads = 1024;  // predict CTA size (one CTA per SM)
 constexpr int kPredictQ = 1;           // queries per thread (2 measured slower: the warp waits
                                        // for the deepest of 64 paths)
@@ -38,7 +49,7 @@ cudaError_t launch_predict_chunk(int bin_bytes, int node_bytes, const void* node
                                  const uint32_t* roots, uint32_t ntrees, const void* bins,
                                  uint64_t q, uint32_t p, double* sum, int first, int last,
                                  double total_trees, double* out, unsigned grid, size_t smem,
-                                 size_t smem_max, cudaStream_t s);
+                                 size_t smem_max, PredFmt fmt, cudaStream_t s);
 
 // device presort of a dataset (presort.cu): per column (value, row) argsort into
 // d_sorted (p x n), dense ranks into d_rank (p x n), distinct values into d_vals
