@@ -1708,19 +1708,23 @@ void build_binned(aiwc_forest* f, uint32_t p) {
   const size_t tile = bin_words(uint64_t{kPredNT} * kPredictQ, p, f->bin_bytes) * 4;
   if (tile + 4096 > kPredSmem) return;
   const size_t budget = kPredSmem - tile - 64;
-  // packed 4-byte nodes: field widths fitted to the forest -- cb column bits (all ones
-  // marks a leaf, so p <= 2^cb - 1), bb bits for the largest threshold index, the rest
-  // for chunk-relative child / leaf indices
+  // a split node names its column by the byte offset of its bin in the warp-transposed
+  // bin words (forest_kernels.cu): column c -> (c / E) * 128 + (c % E) * bin_bytes
+  const uint32_t E = 4 / f->bin_bytes;
+  auto boff = [&](uint32_t c) { return (c / E) * 128u + (c % E) * f->bin_bytes; };
+  if (boff(p - 1) >= 0xffffu) return;
+  // packed 4-byte nodes: the offset in 12 bits (0xfff = leaf), bb bits for the largest
+  // threshold index, the rest for chunk-relative child / leaf indices
   auto bits = [](uint64_t v) {
     uint32_t b = 1;
     while ((uint64_t{1} << b) <= v) ++b;
     return b;
   };
-  const uint32_t cb = bits(p), bbits = bits(maxT ? maxT - 1 : 0);
-  const uint32_t chbits = cb + bbits < 32 ? 32 - cb - bbits : 0;
+  const uint32_t bbits = bits(maxT ? maxT - 1 : 0);
+  const uint32_t chbits = 12 + bbits < 32 ? 32 - 12 - bbits : 0;
   const uint64_t chmax = chbits >= 32 ? UINT32_MAX : (uint64_t{1} << chbits);
-  const bool node4 = chbits >= 12 && std::getenv("AIWC_PRED_NODE8") == nullptr;
-  f->fmt = PredFmt{cb, bbits, cb + bbits, (1u << cb) - 1u, (1u << bbits) - 1u};
+  const bool node4 = chbits >= 12 && boff(p - 1) < 0xfffu && std::getenv("AIWC_PRED_NODE8") == nullptr;
+  f->fmt = PredFmt{12, bbits, 12 + bbits, 0xfffu, (1u << bbits) - 1u};
   const size_t nb = node4 ? 4 : sizeof(BinNode);
   std::vector<double> thr_all;
   for (auto& v : T) thr_all.insert(thr_all.end(), v.begin(), v.end());
@@ -1752,8 +1756,8 @@ void build_binned(aiwc_forest* f, uint32_t p) {
       } else {
         const auto& v = T[fe[i]];
         const uint32_t j = static_cast<uint32_t>(std::lower_bound(v.begin(), v.end(), th[i]) - v.begin());
-        nodes.push_back(BinNode{static_cast<uint16_t>(fe[i]), static_cast<uint16_t>(j),
-                                ch.nnodes + static_cast<uint32_t>(le[i])});
+        nodes.push_back(BinNode{static_cast<uint16_t>(boff(static_cast<uint32_t>(fe[i]))),
+                                static_cast<uint16_t>(j), ch.nnodes + static_cast<uint32_t>(le[i])});
       }
     }
     ch.nnodes += static_cast<uint32_t>(e - b);

@@ -300,26 +300,25 @@ __global__ void bin_queries_kernel(const double* __restrict__ rows, uint64_t q, 
   }
 }
 
-// Node accessors: 8-byte BinNode, or the packed 4-byte form -- column in the low cb
-// bits (all ones = leaf), threshold bin in the next bb bits, chunk-relative left child
-// (right = left + 1) or leaf index in the rest; widths fit the forest (PredFmt) --
-// half the shared-memory wavefronts per visit and twice the trees per chunk.
+// Node accessors.  A split node names its column by the BYTE OFFSET of that column's bin
+// inside a query's transposed bin words (column c: word c/E at +128 bytes each, byte
+// (c%E)*sizeof(BinT)), so a visit reads its bin with one shared-memory load at
+// thread_base + off -- no column arithmetic.  8-byte BinNode {off, j, child}, or the
+// packed 4-byte form: off in the low 12 bits (0xfff = leaf), threshold bin in the next bb
+// bits, chunk-relative left child (right = left + 1) or leaf index above (PredFmt) --
+// half the node wavefronts per visit and twice the trees per chunk.
 struct Node8 {
   using T = BinNode;
   static __device__ __forceinline__ bool leaf(const BinNode& v, PredFmt) { return v.feat == 0xffffu; }
-  static __device__ __forceinline__ uint32_t feat(const BinNode& v, PredFmt) { return v.feat; }
+  static __device__ __forceinline__ uint32_t off(const BinNode& v, PredFmt) { return v.feat; }
   static __device__ __forceinline__ uint32_t j(const BinNode& v, PredFmt) { return v.j; }
   static __device__ __forceinline__ uint32_t child(const BinNode& v, PredFmt) { return v.child; }
 };
 struct Node4 {
   using T = uint32_t;
-  static __device__ __forceinline__ bool leaf(uint32_t v, PredFmt f) {
-    return (v & f.cmask) == f.cmask;
-  }
-  static __device__ __forceinline__ uint32_t feat(uint32_t v, PredFmt f) { return v & f.cmask; }
-  static __device__ __forceinline__ uint32_t j(uint32_t v, PredFmt f) {
-    return (v >> f.cb) & f.bmask;
-  }
+  static __device__ __forceinline__ bool leaf(uint32_t v, PredFmt) { return (v & 0xfffu) == 0xfffu; }
+  static __device__ __forceinline__ uint32_t off(uint32_t v, PredFmt) { return v & 0xfffu; }
+  static __device__ __forceinline__ uint32_t j(uint32_t v, PredFmt f) { return (v >> 12) & f.bmask; }
   static __device__ __forceinline__ uint32_t child(uint32_t v, PredFmt f) { return v >> f.sh; }
 };
 
@@ -369,13 +368,13 @@ __global__ void __launch_bounds__(NT, 1)
     }
     __syncthreads();
     if (threadIdx.x >= cnt) continue;
-    const uint32_t* bq[Q];
+    const unsigned char* bq[Q];
     double s[Q];
 #pragma unroll
     for (int u = 0; u < Q; ++u) {
       // a query slot past the tile's end re-walks query threadIdx.x (result dropped)
       const uint32_t qi = threadIdx.x + u * NT < cnt ? threadIdx.x + u * NT : threadIdx.x;
-      bq[u] = sb + (qi / 32) * W * 32 + lane;
+      bq[u] = reinterpret_cast<const unsigned char*>(sb + (qi / 32) * W * 32 + lane);
       s[u] = first ? 0.0 : sum[tile + qi];
     }
     for (uint32_t t = 0; t < ntrees; ++t) {
@@ -394,10 +393,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int u = 0; u < Q; ++u) {
           const bool lf = NA::leaf(v[u], fmt);
-          const uint32_t f = lf ? 0u : NA::feat(v[u], fmt);
-          const uint32_t w = bq[u][(f / E) * 32];
-          const uint32_t bin = sizeof(BinT) == 1 ? (w >> (8 * (f % E))) & 0xffu
-                                                 : (w >> (16 * (f % E))) & 0xffffu;
+          const uint32_t bin = *reinterpret_cast<const BinT*>(bq[u] + (lf ? 0u : NA::off(v[u], fmt)));
           idx[u] = lf ? idx[u] : NA::child(v[u], fmt) + (bin <= NA::j(v[u], fmt) ? 0u : 1u);
         }
 #pragma unroll
