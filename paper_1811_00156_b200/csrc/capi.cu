@@ -1737,7 +1737,7 @@ void build_binned(aiwc_forest* f, uint32_t p) {
     const uint64_t b = f->off[t], e = f->off[t + 1];
     uint32_t nl = 0;
     for (uint64_t i = b; i < e; ++i) nl += fe[i] < 0;
-    const size_t need = (ch.nnodes + (e - b)) * nb + 32 + (ch.nleaves + nl) * 8 + (ch.ntrees + 1) * 4;
+    const size_t need = (ch.nnodes + (e - b)) * nb + 32 + (ch.nleaves + nl) * 8;
     const bool idx_full = node4 && (ch.nnodes + (e - b) >= chmax || ch.nleaves + nl >= chmax);
     if (ch.ntrees > 0 && (need > budget || idx_full)) {
       f->chunks.push_back(ch);
@@ -1824,8 +1824,7 @@ void predict_binned(aiwc_forest* f, const double* d_rows, uint64_t q, uint32_t p
     const auto& ch = f->chunks[k];
     const size_t smem = ((size_t{ch.nnodes} * f->node_bytes + 15) & ~size_t{15}) +
                         ((size_t{ch.nleaves} * 8 + 15) & ~size_t{15}) +
-                        bin_words(uint64_t{kPredNT} * kPredictQ, p, f->bin_bytes) * 4 +
-                        size_t{ch.ntrees} * 4;
+                        bin_words(uint64_t{kPredNT} * kPredictQ, p, f->bin_bytes) * 4;
     const void* nodes = f->node_bytes == 4 ? static_cast<const void*>(f->bnodes4.p + ch.node0)
                                            : static_cast<const void*>(f->bnodes.p + ch.node0);
     CK(launch_predict_chunk(f->bin_bytes, f->node_bytes, nodes, ch.nnodes,

@@ -344,10 +344,8 @@ __global__ void __launch_bounds__(NT, 1)
   double* sl = reinterpret_cast<double*>(smem + ((nnodes * sizeof(NodeT) + 15) & ~size_t{15}));
   uint32_t* sb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sl) +
                                              ((size_t{nleaves} * 8 + 15) & ~size_t{15}));
-  uint32_t* sr = sb + bin_words(TQ, p, sizeof(BinT));  // the chunk's tree roots
   for (uint32_t i = threadIdx.x; i < nnodes; i += NT) sn[i] = nodes[i];
   for (uint32_t i = threadIdx.x; i < nleaves; i += NT) sl[i] = leaves[i];
-  for (uint32_t i = threadIdx.x; i < ntrees; i += NT) sr[i] = roots[i];
   const unsigned lane = threadIdx.x & 31u;
   for (uint64_t tile = uint64_t{blockIdx.x} * TQ; tile < q; tile += uint64_t{gridDim.x} * TQ) {
     __syncthreads();
@@ -379,35 +377,33 @@ __global__ void __launch_bounds__(NT, 1)
       bq[u] = reinterpret_cast<const unsigned char*>(sb + (qi / 32) * W * 32 + lane);
       s[u] = first ? 0.0 : sum[tile + qi];
     }
-    // Every lane walks its own query through the chunk's trees in order and moves on to
-    // the next tree's root as soon as it reaches a leaf (no waiting for the warp's
-    // deepest path per tree); its running sum still adds the leaves in tree order.
-    uint32_t t[Q], idx[Q];
-    NodeT v[Q];
-#pragma unroll
-    for (int u = 0; u < Q; ++u) {
-      t[u] = 0;
-      idx[u] = sr[0];
-      v[u] = sn[idx[u]];
-    }
-    for (;;) {
-      bool any = false;
-#pragma unroll
-      for (int u = 0; u < Q; ++u) any = any || t[u] < ntrees;
-      if (!any) break;
+    for (uint32_t t = 0; t < ntrees; ++t) {
+      const uint32_t r = roots[t];
+      uint32_t idx[Q];
+      NodeT v[Q];
+      bool done = true;
 #pragma unroll
       for (int u = 0; u < Q; ++u) {
-        if (t[u] >= ntrees) continue;
-        const bool lf = NA::leaf(v[u], fmt);
-        if (lf) {
-          s[u] = __dadd_rn(s[u], sl[NA::child(v[u], fmt)]);
-          if (++t[u] < ntrees) idx[u] = sr[t[u]];
-        } else {
-          const uint32_t bin = *reinterpret_cast<const BinT*>(bq[u] + NA::off(v[u], fmt));
-          idx[u] = NA::child(v[u], fmt) + (bin <= NA::j(v[u], fmt) ? 0u : 1u);
-        }
-        if (t[u] < ntrees) v[u] = sn[idx[u]];
+        idx[u] = r;
+        v[u] = sn[r];
+        done = done && NA::leaf(v[u], fmt);
       }
+      while (!done) {
+        done = true;
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          const bool lf = NA::leaf(v[u], fmt);
+          const uint32_t bin = *reinterpret_cast<const BinT*>(bq[u] + (lf ? 0u : NA::off(v[u], fmt)));
+          idx[u] = lf ? idx[u] : NA::child(v[u], fmt) + (bin <= NA::j(v[u], fmt) ? 0u : 1u);
+        }
+#pragma unroll
+        for (int u = 0; u < Q; ++u) {
+          v[u] = sn[idx[u]];
+          done = done && NA::leaf(v[u], fmt);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < Q; ++u) s[u] = __dadd_rn(s[u], sl[NA::child(v[u], fmt)]);
     }
 #pragma unroll
     for (int u = 0; u < Q; ++u) {

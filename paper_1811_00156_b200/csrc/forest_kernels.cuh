@@ -30,7 +30,7 @@ struct PredFmt {
   uint32_t cb, bb, sh, cmask, bmask;
 };
 // 32-bit words of the warp-transposed bins of q queries x p columns
-__host__ __device__ inline uint64_t bin_words(uint64_t q, uint32_t p, uint32_t bin_bytes) {
+inline uint64_t bin_words(uint64_t q, uint32_t p, uint32_t bin_bytes) {
   const uint64_t e = 4 / bin_bytes;
   return (q + 31) / 32 * ((p + e - 1) / e) * 32;
 }
