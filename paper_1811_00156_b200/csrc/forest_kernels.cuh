@@ -35,9 +35,15 @@ inline uint64_t bin_words(uint64_t q, uint32_t p, uint32_t bin_bytes) {
   return (q + 31) / 32 * ((p + e - 1) / e) * 32;
 }
 
-constexpr int kPredictThreads = 1024;  // predict CTA size (one CTA per SM)
-constexpr int kPredictQ = 1;           // queries per thread (2 measured slower: the warp waits
-                                       // for the deepest of 64 paths)
+#ifndef AIWC_PRED_NT
+#define AIWC_PRED_NT 1024
+#endif
+#ifndef AIWC_PRED_Q
+#define AIWC_PRED_Q 1
+#endif
+constexpr int kPredictThreads = AIWC_PRED_NT;  // predict CTA size (one CTA per SM)
+constexpr int kPredictQ = AIWC_PRED_Q;         // queries per thread (2 measured slower: the
+                                               // warp waits for the deepest of 64 paths)
 
 // binned shared-memory predict (kernels live in forest_kernels.cu and are launched there)
 cudaError_t launch_bin_queries(int bin_bytes, const double* rows, uint64_t q, uint32_t p,
