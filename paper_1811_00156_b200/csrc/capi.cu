@@ -414,11 +414,10 @@ struct aiwc_forest {
   std::mutex sm_mu;
   cudaStream_t sm_stream = nullptr;
   DevBuf<double> sm_rows, sm_out;
-  double* sm_pin = nullptr;
-  size_t sm_pin_cap = 0;
+  std::pair<char*, size_t> sm_pin{nullptr, 0};  // from PinnedPool
   ~aiwc_forest() {
     if (sm_stream) cudaStreamDestroy(sm_stream);
-    if (sm_pin) cudaFreeHost(sm_pin);
+    PinnedPool::give(sm_pin);
     PinnedPool::give(pinned);
   }
 };
@@ -1914,22 +1913,21 @@ int aiwc_predict(aiwc_forest* f, const double* rows, uint64_t q, uint32_t p,
       std::lock_guard<std::mutex> lock(f->sm_mu);
       if (!f->sm_stream) CK(cudaStreamCreateWithFlags(&f->sm_stream, cudaStreamNonBlocking));
       const cudaStream_t s = f->sm_stream;
-      const size_t need = q * p + q;
-      if (f->sm_pin_cap < need) {
-        if (f->sm_pin) CK(cudaFreeHost(f->sm_pin));
-        f->sm_pin = nullptr;
-        CK(cudaMallocHost(reinterpret_cast<void**>(&f->sm_pin), need * 8));
-        f->sm_pin_cap = need;
+      const size_t need = (q * p + q) * 8;
+      if (f->sm_pin.second < need) {
+        PinnedPool::give(f->sm_pin);
+        f->sm_pin = PinnedPool::take(need);
       }
+      double* const pin = reinterpret_cast<double*>(f->sm_pin.first);
       if (f->sm_rows.count < q * p) f->sm_rows.alloc(std::max<size_t>(q * p, 64 * size_t{p}));
       if (f->sm_out.count < q) f->sm_out.alloc(std::max<uint64_t>(q, 64));
-      std::memcpy(f->sm_pin, rows, q * p * 8);
-      CK(cudaMemcpyAsync(f->sm_rows.p, f->sm_pin, q * p * 8, cudaMemcpyHostToDevice, s));
+      std::memcpy(pin, rows, q * p * 8);
+      CK(cudaMemcpyAsync(f->sm_rows.p, pin, q * p * 8, cudaMemcpyHostToDevice, s));
       PredScratch none;
       predict_dispatch(f, f->sm_rows.p, q, p, f->sm_out.p, s, none);
-      CK(cudaMemcpyAsync(f->sm_pin + q * p, f->sm_out.p, q * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(pin + q * p, f->sm_out.p, q * 8, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      std::memcpy(out_response, f->sm_pin + q * p, q * 8);
+      std::memcpy(out_response, pin + q * p, q * 8);
       return;
     }
     // row chunks on two streams: the upload of chunk i+1 (host copy into pinned memory,
