@@ -27,8 +27,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <charconv>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <limits>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -207,7 +210,9 @@ class Forest {
 
   nlohmann::ordered_json to_json() const;
   static Forest from_json(const nlohmann::json& j);
-  void save(const std::string& path) const { write_text_file(path, to_json().dump() + "\n"); }
+  // model files (forest.hpp:596-604): the canonical bytes of to_json().dump() + "\n",
+  // written / read directly (b200::json_write / json_read) without a JSON DOM
+  void save(const std::string& path) const;
   static Forest load(const std::string& path);
 
   void invalidate_device_cache() const {
@@ -459,10 +464,251 @@ inline Forest Forest::from_json(const nlohmann::json& j) {
   return f;
 }
 
+namespace b200 {
+
+// The model file's bytes without building the JSON DOM: the same key order and compact
+// separators as to_json().dump(), numbers through nlohmann's own shortest round-trip
+// double printer (detail::to_chars, what dump() calls) and decimal integers, so the
+// output is byte-identical (the C1 model's FNV-1a is pinned in tests/test_dropin.py).
+inline void put_double(std::string& o, double x) {
+  if (!std::isfinite(x)) {
+    o += "null";
+    return;
+  }
+  char buf[64];
+  char* e = ::nlohmann::detail::to_chars(buf, buf + sizeof(buf), x);
+  o.append(buf, static_cast<std::size_t>(e - buf));
+}
+template <typename I>
+inline void put_int(std::string& o, I v) {
+  char buf[32];
+  const auto r = std::to_chars(buf, buf + sizeof(buf), v);
+  o.append(buf, static_cast<std::size_t>(r.ptr - buf));
+}
+inline void put_str(std::string& o, const std::string& s) { o += nlohmann::json(s).dump(); }
+
+inline std::string json_write(const Forest& f) {
+  std::size_t nodes = 0, draws = 0;
+  for (const Tree& t : f.trees) nodes += t.nodes.size();
+  for (const auto& v : f.inbag) draws += v.size();
+  std::string o;
+  o.reserve(nodes * 48 + draws * 8 + 4096);
+  o += "{\"format\":\"aiwc-forest\",\"version\":1,\"response\":";
+  put_str(o, response_name(f.response));
+  o += ",\"columns\":[";
+  for (std::size_t i = 0; i < f.columns.size(); ++i) {
+    if (i) o += ',';
+    put_str(o, f.columns[i]);
+  }
+  o += "],\"schema_fingerprint\":";
+  put_str(o, fingerprint_hex(f.fingerprint));
+  o += ",\"params\":{\"num_trees\":";
+  put_int(o, f.params.num_trees);
+  o += ",\"mtry\":";
+  put_int(o, f.params.mtry);
+  o += ",\"min_node_size\":";
+  put_int(o, f.params.min_node_size);
+  o += ",\"seed\":";
+  put_int(o, f.params.seed);
+  o += "},\"oob\":{\"degenerate\":";
+  o += f.oob.degenerate ? "true" : "false";
+  o += ",\"mse\":";
+  put_double(o, f.oob.mse);
+  o += ",\"response_variance\":";
+  put_double(o, f.oob.response_variance);
+  o += ",\"error_pct\":";
+  put_double(o, f.oob.error_pct);
+  o += ",\"r_squared\":";
+  put_double(o, f.oob.r_squared);
+  o += ",\"rows_evaluated\":";
+  put_int(o, f.oob.rows_evaluated);
+  o += "},\"trees\":[";
+  for (std::size_t t = 0; t < f.trees.size(); ++t) {
+    if (t) o += ',';
+    o += '[';
+    const auto& ns = f.trees[t].nodes;
+    for (std::size_t i = 0; i < ns.size(); ++i) {
+      if (i) o += ',';
+      o += '[';
+      put_int(o, ns[i].feature);
+      o += ',';
+      put_double(o, ns[i].threshold);
+      o += ',';
+      put_int(o, ns[i].left);
+      o += ',';
+      put_int(o, ns[i].right);
+      o += ',';
+      put_double(o, ns[i].value);
+      o += ']';
+    }
+    o += ']';
+  }
+  o += "],\"inbag\":[";
+  for (std::size_t t = 0; t < f.inbag.size(); ++t) {
+    if (t) o += ',';
+    o += '[';
+    const auto& v = f.inbag[t];
+    for (std::size_t i = 0; i < v.size(); ++i) {
+      if (i) o += ',';
+      put_int(o, v[i]);
+    }
+    o += ']';
+  }
+  o += "]}\n";
+  return o;
+}
+
+// Reader of exactly that layout (the canonical file): false on any deviation, and the
+// caller falls back to the general JSON parser.  Numbers are parsed with from_chars
+// (correctly rounded, as the JSON parser's strtod).
+struct JsonCursor {
+  const char* p;
+  const char* e;
+  bool lit(const char* s) {
+    const std::size_t n = std::strlen(s);
+    if (static_cast<std::size_t>(e - p) < n || std::memcmp(p, s, n) != 0) return false;
+    p += n;
+    return true;
+  }
+  bool ch(char c) {
+    if (p < e && *p == c) {
+      ++p;
+      return true;
+    }
+    return false;
+  }
+  template <typename I>
+  bool integer(I& v) {
+    const auto r = std::from_chars(p, e, v);
+    if (r.ec != std::errc()) return false;
+    p = r.ptr;
+    return true;
+  }
+  bool number(double& v) {
+    if (lit("null")) {
+      v = std::numeric_limits<double>::quiet_NaN();
+      return true;
+    }
+    const auto r = std::from_chars(p, e, v);
+    if (r.ec != std::errc()) return false;
+    p = r.ptr;
+    return true;
+  }
+  bool string(std::string& s) {  // plain strings only (no escapes in canonical names)
+    if (!ch('"')) return false;
+    const char* q = p;
+    while (q < e && *q != '"') {
+      if (*q == '\\') return false;
+      ++q;
+    }
+    if (q >= e) return false;
+    s.assign(p, q);
+    p = q + 1;
+    return true;
+  }
+};
+
+inline bool json_read(const std::string& text, Forest& f) {
+  JsonCursor c{text.data(), text.data() + text.size()};
+  std::string resp, fp;
+  if (!c.lit("{\"format\":\"aiwc-forest\",\"version\":1,\"response\":") || !c.string(resp))
+    return false;
+  try {
+    f.response = parse_response(resp);
+  } catch (...) {
+    return false;
+  }
+  if (!c.lit(",\"columns\":[")) return false;
+  f.columns.clear();
+  if (!c.ch(']')) {
+    for (;;) {
+      std::string col;
+      if (!c.string(col)) return false;
+      f.columns.push_back(std::move(col));
+      if (c.ch(']')) break;
+      if (!c.ch(',')) return false;
+    }
+  }
+  if (!c.lit(",\"schema_fingerprint\":") || !c.string(fp)) return false;
+  f.fingerprint = schema_fingerprint(f.columns, f.response);
+  if (fp != fingerprint_hex(f.fingerprint)) throw ParseError("model file: schema fingerprint does not match columns");
+  if (!c.lit(",\"params\":{\"num_trees\":") || !c.integer(f.params.num_trees) ||
+      !c.lit(",\"mtry\":") || !c.integer(f.params.mtry) || !c.lit(",\"min_node_size\":") ||
+      !c.integer(f.params.min_node_size) || !c.lit(",\"seed\":") || !c.integer(f.params.seed) ||
+      !c.lit("},\"oob\":{\"degenerate\":"))
+    return false;
+  if (c.lit("true")) f.oob.degenerate = true;
+  else if (c.lit("false")) f.oob.degenerate = false;
+  else return false;
+  if (!c.lit(",\"mse\":") || !c.number(f.oob.mse) || !c.lit(",\"response_variance\":") ||
+      !c.number(f.oob.response_variance) || !c.lit(",\"error_pct\":") ||
+      !c.number(f.oob.error_pct) || !c.lit(",\"r_squared\":") || !c.number(f.oob.r_squared) ||
+      !c.lit(",\"rows_evaluated\":") || !c.integer(f.oob.rows_evaluated) ||
+      !c.lit("},\"trees\":["))
+    return false;
+  f.trees.clear();
+  if (!c.ch(']')) {
+    for (;;) {
+      Tree t;
+      if (!c.ch('[')) return false;
+      if (!c.ch(']')) {
+        for (;;) {
+          TreeNode nd;
+          if (!c.ch('[') || !c.integer(nd.feature) || !c.ch(',') || !c.number(nd.threshold) ||
+              !c.ch(',') || !c.integer(nd.left) || !c.ch(',') || !c.integer(nd.right) ||
+              !c.ch(',') || !c.number(nd.value) || !c.ch(']'))
+            return false;
+          t.nodes.push_back(nd);
+          if (c.ch(']')) break;
+          if (!c.ch(',')) return false;
+        }
+      }
+      f.trees.push_back(std::move(t));
+      if (c.ch(']')) break;
+      if (!c.ch(',')) return false;
+    }
+  }
+  if (!c.lit(",\"inbag\":[")) return false;
+  f.inbag.clear();
+  if (!c.ch(']')) {
+    for (;;) {
+      std::vector<std::uint32_t> v;
+      if (!c.ch('[')) return false;
+      if (!c.ch(']')) {
+        for (;;) {
+          std::uint32_t x;
+          if (!c.integer(x)) return false;
+          v.push_back(x);
+          if (c.ch(']')) break;
+          if (!c.ch(',')) return false;
+        }
+      }
+      f.inbag.push_back(std::move(v));
+      if (c.ch(']')) break;
+      if (!c.ch(',')) return false;
+    }
+  }
+  if (!c.ch('}')) return false;
+  while (c.p < c.e && (*c.p == '\n' || *c.p == ' ' || *c.p == '\r' || *c.p == '\t')) ++c.p;
+  if (c.p != c.e) return false;
+  if (f.trees.size() != f.params.num_trees || f.inbag.size() != f.trees.size())
+    throw ParseError("model file: tree/inbag counts disagree with params");
+  return true;
+}
+
+}  // namespace b200
+
+inline void Forest::save(const std::string& path) const { write_text_file(path, b200::json_write(*this)); }
+
 inline Forest Forest::load(const std::string& path) {
+  const std::string text = read_text_file(path);
+  {
+    Forest f;
+    if (b200::json_read(text, f)) return f;  // the canonical layout, parsed directly
+  }
   nlohmann::json j;
   try {
-    j = nlohmann::json::parse(read_text_file(path));
+    j = nlohmann::json::parse(text);
   } catch (const nlohmann::json::exception& e) {
     throw ParseError("model file: " + std::string(e.what()));
   }

@@ -43,7 +43,76 @@ static int heatmap() {
   return 0;
 }
 
+// json mode: the model file path (forest.hpp:527-604) -- the reference's DOM route
+// (to_json().dump() / json::parse + from_json) against the drop-in's direct
+// writer / reader (b200::json_write / Forest::load), same bytes, timed
+static int json_mode() {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const SynthResult s = synthesize(SynthConfig{});
+  const Dataset d = make_dataset(s.features, s.runtimes);
+  const Forest f = fit(d, ForestParams{500, 6, 5, derive_seed(1, "forest")});
+  auto t0 = clk::now();
+  const std::string dom = f.to_json().dump() + "\n";
+  auto t1 = clk::now();
+  const std::string fast = b200::json_write(f);
+  auto t2 = clk::now();
+  const std::string path = "/tmp/aiwc_dropin_model.json";
+  write_text_file(path, fast);
+  auto t3 = clk::now();
+  const Forest g = Forest::from_json(nlohmann::json::parse(read_text_file(path)));
+  auto t4 = clk::now();
+  const Forest h = Forest::load(path);
+  auto t5 = clk::now();
+  const bool same = dom == fast && g.to_json().dump() + "\n" == fast && b200::json_write(h) == fast;
+  const std::string body = fast.substr(0, fast.size() - 1);  // the JSON text (no newline)
+  std::printf("{\"bytes\": %zu, \"fnv\": %llu, \"identical\": %s, \"dom_write_ms\": %.3f, "
+              "\"fast_write_ms\": %.3f, \"dom_read_ms\": %.3f, \"fast_read_ms\": %.3f}\n",
+              body.size(), static_cast<unsigned long long>(fnv1a64(body)), same ? "true" : "false",
+              ms(t0, t1), ms(t1, t2), ms(t3, t4), ms(t4, t5));
+  return same ? 0 : 4;
+}
+
+// jsonfile mode (no GPU): a model file written by the reference -> Forest::load (direct
+// reader) -> b200::json_write must give the file's bytes back; DOM route timed alongside
+static int jsonfile_mode(const std::string& path) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const std::string text = read_text_file(path);
+  auto t0 = clk::now();
+  const Forest g = Forest::from_json(nlohmann::json::parse(text));
+  auto t1 = clk::now();
+  const Forest h = Forest::load(path);
+  auto t2 = clk::now();
+  const std::string dom = g.to_json().dump() + "\n";
+  auto t3 = clk::now();
+  const std::string fast = b200::json_write(h);
+  auto t4 = clk::now();
+  const bool same = dom == text && fast == text;
+  std::printf("{\"bytes\": %zu, \"fnv\": %llu, \"identical\": %s, \"dom_read_ms\": %.3f, "
+              "\"fast_read_ms\": %.3f, \"dom_write_ms\": %.3f, \"fast_write_ms\": %.3f}\n",
+              text.size(), static_cast<unsigned long long>(fnv1a64(text)), same ? "true" : "false",
+              ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+  return same ? 0 : 4;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 2 && std::string(argv[1]) == "jsonfile") {
+    try {
+      return jsonfile_mode(argv[2]);
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "dropin_test jsonfile: %s\n", e.what());
+      return 3;
+    }
+  }
+  if (argc > 1 && std::string(argv[1]) == "json") {
+    try {
+      return json_mode();
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "dropin_test json: %s\n", e.what());
+      return 3;
+    }
+  }
   if (argc > 1 && std::string(argv[1]) == "heatmap") {
     try {
       return heatmap();

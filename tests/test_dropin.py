@@ -64,3 +64,45 @@ def test_heatmap_scan_batches_concurrent_fits():
     print(f"heatmap_scan: serial {runs['serial']['seconds']:.3f} s, batched "
           f"{runs['batched']['seconds']:.3f} s, x{speedup:.2f}")
     assert speedup > 1.5  # measured 1.9-3.4x on B200 boxes (profiles/r2_heatmap_batching.txt)
+
+
+@needs_bin
+@pytest.mark.gpu
+def test_model_file_fast_path_is_byte_identical():
+    """Forest::save / load write and read the canonical model bytes directly (no JSON DOM):
+    byte-identical to the reference's to_json().dump() (the C1 500/6/5 model, FNV-1a
+    pinned), and the loaded forest re-serialises to the same bytes."""
+    r = subprocess.run([BIN, "json"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["identical"] is True
+    assert got["bytes"] == C1_JSON_SIZE and got["fnv"] == C1_JSON_FNV
+    print(f"model file: DOM write {got['dom_write_ms']:.1f} ms / direct {got['fast_write_ms']:.1f} ms, "
+          f"DOM read {got['dom_read_ms']:.1f} ms / direct {got['fast_read_ms']:.1f} ms")
+
+
+@needs_bin
+def test_model_file_reader_writer_on_reference_bytes(golden, tmp_path):
+    """CPU: a model file written by the REFERENCE (oracle/_ref, the C1 500/6/5 forest) read by
+    Forest::load's direct reader and written back by b200::json_write gives the very same
+    bytes (and the reference's own DOM route agrees) -- the drop-in's model I/O path."""
+    import ctypes as C
+    os.environ.setdefault("AIWC_REF_QUARANTINE", "1")  # deterministic multi-threaded fit
+    from oracle_lib import Ref, RefData, RefForest
+    if not Ref.available():
+        pytest.skip("oracle/_ref not built")
+    L = Ref.lib()
+    d = RefData()
+    f = RefForest.fit(d, 500, 6, 5, golden["forest_seed"], jobs=8)
+    L.ref_forest_json.restype = C.c_uint64
+    L.ref_forest_json.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64]
+    n = L.ref_forest_json(f.h, None, 0)
+    buf = C.create_string_buffer(n)
+    L.ref_forest_json(f.h, buf, n)
+    path = tmp_path / "c1_500.json"
+    path.write_bytes(buf.raw[:n])
+    r = subprocess.run([BIN, "jsonfile", str(path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr + r.stdout
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    assert got["identical"] is True and got["bytes"] == C1_JSON_SIZE + 1
+    assert got["fnv"] == golden["c1_500_6_5"]["json_fnv_with_newline"]
