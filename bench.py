@@ -327,7 +327,7 @@ def main():
         stream = torch.cuda.current_stream()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         r = {"grow_ms": 0.0, "split_rows": 0, "grow_launches": 0, "oob": None, "nodes": 0,
-             "trees_total": total, "trees_rank": te - tb, "step_ms": []}
+             "trees_total": total, "trees_rank": te - tb, "step_ms": [], "step_grow_ms": []}
         last = None
         with ClockSampler(local) as clk:
             barrier()
@@ -340,6 +340,7 @@ def main():
                 e1.synchronize()
                 r["step_ms"].append(e0.elapsed_time(e1))
                 prof = f.profile()
+                r["step_grow_ms"].append(prof["grow_ms"])
                 r["grow_ms"] += prof["grow_ms"]
                 r["split_rows"] += prof["split_rows"]
                 r["grow_launches"] += prof["grow_launches"]
@@ -455,6 +456,7 @@ def main():
                    "l2": "inputs (512 MB f64 column store + 128 MB ranks) exceed L2"},
         "oob_error_pct": None if oob < 0 else oob,
         "step_ms": head["step_ms"],
+        "step_outside_grow_ms": [a - b for a, b in zip(head["step_ms"], head["step_grow_ms"])],
         "nodes_per_tree": nodes_last / per,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_per_launch(per * args.steps,
