@@ -1206,14 +1206,21 @@ __global__ void w_pay(const WideArgs a) {
 constexpr uint32_t kLwStep = 256;
 constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
 struct LwStage {
-  uint32_t q[8];  // raw 16-bit entries (node-relative), prefetched a step ahead
+  uint32_t q[8];  // raw 16-bit entries (node-relative)
+  int4 t[8];      // their segment's (offL, offR, fb, bLf)
 };
 
-__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint16_t* list) {
+__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint16_t* list,
+                                        const int4* off2) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t k = k0 + 32u * j + lane_id();
-    v.q[j] = k < A ? list[k] : 0u;
+    if (k < A) {
+      v.q[j] = list[k];
+      v.t[j] = off2[k];
+    } else {
+      v.t[j] = make_int4(INT_MIN, 0, 0, 0);
+    }
   }
 }
 
@@ -1256,54 +1263,44 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
     uint8_t* dsth = P.lhi_n + static_cast<size_t>(li) * stride;
     uint32_t carry = 0;  // left-going entries of this list before the sub-row
     LwStage cur, nxt;
-    lw_load(cur, 0, A, src);
+    lw_load(cur, 0, A, src, P.off2);
     for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
-      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src);
-      // per half step (4 sub-rows, register budget): the segment offsets (shared by
-      // every list: L1 hits after the first warp), absolute positions (high bytes only
-      // in segments of more than kBigSeg rows), the shared-memory lookups, the scatter
+      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
+      // absolute positions (high bytes only in segments of more than kBigSeg rows), then
+      // all 16 shared-memory lookups of the lane (branch-free), then the scatter
+      uint32_t qa[8], wv[8], pv[8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int4 tt[4];
-        uint32_t qa[4], wv[4], pv[4];
+      for (int j = 0; j < 8; ++j) {
+        const int4 t = cur.t[j];
+        uint32_t r = cur.q[j];
+        if (t.x != INT_MIN && (static_cast<uint32_t>(t.w) & (1u << 29)))
+          r |= static_cast<uint32_t>(srch[k0 + 32u * j + lane]) << 16;
+        qa[j] = t.x != INT_MIN ? static_cast<uint32_t>(t.z) + r : 0u;
+      }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t k = k0 + 32u * (4 * h + i) + lane;
-          tt[i] = k < A ? P.off2[k] : make_int4(INT_MIN, 0, 0, 0);
+      for (int j = 0; j < 8; ++j) {
+        wv[j] = sbits[qa[j] >> 5];
+        pv[j] = spref[qa[j] >> 5];
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int4 t = cur.t[j];
+        const bool keep = t.x != INT_MIN;
+        const uint32_t qq = qa[j];
+        const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
+        const bool l = keep && bit;
+        const unsigned bl = __ballot_sync(kFull, l);
+        const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
+        if (keep) {
+          const uint32_t lq = pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u));
+          const uint32_t k = k0 + 32u * j + lane;
+          const uint32_t bLf = static_cast<uint32_t>(t.w);
+          const uint32_t rel = child_rel(l, qq, static_cast<uint32_t>(t.z), lq, bLf & 0x1fffffffu);
+          const uint32_t dst =
+              static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
+          put_entry(dstl, dsth, dst, rel, (bLf >> (l ? 30 : 31)) & 1u);
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int4 t = tt[i];
-          uint32_t r = cur.q[4 * h + i];
-          if (t.x != INT_MIN && (static_cast<uint32_t>(t.w) & (1u << 29)))
-            r |= static_cast<uint32_t>(srch[k0 + 32u * (4 * h + i) + lane]) << 16;
-          qa[i] = t.x != INT_MIN ? static_cast<uint32_t>(t.z) + r : 0u;
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          wv[i] = sbits[qa[i] >> 5];
-          pv[i] = spref[qa[i] >> 5];
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int4 t = tt[i];
-          const bool keep = t.x != INT_MIN;
-          const uint32_t qq = qa[i];
-          const uint32_t bit = (wv[i] >> (qq & 31u)) & 1u;
-          const bool l = keep && bit;
-          const unsigned bl = __ballot_sync(kFull, l);
-          const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
-          if (keep) {
-            const uint32_t lq = pv[i] + __popc(wv[i] & ((1u << (qq & 31u)) - 1u));
-            const uint32_t k = k0 + 32u * (4 * h + i) + lane;
-            const uint32_t bLf = static_cast<uint32_t>(t.w);
-            const uint32_t rel = child_rel(l, qq, static_cast<uint32_t>(t.z), lq, bLf & 0x1fffffffu);
-            const uint32_t dst =
-                static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
-            put_entry(dstl, dsth, dst, rel, (bLf >> (l ? 30 : 31)) & 1u);
-          }
-          carry += __popc(bl);
-        }
+        carry += __popc(bl);
       }
       cur = nxt;
     }
