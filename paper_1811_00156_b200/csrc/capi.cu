@@ -723,9 +723,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   bool wide = !small_table || T >= 64;
   if (const char* e = std::getenv("AIWC_GROW_WIDE")) wide = std::atoi(e) != 0;
   if (wide) {
-    L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true, true);
-    // node-relative list entries: 16 bits + a high byte
-    if (L.stride >= (1u << 24)) throw Status(AIWC_EARG, "more than 2^24 in-bag rows per tree");
+    L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
     a.L = L;
     a.bits_in_smem = 0;
   }

@@ -78,42 +78,6 @@ __device__ __forceinline__ double gain_at(double sl, double wl, double W, double
   return __dadd_rn(__ddiv_rn(__dmul_rn(sl, sl), wl), __ddiv_rn(__dmul_rn(d, d), wr));
 }
 
-// ---- sorted-list accessors ----------------------------------------------------------
-// The CTA-per-tree grower keeps u32 payload positions (List32).  The wide grower keeps
-// 16-bit positions relative to the node's first position and, for nodes of more than
-// kBigSeg rows only, a high byte in a parallel array (ListRef): half the list bytes the
-// level pass moves, chains and routes read (the top few levels are the only big nodes).
-struct List32 {
-  const uint32_t* p;
-  __device__ __forceinline__ uint32_t at(uint32_t k) const { return p[k]; }
-  // entries k .. k+3 (k a multiple of 4)
-  __device__ __forceinline__ void at4(uint32_t k, uint32_t* q) const {
-    const uint4 x = *reinterpret_cast<const uint4*>(p + k);
-    q[0] = x.x; q[1] = x.y; q[2] = x.z; q[3] = x.w;
-  }
-};
-struct ListRef {
-  const uint16_t* lo;
-  const uint8_t* hi;
-  uint32_t base;  // the node's first position
-  bool big;       // node of more than kBigSeg rows: entries have a high byte
-  __device__ __forceinline__ uint32_t at(uint32_t k) const {
-    uint32_t r = lo[k];
-    if (big) r |= static_cast<uint32_t>(hi[k]) << 16;
-    return base + r;
-  }
-  __device__ __forceinline__ void at4(uint32_t k, uint32_t* q) const {
-    const uint2 x = *reinterpret_cast<const uint2*>(lo + k);
-    q[0] = x.x & 0xffffu; q[1] = x.x >> 16; q[2] = x.y & 0xffffu; q[3] = x.y >> 16;
-    if (big) {
-      const uint32_t h = *reinterpret_cast<const uint32_t*>(hi + k);
-      q[0] |= (h & 0xffu) << 16; q[1] |= ((h >> 8) & 0xffu) << 16;
-      q[2] |= ((h >> 16) & 0xffu) << 16; q[3] |= (h >> 24) << 16;
-    }
-    q[0] += base; q[1] += base; q[2] += base; q[3] += base;
-  }
-};
-
 // ---- sequential FP64 accumulation over one 32-element tile -----------------------
 // The values go through this warp's shared-memory stage and every lane runs the same
 // fully unrolled add chain, so the chain is bound by DADD latency alone (the loads are
@@ -330,8 +294,8 @@ __device__ void chain_warp(const uint32_t* list, uint32_t b, uint32_t e,
 // Pipelined warp chains for the wide grower: tiles of 32*G positions; while tile i is
 // scanned, the payload gathers of tile i+1 and the list loads of tile i+2 are in
 // flight.  Same arithmetic (and order) as chain_warp / chain_bin_warp.
-template <typename RankT, int G, typename L>
-__device__ void chain_warp_p(bool listed, const L list, uint32_t b, uint32_t e,
+template <typename RankT, int G>
+__device__ void chain_warp_p(bool listed, const uint32_t* list, uint32_t b, uint32_t e,
                              const Payload* pay, const RankT* __restrict__ rk_c, double W,
                              double S, double& best_gain, uint32_t& best_pos, double* st) {
   const unsigned lane = lane_id();
@@ -344,7 +308,7 @@ __device__ void chain_warp_p(bool listed, const L list, uint32_t b, uint32_t e,
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      q[g] = k < e ? (listed ? list.at(k) : k) : 0u;
+      q[g] = k < e ? (listed ? list[k] : k) : 0u;
     }
   };
   auto load_p = [&](uint32_t k0, const uint32_t (&q)[G], uint32_t (&row)[G], uint32_t (&mu)[G],
@@ -444,8 +408,8 @@ __device__ void chain_warp_p(bool listed, const L list, uint32_t b, uint32_t e,
 }
 
 // ---- split chain over a sorted list, one lane (small nodes) -----------------------
-template <typename RankT, typename L>
-__device__ void chain_lane(const L list, uint32_t b, uint32_t e,
+template <typename RankT>
+__device__ void chain_lane(const uint32_t* list, uint32_t b, uint32_t e,
                            const Payload* pay, const RankT* __restrict__ rk_c,
                            double W, double S, double& best_gain, uint32_t& best_pos) {
   double sl = 0.0, bg = -INFINITY;
@@ -454,7 +418,7 @@ __device__ void chain_lane(const L list, uint32_t b, uint32_t e,
     uint32_t q[4], rk[4], mu[4];
     double wy[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list.at(k + g) : 0u;
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list[k + g] : 0u;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       if (k + g < e) {
@@ -581,8 +545,8 @@ __device__ void chain_bin_lane(const Payload* pay, uint32_t b, uint32_t e,
 // `listed`: the column's sorted list gives the order (forest.hpp:268-297); otherwise the
 // column is two-level and its chain is the row-order sum of the value-0 rows (a masked
 // add of +0.0 is exact: the running sum starts at +0.0 and can never become -0.0).
-template <typename RankT, int G, int U, typename L>
-__device__ __forceinline__ void chain_grp(bool active, bool listed, const L list,
+template <typename RankT, int G, int U>
+__device__ __forceinline__ void chain_grp(bool active, bool listed, const uint32_t* list,
                                           uint32_t b, uint32_t e, const Payload* pay,
                                           const RankT* __restrict__ rk_c, double W, double S,
                                           double& best_gain, uint32_t& best_pos, double* st) {
@@ -601,7 +565,8 @@ __device__ __forceinline__ void chain_grp(bool active, bool listed, const L list
 #pragma unroll
       for (int v = 0; v < U; v += 4) {
         if (kb + v < e) {
-          list.at4(kb + v, q + v);
+          const uint4 x = *reinterpret_cast<const uint4*>(list + kb + v);
+          q[v] = x.x; q[v + 1] = x.y; q[v + 2] = x.z; q[v + 3] = x.w;
         } else {
           q[v] = q[v + 1] = q[v + 2] = q[v + 3] = 0u;
         }
@@ -814,8 +779,8 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
 // The four sequential sums (left/right x sum/sumsq) run in four 8-lane groups over a
 // staged tile in which elements of the other side are +0.0 (an exact no-op, see
 // chain_grp), so every tile costs 32 dependent DADDs per group and no masked loops.
-template <typename RankT, int G, typename L>
-__device__ void route_warp_p(const L list0, uint32_t b, uint32_t e,
+template <typename RankT, int G>
+__device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
                              const Payload* pay, const double* wyy,
                              const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                              RouteOut& o, double* st /* 4*32 doubles */) {
@@ -828,7 +793,7 @@ __device__ void route_warp_p(const L list0, uint32_t b, uint32_t e,
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      q[g] = k < e ? list0.at(k) : 0u;
+      q[g] = k < e ? list0[k] : 0u;
     }
   };
   auto load_p = [&](uint32_t k0, const uint32_t (&q)[G], uint32_t (&row)[G], uint32_t (&mu)[G],
@@ -916,8 +881,8 @@ __device__ void route_warp_p(const L list0, uint32_t b, uint32_t e,
   o.qr = __shfl_sync(kFull, acc, 24);
 }
 
-template <typename RankT, typename L>
-__device__ void route_lane(const L list0, uint32_t b, uint32_t e,
+template <typename RankT>
+__device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
                            const Payload* pay, const double* wyy,
                            const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                            RouteOut& o) {
@@ -925,7 +890,7 @@ __device__ void route_lane(const L list0, uint32_t b, uint32_t e,
     uint32_t q[4], row[4], mu[4];
     double wy[4], yy[4];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list0.at(k + g) : 0u;
+    for (int g = 0; g < 4; ++g) q[g] = k + g < e ? list0[k + g] : 0u;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
       if (k + g < e) {
@@ -1330,7 +1295,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         double bg;
         uint32_t bp;
         if (li >= 0)
-          chain_lane<RankT>(List32{lists[cur] + static_cast<size_t>(li) * stride}, nw.b, nw.e,
+          chain_lane<RankT>(lists[cur] + static_cast<size_t>(li) * stride, nw.b, nw.e,
                             pay[cur], rk_c, nw.w, nw.s, bg, bp);
         else
           chain_bin_lane<RankT>(pay[cur], nw.b, nw.e, rk_c, nw.w, nw.s, bg, bp);
@@ -1460,7 +1425,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
               if (lane != 0) continue;
             } else {
               if (l0)
-                route_lane<RankT>(List32{l0}, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank, bits,
+                route_lane<RankT>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank, bits,
                                   o);
               else
                 route_groups_lane<RankT>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels, rk_f,
@@ -1681,7 +1646,7 @@ cudaError_t launch_grow(int nt, int rank_bytes, const GrowArgs& a, int slots, si
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, uint32_t mns,
-                       bool gbits, bool wide) {
+                       bool gbits) {
   (void)p;
   SlotLayout L{};
   // in-bag distinct rows: 0.632 n on average; bound it generously (checked at run time)
@@ -1708,13 +1673,8 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_pay1 = take(stride * sizeof(Payload));
   L.off_wyy0 = take(stride * 8);
   L.off_wyy1 = take(stride * 8);
-  const size_t lb = wide ? 2 : 4;  // list entry bytes (wide: + a high byte array)
-  L.off_list0 = take(size_t{nlisted} * stride * lb + 64);
-  L.off_list1 = take(size_t{nlisted} * stride * lb + 64);
-  if (wide) {
-    L.off_hi0 = take(size_t{nlisted} * stride + 64);
-    L.off_hi1 = take(size_t{nlisted} * stride + 64);
-  }
+  L.off_list0 = take(size_t{nlisted} * stride * 4 + 64);
+  L.off_list1 = take(size_t{nlisted} * stride * 4 + 64);
   L.off_seg0 = take(stride * 4 + 64);
   L.off_seg1 = take(stride * 4 + 64);
   L.off_front0 = take(fmax * sizeof(NodeWork));
@@ -1735,7 +1695,7 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   // (nlisted x padded n)
   L.off_chunk = take((size_t{nlisted} * std::max<uint64_t>(stride, (n + 15) & ~uint64_t{15}) /
                           kListChunk + 4) * 4);
-  L.off_off2 = take(stride * (wide ? 16 : 8) + 64);
+  L.off_off2 = take(stride * 8 + 64);
   if (gbits) {
     L.off_gbits = take(grow_bits_words(n, L.stride) * 4);
     L.off_gpref = take(grow_pref_words(n, L.stride) * 4);

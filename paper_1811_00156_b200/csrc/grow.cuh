@@ -36,18 +36,12 @@ struct SplitInfo {
   uint32_t pad0, pad1;
 };
 
-// per segment (frontier node) partition offsets; offL == INT32_MIN => leaf (drop).
-// Wide grower: bLf = left-going rows of the level before this segment (bits 0-28) plus
-// "segment / left child / right child has > 65,536 rows" flags (bits 29 / 30 / 31: its
-// list entries carry a high byte, see ListRef); fb = the segment's first position.
+// per segment (frontier node) partition offsets; offL == INT32_MIN => leaf (drop)
 struct SegTab {
   int32_t offL, offR;
   uint32_t child;  // next-frontier index of the left child
-  uint32_t bLf;
-  uint32_t fb;
   uint32_t pad;
 };
-constexpr uint32_t kBigSeg = 65536;  // wide-grower list entries: 16 bits below this size
 
 // Device view of a PreparedDataset (forest.hpp:134-161): column store, responses,
 // per-column (value,row) argsort, dense value ranks and the distinct values.
@@ -76,8 +70,7 @@ struct SlotLayout {
   uint32_t fmax;    // max frontier width
   uint32_t emax;    // max eligible nodes per level
   uint32_t nodes_cap;
-  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_hi0, off_hi1,
-      off_seg0,
+  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
       off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
       off_ecls, off_wsplit;
@@ -155,9 +148,7 @@ __host__ __device__ inline size_t grow_pref_words(uint64_t n, uint32_t stride) {
   return (a > b ? a : b) + 2;
 }
 
-// wide: the batched grower's list format (16-bit segment-relative entries + a high byte
-// array used by segments of more than kBigSeg rows) and 16-byte per-position offsets
 SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, uint32_t mns,
-                       bool gbits, bool wide = false);
+                       bool gbits);
 
 }  // namespace aiwc_b200

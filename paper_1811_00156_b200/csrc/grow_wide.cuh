@@ -19,8 +19,7 @@ struct SlotPtrs {
   uint32_t* mult;
   Payload *pay, *pay_n;
   double *wyy, *wyy_n;
-  uint16_t *lists, *lists_n;  // 16-bit node-relative list entries (see ListRef)
-  uint8_t *lhi, *lhi_n;        // their high bytes (nodes of more than kBigSeg rows)
+  uint32_t *lists, *lists_n;
   uint32_t *seg, *seg_n;
   NodeWork *front, *front_n;
   SegTab* segtab;
@@ -36,7 +35,7 @@ struct SlotPtrs {
   double* nval;
   uint32_t* nrank;
   uint32_t* chunk;
-  int4* off2;  // per position: (offL, offR, fb, bLf) of its segment (SegTab)
+  int2* off2;
   uint32_t* bits;
   uint32_t* pref;
 };
@@ -51,10 +50,8 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.pay_n = reinterpret_cast<Payload*>(s + (c ? L.off_pay0 : L.off_pay1));
   p.wyy = reinterpret_cast<double*>(s + (c ? L.off_wyy1 : L.off_wyy0));
   p.wyy_n = reinterpret_cast<double*>(s + (c ? L.off_wyy0 : L.off_wyy1));
-  p.lists = reinterpret_cast<uint16_t*>(s + (c ? L.off_list1 : L.off_list0));
-  p.lists_n = reinterpret_cast<uint16_t*>(s + (c ? L.off_list0 : L.off_list1));
-  p.lhi = reinterpret_cast<uint8_t*>(s + (c ? L.off_hi1 : L.off_hi0));
-  p.lhi_n = reinterpret_cast<uint8_t*>(s + (c ? L.off_hi0 : L.off_hi1));
+  p.lists = reinterpret_cast<uint32_t*>(s + (c ? L.off_list1 : L.off_list0));
+  p.lists_n = reinterpret_cast<uint32_t*>(s + (c ? L.off_list0 : L.off_list1));
   p.seg = reinterpret_cast<uint32_t*>(s + (c ? L.off_seg1 : L.off_seg0));
   p.seg_n = reinterpret_cast<uint32_t*>(s + (c ? L.off_seg0 : L.off_seg1));
   p.front = reinterpret_cast<NodeWork*>(s + (c ? L.off_front1 : L.off_front0));
@@ -72,23 +69,10 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.nval = reinterpret_cast<double*>(s + L.off_nval);
   p.nrank = reinterpret_cast<uint32_t*>(s + L.off_nrank);
   p.chunk = reinterpret_cast<uint32_t*>(s + L.off_chunk);
-  p.off2 = reinterpret_cast<int4*>(s + L.off_off2);
+  p.off2 = reinterpret_cast<int2*>(s + L.off_off2);
   p.bits = reinterpret_cast<uint32_t*>(s + L.off_gbits);
   p.pref = reinterpret_cast<uint32_t*>(s + L.off_gpref);
   return p;
-}
-
-// list slot li of the node at positions [b, e)
-__device__ __forceinline__ ListRef list_ref(const SlotPtrs& P, uint32_t stride, int32_t li,
-                                            uint32_t b, uint32_t e) {
-  const size_t o = static_cast<size_t>(li >= 0 ? li : 0) * stride;
-  return ListRef{P.lists + o, P.lhi + o, b, e - b > kBigSeg};
-}
-// a list entry's (16-bit part, high byte) for the node-relative position r
-__device__ __forceinline__ void put_entry(uint16_t* lo, uint8_t* hi, uint32_t k, uint32_t r,
-                                          bool big) {
-  lo[k] = static_cast<uint16_t>(r);
-  if (big) hi[k] = static_cast<uint8_t>(r >> 16);
 }
 
 // tree index b of flattened item t given exclusive prefix off[0..B] (off[B] = total)
@@ -138,7 +122,7 @@ __device__ __forceinline__ uint32_t nchunks_of(uint32_t A, uint32_t nl) {
 // true when list-pass chunk [cb, ce) lies inside one list and one segment; then `u`
 // holds that segment's (offL, offR) and the chunk needs no per-position offsets
 __device__ __forceinline__ bool chunk_uniform(uint32_t cb, uint32_t ce, uint32_t A16, uint32_t A,
-                                              const uint32_t* seg, const int4* off2, int4& u) {
+                                              const uint32_t* seg, const int2* off2, int2& u) {
   const uint32_t li = cb / A16;
   if ((ce - 1) / A16 != li) return false;
   const uint32_t k0 = cb - li * A16;
@@ -310,12 +294,10 @@ __global__ void w_l0scatter(const WideArgs a) {
       const uint32_t mine = __popc(in);
       const uint32_t inc = warp_incl_scan(mine);
       uint32_t o = run + inc - mine - li * A0;
-      uint16_t* out = P.lists + static_cast<size_t>(li) * stride;
-      uint8_t* outh = P.lhi + static_cast<size_t>(li) * stride;
-      const bool big = A0 > kBigSeg;  // the root: positions relative to 0
+      uint32_t* out = P.lists + static_cast<size_t>(li) * stride;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if ((in >> j) & 1u) put_entry(out, outh, o++, inbag_pos(P.bits, P.pref, r4[j]), big);
+        if ((in >> j) & 1u) out[o++] = inbag_pos(P.bits, P.pref, r4[j]);
       run += __shfl_sync(kFull, inc, 31);
     }
   }
@@ -520,7 +502,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
       double bg;
       uint32_t bp;
       chain_grp<RankT, (GB < 32 ? GB : 16), UB>(
-          act, li >= 0, list_ref(P, stride, li, nw_.b, nw_.e), nw_.b,
+          act, li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride, nw_.b,
           nw_.e, P.pay, rank + static_cast<size_t>(c) * n, nw_.w, nw_.s, bg, bp,
           stage[warp_id()] + grp * UB * GB);
       if (act && (lane_id() % GB) == 0) P.res[e * m + jj] = ChainRes{bg, bp, 0u};
@@ -531,7 +513,7 @@ __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     double bg;
     uint32_t bp;
-    chain_warp_p<RankT, 2>(li >= 0, list_ref(P, stride, li, nw_.b, nw_.e),
+    chain_warp_p<RankT, 2>(li >= 0, P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride,
                            nw_.b, nw_.e, P.pay, rk_c, nw_.w, nw_.s, bg, bp, stage[warp_id()]);
     if (lane_id() == 0) P.res[slot] = ChainRes{bg, bp, 0u};
   }
@@ -591,7 +573,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
     const uint32_t c = P.samp[slot];
     const int32_t li = a.g.d.list_of[c];
     const bool listed = li >= 0;
-    const ListRef list = list_ref(P, stride, li, nw.b, nw.e);
+    const uint32_t* list = P.lists + static_cast<size_t>(listed ? li : 0) * stride;
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
     const uint32_t R = nw.e - nw.b, nblk = (R + kCB - 1) / kCB;
     // producers: a register pipeline over blocks -- at step i a producer lane writes
@@ -651,9 +633,7 @@ __global__ void __launch_bounds__(128) w_chains_coop(const WideArgs a) {
 #pragma unroll
       for (int j = 0; j < kCoopE; ++j) {  // list entries of block i+4
         const int64_t x = pos(i + 4, j);
-        q4[j] = (x >= 0 && x < R) ? (listed ? list.at(nw.b + static_cast<uint32_t>(x))
-                                             : nw.b + static_cast<uint32_t>(x))
-                                  : 0u;
+        q4[j] = (x >= 0 && x < R) ? (listed ? list[nw.b + x] : nw.b + static_cast<uint32_t>(x)) : 0u;
       }
     };
     // producer scoring state: weight prefix carry, last rank, best gain (first max)
@@ -807,7 +787,7 @@ __global__ void __launch_bounds__(256) w_chains_grp(const WideArgs a) {
     const uint32_t c = act ? P.samp[e * m + j] : 0u;
     const int32_t li = a.g.d.list_of[c];
     const RankT* rk_c = rank + static_cast<size_t>(c) * n;
-    const ListRef list = list_ref(P, stride, li, nw_.b, nw_.e);
+    const uint32_t* list = P.lists + static_cast<size_t>(li >= 0 ? li : 0) * stride;
     double bg;
     uint32_t bp;
     chain_grp<RankT, G, U>(act, li >= 0, list, nw_.b, nw_.e, P.pay, rk_c, nw_.w, nw_.s,
@@ -835,7 +815,7 @@ __global__ void __launch_bounds__(256) w_chains_lane(const WideArgs a) {
     double bg;
     uint32_t bp;
     if (li >= 0)
-      chain_lane<RankT>(list_ref(P, stride, li, nw_.b, nw_.e), nw_.b, nw_.e,
+      chain_lane<RankT>(P.lists + static_cast<size_t>(li) * stride, nw_.b, nw_.e,
                         P.pay, rk_c, nw_.w, nw_.s, bg, bp);
     else
       chain_bin_lane<RankT>(P.pay, nw_.b, nw_.e, rk_c, nw_.w, nw_.s, bg, bp);
@@ -886,9 +866,9 @@ __global__ void __launch_bounds__(NT) w_decide(const WideArgs a) {
         double prev, v;
         uint32_t lo, hi;
         if (li >= 0) {
-          const ListRef lc = list_ref(P, stride, li, nw.b, nw.e);
-          const uint32_t r1 = P.pay[lc.at(bp - 1)].row;
-          const uint32_t r0 = P.pay[lc.at(bp)].row;
+          const uint32_t* lc = P.lists + static_cast<size_t>(li) * stride;
+          const uint32_t r1 = P.pay[lc[bp - 1]].row;
+          const uint32_t r0 = P.pay[lc[bp]].row;
           prev = d.col[static_cast<size_t>(c) * n + r1];
           v = d.col[static_cast<size_t>(c) * n + r0];
           lo = rank_of(rank + static_cast<size_t>(c) * n, r1);
@@ -998,10 +978,10 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     if (!kWarp && si.cnt >= kLaneMax) continue;
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
-    const ListRef l0 = list_ref(P, stride, list0, nw.b, nw.e);
+    const uint32_t* l0 = list0 >= 0 ? P.lists + static_cast<size_t>(list0) * stride : nullptr;
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
-      if (list0 >= 0)
+      if (l0)
         route_warp_p<RankT, 2>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
                                P.bits, o, stage[warp_id()]);
       else
@@ -1009,7 +989,7 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
                                     rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
       if (lane_id() != 0) continue;
     } else {
-      if (list0 >= 0)
+      if (l0)
         route_lane<RankT>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank, P.bits, o);
       else
         route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels, rk_f,
@@ -1044,7 +1024,7 @@ __global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
     const SplitInfo si = P.spl[s];
     const NodeWork nw = P.front[si.f];
     const RankT* rk_f = rank + static_cast<size_t>(si.c) * n;
-    const ListRef l0 = list_ref(P, stride, list0, nw.b, nw.e);
+    const uint32_t* l0 = P.lists + static_cast<size_t>(list0) * stride;
     const uint32_t nblk = (nw.e - nw.b + kCoopBlock - 1) / kCoopBlock;
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0u;
     __syncthreads();
@@ -1057,7 +1037,7 @@ __global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
 #pragma unroll
       for (int j = 0; j < kCoopPerLane; ++j) {
         const uint32_t kk = base + j * 32 + lane;
-        q[j] = kk < nw.e ? l0.at(kk) : 0u;
+        q[j] = kk < nw.e ? l0[kk] : 0u;
       }
 #pragma unroll
       for (int j = 0; j < kCoopPerLane; ++j)
@@ -1153,12 +1133,10 @@ __global__ void __launch_bounds__(NT) w_segtab(const WideArgs a) {
       const SplitInfo si = P.spl[s];
       const uint32_t bL = carry + ex;
       const uint32_t bb = fr[si.f].b;
-      const uint32_t flags = (si.cnt > kBigSeg ? 1u << 29 : 0u) | (nl > kBigSeg ? 1u << 30 : 0u) |
-                             (si.cnt - nl > kBigSeg ? 1u << 31 : 0u);
       P.segtab[si.f] = SegTab{static_cast<int32_t>(si.base) - static_cast<int32_t>(bL),
                               static_cast<int32_t>(si.base + nl) - static_cast<int32_t>(bb) +
                                   static_cast<int32_t>(bL),
-                              2 * s, bL | flags, bb, 0u};
+                              2 * s, 0u};
     }
     carry += tot;
   }
@@ -1183,7 +1161,7 @@ __global__ void w_pay(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t f = P.seg[k];
     const SegTab tb = P.segtab[f];
-    P.off2[k] = make_int4(tb.offL, tb.offR, static_cast<int32_t>(tb.fb), static_cast<int32_t>(tb.bLf));
+    P.off2[k] = make_int2(tb.offL, tb.offR);
     if (tb.offL == INT_MIN) continue;
     const bool l = get_bit(P.bits, k);
     const int32_t lp = static_cast<int32_t>(bits_before(P.bits, P.pref, k));
@@ -1206,12 +1184,12 @@ __global__ void w_pay(const WideArgs a) {
 constexpr uint32_t kLwStep = 256;
 constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
 struct LwStage {
-  uint32_t q[8];  // raw 16-bit entries (node-relative)
-  int4 t[8];      // their segment's (offL, offR, fb, bLf)
+  uint32_t q[8];
+  int2 t[8];
 };
 
-__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint16_t* list,
-                                        const int4* off2) {
+__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
+                                        const int2* off2) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t k = k0 + 32u * j + lane_id();
@@ -1219,18 +1197,9 @@ __device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, con
       v.q[j] = list[k];
       v.t[j] = off2[k];
     } else {
-      v.t[j] = make_int4(INT_MIN, 0, 0, 0);
+      v.t[j] = make_int2(INT_MIN, 0);
     }
   }
-}
-
-// A kept entry's next-level list entry: node-relative position among the child's rows --
-// the left-going rows before it in its segment (left child) or the right-going ones
-// (right child); bL = left-going rows of the level before the segment.
-__device__ __forceinline__ uint32_t child_rel(bool l, uint32_t qq, uint32_t fb, uint32_t lq,
-                                              uint32_t bL) {
-  const uint32_t lefts = lq - bL;
-  return l ? lefts : (qq - fb) - lefts;
 }
 
 template <int NW>
@@ -1257,113 +1226,43 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   __syncthreads();
   const unsigned lane = lane_id(), lt = lanemask_lt();
   for (uint32_t li = warp_id(); li < nl; li += blockDim.x >> 5) {
-    const uint16_t* src = P.lists + static_cast<size_t>(li) * stride;
-    const uint8_t* srch = P.lhi + static_cast<size_t>(li) * stride;
-    uint16_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
-    uint8_t* dsth = P.lhi_n + static_cast<size_t>(li) * stride;
+    const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
+    uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
     uint32_t carry = 0;  // left-going entries of this list before the sub-row
     LwStage cur, nxt;
     lw_load(cur, 0, A, src, P.off2);
     for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
       if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
-      // absolute positions (high bytes only in segments of more than kBigSeg rows), then
-      // all 16 shared-memory lookups of the lane (branch-free), then the scatter
-      uint32_t qa[8], wv[8], pv[8];
+      // all 16 shared-memory lookups of the lane first (branch-free), then the scatter
+      uint32_t wv[8], pv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int4 t = cur.t[j];
-        uint32_t r = cur.q[j];
-        if (t.x != INT_MIN && (static_cast<uint32_t>(t.w) & (1u << 29)))
-          r |= static_cast<uint32_t>(srch[k0 + 32u * j + lane]) << 16;
-        qa[j] = t.x != INT_MIN ? static_cast<uint32_t>(t.z) + r : 0u;
+        const uint32_t wi = cur.t[j].x != INT_MIN ? cur.q[j] >> 5 : 0u;
+        wv[j] = sbits[wi];
+        pv[j] = spref[wi];
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        wv[j] = sbits[qa[j] >> 5];
-        pv[j] = spref[qa[j] >> 5];
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int4 t = cur.t[j];
+        const int2 t = cur.t[j];
         const bool keep = t.x != INT_MIN;
-        const uint32_t qq = qa[j];
+        const uint32_t qq = cur.q[j];
         const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
         const bool l = keep && bit;
         const unsigned bl = __ballot_sync(kFull, l);
         const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
         if (keep) {
-          const uint32_t lq = pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u));
+          const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
           const uint32_t k = k0 + 32u * j + lane;
-          const uint32_t bLf = static_cast<uint32_t>(t.w);
-          const uint32_t rel = child_rel(l, qq, static_cast<uint32_t>(t.z), lq, bLf & 0x1fffffffu);
+          const uint32_t nq = static_cast<uint32_t>(l ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
           const uint32_t dst =
               static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
-          put_entry(dstl, dsth, dst, rel, (bLf >> (l ? 30 : 31)) & 1u);
+          dstl[dst] = nq;
         }
         carry += __popc(bl);
       }
       cur = nxt;
     }
   }
-}
-
-// Global-bitmap list pass (tables whose bitmap exceeds shared memory): flat over
-// (tree, chunk of (list, position)).  Four consecutive positions of one list per lane.
-struct WQuad {
-  uint32_t q[4];    // absolute positions (after w_side_quad: next-level entries)
-  uint32_t f[4];    // after w_side_quad: destination offset (offL or offR)
-  uint32_t big[4];  // after w_side_quad: destination child has > kBigSeg rows
-  int4 t[4];        // segment (offL, offR, fb, bLf); offL == INT_MIN: leaf
-  uint32_t li, k0, keep;
-};
-
-__device__ __forceinline__ void w_load_quad(WQuad& v, uint32_t g0, uint32_t A16, uint32_t A,
-                                            uint32_t end, uint32_t stride, const uint16_t* lists,
-                                            const uint8_t* lhi, const int4* off2,
-                                            const int4* uniform) {
-  v.keep = 0;
-  v.li = g0 / A16;
-  v.k0 = g0 - v.li * A16;
-  if (g0 < end && v.k0 < A) {
-    const size_t o = static_cast<size_t>(v.li) * stride + v.k0;
-    const uint2 x = *reinterpret_cast<const uint2*>(lists + o);
-    v.q[0] = x.x & 0xffffu; v.q[1] = x.x >> 16; v.q[2] = x.y & 0xffffu; v.q[3] = x.y >> 16;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v.t[j] = uniform ? *uniform : off2[v.k0 + j];
-    const uint32_t left = A - v.k0;
-    v.keep = left >= 4 ? 0xfu : ((1u << left) - 1u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!((v.keep >> j) & 1u) || v.t[j].x == INT_MIN) continue;
-      if (static_cast<uint32_t>(v.t[j].w) & (1u << 29)) v.q[j] |= static_cast<uint32_t>(lhi[o + j]) << 16;
-      v.q[j] += static_cast<uint32_t>(v.t[j].z);
-    }
-  }
-}
-
-// side bits of the quad's kept entries (leaf segments dropped); rewrites q to the
-// entries' next-level (node-relative) list entries, f to their offsets
-__device__ __forceinline__ uint32_t w_side_quad(WQuad& v, const uint32_t* bits,
-                                                const uint32_t* pref) {
-  uint32_t lf = 0, keep = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (!((v.keep >> j) & 1u)) continue;
-    const int4 t = v.t[j];
-    if (t.x == INT_MIN) continue;
-    keep |= 1u << j;
-    const uint32_t qq = v.q[j];
-    const uint32_t w = bits[qq >> 5];
-    const uint32_t b = (w >> (qq & 31u)) & 1u;
-    const uint32_t lq = pref[qq >> 5] + __popc(w & ((1u << (qq & 31u)) - 1u));
-    const uint32_t bLf = static_cast<uint32_t>(t.w);
-    lf |= b << j;
-    v.q[j] = child_rel(b, qq, static_cast<uint32_t>(t.z), lq, bLf & 0x1fffffffu);
-    v.f[j] = static_cast<uint32_t>(b ? t.x : t.y);
-    v.big[j] = (bLf >> (b ? 30 : 31)) & 1u;
-  }
-  v.keep = keep;
-  return lf;
 }
 
 // list pass, phase 1: kept-left counts per (tree, chunk)
@@ -1376,15 +1275,15 @@ __global__ void w_lcount(const WideArgs a) {
     const SlotPtrs P = slot_ptrs(a, b);
     const uint32_t A = a.ts[b].A, A16 = (A + 15u) & ~15u;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
-    int4 u;
+    int2 u;
     const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg, P.off2, u);
     uint32_t cnt = 0;
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
-      WQuad v;
-      w_load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.lhi, P.off2,
-                  uni ? &u : nullptr);
-      cnt += __popc(w_side_quad(v, P.bits, P.pref));
+      ListQuad v;
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.off2,
+                uni ? &u : nullptr);
+      cnt += __popc(side_quad(v, P.bits, P.pref));
     }
     cnt = warp_sum(cnt);
     if (lane_id() == 0) P.chunk[c] = cnt;
@@ -1402,20 +1301,19 @@ __global__ void w_lscatter(const WideArgs a) {
     const TreeState& st = a.ts[b];
     const uint32_t A = st.A, A16 = (A + 15u) & ~15u, totL = st.totL;
     const uint32_t ce = min(nl * A16, (c + 1) * kChunk);
-    int4 u;
+    int2 u;
     const bool uni = chunk_uniform(c * kChunk, ce, A16, A, P.seg, P.off2, u);
     uint32_t run = P.chunk[c];
 #pragma unroll 2
     for (uint32_t s = c * kChunk; s < ce; s += 128) {
-      WQuad v;
-      w_load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.lhi, P.off2,
-                  uni ? &u : nullptr);
-      const uint32_t lf = w_side_quad(v, P.bits, P.pref);
+      ListQuad v;
+      load_quad(v, s + lane_id() * 4, A16, A, ce, stride, P.lists, P.off2,
+                uni ? &u : nullptr);
+      const uint32_t lf = side_quad(v, P.bits, P.pref);
       const uint32_t mine = __popc(lf);
       const uint32_t inc = warp_incl_scan(mine);
       int32_t pl = static_cast<int32_t>(run + inc - mine - v.li * totL);
-      uint16_t* dstl = P.lists_n + static_cast<size_t>(v.li) * stride;
-      uint8_t* dsth = P.lhi_n + static_cast<size_t>(v.li) * stride;
+      uint32_t* dstl = P.lists_n + static_cast<size_t>(v.li) * stride;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (!((v.keep >> j) & 1u)) continue;
@@ -1424,7 +1322,7 @@ __global__ void w_lscatter(const WideArgs a) {
         const uint32_t dst =
             static_cast<uint32_t>(l ? off + pl : off + static_cast<int32_t>(v.k0 + j) - pl);
         pl += l ? 1 : 0;
-        put_entry(dstl, dsth, dst, v.q[j], v.big[j] != 0);
+        dstl[dst] = v.q[j];
       }
       run += __shfl_sync(kFull, inc, 31);
     }
