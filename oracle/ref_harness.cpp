@@ -253,6 +253,36 @@ int ref_grow_range(void* prep, uint32_t num_trees, uint32_t mtry, uint32_t mns,
   });
 }
 
+// The reference's fit body (forest.hpp:492-508) over the tree range [t0, t1) of a
+// num_trees forest: TreeGrower::grow for each tree via parallel_for_with_state with
+// `jobs` threads, then compute_oob over those trees -- the bounded CPU sample of a big
+// fit that includes OOB (bench.py's reference arm: distinct trees per step).
+int ref_fit_range(void* prep, uint32_t num_trees, uint32_t mtry, uint32_t mns, uint64_t seed,
+                  uint32_t t0, uint32_t t1, unsigned jobs, double* out6) {
+  return guarded([&] {
+    const auto& ctx = static_cast<PreparedDataset*>(prep)->context();
+    ForestParams params{num_trees, mtry, mns, seed};
+    Forest f;
+    f.params = params;
+    f.trees.resize(t1 - t0);
+    f.inbag.resize(t1 - t0);
+    parallel_for_with_state(
+        t1 - t0, jobs, [&] { return detail::TreeGrower(ctx, params); },
+        [&](detail::TreeGrower& g, std::size_t i) {
+          f.trees[i] = g.grow(t0 + i, f.inbag[i]);
+        });
+    const OobStats o = compute_oob(f, ctx);
+    if (out6) {
+      out6[0] = o.degenerate ? 1.0 : 0.0;
+      out6[1] = o.mse;
+      out6[2] = o.response_variance;
+      out6[3] = o.error_pct;
+      out6[4] = o.r_squared;
+      out6[5] = static_cast<double>(o.rows_evaluated);
+    }
+  });
+}
+
 // Grow tree t alone (single thread, the intended semantics -- REFERENCE_DEFECT.md) and
 // walk its out-of-bag rows exactly as compute_oob does (forest.hpp:418-433): oob[i] =
 // the leaf value tree t gives row i, NaN for in-bag rows.  Node arrays go to the caller
