@@ -305,6 +305,67 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 using namespace aiwc_b200;
 
 // ---------------------------------------------------------------------------------
+// Slot arena: one per device, holds the wide grower's tree slots between fits; released
+// when the device's last dataset context is freed.
+// ---------------------------------------------------------------------------------
+namespace aiwc_b200 {
+struct SlotArena {
+  std::mutex mu;
+  DevBuf<char> buf;
+  bool busy = false;
+  int ctxs = 0;
+};
+SlotArena& slot_arena(int dev) {
+  static SlotArena arenas[64];
+  return arenas[dev & 63];
+}
+size_t slot_arena_size(int dev) {
+  SlotArena& a = slot_arena(dev);
+  std::lock_guard<std::mutex> g(a.mu);
+  return a.busy ? 0 : a.buf.count;
+}
+// exclusive use of the device's arena for one fit (grown to `bytes` if needed), or a
+// temporary block when another fit holds it
+struct SlotLease {
+  SlotArena* ar = nullptr;
+  DevBuf<char> own;
+  char* p = nullptr;
+  SlotLease(int dev, size_t bytes) {
+    SlotArena& a = slot_arena(dev);
+    {
+      std::lock_guard<std::mutex> g(a.mu);
+      if (!a.busy) {
+        a.busy = true;
+        ar = &a;
+      }
+    }
+    if (ar) {
+      try {
+        if (ar->buf.count < bytes) {
+          ar->buf.release();
+          ar->buf.alloc(bytes);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> g(ar->mu);
+        ar->busy = false;
+        throw;
+      }
+      p = ar->buf.p;
+    } else {
+      own.alloc(bytes);
+      p = own.p;
+    }
+  }
+  ~SlotLease() {
+    if (ar) {
+      std::lock_guard<std::mutex> g(ar->mu);
+      ar->busy = false;
+    }
+  }
+};
+}  // namespace aiwc_b200
+
+// ---------------------------------------------------------------------------------
 // PreparedDataset on the device
 // ---------------------------------------------------------------------------------
 struct aiwc_ctx {
@@ -333,7 +394,6 @@ struct aiwc_ctx {
   } q;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
-  DevBuf<char> scratch;
   cudaStream_t stream = nullptr;
   ~aiwc_ctx() {
     if (stream) cudaStreamDestroy(stream);
@@ -546,6 +606,11 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p, 
       CK(cudaMemcpyAsync(ctx->listed.p, listed.data(), listed.size() * 4, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ctx->vals_off.p, voff.data(), voff.size() * 8, cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // the temporaries above are freed on return
+    {
+      SlotArena& ar = slot_arena(device);
+      std::lock_guard<std::mutex> g(ar.mu);
+      ++ar.ctxs;
+    }
     *out = ctx.release();
   });
 }
@@ -555,6 +620,14 @@ int aiwc_ctx_free(aiwc_ctx* ctx) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(ctx->device);
+  {  // the device's last dataset: hand the slot arena back to the pool
+    SlotArena& ar = slot_arena(ctx->device);
+    std::lock_guard<std::mutex> g(ar.mu);
+    if (--ar.ctxs <= 0 && !ar.busy) {
+      ar.ctxs = 0;
+      ar.buf.release();
+    }
+  }
   delete ctx;
   cudaSetDevice(prev);
   return AIWC_OK;
@@ -794,22 +867,20 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
         cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used_now) == cudaSuccess &&
         reserved > used_now)
       free_b += reserved - used_now;
-    free_b += ctx->scratch.count;
+    free_b += slot_arena_size(dev);
   }
   const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
   slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
   if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
   const size_t need = size_t(slots) * L.bytes;
   tmark("budget");
-  if (ctx->scratch.count < need) ctx->scratch.alloc(need);
+  // the slots live in the device's slot arena (kept between fits: a 100+ GB block
+  // re-allocated every fit fragmented the pool around the forests' own allocations and
+  // the next fit stalled for seconds while the pool grew); a second fit running on the
+  // device at the same time gets its own temporary block
+  SlotLease lease(dev, need);
   tmark("scratch");
-  a.scratch = ctx->scratch.p;
-  // hand the slots back to the stream-ordered pool when the fit ends (the pool keeps
-  // them reserved, so the next fit -- on this or another dataset -- reuses them)
-  struct ScratchRelease {
-    DevBuf<char>& b;
-    ~ScratchRelease() { b.release(); }
-  } scratch_release{ctx->scratch};
+  a.scratch = lease.p;
   int nlanes = 1;
   if (wide) {
     // concurrent batches (streams + host threads): 2 -> 4 measured +3 % at C4; a small
