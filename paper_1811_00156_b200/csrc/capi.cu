@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <condition_variable>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include "aiwc_cuda.h"
 #include "forest_kernels.cuh"
@@ -198,57 +200,133 @@ unsigned copy_threads() {
   return n;
 }
 
+// Persistent host copy workers (the pinned <-> pageable copies): a job is split into
+// parts run by the workers and the calling thread; one job at a time.  Round 1 started
+// 16 fresh threads per 64 MB chunk (2,500 thread starts per 10 GB export).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool(copy_threads() - 1);  // never destroyed (exit-safe)
+    return *p;
+  }
+  // f(i) for i < n, spread over the workers and the caller; returns when all are done
+  void run(unsigned n, const std::function<void(unsigned)>& f) {
+    std::lock_guard<std::mutex> job_lock(job_mu_);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      parts_ = n;
+      next_ = 0;
+      pending_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  explicit CopyPool(unsigned workers) {
+    for (unsigned i = 0; i < workers; ++i)
+      th_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> g(mu_);
+            cv_.wait(g, [&] { return gen_ != seen; });
+            seen = gen_;
+          }
+          work();
+        }
+      });
+    for (auto& t : th_) t.detach();
+  }
+  void work() {
+    for (;;) {
+      unsigned i;
+      const std::function<void(unsigned)>* f;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!job_ || next_ >= parts_) return;
+        i = next_++;
+        f = job_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<std::thread> th_;
+  const std::function<void(unsigned)>* job_ = nullptr;
+  unsigned parts_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+};
+
+// memcpy of `len` bytes split over the copy pool
+void par_memcpy(char* d, const char* p, size_t len) {
+  const unsigned nt = copy_threads();
+  if (nt <= 1 || len < (size_t{1} << 20)) {
+    std::memcpy(d, p, len);
+    return;
+  }
+  const size_t part = ((len + nt - 1) / nt + 63) & ~size_t{63};
+  CopyPool::get().run(nt, [=](unsigned t) {
+    const size_t b = size_t{t} * part;
+    if (b < len) std::memcpy(d + b, p + b, std::min(part, len - b));
+  });
+}
+
 // Device -> pageable host copy through two pinned bounce buffers (allocated once per
 // process): the DMA of chunk i+1 overlaps the multi-threaded host copy of chunk i, so
 // large exports (10 GB of C4 nodes) run at PCIe speed instead of the driver's pageable
 // path.  Small copies go straight through cudaMemcpy.
 void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   constexpr size_t kChunk = size_t{64} << 20;
+  constexpr int kBufs = 4;  // DMA runs up to three chunks ahead of the host copies
   if (bytes < (size_t{8} << 20)) {
     CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return;
   }
-  static std::mutex mu;
-  static char* pin[2] = {nullptr, nullptr};
-  std::lock_guard<std::mutex> lock(mu);
-  if (!pin[0]) {
-    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[0]), kChunk));
-    CK(cudaMallocHost(reinterpret_cast<void**>(&pin[1]), kChunk));
+  // a fresh destination (numpy zeros, std::vector) faults in 4 KB pages under the copy;
+  // transparent huge pages on request ("madvise" mode) fault 512x fewer times
+  {
+    constexpr uintptr_t kHuge = uintptr_t{2} << 20;
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(dst) + kHuge - 1) & ~(kHuge - 1);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(kHuge - 1);
+    if (e > b) madvise(reinterpret_cast<void*>(b), e - b, MADV_HUGEPAGE);  // a hint only
   }
-  cudaEvent_t ev[2];
-  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  static std::mutex mu;
+  static char* pin[kBufs] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pin[0])
+    for (int k = 0; k < kBufs; ++k) CK(cudaMallocHost(reinterpret_cast<void**>(&pin[k]), kChunk));
+  cudaEvent_t ev[kBufs];
+  for (int k = 0; k < kBufs; ++k) CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
   struct EvG {
     cudaEvent_t* e;
     ~EvG() {
-      cudaEventDestroy(e[0]);
-      cudaEventDestroy(e[1]);
+      for (int k = 0; k < kBufs; ++k) cudaEventDestroy(e[k]);
     }
   } eg{ev};
   const size_t nchunk = (bytes + kChunk - 1) / kChunk;
   auto issue = [&](size_t i) {
     const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    CK(cudaMemcpyAsync(pin[i & 1], static_cast<const char*>(src) + off, len,
+    CK(cudaMemcpyAsync(pin[i % kBufs], static_cast<const char*>(src) + off, len,
                        cudaMemcpyDeviceToHost, s));
-    CK(cudaEventRecord(ev[i & 1], s));
+    CK(cudaEventRecord(ev[i % kBufs], s));
   };
-  const unsigned nt = copy_threads();
-  issue(0);
+  for (size_t i = 0; i + 1 < kBufs && i < nchunk; ++i) issue(i);
   for (size_t i = 0; i < nchunk; ++i) {
-    if (i + 1 < nchunk) issue(i + 1);  // buffer (i+1)&1 was drained in iteration i-1
-    CK(cudaEventSynchronize(ev[i & 1]));
+    // buffer (i + kBufs - 1) % kBufs was drained in iteration i - 1
+    if (i + kBufs - 1 < nchunk) issue(i + kBufs - 1);
+    CK(cudaEventSynchronize(ev[i % kBufs]));
     const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    char* d = static_cast<char*>(dst) + off;
-    const char* p = pin[i & 1];
-    std::vector<std::thread> th;
-    const size_t part = (len + nt - 1) / nt;
-    for (unsigned t = 0; t < nt; ++t) {
-      const size_t b = t * part;
-      if (b >= len) break;
-      th.emplace_back([=] { std::memcpy(d + b, p + b, std::min(part, len - b)); });
-    }
-    for (auto& x : th) x.join();
+    par_memcpy(static_cast<char*>(dst) + off, pin[i % kBufs], len);
   }
 }
 
@@ -279,22 +357,12 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
       cudaEventDestroy(e[1]);
     }
   } eg{ev};
-  const unsigned nt = copy_threads();
   const size_t nchunk = (bytes + kChunk - 1) / kChunk;
   for (size_t i = 0; i < nchunk; ++i) {
     if (i >= 2) CK(cudaEventSynchronize(ev[i & 1]));  // DMA out of this buffer finished
     const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
-    const char* h = static_cast<const char*>(src) + off;
-    char* p = pin[i & 1];
-    std::vector<std::thread> th;
-    const size_t part = (len + nt - 1) / nt;
-    for (unsigned t = 0; t < nt; ++t) {
-      const size_t b = t * part;
-      if (b >= len) break;
-      th.emplace_back([=] { std::memcpy(p + b, h + b, std::min(part, len - b)); });
-    }
-    for (auto& x : th) x.join();
-    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, p, len, cudaMemcpyHostToDevice, s));
+    par_memcpy(pin[i & 1], static_cast<const char*>(src) + off, len);
+    CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin[i & 1], len, cudaMemcpyHostToDevice, s));
     CK(cudaEventRecord(ev[i & 1], s));
   }
   CK(cudaStreamSynchronize(s));
@@ -1426,12 +1494,12 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
     const uint64_t N = f->off.back();
     if (offsets) std::copy(f->off.begin(), f->off.end(), offsets);
     if (f->host_cached) {  // a batched fit's forest: the batch's pinned host copy
-      if (feature) std::memcpy(feature, f->h_feature, N * 4);
-      if (threshold) std::memcpy(threshold, f->h_thr, N * 8);
-      if (left) std::memcpy(left, f->h_left, N * 4);
+      if (feature) par_memcpy(reinterpret_cast<char*>(feature), reinterpret_cast<const char*>(f->h_feature), N * 4);
+      if (threshold) par_memcpy(reinterpret_cast<char*>(threshold), reinterpret_cast<const char*>(f->h_thr), N * 8);
+      if (left) par_memcpy(reinterpret_cast<char*>(left), reinterpret_cast<const char*>(f->h_left), N * 4);
       if (right)
         for (uint64_t i = 0; i < N; ++i) right[i] = f->h_left[i] < 0 ? -1 : f->h_left[i] + 1;
-      if (value) std::memcpy(value, f->h_value, N * 8);
+      if (value) par_memcpy(reinterpret_cast<char*>(value), reinterpret_cast<const char*>(f->h_value), N * 8);
       return;
     }
     DeviceGuard dg(f->device);
@@ -1456,7 +1524,8 @@ int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag) {
     if (!f || !inbag) throw Status(AIWC_EARG, "NULL argument");
     if (!f->inbag.p) throw Status(AIWC_EEXEC, "forest holds no in-bag lists");
     if (f->host_cached) {
-      std::memcpy(inbag, f->h_inbag, size_t{f->trees} * f->n * 4);
+      par_memcpy(reinterpret_cast<char*>(inbag), reinterpret_cast<const char*>(f->h_inbag),
+                 size_t{f->trees} * f->n * 4);
       return;
     }
     DeviceGuard dg(f->device);
