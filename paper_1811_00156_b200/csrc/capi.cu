@@ -791,6 +791,11 @@ struct CellSpec {
   const uint64_t* seed;
   const uint32_t* tb;
   const uint32_t* te;
+  // hold-out folds: forest c trains on the nrows[c] table rows rows[rows_off[c] ..];
+  // no in-bag lists or OOB leaves are kept (evaluate predicts the held-out rows only)
+  const uint32_t* nrows = nullptr;
+  const uint32_t* rows = nullptr;
+  const uint64_t* rows_off = nullptr;
 };
 
 void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_node_size,
@@ -828,8 +833,9 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   a.tree_end = tree_end;
   a.L = L;
   a.bits_in_smem = smem_bits ? 1 : 0;
-  DevBuf<uint32_t> cell_m, cell_n, tcell, tidx;
-  DevBuf<uint64_t> cell_s;
+  DevBuf<uint32_t> cell_m, cell_n, tcell, tidx, fold_n, fold_rows;
+  DevBuf<uint64_t> cell_s, fold_off;
+  const bool folds = cells && cells->rows;
   if (cells) {
     std::vector<uint32_t> hc, ht;
     for (uint32_t c = 0; c < cells->n; ++c)
@@ -853,6 +859,18 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
     a.cell_seed = cell_s.p;
     a.tree_cell = tcell.p;
     a.tree_t = tidx.p;
+    if (folds) {
+      const uint64_t total_rows = cells->rows_off[cells->n];
+      fold_n.alloc(cells->n);
+      fold_off.alloc(cells->n + 1);
+      fold_rows.alloc(total_rows);
+      CK(cudaMemcpy(fold_n.p, cells->nrows, cells->n * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(fold_off.p, cells->rows_off, (cells->n + 1) * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(fold_rows.p, cells->rows, total_rows * 4, cudaMemcpyHostToDevice));
+      a.cell_nrows = fold_n.p;
+      a.cell_rows = fold_rows.p;
+      a.cell_rows_off = fold_off.p;
+    }
   }
 
   // large tables grow batches of trees level-synchronously with one grid-wide kernel
@@ -863,6 +881,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   const bool small_table = n < 65536;
   bool wide = !small_table || T >= 64;
   if (const char* e = std::getenv("AIWC_GROW_WIDE")) wide = std::atoi(e) != 0;
+  if (folds) wide = true;  // only the batched grower maps fold rows
   if (wide) {
     L = make_layout(n, p, ctx->nlisted, mtry, min_node_size, true);
     a.L = L;
@@ -899,8 +918,10 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   f->mns = min_node_size;
   f->seed = seed;
   // every (tree, row) entry of both is written by the grower (no fill needed)
-  f->inbag.alloc(size_t{T} * n);
-  f->oobleaf.alloc(size_t{T} * n);
+  if (!folds) {
+    f->inbag.alloc(size_t{T} * n);
+    f->oobleaf.alloc(size_t{T} * n);
+  }
   f->oob_ctx = ctx->uid;
   tmark("inbag+oobleaf");
   a.inbag = f->inbag.p;
@@ -922,8 +943,11 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   }
   const size_t dev_total = dev < 64 ? total_mem[dev] : 0;
   const bool small = dev_total && pool_bytes + size_t(slots) * L.bytes < dev_total / 16;
-  if (small) {
-    free_b = dev_total;  // ample: the budget below keeps every slot
+  // the device's slot arena already holds every slot this fit wants (a repeated fit of
+  // the same shape): no query either
+  const bool arena_fits = slot_arena_size(dev) >= size_t(slots) * L.bytes;
+  if (small || arena_fits) {
+    free_b = dev_total ? dev_total : ~size_t{0} >> 1;  // ample: the budget keeps every slot
   } else {
     CK(cudaMemGetInfo(&free_b, &total_b));
     // memory parked in the stream-ordered pool (and this ctx's scratch, which is
@@ -2172,56 +2196,97 @@ int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t
     if (!col || !y || !kernel_of_row || !predicted_seconds)
       throw Status(AIWC_EARG, "NULL argument");
     if (fold_begin > fold_end || fold_end > K) throw Status(AIWC_EARG, "fold range out of [0, K]");
-    // folds are independent (own dataset copy, stream and forest): a few host threads
-    // keep several folds' fits in flight; each writes only its own held-out rows
-    std::atomic<uint32_t> next{fold_begin};
-    std::mutex emu;
-    int err_rc = 0;
-    std::string err_msg;
-    auto work = [&] {
-      for (;;) {
-        const uint32_t k = next.fetch_add(1);
-        if (k >= fold_end) return;
-        {
-          std::lock_guard<std::mutex> g(emu);
-          if (err_rc) return;
-        }
-        std::vector<uint64_t> train, test;
-        for (uint64_t i = 0; i < n; ++i) (kernel_of_row[i] == k ? test : train).push_back(i);
-        if (test.empty()) continue;
-        const uint64_t m = train.size();
-        std::vector<double> tc(m * p), ty(m), rows(test.size() * p), resp(test.size());
-        for (uint32_t c = 0; c < p; ++c)
-          for (uint64_t i = 0; i < m; ++i) tc[c * m + i] = col[c * n + train[i]];
-        for (uint64_t i = 0; i < m; ++i) ty[i] = y[train[i]];
-        for (uint64_t j = 0; j < test.size(); ++j)
-          for (uint32_t c = 0; c < p; ++c) rows[j * p + c] = col[c * n + test[j]];
-        aiwc_ctx* ctx = nullptr;
-        aiwc_forest* f = nullptr;
-        int rc = aiwc_ctx_create(tc.data(), ty.data(), m, p, device, &ctx);
-        if (!rc)
-          rc = aiwc_fit(ctx, num_trees, mtry, min_node_size, host_derive_seed(seed, "holdout", k),
-                        0, num_trees, 0, &f);
-        if (!rc) rc = aiwc_predict(f, rows.data(), test.size(), p, resp.data());
-        if (f) aiwc_forest_free(f);
-        if (ctx) aiwc_ctx_free(ctx);
-        if (rc) {
-          std::lock_guard<std::mutex> g(emu);
-          if (!err_rc) {
-            err_rc = rc;
-            err_msg = g_last_error;
-          }
-          return;
-        }
-        for (uint64_t j = 0; j < test.size(); ++j)  // from_response, dataset.hpp:89-91
-          predicted_seconds[test[j]] = std::pow(10.0, resp[j]);
+    // Every fold trains on the table minus its kernel's rows (experiments.hpp:393-397),
+    // i.e. on a row subset of ONE dataset: the folds' forests grow together as one
+    // multi-forest launch over a single device copy of the table (one presort), each
+    // fold's trees drawing their bootstrap from the fold's own training rows; the
+    // held-out rows are then predicted by their fold's trees in tree order.
+    std::vector<uint32_t> fk, nrows, rows;
+    std::vector<uint64_t> roff{0};
+    std::vector<std::vector<uint64_t>> tests;
+    for (uint32_t k = fold_begin; k < fold_end; ++k) {
+      std::vector<uint64_t> test;
+      for (uint64_t i = 0; i < n; ++i)
+        if (kernel_of_row[i] == k) test.push_back(i);
+      if (test.empty()) continue;
+      for (uint64_t i = 0; i < n; ++i)
+        if (kernel_of_row[i] != k) rows.push_back(static_cast<uint32_t>(i));
+      nrows.push_back(static_cast<uint32_t>(rows.size() - roff.back()));
+      roff.push_back(rows.size());
+      fk.push_back(k);
+      tests.push_back(std::move(test));
+    }
+    if (fk.empty()) return;
+    // the checks of forest.hpp:482-490 on every fold's training set
+    for (uint32_t nk : nrows)
+      if (nk < 2) throw Status(AIWC_EEXEC, "dataset must have at least 2 rows");
+    if (num_trees < 1) throw Status(AIWC_EEXEC, "num_trees must be >= 1");
+    if (min_node_size < 1) throw Status(AIWC_EEXEC, "min_node_size must be >= 1");
+    if (mtry < 1 || mtry > p)
+      throw Status(AIWC_EEXEC, "mtry must be in [1, " + std::to_string(p) + "], got " +
+                                   std::to_string(mtry));
+    aiwc_ctx* ctx = nullptr;
+    {
+      const int rc = aiwc_ctx_create(col, y, n, p, device, &ctx);
+      if (rc) throw Status(rc, g_last_error);
+    }
+    struct CtxG {
+      aiwc_ctx* c;
+      ~CtxG() { aiwc_ctx_free(c); }
+    } cg{ctx};
+    // folds per launch: node pools of at most ~8 GB
+    const double stride = 0.6322 * static_cast<double>(n) + 8.0 * std::sqrt(static_cast<double>(n)) + 64.0;
+    const double tree_bytes = std::max(1024.0, stride) * 68.0;
+    const uint64_t cap_trees = std::max<uint64_t>(num_trees, static_cast<uint64_t>(8e9 / tree_bytes));
+    const uint32_t per_launch = static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(
+        fk.size(), std::min<uint64_t>(cap_trees / num_trees, ((uint64_t{1} << 31) - 1) / num_trees))));
+    for (uint32_t g0 = 0; g0 < fk.size(); g0 += per_launch) {
+      const uint32_t G = std::min<uint32_t>(per_launch, static_cast<uint32_t>(fk.size()) - g0);
+      std::vector<uint32_t> vm(G, mtry), vn(G, min_node_size), vtb(G, 0u), vte(G, num_trees);
+      std::vector<uint64_t> vs(G), off(G + 1);
+      for (uint32_t c = 0; c < G; ++c) {
+        vs[c] = host_derive_seed(seed, "holdout", fk[g0 + c]);
+        off[c] = roff[g0 + c] - roff[g0];
       }
-    };
-    const uint32_t nth = std::min<uint32_t>(4u, fold_end - fold_begin);
-    std::vector<std::thread> th;
-    for (uint32_t i = 0; i < nth; ++i) th.emplace_back(work);
-    for (auto& t : th) t.join();
-    if (err_rc) throw Status(err_rc, err_msg);
+      off[G] = roff[g0 + G] - roff[g0];
+      CellSpec cs{G, vm.data(), vn.data(), vs.data(), vtb.data(), vte.data()};
+      cs.nrows = nrows.data() + g0;
+      cs.rows = rows.data() + roff[g0];
+      cs.rows_off = off.data();
+      aiwc_forest* F = nullptr;
+      fit_body(ctx, G * num_trees, mtry, min_node_size, vs[0], 0, G * num_trees, 0, &cs, &F);
+      const std::unique_ptr<aiwc_forest, int (*)(aiwc_forest*)> fg(F, aiwc_forest_free);
+      // held-out rows, grouped by fold, row-major (Dataset::predictor_row)
+      std::vector<uint64_t> qoff(G + 1, 0);
+      for (uint32_t c = 0; c < G; ++c) qoff[c + 1] = qoff[c] + tests[g0 + c].size();
+      const uint64_t Q = qoff[G];
+      std::vector<double> hrows(Q * p), resp(Q);
+      for (uint32_t c = 0; c < G; ++c)
+        for (uint64_t j = 0; j < tests[g0 + c].size(); ++j)
+          for (uint32_t k = 0; k < p; ++k)
+            hrows[(qoff[c] + j) * p + k] = col[size_t{k} * n + tests[g0 + c][j]];
+      {
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        DeviceGuard dg(ctx->device);
+        const cudaStream_t st = ctx->stream;
+        DevBuf<double> drows(Q * p), dout(Q);
+        CK(cudaMemcpyAsync(drows.p, hrows.data(), Q * p * 8, cudaMemcpyHostToDevice, st));
+        ensure_packed(F, st);
+        for (uint32_t c = 0; c < G; ++c) {  // fold c: trees [c T, (c+1) T) of F
+          const uint64_t q = qoff[c + 1] - qoff[c];
+          predict_small_kernel<<<static_cast<unsigned>((q + 7) / 8), 256, 0, st>>>(
+              F->packed.p, F->d_off.p + size_t{c} * num_trees, num_trees, drows.p + qoff[c] * p,
+              q, p, dout.p + qoff[c]);
+          CK(cudaGetLastError());
+          g_launches += 1;
+        }
+        CK(cudaMemcpyAsync(resp.data(), dout.p, Q * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      for (uint32_t c = 0; c < G; ++c)  // from_response, dataset.hpp:89-91
+        for (uint64_t j = 0; j < tests[g0 + c].size(); ++j)
+          predicted_seconds[tests[g0 + c][j]] = std::pow(10.0, resp[qoff[c] + j]);
+    }
   });
 }
 

@@ -88,6 +88,12 @@ struct GrowArgs {
   const uint32_t* cell_mtry;
   const uint32_t* cell_mns;
   const uint64_t* cell_seed;
+  // hold-out folds (evaluate, experiments.hpp:393-397): forest c trains on
+  // cell_nrows[c] rows of the table, its local row i being table row
+  // cell_rows[cell_rows_off[c] + i] (ascending).  Null: every forest trains on all n rows.
+  const uint32_t* cell_nrows;
+  const uint32_t* cell_rows;
+  const uint64_t* cell_rows_off;
   uint64_t seed;
   uint64_t tag_tree;  // fnv1a64("tree")
   uint32_t tree_begin, tree_end;

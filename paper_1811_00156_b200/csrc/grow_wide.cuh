@@ -101,6 +101,11 @@ __device__ __forceinline__ uint32_t tree_m(const WideArgs& a, uint32_t b) {
 __device__ __forceinline__ uint32_t tree_mns(const WideArgs& a, uint32_t b) {
   return a.g.tree_cell ? a.g.cell_mns[a.g.tree_cell[a.t0 + b]] : a.g.mns;
 }
+// training rows of the batch's tree b: its fold's row count, or the whole table
+__device__ __forceinline__ uint32_t tree_n(const WideArgs& a, uint32_t b) {
+  return a.g.cell_nrows ? a.g.cell_nrows[a.g.tree_cell[a.t0 + b]]
+                        : static_cast<uint32_t>(a.g.d.n);
+}
 __device__ __forceinline__ uint64_t tree_key(const WideArgs& a, uint32_t b) {
   const uint32_t tl = a.t0 + b;
   if (a.g.tree_cell)
@@ -147,10 +152,15 @@ __global__ void w_boot(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t n = static_cast<uint32_t>(a.g.d.n);
   const uint64_t key = tree_key(a, b);
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const uint32_t r = static_cast<uint32_t>(draw_bounded(key, uint64_t{j} + 1u, n));
+  // a hold-out fold draws local rows of its training subset (forest.hpp:184-190 on the
+  // fold's own dataset) and maps them to table rows
+  const uint32_t nk = tree_n(a, b);
+  const uint32_t* map =
+      a.g.cell_rows ? a.g.cell_rows + a.g.cell_rows_off[a.g.tree_cell[tl]] : nullptr;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nk; j += gridDim.x * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(draw_bounded(key, uint64_t{j} + 1u, nk));
     if (a.g.inbag) a.g.inbag[static_cast<size_t>(tl) * n + j] = r;
-    atomicAdd(P.mult + r, 1u);
+    atomicAdd(P.mult + (map ? map[r] : r), 1u);
   }
 }
 
@@ -313,7 +323,7 @@ __global__ void w_root(const WideArgs a) {
   double sum, sq;
   root_sums_warp<4>(P.pay, P.wyy, s.A, sum, sq, st);
   if (lane_id() == 0) {
-    P.front[0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(a.g.d.n), sum, sq};
+    P.front[0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(tree_n(a, b)), sum, sq};
     P.nf[0] = -1;
     P.nthr[0] = 0.0;
     P.nleft[0] = -1;
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   const SlotPtrs P = slot_ptrs(a, b);
   const NodeWork* fr = P.front;
   const uint32_t F = s.F, A = s.A, m = tree_m(a, b), p = a.g.d.p;
-  const uint32_t n = static_cast<uint32_t>(a.g.d.n);
+  const uint32_t n = tree_n(a, b);  // mtry draws continue after the n bootstrap draws
   uint32_t carry = 0;
   for (uint32_t base = 0; base < F; base += NT) {
     const uint32_t f = base + threadIdx.x;

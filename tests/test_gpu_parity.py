@@ -453,3 +453,31 @@ def test_grid_cells_batched_equal_separate_fits(c1, seed):
         f = pkg.fit(prep, pkg.ForestParams(counts[-1], m, mns, seed), compute_oob_stats=False)
         want = [s.error_pct for s in pkg.oob_prefix(f, prep, counts)]
         assert list(got[i]) == want, (m, mns)
+
+
+def test_evaluate_ragged_interleaved_folds(c1, seed):
+    """Fold-batched evaluate (all folds as one multi-forest launch on one device copy of
+    the table, each fold bootstrapping from its own training rows) on folds that are
+    neither contiguous nor equal-sized: every held-out row equals the oracle's forest fit
+    on that fold's training subset (experiments.hpp:393-402), predict_time with pow."""
+    import math
+
+    from paper_1811_00156_b200 import _check, _p, f64, lib, u32
+
+    t, _ = c1
+    K, T, m, mns = 4, 24, 6, 5
+    label = ((np.arange(t.n) * 7) // 13 % K).astype(np.uint32)
+    label[label == 3] = np.where(np.arange(t.n)[label == 3] % 3 == 0, 3, 1)  # uneven sizes
+    out = np.zeros(t.n)
+    _check(lib().aiwc_evaluate_folds(_p(t.col, f64), _p(t.y, f64), t.n, t.p, _p(label, u32), K,
+                                     0, K, T, m, mns, seed, 0, _p(out, f64)))
+    col = t.col.reshape(t.p, t.n)
+    rows_all = t.predictor_rows()
+    for k in range(K):
+        tr = np.flatnonzero(label != k)
+        te = np.flatnonzero(label == k)
+        sub = np.ascontiguousarray(col[:, tr]).reshape(-1)
+        want = Oracle.fit(sub, t.y[tr], len(tr), t.p, T, m, mns, pkg.derive_seed(seed, "holdout", k))
+        resp = Oracle.predict(rows_all[te], want)
+        exp = np.array([math.pow(10.0, r) for r in resp])
+        assert np.array_equal(out[te].view(np.uint64), exp.view(np.uint64)), f"fold {k}"
