@@ -431,12 +431,14 @@ def main():
                 a0, a1 = shard.tree_range(rank, world, T)
                 last = pkg.fit(prep, pkg.ForestParams(T, C4_MTRY, C4_MNS, seed), a0, a1,
                                compute_oob_stats=False)
+            pkg.release_cached(local)  # room for the gathered forest's torch buffers
             other["forest_gather"] = bench_forest_gather(pkg, torch, shard, last, rank, world,
                                                          local, barrier, max_over_ranks,
                                                          sum_over_ranks)
             del last
 
     del prep
+    pkg.release_cached(local)
     torch.cuda.empty_cache()
 
     # ---------------- C5 predict ----------------

@@ -192,6 +192,11 @@ int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t
                         uint32_t min_node_size, uint64_t seed, int device,
                         double* predicted_seconds);
 
+/* Hands the device's recycled fit memory (the grower's slot arena, idle per-fit blocks,
+ * the stream-ordered pool's reserve) back to the driver, e.g. before other libraries
+ * allocate large buffers.  The next large fit re-allocates what it needs. */
+int aiwc_release_cached(int device);
+
 /* ---- measurement (not part of the reference API) ----------------------------------
  * grow-kernel device time of the fit (CUDA events on the launching stream), whole fit
  * device time, sum over split nodes of their in-bag row counts (SURVEY 8d unit),

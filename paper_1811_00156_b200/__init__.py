@@ -143,6 +143,12 @@ def device_count() -> int:
     return c.value
 
 
+def release_cached(device: int = 0) -> None:
+    """Return the library's recycled device memory (slot arena, idle per-fit blocks,
+    pool reserve) to the driver (aiwc_release_cached)."""
+    _check(lib().aiwc_release_cached(device))
+
+
 def derive_seed(seed: int, tag: str, index: int = 0) -> int:
     """rng.hpp:32-35"""
     return int(lib().aiwc_derive_seed(seed, tag.encode(), index))

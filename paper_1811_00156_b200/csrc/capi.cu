@@ -44,11 +44,84 @@ void set_last_error(const std::string& m) { g_last_error = m; }
       throw Status(AIWC_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Idle large device blocks per device, kept for the next fit.  Every C4 fit allocates
+// ~45 GB of per-fit buffers (in-bag draws, OOB leaves, node pool, compacted forest);
+// taken from and returned to the stream-ordered pool they fragmented it, and a later
+// fit's allocation could stall 0.1-1.3 s while the pool mapped fresh memory
+// (profiles/r2_bench_v3_phases.txt: 0.1-1.3 s compaction allocs before).  Blocks of at least kCacheMin bytes are recycled here
+// instead: a request takes the smallest idle block of 1x-1.5x its size.
+constexpr size_t kCacheMin = size_t{64} << 20;
+struct BlockCache {
+  std::mutex mu;
+  std::vector<std::pair<char*, size_t>> idle;
+  size_t bytes = 0;
+};
+inline BlockCache& block_cache(int dev) {
+  static BlockCache c[64];
+  return c[dev & 63];
+}
+inline size_t cache_idle_bytes(int dev) {
+  BlockCache& c = block_cache(dev);
+  std::lock_guard<std::mutex> g(c.mu);
+  return c.bytes;
+}
+inline void cache_flush(int dev) {
+  BlockCache& c = block_cache(dev);
+  std::lock_guard<std::mutex> g(c.mu);
+  for (auto& b : c.idle) cudaFreeAsync(b.first, 0);
+  c.idle.clear();
+  c.bytes = 0;
+}
+inline char* cache_take(int dev, size_t need, size_t* got) {
+  {
+    BlockCache& c = block_cache(dev);
+    std::lock_guard<std::mutex> g(c.mu);
+    size_t best = SIZE_MAX;
+    for (size_t i = 0; i < c.idle.size(); ++i)
+      if (c.idle[i].second >= need && c.idle[i].second <= need + need / 2 &&
+          (best == SIZE_MAX || c.idle[i].second < c.idle[best].second))
+        best = i;
+    if (best != SIZE_MAX) {
+      char* q = c.idle[best].first;
+      *got = c.idle[best].second;
+      c.bytes -= *got;
+      c.idle.erase(c.idle.begin() + static_cast<long>(best));
+      return q;
+    }
+  }
+  char* q = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&q), need, 0) != cudaSuccess) {
+    cudaGetLastError();
+    cache_flush(dev);  // idle blocks back to the pool, then once more
+    if (cudaMallocAsync(reinterpret_cast<void**>(&q), need, 0) != cudaSuccess) {
+      cudaGetLastError();
+      throw Status(AIWC_ECUDA, "out of device memory (" + std::to_string(need >> 20) + " MB)");
+    }
+  }
+  *got = need;
+  return q;
+}
+inline void cache_give(int dev, char* q, size_t bytes) {
+  BlockCache& c = block_cache(dev);
+  std::lock_guard<std::mutex> g(c.mu);
+  c.idle.emplace_back(q, bytes);
+  c.bytes += bytes;
+  // at most 16 idle blocks (a C4 fit cycles 11: in-bag, OOB leaves, 5 node-pool
+  // arrays, 4 forest arrays): the oldest go back to the pool
+  while (c.idle.size() > 16) {
+    cudaFreeAsync(c.idle.front().first, 0);
+    c.bytes -= c.idle.front().second;
+    c.idle.erase(c.idle.begin());
+  }
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
   bool owned = true;  // false: a view into memory another object owns (never freed here)
+  int cache_dev = -1;  // >= 0: a recycled block of block_cache(cache_dev), blk_bytes long
+  size_t blk_bytes = 0;
   DevBuf() = default;
   explicit DevBuf(size_t c) { alloc(c); }
   void view(T* q, size_t c) {
@@ -65,28 +138,54 @@ struct DevBuf {
     if (c) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), 0));
     count = c;
   }
+  // large per-fit buffers: recycled through the device's block cache
+  void alloc_cached(size_t c, int dev) {
+    release();
+    count = c;
+    if (!c) return;
+    if (c * sizeof(T) < kCacheMin) {
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), 0));
+      return;
+    }
+    p = reinterpret_cast<T*>(cache_take(dev, c * sizeof(T), &blk_bytes));
+    cache_dev = dev;
+  }
   void release() {
-    if (p && owned) cudaFreeAsync(p, 0);
+    if (p && owned) {
+      if (cache_dev >= 0)
+        cache_give(cache_dev, reinterpret_cast<char*>(p), blk_bytes);
+      else
+        cudaFreeAsync(p, 0);
+    }
     p = nullptr;
     count = 0;
     owned = true;
+    cache_dev = -1;
+    blk_bytes = 0;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), count(o.count), owned(o.owned) {
+  DevBuf(DevBuf&& o) noexcept
+      : p(o.p), count(o.count), owned(o.owned), cache_dev(o.cache_dev), blk_bytes(o.blk_bytes) {
     o.p = nullptr;
     o.count = 0;
     o.owned = true;
+    o.cache_dev = -1;
+    o.blk_bytes = 0;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
     release();
     p = o.p;
     count = o.count;
     owned = o.owned;
+    cache_dev = o.cache_dev;
+    blk_bytes = o.blk_bytes;
     o.p = nullptr;
     o.count = 0;
     o.owned = true;
+    o.cache_dev = -1;
+    o.blk_bytes = 0;
     return *this;
   }
 };
@@ -694,11 +793,27 @@ int aiwc_ctx_free(aiwc_ctx* ctx) {
     if (--ar.ctxs <= 0 && !ar.busy) {
       ar.ctxs = 0;
       ar.buf.release();
+      cache_flush(ctx->device);
     }
   }
   delete ctx;
   cudaSetDevice(prev);
   return AIWC_OK;
+}
+
+int aiwc_release_cached(int device) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    {
+      SlotArena& ar = slot_arena(device);
+      std::lock_guard<std::mutex> g(ar.mu);
+      if (!ar.busy) ar.buf.release();
+    }
+    cache_flush(device);
+    CK(cudaDeviceSynchronize());
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
+  });
 }
 
 int aiwc_ctx_info(const aiwc_ctx* ctx, uint64_t* n, uint32_t* p, int* device) {
@@ -919,8 +1034,8 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   f->seed = seed;
   // every (tree, row) entry of both is written by the grower (no fill needed)
   if (!folds) {
-    f->inbag.alloc(size_t{T} * n);
-    f->oobleaf.alloc(size_t{T} * n);
+    f->inbag.alloc_cached(size_t{T} * n, dev);
+    f->oobleaf.alloc_cached(size_t{T} * n, dev);
   }
   f->oob_ctx = ctx->uid;
   tmark("inbag+oobleaf");
@@ -959,7 +1074,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
         cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used_now) == cudaSuccess &&
         reserved > used_now)
       free_b += reserved - used_now;
-    free_b += slot_arena_size(dev);
+    free_b += slot_arena_size(dev) + cache_idle_bytes(dev);
   }
   const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
   slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
@@ -1038,11 +1153,11 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
       tmark("streams+events+pool");
   const auto t_grow0 = std::chrono::steady_clock::now();
   for (int attempt = 0; attempt < 2; ++attempt) {
-    pf.alloc(cap);
-    pl.alloc(cap);
-    pt.alloc(cap);
-    pv.alloc(cap);
-    pr.alloc(cap);
+    pf.alloc_cached(cap, dev);
+    pl.alloc_cached(cap, dev);
+    pt.alloc_cached(cap, dev);
+    pv.alloc_cached(cap, dev);
+    pr.alloc_cached(cap, dev);
     a.pool_feature = pf.p;
     a.pool_left = pl.p;
     a.pool_thr = pt.p;
@@ -1159,11 +1274,13 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   f->off.assign(T + 1, 0);
   for (uint32_t t = 0; t < T; ++t) f->off[t + 1] = f->off[t] + cnt[t];
   const uint64_t N = f->off[T];
-  f->feature.alloc(N);
-  f->left.alloc(N);
-  f->thr.alloc(N);
-  f->value.alloc(N);
+  const auto t_alloc0 = std::chrono::steady_clock::now();
+  f->feature.alloc_cached(N, dev);
+  f->left.alloc_cached(N, dev);
+  f->thr.alloc_cached(N, dev);
+  f->value.alloc_cached(N, dev);
   f->d_off.alloc(T + 1);
+  const auto t_alloc1 = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(f->d_off.p, f->off.data(), (T + 1) * 8, cudaMemcpyHostToDevice, st.s));
   compact_kernel<<<T, 256, 0, st.s>>>(pf.p, pt.p, pl.p, pv.p, tree_off.p, f->d_off.p,
                                       f->feature.p, f->thr.p, f->left.p, f->value.p, nullptr);
@@ -1172,6 +1289,10 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   CK(cudaMemcpyAsync(&f->split_rows, split_rows.p, 8, cudaMemcpyDeviceToHost, st.s));
   CK(cudaStreamSynchronize(st.s));
   const auto t_compact = std::chrono::steady_clock::now();
+  if (want_prof)
+    std::fprintf(stderr, "[aiwc compact] alloc %.1f ms, kernel+sync %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(t_alloc1 - t_alloc0).count(),
+                 std::chrono::duration<double, std::milli>(t_compact - t_alloc1).count());
   if (compute_oob && tree_begin == 0 && tree_end == num_trees) {
     std::vector<double> sum(n, 0.0);
     std::vector<uint32_t> count(n, 0);
