@@ -662,7 +662,8 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
                      "cell": cells[int(err.argmin() // len(counts))],
                      "num_trees": counts[int(err.argmin() % len(counts))]}}
     prm = pkg.ForestParams(505, 30, 9, 0)
-    _ = pkg.evaluate(t, prm, seed, device=local, folds=(0, 1))  # warm-up
+    _ = pkg.evaluate(t, prm, seed, device=local,  # warm-up: this rank's whole fold share
+                     folds=shard.fold_range(rank, world, t.kernels))
     loko_runs = []
     for _ in range(3):  # every run reported; the headline is their mean
         barrier()
