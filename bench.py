@@ -624,7 +624,8 @@ def bench_grid_loko(pkg, torch, local, rank, world, barrier, max_over_ranks):
     nccl = os.environ.get("AIWC_BENCH_BACKEND", "nccl") == "nccl"
     allreduce = (shard.torch_allreduce_sum(torch.device("cuda", local) if nccl else None)
                  if world > 1 else (lambda a: a))
-    _ = pkg.grid_oob(prep, sample, counts, seed)  # warm-up (same batch sizes)
+    # warm-up: the sample plus the grid's largest batch (mtry 34, min.node.size 1..34)
+    _ = pkg.grid_oob(prep, sample + [(34, k) for k in range(1, 35)], counts, seed)
     grid_runs = []
     for _ in range(ARGS.grid_runs):  # every run reported; the headline is their mean
         barrier()

@@ -464,8 +464,12 @@ def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
     out = np.zeros((len(cells), len(cps)))
     if prepared.n < 65536 and cell_batch > 0:  # many cells' forests per launch
         cpa = np.ascontiguousarray(cps, np.uint32)
+        # largest per-tree scratch first (mtry descending, min.node.size ascending): the
+        # first batch sizes the device's slot arena and every later batch reuses it
+        order = sorted(range(len(cells)), key=lambda i: (-cells[i][0], cells[i][1]))
         for i0 in range(0, len(cells), cell_batch):
-            cs = cells[i0:i0 + cell_batch]
+            idx = order[i0:i0 + cell_batch]
+            cs = [cells[i] for i in idx]
             mt = np.ascontiguousarray([c[0] for c in cs], np.uint32)
             mn = np.ascontiguousarray([c[1] for c in cs], np.uint32)
             h = vp()
@@ -474,8 +478,8 @@ def grid_oob(prepared: PreparedDataset, cells, tree_counts, seed: int,
             try:
                 st = (OobStatsC * (len(cs) * len(cps)))()
                 _check(lib().aiwc_oob_prefix_cells(prepared._h, h, _p(cpa, u32), len(cps), st))
-                for j in range(len(cs)):
-                    out[i0 + j] = [st[j * len(cps) + i].error_pct for i in range(len(cps))]
+                for j, i in enumerate(idx):
+                    out[i] = [st[j * len(cps) + k].error_pct for k in range(len(cps))]
             finally:
                 lib().aiwc_forest_free(h)
         return out
