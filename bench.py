@@ -396,20 +396,25 @@ def main():
     # ---------------- e2e through the C-ABI with host buffers ----------------
     # one untimed warm-up step (the first new context grows the memory pool), then
     # --e2e-steps timed steps; every step is reported, the headline is their median
-    e2e_times, h2d, d2h = [], 0, 0
+    e2e_times, e2e_parts, h2d, d2h = [], [], 0, 0
     barrier()
     for it in range(1 + max(1, args.e2e_steps)):
         s = time.perf_counter()
         p2 = pkg.PreparedDataset(table.col, table.y, table.n, table.p, device=local)
+        s1 = time.perf_counter()
         if world == 1:
             f2 = pkg.fit(p2, params)
             _ = f2.oob
         else:
             f2 = pkg.fit(p2, params, int(tb), int(te), compute_oob_stats=False)
+        s2 = time.perf_counter()
         arrs = f2.export()
+        s3 = time.perf_counter()
         ib = f2.inbag()
+        s4 = time.perf_counter()
         if it > 0:
-            e2e_times.append(time.perf_counter() - s)
+            e2e_times.append(s4 - s)
+            e2e_parts.append([round(x, 4) for x in (s1 - s, s2 - s1, s3 - s2, s4 - s3)])
         h2d = table.col.nbytes + table.y.nbytes
         d2h = sum(a.nbytes for a in arrs) + ib.nbytes
         del f2, p2, arrs, ib
@@ -491,6 +496,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "trees/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": len(e2e_times), "warmup": 1,
                 "step_s": [round(x, 4) for x in e2e_times],
+                "step_parts_s": {"ctx_create,fit,export,inbag": e2e_parts},
                 "path": "aiwc_ctx_create(host col,y)+aiwc_fit+export(nodes,inbag)"},
         "gpu_launches": launches,
         "clocks": clk_summary,

@@ -391,9 +391,12 @@ void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     CK(cudaStreamSynchronize(s));
     return;
   }
-  // a fresh destination (numpy zeros, std::vector) faults in 4 KB pages under the copy;
-  // transparent huge pages on request ("madvise" mode) fault 512x fewer times
-  {
+  // AIWC_HUGE=1: ask for transparent huge pages on the destination ("madvise" mode, 512x
+  // fewer faults on a fresh buffer).  Off by default: measured no faster on a clean host,
+  // and with THP defrag "madvise" a fragmented host memory turns the faults into direct
+  // compaction stalls
+  static const bool huge = std::getenv("AIWC_HUGE") != nullptr;
+  if (huge) {
     constexpr uintptr_t kHuge = uintptr_t{2} << 20;
     const uintptr_t b = (reinterpret_cast<uintptr_t>(dst) + kHuge - 1) & ~(kHuge - 1);
     const uintptr_t e = (reinterpret_cast<uintptr_t>(dst) + bytes) & ~(kHuge - 1);
