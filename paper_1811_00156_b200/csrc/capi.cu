@@ -49,7 +49,7 @@ void set_last_error(const std::string& m) { g_last_error = m; }
 // taken from and returned to the stream-ordered pool they fragmented it, and a later
 // fit's allocation could stall 0.1-1.3 s while the pool mapped fresh memory
 // (profiles/r2_bench_v3_phases.txt: 0.1-1.3 s compaction allocs before).  Blocks of at least kCacheMin bytes are recycled here
-// instead: a request takes the smallest idle block of 1x-1.5x its size.
+// instead: a request takes the smallest idle block of 1x-1.125x its size.
 constexpr size_t kCacheMin = size_t{64} << 20;
 struct BlockCache {
   std::mutex mu;
@@ -78,7 +78,7 @@ inline char* cache_take(int dev, size_t need, size_t* got) {
     std::lock_guard<std::mutex> g(c.mu);
     size_t best = SIZE_MAX;
     for (size_t i = 0; i < c.idle.size(); ++i)
-      if (c.idle[i].second >= need && c.idle[i].second <= need + need / 2 &&
+      if (c.idle[i].second >= need && c.idle[i].second <= need + need / 8 &&
           (best == SIZE_MAX || c.idle[i].second < c.idle[best].second))
         best = i;
     if (best != SIZE_MAX) {
@@ -500,7 +500,7 @@ struct SlotLease {
   SlotArena* ar = nullptr;
   DevBuf<char> own;
   char* p = nullptr;
-  SlotLease(int dev, size_t bytes) {
+  SlotLease(int dev, size_t bytes, bool exact = false) {
     SlotArena& a = slot_arena(dev);
     {
       std::lock_guard<std::mutex> g(a.mu);
@@ -511,7 +511,7 @@ struct SlotLease {
     }
     if (ar) {
       try {
-        if (ar->buf.count < bytes) {
+        if (ar->buf.count < bytes || (exact && ar->buf.count > bytes)) {
           ar->buf.release();
           ar->buf.alloc(bytes);
         }
@@ -1061,11 +1061,8 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   }
   const size_t dev_total = dev < 64 ? total_mem[dev] : 0;
   const bool small = dev_total && pool_bytes + size_t(slots) * L.bytes < dev_total / 16;
-  // the device's slot arena already holds every slot this fit wants (a repeated fit of
-  // the same shape): no query either
-  const bool arena_fits = slot_arena_size(dev) >= size_t(slots) * L.bytes;
-  if (small || arena_fits) {
-    free_b = dev_total ? dev_total : ~size_t{0} >> 1;  // ample: the budget keeps every slot
+  if (small) {
+    free_b = dev_total;  // ample: the budget below keeps every slot
   } else {
     CK(cudaMemGetInfo(&free_b, &total_b));
     // memory parked in the stream-ordered pool (and this ctx's scratch, which is
@@ -1080,6 +1077,9 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
     free_b += slot_arena_size(dev) + cache_idle_bytes(dev);
   }
   const size_t budget = free_b > pool_bytes + (size_t{2} << 30) ? free_b - pool_bytes - (size_t{2} << 30) : 0;
+  // memory-limited (e.g. the caller still holds an earlier forest): the arena must shrink
+  // to what this fit uses, since the budget counted all of it as available
+  const bool tight = budget / L.bytes < static_cast<size_t>(slots);
   slots = static_cast<int>(std::min<size_t>(slots, budget / L.bytes));
   if (slots < 1) throw Status(AIWC_ECUDA, "not enough device memory for one tree slot");
   const size_t need = size_t(slots) * L.bytes;
@@ -1088,7 +1088,7 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   // re-allocated every fit fragmented the pool around the forests' own allocations and
   // the next fit stalled for seconds while the pool grew); a second fit running on the
   // device at the same time gets its own temporary block
-  SlotLease lease(dev, need);
+  SlotLease lease(dev, need, tight);
   tmark("scratch");
   a.scratch = lease.p;
   int nlanes = 1;

@@ -1239,38 +1239,48 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
     const uint32_t* src = P.lists + static_cast<size_t>(li) * stride;
     uint32_t* dstl = P.lists_n + static_cast<size_t>(li) * stride;
     uint32_t carry = 0;  // left-going entries of this list before the sub-row
-    LwStage cur, nxt;
-    lw_load(cur, 0, A, src, P.off2);
+    // only the list entries are prefetched a step ahead (8 registers); the step's segment
+    // offsets (mostly L2 hits: every list reads the same off2) are loaded at its start
+    uint32_t qn[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t k = 32u * j + lane;
+      qn[j] = k < A ? src[k] : 0u;
+    }
     for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
-      if (k0 + kLwStep < A) lw_load(nxt, k0 + kLwStep, A, src, P.off2);
-      // all 16 shared-memory lookups of the lane first (branch-free), then the scatter
-      uint32_t wv[8], pv[8];
+      uint32_t q[8];
+      int2 t[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t wi = cur.t[j].x != INT_MIN ? cur.q[j] >> 5 : 0u;
-        wv[j] = sbits[wi];
-        pv[j] = spref[wi];
+        q[j] = qn[j];
+        const uint32_t k = k0 + 32u * j + lane;
+        t[j] = k < A ? P.off2[k] : make_int2(INT_MIN, 0);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int2 t = cur.t[j];
-        const bool keep = t.x != INT_MIN;
-        const uint32_t qq = cur.q[j];
-        const uint32_t bit = (wv[j] >> (qq & 31u)) & 1u;
-        const bool l = keep && bit;
+        const uint32_t k = k0 + kLwStep + 32u * j + lane;
+        qn[j] = k < A ? src[k] : 0u;
+      }
+      // branch-free per entry: every lane computes its destination, the store is
+      // predicated on `keep` (entries of leaf segments are dropped)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const bool keep = t[j].x != INT_MIN;
+        const uint32_t qq = keep ? q[j] : 0u;
+        const uint32_t w = sbits[qq >> 5], pf = spref[qq >> 5];
+        const uint32_t sh = qq & 31u;
+        const bool l = keep && ((w >> sh) & 1u);
         const unsigned bl = __ballot_sync(kFull, l);
         const int32_t pl = static_cast<int32_t>(carry + __popc(bl & lt));
-        if (keep) {
-          const int32_t lq = static_cast<int32_t>(pv[j] + __popc(wv[j] & ((1u << (qq & 31u)) - 1u)));
-          const uint32_t k = k0 + 32u * j + lane;
-          const uint32_t nq = static_cast<uint32_t>(l ? t.x + lq : t.y + static_cast<int32_t>(qq) - lq);
-          const uint32_t dst =
-              static_cast<uint32_t>(l ? t.x + pl : t.y + static_cast<int32_t>(k) - pl);
-          dstl[dst] = nq;
-        }
+        const int32_t lq = static_cast<int32_t>(pf + __popc(w & ((1u << sh) - 1u)));
+        const uint32_t kk = k0 + 32u * j + lane;
+        // left: offL + (lefts before); right: offR + (position - lefts before), as selects
+        const uint32_t off = static_cast<uint32_t>(l ? t[j].x : t[j].y);
+        const uint32_t nq = off + (l ? static_cast<uint32_t>(lq) : qq - static_cast<uint32_t>(lq));
+        const uint32_t dst = off + (l ? static_cast<uint32_t>(pl) : kk - static_cast<uint32_t>(pl));
+        if (keep) dstl[dst] = nq;
         carry += __popc(bl);
       }
-      cur = nxt;
     }
   }
 }

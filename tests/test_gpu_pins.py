@@ -174,6 +174,12 @@ def test_c4_1000_tree_forest_matches_reference(c4, monkeypatch):
     rows = np.ascontiguousarray(t.col.reshape(t.p, t.n)[:, ::488].T)[:2048]
     s = ForestSoA(off, fe, th, le, ri, va)
     assert np.array_equal(bits(f.predict_response(rows)), bits(Oracle.predict(rows, s)))
+    # a second full fit while the first forest is still held: device memory is near full
+    # (the slot arena must shrink to what the budget leaves, recycled blocks must not be
+    # taken by buffers of another size)
+    f2 = pkg.fit(prep, pkg.ForestParams(cfg["trees"], cfg["mtry"], cfg["mns"], cfg["seed"]))
+    assert f2.oob.error_pct == g["oob"]["error_pct"]
+    assert np.diff(f2.offsets()).astype(int).tolist() == counts
 
 
 def test_more_than_65535_trees_small_table():
