@@ -1214,23 +1214,24 @@ __device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, con
 
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
-  extern __shared__ uint32_t sm[];
+  extern __shared__ __align__(16) uint32_t sm[];
   const uint32_t b = blockIdx.x;
   const TreeState& st = a.ts[b];
   if (st.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
   const uint32_t A = st.A, aw = (A + 31u) / 32u;
   const uint32_t nl = a.g.d.nlisted, stride = a.g.L.stride;
-  uint32_t* sbits = sm;
-  uint32_t* spref = sm + (aw + 3u) / 4u * 4u;
+  // bitmap word and its prefix interleaved: one 8-byte shared load per entry
+  uint2* sbp = reinterpret_cast<uint2*>(sm);
   {  // stage bitmap + prefix (word counts rounded up to 4: both arrays are padded)
     const uint32_t aw4 = (aw + 3u) / 4u;
     const uint4* gb = reinterpret_cast<const uint4*>(P.bits);
     const uint4* gp = reinterpret_cast<const uint4*>(P.pref);
     for (uint32_t w = threadIdx.x; w < aw4; w += blockDim.x) {
       const uint4 x = gb[w], y = gp[w];
-      sbits[4 * w] = x.x; sbits[4 * w + 1] = x.y; sbits[4 * w + 2] = x.z; sbits[4 * w + 3] = x.w;
-      spref[4 * w] = y.x; spref[4 * w + 1] = y.y; spref[4 * w + 2] = y.z; spref[4 * w + 3] = y.w;
+      uint4* d = reinterpret_cast<uint4*>(sbp + 4 * w);
+      d[0] = make_uint4(x.x, y.x, x.y, y.y);
+      d[1] = make_uint4(x.z, y.z, x.w, y.w);
     }
   }
   __syncthreads();
@@ -1267,7 +1268,8 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
       for (int j = 0; j < 8; ++j) {
         const bool keep = t[j].x != INT_MIN;
         const uint32_t qq = keep ? q[j] : 0u;
-        const uint32_t w = sbits[qq >> 5], pf = spref[qq >> 5];
+        const uint2 wp = sbp[qq >> 5];
+        const uint32_t w = wp.x, pf = wp.y;
         const uint32_t sh = qq & 31u;
         const bool l = keep && ((w >> sh) & 1u);
         const unsigned bl = __ballot_sync(kFull, l);
