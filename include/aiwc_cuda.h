@@ -95,6 +95,13 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
                        double* threshold, int32_t* left, int32_t* right, double* value);
 /* in-bag draws (forest.hpp:73), trees x n uint32, draw order */
 int aiwc_forest_export_inbag(const aiwc_forest* f, uint32_t* inbag);
+/* The same SoA and in-bag draws as host memory the forest owns: on first call the
+ * device arrays are DMA'd straight into a pinned host mirror (no bounce copy into
+ * pageable memory); the pointers stay valid until aiwc_forest_free.  inbag is set to
+ * NULL when the forest holds no in-bag lists.  Any output pointer may be NULL. */
+int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double** threshold,
+                          const int32_t** left, const int32_t** right, const double** value,
+                          const uint32_t** inbag);
 int aiwc_forest_oob_stats(const aiwc_forest* f, aiwc_oob_stats* out);
 
 /* Build a device forest from host SoA (Forest::load path).  inbag may be NULL

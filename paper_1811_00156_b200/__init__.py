@@ -96,6 +96,7 @@ def lib():
         L.aiwc_forest_node_counts.argtypes = [vp, P(u64)]
         L.aiwc_forest_export.argtypes = [vp, P(u64), P(i32), P(f64), P(i32), P(i32), P(f64)]
         L.aiwc_forest_export_inbag.argtypes = [vp, P(u32)]
+        L.aiwc_forest_host_view.argtypes = [vp] + [P(vp)] * 6
         L.aiwc_forest_oob_stats.argtypes = [vp, P(OobStatsC)]
         L.aiwc_forest_import.argtypes = [u32, P(u64), P(i32), P(f64), P(i32), P(i32), P(f64),
                                          P(u32), u64, C.c_int, P(vp)]
@@ -256,7 +257,12 @@ class Forest:
         self.num_trees, self.total_nodes, self.tree_begin = t.value, nodes.value, tb.value
 
     # --- Forest::trees (SoA, BFS node order per tree) ---
-    def export(self):
+    def export(self, view: bool = False):
+        """(offsets, feature, threshold, left, right, value).  view=True: arrays over the
+        forest's own pinned host mirror (aiwc_forest_host_view: the device arrays are
+        DMA'd into it once, no copy into pageable memory); they keep the forest alive."""
+        if view:
+            return self._host_view()[:6]
         T, N = self.num_trees, self.total_nodes
         off = np.zeros(T + 1, np.uint64)
         f = np.zeros(N, np.int32)
@@ -291,8 +297,31 @@ class Forest:
                                                device, C.byref(h)))
         return cls(h, None, n)
 
+    def _host_view(self):
+        ptrs = [vp() for _ in range(6)]
+        _check(lib().aiwc_forest_host_view(self._h, *[C.byref(q) for q in ptrs]))
+        T, N = self.num_trees, self.total_nodes
+
+        def arr(q, count, dt, shape=None):
+            if not q.value or count == 0:
+                return np.zeros(shape or (count,), dt)
+            raw = (C.c_char * (count * np.dtype(dt).itemsize)).from_address(q.value)
+            raw._owner = self  # the forest (and its mirror) outlive the array
+            a = np.frombuffer(raw, dt)
+            return a.reshape(shape) if shape else a
+
+        fe, th, le, ri, va, ib = ptrs
+        return (self.offsets(), arr(fe, N, np.int32), arr(th, N, np.float64),
+                arr(le, N, np.int32), arr(ri, N, np.int32), arr(va, N, np.float64),
+                arr(ib, T * self.n, np.uint32, (T, self.n)) if ib.value else None)
+
     # --- Forest::inbag ---
-    def inbag(self) -> np.ndarray:
+    def inbag(self, view: bool = False) -> np.ndarray:
+        if view:
+            ib = self._host_view()[6]
+            if ib is None:
+                raise ExecutionError("[3] forest holds no in-bag lists")
+            return ib
         out = np.zeros((self.num_trees, self.n), np.uint32)
         _check(lib().aiwc_forest_export_inbag(self._h, _p(out, u32)))
         return out

@@ -18,6 +18,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -278,7 +279,10 @@ struct PinnedPool {
         }
     }
     char* p = nullptr;
-    const size_t cap = std::max<size_t>(bytes + bytes / 2, size_t{1} << 20);
+    // small buffers get headroom for reuse; large ones (forest mirrors) are sized to fit
+    const size_t cap = bytes >= (size_t{1} << 30)
+                           ? (bytes + (size_t{2} << 20) - 1) & ~((size_t{2} << 20) - 1)
+                           : std::max<size_t>(bytes + bytes / 2, size_t{1} << 20);
     CK(cudaMallocHost(reinterpret_cast<void**>(&p), cap));
     return {p, cap};
   }
@@ -645,10 +649,15 @@ struct aiwc_forest {
   cudaStream_t sm_stream = nullptr;
   DevBuf<double> sm_rows, sm_out;
   std::pair<char*, size_t> sm_pin{nullptr, 0};  // from PinnedPool
+  // pinned host mirror of the node SoA (+ right children) and in-bag draws, built on the
+  // first aiwc_forest_host_view: [thr N][value N][feature N][left N][right N][inbag T*n]
+  std::mutex view_mu;
+  std::pair<char*, size_t> view_pin{nullptr, 0};  // from PinnedPool
   ~aiwc_forest() {
     if (sm_stream) cudaStreamDestroy(sm_stream);
     PinnedPool::give(sm_pin);
     PinnedPool::give(pinned);
+    PinnedPool::give(view_pin);
   }
 };
 
@@ -1664,6 +1673,69 @@ int aiwc_forest_export(const aiwc_forest* f, uint64_t* offsets, int32_t* feature
       d2h(right, r.p, N * 4, st.s);
     }
     if (value) d2h(value, f->value.p, N * 8, st.s);
+  });
+}
+
+int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double** threshold,
+                          const int32_t** left, const int32_t** right, const double** value,
+                          const uint32_t** inbag) {
+  return guard([&] {
+    if (!f) throw Status(AIWC_EARG, "forest is NULL");
+    std::lock_guard<std::mutex> lock(f->view_mu);
+    const uint64_t N = f->off.back();
+    const bool has_inbag = f->inbag.p != nullptr || (f->host_cached && f->h_inbag);
+    const size_t ib = has_inbag ? size_t{f->trees} * f->n * 4 : 0;
+    auto parts = [&](char* b) {
+      double* t = reinterpret_cast<double*>(b);
+      double* v = t + N;
+      int32_t* fe = reinterpret_cast<int32_t*>(v + N);
+      int32_t* le = fe + N;
+      int32_t* ri = le + N;
+      uint32_t* in = reinterpret_cast<uint32_t*>(ri + N + (N & 1));
+      return std::make_tuple(t, v, fe, le, ri, in);
+    };
+    if (!f->view_pin.first) {
+      const size_t bytes = N * 28 + (N & 1) * 4 + ib + 16;
+      auto pin = PinnedPool::take(bytes);
+      auto [t, v, fe, le, ri, in] = parts(pin.first);
+      try {
+        if (f->host_cached) {  // a batched fit's small forest: already on the host
+          std::memcpy(t, f->h_thr, N * 8);
+          std::memcpy(v, f->h_value, N * 8);
+          std::memcpy(fe, f->h_feature, N * 4);
+          std::memcpy(le, f->h_left, N * 4);
+          for (uint64_t i = 0; i < N; ++i) ri[i] = le[i] < 0 ? -1 : le[i] + 1;
+          if (ib) std::memcpy(in, f->h_inbag, ib);
+        } else {
+          DeviceGuard dg(f->device);
+          Stream st;
+          DevBuf<int32_t> r(N);
+          right_child_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 1u << 20)),
+                               256, 0, st.s>>>(f->left.p, N, r.p);
+          CK(cudaGetLastError());
+          g_launches += 1;
+          // straight DMA into the pinned mirror
+          CK(cudaMemcpyAsync(t, f->thr.p, N * 8, cudaMemcpyDeviceToHost, st.s));
+          CK(cudaMemcpyAsync(v, f->value.p, N * 8, cudaMemcpyDeviceToHost, st.s));
+          CK(cudaMemcpyAsync(fe, f->feature.p, N * 4, cudaMemcpyDeviceToHost, st.s));
+          CK(cudaMemcpyAsync(le, f->left.p, N * 4, cudaMemcpyDeviceToHost, st.s));
+          CK(cudaMemcpyAsync(ri, r.p, N * 4, cudaMemcpyDeviceToHost, st.s));
+          if (ib) CK(cudaMemcpyAsync(in, f->inbag.p, ib, cudaMemcpyDeviceToHost, st.s));
+          CK(cudaStreamSynchronize(st.s));
+        }
+      } catch (...) {
+        PinnedPool::give(pin);
+        throw;
+      }
+      f->view_pin = pin;
+    }
+    auto [t, v, fe, le, ri, in] = parts(f->view_pin.first);
+    if (threshold) *threshold = t;
+    if (value) *value = v;
+    if (feature) *feature = fe;
+    if (left) *left = le;
+    if (right) *right = ri;
+    if (inbag) *inbag = ib ? in : nullptr;
   });
 }
 

@@ -481,3 +481,18 @@ def test_evaluate_ragged_interleaved_folds(c1, seed):
         resp = Oracle.predict(rows_all[te], want)
         exp = np.array([math.pow(10.0, r) for r in resp])
         assert np.array_equal(out[te].view(np.uint64), exp.view(np.uint64)), f"fold {k}"
+
+
+def test_host_view_equals_export(c1, seed):
+    """aiwc_forest_host_view (pinned host mirror, zero-copy numpy views) holds exactly the
+    arrays the copying export returns."""
+    t, prep = c1
+    f = pkg.fit(prep, pkg.ForestParams(64, 6, 5, seed))
+    a = f.export()
+    v = f.export(view=True)
+    for x, y in zip(a, v):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    assert np.array_equal(f.inbag(), f.inbag(view=True))
+    ib = f.inbag(view=True)
+    del f  # the views keep the forest (and its mirror) alive
+    assert ib.shape == (64, t.n) and int(ib.sum()) > 0
