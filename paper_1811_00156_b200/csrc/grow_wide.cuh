@@ -1185,33 +1185,21 @@ __global__ void w_pay(const WideArgs a) {
 
 // List pass, single read: one CTA per tree with the tree's goes-left bitmap + prefix
 // staged in shared memory and one warp per sorted list.  A warp walks its list in
-// position order, 256 positions per step as 8 sub-rows of 32 consecutive positions
+// position order, 384 positions per step as 12 sub-rows of 32 consecutive positions
 // (lane i holds position k0 + 32j + i of sub-row j), so the count of left-going entries
 // before each entry is the warp's running carry plus ballot counts -- no count pass --
 // and each sub-row's left (right) entries land on consecutive destinations: every
-// store instruction writes at most two contiguous runs.  The next step's entries and
-// segment offsets are loaded before this step is scattered.
-constexpr uint32_t kLwStep = 256;
+// store instruction writes at most two contiguous runs.  The next step's entries are
+// loaded before this step is scattered; the step's segment offsets (off2, mostly L2 hits:
+// every list reads the same ones) at its start, and the bitmap word and its prefix come
+// interleaved from shared memory in one 8-byte load (kept lean: 64 registers, no spills,
+// branch-free with a predicated store).
+#ifndef AIWC_LW_SUB
+#define AIWC_LW_SUB 12
+#endif
+constexpr int kLwSub = AIWC_LW_SUB;  // sub-rows of 32 positions per list-pass warp step
+constexpr uint32_t kLwStep = 32u * kLwSub;
 constexpr int kLwWarps = 28;  // warps per list-pass CTA (<= 73 registers per thread)
-struct LwStage {
-  uint32_t q[8];
-  int2 t[8];
-};
-
-__device__ __forceinline__ void lw_load(LwStage& v, uint32_t k0, uint32_t A, const uint32_t* list,
-                                        const int2* off2) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t k = k0 + 32u * j + lane_id();
-    if (k < A) {
-      v.q[j] = list[k];
-      v.t[j] = off2[k];
-    } else {
-      v.t[j] = make_int2(INT_MIN, 0);
-    }
-  }
-}
-
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
   extern __shared__ __align__(16) uint32_t sm[];
@@ -1242,30 +1230,30 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
     uint32_t carry = 0;  // left-going entries of this list before the sub-row
     // only the list entries are prefetched a step ahead (8 registers); the step's segment
     // offsets (mostly L2 hits: every list reads the same off2) are loaded at its start
-    uint32_t qn[8];
+    uint32_t qn[kLwSub];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < kLwSub; ++j) {
       const uint32_t k = 32u * j + lane;
       qn[j] = k < A ? src[k] : 0u;
     }
     for (uint32_t k0 = 0; k0 < A; k0 += kLwStep) {
-      uint32_t q[8];
-      int2 t[8];
+      uint32_t q[kLwSub];
+      int2 t[kLwSub];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kLwSub; ++j) {
         q[j] = qn[j];
         const uint32_t k = k0 + 32u * j + lane;
         t[j] = k < A ? P.off2[k] : make_int2(INT_MIN, 0);
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kLwSub; ++j) {
         const uint32_t k = k0 + kLwStep + 32u * j + lane;
         qn[j] = k < A ? src[k] : 0u;
       }
       // branch-free per entry: every lane computes its destination, the store is
       // predicated on `keep` (entries of leaf segments are dropped)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < kLwSub; ++j) {
         const bool keep = t[j].x != INT_MIN;
         const uint32_t qq = keep ? q[j] : 0u;
         const uint2 wp = sbp[qq >> 5];
