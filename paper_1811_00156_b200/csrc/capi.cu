@@ -271,12 +271,15 @@ struct PinnedPool {
     {
       std::lock_guard<std::mutex> g(mu());
       auto& v = free_list();
+      size_t best = SIZE_MAX;  // best fit: a small request must not take a forest mirror
       for (size_t i = 0; i < v.size(); ++i)
-        if (v[i].second >= bytes) {
-          auto r = v[i];
-          v.erase(v.begin() + static_cast<long>(i));
-          return r;
-        }
+        if (v[i].second >= bytes && (best == SIZE_MAX || v[i].second < v[best].second))
+          best = i;
+      if (best != SIZE_MAX) {
+        auto r = v[best];
+        v.erase(v.begin() + static_cast<long>(best));
+        return r;
+      }
     }
     char* p = nullptr;
     // small buffers get headroom for reuse; large ones (forest mirrors) are sized to fit
@@ -1696,7 +1699,19 @@ int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double*
     };
     if (!f->view_pin.first) {
       const size_t bytes = N * 28 + (N & 1) * 4 + ib + 16;
+      const auto t0 = std::chrono::steady_clock::now();
       auto pin = PinnedPool::take(bytes);
+      const auto t1 = std::chrono::steady_clock::now();
+      struct Mark {
+        std::chrono::steady_clock::time_point t0, t1;
+        ~Mark() {
+          if (std::getenv("AIWC_PROFILE_PHASES"))
+            std::fprintf(stderr, "[aiwc host_view] pinned take %.1f ms, copies %.1f ms\n",
+                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                         std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - t1).count());
+        }
+      } mark{t0, t1};
       auto [t, v, fe, le, ri, in] = parts(pin.first);
       try {
         if (f->host_cached) {  // a batched fit's small forest: already on the host
