@@ -51,7 +51,7 @@ void set_last_error(const std::string& m) { g_last_error = m; }
 // fit's allocation could stall 0.1-1.3 s while the pool mapped fresh memory
 // (profiles/r2_bench_v3_phases.txt: 0.1-1.3 s compaction allocs before).  Blocks of at least kCacheMin bytes are recycled here
 // instead: a request takes the smallest idle block of 1x-1.125x its size.
-constexpr size_t kCacheMin = size_t{64} << 20;
+constexpr size_t kCacheMin = size_t{1} << 30;  // C4-scale buffers; small fits use the pool
 struct BlockCache {
   std::mutex mu;
   std::vector<std::pair<char*, size_t>> idle;
@@ -1724,17 +1724,16 @@ int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double*
         } else {
           DeviceGuard dg(f->device);
           Stream st;
-          DevBuf<int32_t> r(N);
+          // right children written by the device straight into the mapped pinned mirror
+          // (no 1.5 GB device temporary); the other arrays by DMA
           right_child_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 1u << 20)),
-                               256, 0, st.s>>>(f->left.p, N, r.p);
+                               256, 0, st.s>>>(f->left.p, N, ri);
           CK(cudaGetLastError());
           g_launches += 1;
-          // straight DMA into the pinned mirror
           CK(cudaMemcpyAsync(t, f->thr.p, N * 8, cudaMemcpyDeviceToHost, st.s));
           CK(cudaMemcpyAsync(v, f->value.p, N * 8, cudaMemcpyDeviceToHost, st.s));
           CK(cudaMemcpyAsync(fe, f->feature.p, N * 4, cudaMemcpyDeviceToHost, st.s));
           CK(cudaMemcpyAsync(le, f->left.p, N * 4, cudaMemcpyDeviceToHost, st.s));
-          CK(cudaMemcpyAsync(ri, r.p, N * 4, cudaMemcpyDeviceToHost, st.s));
           if (ib) CK(cudaMemcpyAsync(in, f->inbag.p, ib, cudaMemcpyDeviceToHost, st.s));
           CK(cudaStreamSynchronize(st.s));
         }
