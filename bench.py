@@ -38,7 +38,7 @@ def traffic_per_launch(trees: int, launches: int):
     """Measured DRAM bytes of the grow phase per launch (a launch = one fit's grow phase):
     the committed ncu capture's bytes per tree times the trees each launch grew."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_grow_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r2_grow_traffic.json")) as fh:
             d = json.load(fh)
         return d["dram_bytes_per_tree"] * trees / max(1, launches)
     except Exception:
@@ -486,7 +486,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic_per_launch(per * args.steps,
                                                                             grow_launch),
-                     "traffic_source": "profiles/r1_grow_traffic.json (ncu dram__bytes of every "
+                     "traffic_source": "profiles/r2_grow_traffic.json (ncu dram__bytes of every "
                                        "grow kernel, 148-tree fit, per tree x trees per launch)",
                      "peak_kind": peak_kind,
                      "kernel": "wide grower: the level kernels w_* of one fit (grow phase)",
