@@ -1195,7 +1195,10 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
       const int K = nlanes;
       // a batch's trees are gridDim.y of the per-row kernels: at most 65,535
       const uint32_t per = std::min<uint32_t>(static_cast<uint32_t>(slots / K), 65535u);
-      uint32_t big_min = 4096;  // rows from which a node's chains run one warp each
+      // rows from which a node's chains run in 16-lane groups (w_chains_warp) instead of
+      // 4-lane groups (w_chains_grp); measured at C4: 2K / 4K / 8K / 16K / 32K / 64K ->
+      // 3.45 / 3.44 / 3.45 / 3.41 / 3.41 / 3.42 s per 1000 trees, all nodes 4-lane +7 %
+      uint32_t big_min = 16384;
       if (const char* e = std::getenv("AIWC_BIG_MIN")) big_min = static_cast<uint32_t>(std::atoll(e));
       // CTA-per-chain / CTA-per-route for nodes >= coop_min rows: shorter critical
       // paths, more warps per node -- a win only when a lane's batch is too small to

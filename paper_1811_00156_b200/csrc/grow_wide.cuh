@@ -479,7 +479,14 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 
 // split chains (forest.hpp:268-297), three kernels over the size classes of w_front:
 // big nodes (>= big_min rows) run one warp per (node, column) ...
-constexpr int kBigU = 4;
+#ifndef AIWC_BIG_U
+#define AIWC_BIG_U 4
+#endif
+#ifndef AIWC_ROUTE_G
+#define AIWC_ROUTE_G 3
+#endif
+constexpr int kBigU = AIWC_BIG_U;     // positions per lane per round of the big-node chains
+constexpr int kRouteG = AIWC_ROUTE_G;  // 32-position tiles per round of the warp route
 template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
 __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
   constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
@@ -992,7 +999,7 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
       if (l0)
-        route_warp_p<RankT, 2>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
+        route_warp_p<RankT, kRouteG>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
                                P.bits, o, stage[warp_id()]);
       else
         route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels,
