@@ -487,6 +487,10 @@ __global__ void __launch_bounds__(NT) w_prefix(const WideArgs a, int which) {
 #endif
 constexpr int kBigU = AIWC_BIG_U;     // positions per lane per round of the big-node chains
 constexpr int kRouteG = AIWC_ROUTE_G;  // 32-position tiles per round of the warp route
+#ifndef AIWC_GRP_U
+#define AIWC_GRP_U 4
+#endif
+constexpr int kGrpU = AIWC_GRP_U;  // positions per lane per round of the mid-node chains
 template <typename RankT, int GB>  // GB lanes per chain: 32 (warp_p) or 16 / 8 (lane groups)
 __global__ void __launch_bounds__(256) w_chains_warp(const WideArgs a) {
   constexpr int UB = kBigU;  // positions per lane per round of the big-node lane groups
@@ -1455,12 +1459,12 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       WCK((w_chains_warp<RankT, 32><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_chains_coop<RankT><<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(a)));
     switch (grp_width(a.g.mtry)) {
-      case 32: WCK((w_chains_grp<RankT, 32, 4><<<wgrid, 256, 0, st>>>(a))); break;
-      case 16: WCK((w_chains_grp<RankT, 16, 4><<<wgrid, 256, 0, st>>>(a))); break;
-      case 8: WCK((w_chains_grp<RankT, 8, 4><<<wgrid, 256, 0, st>>>(a))); break;
-      case 4: WCK((w_chains_grp<RankT, 4, 4><<<wgrid, 256, 0, st>>>(a))); break;
-      case 2: WCK((w_chains_grp<RankT, 2, 4><<<wgrid, 256, 0, st>>>(a))); break;
-      default: WCK((w_chains_grp<RankT, 1, 4><<<wgrid, 256, 0, st>>>(a))); break;
+      case 32: WCK((w_chains_grp<RankT, 32, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
+      case 16: WCK((w_chains_grp<RankT, 16, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
+      case 8: WCK((w_chains_grp<RankT, 8, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
+      case 4: WCK((w_chains_grp<RankT, 4, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
+      case 2: WCK((w_chains_grp<RankT, 2, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
+      default: WCK((w_chains_grp<RankT, 1, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
     cudaMemsetAsync(a.active, 0, 4, st);
