@@ -1107,7 +1107,9 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
   if (wide) {
     // concurrent batches (streams + host threads): 2 -> 4 measured +3 % at C4; a small
     // table's single batch keeps one lane
-    nlanes = small_table ? 1 : 4;
+    // (round 2, after the list-pass change: 2 / 3 / 4 / 6 / 8 lanes -> 3.39 / 3.39 /
+    // 3.42 / 3.46 / 3.49 s per 1000 C4 trees)
+    nlanes = small_table ? 1 : 3;
     if (const char* e = std::getenv("AIWC_WIDE_LANES")) nlanes = std::max(1, std::atoi(e));
     nlanes = std::max(1, std::min(nlanes, slots));
   }

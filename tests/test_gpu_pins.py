@@ -6,7 +6,7 @@
   (d) the binned shared-memory predict instances <u8, Node8> (AIWC_PRED_NODE8) and
       <u16, Node8> (a forest with > 255 thresholds in a column);
   (e) every tree of the 1000-tree C4 forest (BASELINE configs[3]) grown with the default
-      knobs (4 lanes of ~100-tree batches) against per-tree digests of the REFERENCE's
+      knobs (3 lanes of ~180-tree batches) against per-tree digests of the REFERENCE's
       trees (tests/golden/make_c4_forest.py), and
   (f) that forest's OOB statistics, pinned from the reference.
 
@@ -140,8 +140,8 @@ def _tree_sha(fe, th, le, ri, va) -> str:
 
 @pytest.mark.slow
 def test_c4_1000_tree_forest_matches_reference(c4, monkeypatch):
-    """(e)+(f) The headline forest: 1000 C4 trees, m=8, mns=5, default knobs (4 lanes of
-    ~100-tree batches, no CTA-per-chain kernels) -- every tree's node arrays, in-bag
+    """(e)+(f) The headline forest: 1000 C4 trees, m=8, mns=5, default knobs (3 lanes of
+    ~180-tree batches, no CTA-per-chain kernels) -- every tree's node arrays, in-bag
     draws of every 50th tree and the forest's OOB statistics equal the reference's."""
     path = os.path.join(GOLD, "c4_forest_1000.json")
     if not os.path.exists(path):
