@@ -723,7 +723,7 @@ struct RouteOut {
 // ---- route + child sums in column-0 order (list of column 0), warp-cooperative -----
 template <typename RankT, int G>
 __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
-                           const Payload* pay, const double* wyy,
+                           const Payload* pay, const double* __restrict__ y,
                            const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                            RouteOut& o, double* st) {
   const unsigned lane = lane_id();
@@ -744,7 +744,7 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
         row[g] = P.row;
         mu[g] = P.mult;
         wy[g] = P.wy;
-        yy[g] = wyy[q[g]];
+        yy[g] = __dmul_rn(P.wy, __ldg(y + P.row));  // = the row's wy * y (forest.hpp:344)
       } else {
         row[g] = 0;
         mu[g] = 0;
@@ -781,7 +781,7 @@ __device__ void route_warp(const uint32_t* list0, uint32_t b, uint32_t e,
 // chain_grp), so every tile costs 32 dependent DADDs per group and no masked loops.
 template <typename RankT, int G>
 __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
-                             const Payload* pay, const double* wyy,
+                             const Payload* pay, const double* __restrict__ y,
                              const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                              RouteOut& o, double* st /* 4*32 doubles */) {
   const unsigned lane = lane_id(), grp = lane >> 3;
@@ -806,7 +806,7 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
         row[g] = P.row;
         mu[g] = P.mult;
         wy[g] = P.wy;
-        yy[g] = wyy[q[g]];
+        yy[g] = __dmul_rn(P.wy, __ldg(y + P.row));  // = the row's wy * y (forest.hpp:344)
       } else {
         row[g] = 0u;
         mu[g] = 0u;
@@ -883,7 +883,7 @@ __device__ void route_warp_p(const uint32_t* list0, uint32_t b, uint32_t e,
 
 template <typename RankT>
 __device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
-                           const Payload* pay, const double* wyy,
+                           const Payload* pay, const double* __restrict__ y,
                            const RankT* __restrict__ rk_f, uint32_t thr_rank, uint32_t* bits,
                            RouteOut& o) {
   for (uint32_t k = b; k < e; k += 4) {
@@ -898,7 +898,7 @@ __device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
         row[g] = P.row;
         mu[g] = P.mult;
         wy[g] = P.wy;
-        yy[g] = wyy[q[g]];
+        yy[g] = __dmul_rn(P.wy, __ldg(y + P.row));  // = the row's wy * y (forest.hpp:344)
       }
     }
 #pragma unroll
@@ -924,7 +924,7 @@ __device__ void route_lane(const uint32_t* list0, uint32_t b, uint32_t e,
 // with rank 0, then those with rank 1 (one pass per level of column 0) -------------
 template <typename RankT, int G>
 __device__ void route_groups_warp(const Payload* pay,
-                                  const double* wyy, uint32_t b, uint32_t e,
+                                  const double* __restrict__ y, uint32_t b, uint32_t e,
                                   const RankT* __restrict__ rk0, uint32_t k0levels,
                                   const RankT* __restrict__ rk_f, uint32_t thr_rank,
                                   uint32_t* bits, RouteOut& o, double* st) {
@@ -937,7 +937,7 @@ __device__ void route_groups_warp(const Payload* pay,
       bool sel = false, left = false;
       if (k < e) {
         P = pay[k];
-        yy = wyy[k];
+        yy = __dmul_rn(P.wy, __ldg(y + P.row));
         sel = k0levels == 1 || rank_of(rk0, P.row) == grp;
         left = sel && rank_of(rk_f, P.row) <= thr_rank;
       }
@@ -955,7 +955,7 @@ __device__ void route_groups_warp(const Payload* pay,
 
 template <typename RankT>
 __device__ void route_groups_lane(const Payload* pay,
-                                  const double* wyy, uint32_t b, uint32_t e,
+                                  const double* __restrict__ y, uint32_t b, uint32_t e,
                                   const RankT* __restrict__ rk0, uint32_t k0levels,
                                   const RankT* __restrict__ rk_f, uint32_t thr_rank,
                                   uint32_t* bits, RouteOut& o) {
@@ -963,7 +963,7 @@ __device__ void route_groups_lane(const Payload* pay,
     for (uint32_t k = b; k < e; ++k) {
       const Payload P = pay[k];
       if (k0levels != 1 && rank_of(rk0, P.row) != grp) continue;
-      const double yy = wyy[k];
+      const double yy = __dmul_rn(P.wy, __ldg(y + P.row));
       if (rank_of(rk_f, P.row) <= thr_rank) {
         atomicOr(bits + (k >> 5), 1u << (k & 31u));
         ++o.nl;
@@ -981,7 +981,7 @@ __device__ void route_groups_lane(const Payload* pay,
 
 // sequential FP64 sums over the payload in row order (root stats, forest.hpp:221-226)
 template <int G>
-__device__ void root_sums_warp(const Payload* pay, const double* wyy,
+__device__ void root_sums_warp(const Payload* pay, const double* __restrict__ y,
                                uint32_t A, double& s_out, double& q_out, double* st) {
   const unsigned lane = lane_id();
   double s = 0.0, q = 0.0;
@@ -990,8 +990,9 @@ __device__ void root_sums_warp(const Payload* pay, const double* wyy,
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t k = k0 + g * 32 + lane;
-      x[g] = k < A ? pay[k].wy : 0.0;
-      c[g] = k < A ? wyy[k] : 0.0;
+      const Payload P = k < A ? pay[k] : Payload{0u, 0u, 0.0};
+      x[g] = P.wy;
+      c[g] = k < A ? __dmul_rn(P.wy, __ldg(y + P.row)) : 0.0;
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -1033,8 +1034,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
   uint32_t* mult_g = reinterpret_cast<uint32_t*>(slot + L.off_mult);
   Payload* pay[2] = {reinterpret_cast<Payload*>(slot + L.off_pay0),
                      reinterpret_cast<Payload*>(slot + L.off_pay1)};
-  double* wyy[2] = {reinterpret_cast<double*>(slot + L.off_wyy0),
-                    reinterpret_cast<double*>(slot + L.off_wyy1)};
   uint32_t* lists[2] = {reinterpret_cast<uint32_t*>(slot + L.off_list0),
                         reinterpret_cast<uint32_t*>(slot + L.off_list1)};
   uint32_t* seg[2] = {reinterpret_cast<uint32_t*>(slot + L.off_seg0),
@@ -1140,7 +1139,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
       const double yr = __ldg(d.y + r);
       const double wy = __dmul_rn(static_cast<double>(mu), yr);
       pay[0][pos] = Payload{r, mu, wy};
-      wyy[0][pos] = __dmul_rn(wy, yr);
       seg[0][pos] = 0u;
     }
     __syncthreads();
@@ -1196,7 +1194,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
     __syncthreads();
     if (wid == 0) {
       double s, q;
-      root_sums_warp<G>(pay[0], wyy[0], A0, s, q, s_stage[wid]);
+      root_sums_warp<G>(pay[0], a.d.y, A0, s, q, s_stage[wid]);
       if (lane == 0) {
         front[0][0] = NodeWork{0u, A0, 0u, 0u, static_cast<double>(n), s, q};
         nf[0] = -1;
@@ -1417,18 +1415,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
             RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
             if (pass == 0) {
               if (l0)
-                route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank,
+                route_warp<RankT, G>(l0, nw.b, nw.e, pay[cur], a.d.y, rk_f, si.thr_rank,
                                      bits, o, s_stage[wid]);
               else
-                route_groups_warp<RankT, G>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels,
+                route_groups_warp<RankT, G>(pay[cur], a.d.y, nw.b, nw.e, rk0, k0levels,
                                             rk_f, si.thr_rank, bits, o, s_stage[wid]);
               if (lane != 0) continue;
             } else {
               if (l0)
-                route_lane<RankT>(l0, nw.b, nw.e, pay[cur], wyy[cur], rk_f, si.thr_rank, bits,
+                route_lane<RankT>(l0, nw.b, nw.e, pay[cur], a.d.y, rk_f, si.thr_rank, bits,
                                   o);
               else
-                route_groups_lane<RankT>(pay[cur], wyy[cur], nw.b, nw.e, rk0, k0levels, rk_f,
+                route_groups_lane<RankT>(pay[cur], a.d.y, nw.b, nw.e, rk0, k0levels, rk_f,
                                          si.thr_rank, bits, o);
             }
             spl[s].nl = o.nl;
@@ -1488,7 +1486,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1)) grow_kernel(const Gro
         const uint32_t dst = static_cast<uint32_t>(l ? tb.offL + lp
                                                      : tb.offR + static_cast<int32_t>(k) - lp);
         pay[nxt][dst] = pay[cur][k];
-        wyy[nxt][dst] = wyy[cur][k];
         seg[nxt][dst] = tb.child + (l ? 0u : 1u);
       }
       __syncthreads();
@@ -1671,8 +1668,6 @@ SlotLayout make_layout(uint64_t n, uint32_t p, uint32_t nlisted, uint32_t mtry, 
   L.off_mult = take(n * 4);
   L.off_pay0 = take(stride * sizeof(Payload));
   L.off_pay1 = take(stride * sizeof(Payload));
-  L.off_wyy0 = take(stride * 8);
-  L.off_wyy1 = take(stride * 8);
   L.off_list0 = take(size_t{nlisted} * stride * 4 + 64);
   L.off_list1 = take(size_t{nlisted} * stride * 4 + 64);
   L.off_seg0 = take(stride * 4 + 64);

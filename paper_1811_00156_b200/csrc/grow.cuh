@@ -70,7 +70,7 @@ struct SlotLayout {
   uint32_t fmax;    // max frontier width
   uint32_t emax;    // max eligible nodes per level
   uint32_t nodes_cap;
-  size_t off_mult, off_pay0, off_pay1, off_wyy0, off_wyy1, off_list0, off_list1, off_seg0,
+  size_t off_mult, off_pay0, off_pay1, off_list0, off_list1, off_seg0,
       off_seg1, off_front0, off_front1, off_segtab, off_e2f, off_samp, off_res, off_split,
       off_nf, off_nthr, off_nleft, off_nval, off_nrank, off_chunk, off_off2, off_gbits, off_gpref,
       off_ecls, off_wsplit;

@@ -18,7 +18,6 @@ namespace aiwc_b200 {
 struct SlotPtrs {
   uint32_t* mult;
   Payload *pay, *pay_n;
-  double *wyy, *wyy_n;
   uint32_t *lists, *lists_n;
   uint32_t *seg, *seg_n;
   NodeWork *front, *front_n;
@@ -48,8 +47,6 @@ __device__ __forceinline__ SlotPtrs slot_ptrs(const WideArgs& a, uint32_t b) {
   p.mult = reinterpret_cast<uint32_t*>(s + L.off_mult);
   p.pay = reinterpret_cast<Payload*>(s + (c ? L.off_pay1 : L.off_pay0));
   p.pay_n = reinterpret_cast<Payload*>(s + (c ? L.off_pay0 : L.off_pay1));
-  p.wyy = reinterpret_cast<double*>(s + (c ? L.off_wyy1 : L.off_wyy0));
-  p.wyy_n = reinterpret_cast<double*>(s + (c ? L.off_wyy0 : L.off_wyy1));
   p.lists = reinterpret_cast<uint32_t*>(s + (c ? L.off_list1 : L.off_list0));
   p.lists_n = reinterpret_cast<uint32_t*>(s + (c ? L.off_list0 : L.off_list1));
   p.seg = reinterpret_cast<uint32_t*>(s + (c ? L.off_seg1 : L.off_seg0));
@@ -219,7 +216,6 @@ __global__ void w_payload(const WideArgs a) {
     const double yr = __ldg(a.g.d.y + r);
     const double wy = __dmul_rn(static_cast<double>(mu), yr);
     P.pay[pos] = Payload{r, mu, wy};
-    P.wyy[pos] = __dmul_rn(wy, yr);
     P.seg[pos] = 0u;
   }
 }
@@ -321,7 +317,7 @@ __global__ void w_root(const WideArgs a) {
   TreeState& s = a.ts[b];
   if (s.done) return;
   double sum, sq;
-  root_sums_warp<4>(P.pay, P.wyy, s.A, sum, sq, st);
+  root_sums_warp<4>(P.pay, a.g.d.y, s.A, sum, sq, st);
   if (lane_id() == 0) {
     P.front[0] = NodeWork{0u, s.A, 0u, 0u, static_cast<double>(tree_n(a, b)), sum, sq};
     P.nf[0] = -1;
@@ -1003,17 +999,17 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
     RouteOut o{0, 0, 0, 0.0, 0.0, 0.0, 0.0};
     if (kWarp) {
       if (l0)
-        route_warp_p<RankT, kRouteG>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank,
+        route_warp_p<RankT, kRouteG>(l0, nw.b, nw.e, P.pay, a.g.d.y, rk_f, si.thr_rank,
                                P.bits, o, stage[warp_id()]);
       else
-        route_groups_warp<RankT, 4>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels,
+        route_groups_warp<RankT, 4>(P.pay, a.g.d.y, nw.b, nw.e, rank, k0levels,
                                     rk_f, si.thr_rank, P.bits, o, stage[warp_id()]);
       if (lane_id() != 0) continue;
     } else {
       if (l0)
-        route_lane<RankT>(l0, nw.b, nw.e, P.pay, P.wyy, rk_f, si.thr_rank, P.bits, o);
+        route_lane<RankT>(l0, nw.b, nw.e, P.pay, a.g.d.y, rk_f, si.thr_rank, P.bits, o);
       else
-        route_groups_lane<RankT>(P.pay, P.wyy, nw.b, nw.e, rank, k0levels, rk_f,
+        route_groups_lane<RankT>(P.pay, a.g.d.y, nw.b, nw.e, rank, k0levels, rk_f,
                                  si.thr_rank, P.bits, o);
     }
     P.spl[s].nl = o.nl;
@@ -1026,7 +1022,7 @@ __global__ void __launch_bounds__(256) w_route(const WideArgs a) {
 }
 
 // route of huge split nodes (column 0 listed): one CTA per node, three producer warps
-// gather blocks (list-0 entry -> payload, wyy -> split-column rank), set the goes-left
+// gather blocks (list-0 entry -> payload -> y of the row and split-column rank), set the goes-left
 // bits and stage the four masked addend streams; warp 0 runs the four sequential sums
 // (one 8-lane group each) over the previous block
 template <typename RankT>
@@ -1064,7 +1060,7 @@ __global__ void __launch_bounds__(128) w_route_coop(const WideArgs a) {
       for (int j = 0; j < kCoopPerLane; ++j)
         if (base + j * 32 + lane < nw.e) {
           pv[j] = P.pay[q[j]];
-          yy[j] = P.wyy[q[j]];
+          yy[j] = __dmul_rn(pv[j].wy, __ldg(a.g.d.y + pv[j].row));
         }
 #pragma unroll
       for (int j = 0; j < kCoopPerLane; ++j) {
@@ -1189,7 +1185,6 @@ __global__ void w_pay(const WideArgs a) {
     const uint32_t dst =
         static_cast<uint32_t>(l ? tb.offL + lp : tb.offR + static_cast<int32_t>(k) - lp);
     P.pay_n[dst] = P.pay[k];
-    P.wyy_n[dst] = P.wyy[k];
     P.seg_n[dst] = tb.child + (l ? 0u : 1u);
   }
 }
