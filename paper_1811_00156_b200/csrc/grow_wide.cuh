@@ -1442,17 +1442,26 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_l0scatter<<<wgrid, 256, 0, st>>>(a)));
   }
   WCK((w_root<<<a.B, 32, 0, st>>>(a)));
+  // small tables: a level is tens of microseconds of GPU work, so a host round trip per
+  // level would dominate; large ones check every level
+  uint32_t sync_every = n < 65536 ? 4u : 1u;
+  if (const char* e = std::getenv("AIWC_SYNC_EVERY")) sync_every = std::max(1, std::atoi(e));
   for (uint32_t level = 0;; ++level) {
     a.cur = level & 1u;
     WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
-    if (a.pair_big == 16)
-      WCK((w_chains_warp<RankT, 16><<<wgrid, 256, 0, st>>>(a)));
-    else if (a.pair_big == 8)
-      WCK((w_chains_warp<RankT, 8><<<wgrid, 256, 0, st>>>(a)));
-    else
-      WCK((w_chains_warp<RankT, 32><<<wgrid, 256, 0, st>>>(a)));
-    WCK((w_chains_coop<RankT><<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(a)));
+    // kernels whose size class cannot occur on this table (a node has at most n rows)
+    // are not launched: on a 2,220-row table a level is launch-bound
+    if (n >= a.big_min) {
+      if (a.pair_big == 16)
+        WCK((w_chains_warp<RankT, 16><<<wgrid, 256, 0, st>>>(a)));
+      else if (a.pair_big == 8)
+        WCK((w_chains_warp<RankT, 8><<<wgrid, 256, 0, st>>>(a)));
+      else
+        WCK((w_chains_warp<RankT, 32><<<wgrid, 256, 0, st>>>(a)));
+    }
+    if (n >= a.coop_min)
+      WCK((w_chains_coop<RankT><<<static_cast<unsigned>(sms) * 8, 128, 0, st>>>(a)));
     switch (grp_width(a.g.mtry)) {
       case 32: WCK((w_chains_grp<RankT, 32, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
       case 16: WCK((w_chains_grp<RankT, 16, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
@@ -1464,12 +1473,16 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
     cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
-    cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return e;
-    if (*h_active == 0) break;
+    // the host reads "any tree still splitting" every sync_every levels; levels launched
+    // after every tree is done find no work (each kernel skips done trees)
+    if ((level + 1) % sync_every == 0) {
+      cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return e;
+      if (*h_active == 0) break;
+    }
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 1)));
-    WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
+    if (n >= a.coop_min) WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
