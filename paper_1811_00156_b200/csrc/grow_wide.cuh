@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
   const uint32_t b = blockIdx.x;
+  if (b == 0 && threadIdx.x == 0) *a.active = 0u;  // w_decide counts this level's splitters
   TreeState& s = a.ts[b];
   if (s.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
@@ -1279,6 +1280,14 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
       }
     }
   }
+  // this tree's level state advances here (w_advance's work, one launch fewer per level),
+  // once every warp is done with this level's A
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TreeState& sw = a.ts[b];
+    sw.F = 2 * sw.S;
+    sw.A = sw.A_next;
+  }
 }
 
 // list pass, phase 1: kept-left counts per (tree, chunk)
@@ -1471,7 +1480,6 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       default: WCK((w_chains_grp<RankT, 1, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
-    cudaMemsetAsync(a.active, 0, 4, st);
     WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
     // the host reads "any tree still splitting" every sync_every levels; levels launched
     // after every tree is done find no work (each kernel skips done trees)
@@ -1496,7 +1504,7 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
         WCK((w_lscatter<<<wgrid, 256, 0, st>>>(a)));
       }
     }
-    WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
+    if (!a.g.d.nlisted || !lw_smem) WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
   }
   WCK((w_emit<<<a.B, 256, 0, st>>>(a)));
   if (a.g.oobleaf) WCK((w_oob<RankT><<<rowsgrid, 256, 0, st>>>(a)));
