@@ -335,7 +335,6 @@ __global__ void __launch_bounds__(NT) w_front(const WideArgs a) {
   constexpr int NW = NT / 32;
   __shared__ uint32_t sh[NW + 2];
   const uint32_t b = blockIdx.x;
-  if (b == 0 && threadIdx.x == 0) *a.active = 0u;  // w_decide counts this level's splitters
   TreeState& s = a.ts[b];
   if (s.done) return;
   const SlotPtrs P = slot_ptrs(a, b);
@@ -1280,14 +1279,6 @@ __global__ void __launch_bounds__(NW * 32) w_lwarp(const WideArgs a) {
       }
     }
   }
-  // this tree's level state advances here (w_advance's work, one launch fewer per level),
-  // once every warp is done with this level's A
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    TreeState& sw = a.ts[b];
-    sw.F = 2 * sw.S;
-    sw.A = sw.A_next;
-  }
 }
 
 // list pass, phase 1: kept-left counts per (tree, chunk)
@@ -1451,12 +1442,13 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     WCK((w_l0scatter<<<wgrid, 256, 0, st>>>(a)));
   }
   WCK((w_root<<<a.B, 32, 0, st>>>(a)));
-  // small tables: a level is tens of microseconds of GPU work, so a host round trip per
-  // level would dominate; large ones check every level
-  uint32_t sync_every = n < 65536 ? 4u : 1u;
+  // graph-launched levels (small batches, below): the host reads the split count every
+  // sync_every levels (a level is tens of microseconds of GPU work)
+  uint32_t sync_every = 4u;
   if (const char* e = std::getenv("AIWC_SYNC_EVERY")) sync_every = std::max(1, std::atoi(e));
-  for (uint32_t level = 0;; ++level) {
-    a.cur = level & 1u;
+  // one level's kernels for buffer parity a.cur: part 1 front .. decide, part 2 route ..
+  // list pass
+  auto level_part1 = [&](WideArgs& a) -> cudaError_t {
     WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
     // kernels whose size class cannot occur on this table (a node has at most n rows)
@@ -1480,15 +1472,14 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       default: WCK((w_chains_grp<RankT, 1, kGrpU><<<wgrid, 256, 0, st>>>(a))); break;
     }
     WCK((w_chains_lane<RankT><<<wgrid, 256, 0, st>>>(a)));
-    WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
-    // the host reads "any tree still splitting" every sync_every levels; levels launched
-    // after every tree is done find no work (each kernel skips done trees)
-    if ((level + 1) % sync_every == 0) {
-      cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
-      cudaError_t e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) return e;
-      if (*h_active == 0) break;
+    {  // w_decide counts this level's splitters
+      const cudaError_t em = cudaMemsetAsync(a.active, 0, 4, st);
+      if (em != cudaSuccess) return em;
     }
+    WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
+    return cudaSuccess;
+  };
+  auto level_part2 = [&](WideArgs& a) -> cudaError_t {  // route .. list pass
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 1)));
     if (n >= a.coop_min) WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
@@ -1504,7 +1495,75 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
         WCK((w_lscatter<<<wgrid, 256, 0, st>>>(a)));
       }
     }
-    if (!a.g.d.nlisted || !lw_smem) WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
+    WCK((w_advance<<<(a.B + 255) / 256, 256, 0, st>>>(a)));
+    return cudaSuccess;
+  };
+  // small batches on small tables (a paper-sized 500-tree fit): each level's ~12 kernels
+  // replayed as one CUDA graph per buffer parity -- the levels are launch-bound (C1 fit
+  // 6.3 -> 5.8 ms); a 34K-tree grid batch measured slower with graphs (277 vs 198 ms).
+  // AIWC_LEVEL_GRAPHS=0/1 forces it off/on
+  bool graphs = n < 65536 && a.B <= 4096;
+  if (const char* e = std::getenv("AIWC_LEVEL_GRAPHS")) graphs = std::atoi(e) != 0;
+  cudaGraphExec_t gx[2] = {nullptr, nullptr};
+  uint64_t per_level = 0;
+  struct GxGuard {
+    cudaGraphExec_t* g;
+    ~GxGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (g[i]) cudaGraphExecDestroy(g[i]);
+    }
+  } gxg{gx};
+  if (graphs) {
+    for (uint32_t par = 0; par < 2; ++par) {
+      a.cur = par;
+      const uint64_t l0 = *launches;
+      cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return e;
+      cudaError_t eb = level_part1(a);
+      if (eb == cudaSuccess) eb = level_part2(a);
+      cudaGraph_t g = nullptr;
+      e = cudaStreamEndCapture(st, &g);
+      if (eb != cudaSuccess) return eb;
+      if (e != cudaSuccess) return e;
+      e = cudaGraphInstantiate(&gx[par], g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return e;
+      per_level = *launches - l0;
+      *launches = l0;
+    }
+  }
+  auto any_active = [&](bool& more) -> cudaError_t {  // w_decide's count of splitters
+    cudaMemcpyAsync(h_active, a.active, 4, cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    more = *h_active != 0;
+    return e;
+  };
+  for (uint32_t level = 0;; ++level) {
+    a.cur = level & 1u;
+    bool more = true;
+    if (graphs) {
+      // whole levels as graphs; the host checks every sync_every levels (levels run after
+      // every tree is done find no work: each kernel skips done trees)
+      cudaError_t e = cudaGraphLaunch(gx[a.cur], st);
+      if (e != cudaSuccess) return e;
+      *launches += per_level;
+      if ((level + 1) % sync_every == 0) {
+        e = any_active(more);
+        if (e != cudaSuccess) return e;
+      }
+    } else {
+      // large batches: a level without work still costs its grids, so the host checks
+      // every level, before the route
+      cudaError_t e = level_part1(a);
+      if (e != cudaSuccess) return e;
+      e = any_active(more);
+      if (e != cudaSuccess) return e;
+      if (more) {
+        e = level_part2(a);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    if (!more) break;
   }
   WCK((w_emit<<<a.B, 256, 0, st>>>(a)));
   if (a.g.oobleaf) WCK((w_oob<RankT><<<rowsgrid, 256, 0, st>>>(a)));
