@@ -1446,10 +1446,17 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
   // sync_every levels (a level is tens of microseconds of GPU work)
   uint32_t sync_every = 4u;
   if (const char* e = std::getenv("AIWC_SYNC_EVERY")) sync_every = std::max(1, std::atoi(e));
+  // per-tree bookkeeping kernels (front, decide, segtab) with 128-thread CTAs when a tree
+  // has at most a few thousand rows (AIWC_SMALL_CTA=0/1 forces 512 / 128)
+  bool small_ct = n < 65536;
+  if (const char* e = std::getenv("AIWC_SMALL_CTA")) small_ct = std::atoi(e) != 0;
   // one level's kernels for buffer parity a.cur: part 1 front .. decide, part 2 route ..
   // list pass
   auto level_part1 = [&](WideArgs& a) -> cudaError_t {
-    WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
+    if (small_ct)
+      WCK((w_front<128><<<a.B, 128, 0, st>>>(a)));
+    else
+      WCK((w_front<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_prefix<1024><<<1, 1024, 0, st>>>(a, 0)));
     // kernels whose size class cannot occur on this table (a node has at most n rows)
     // are not launched: on a 2,220-row table a level is launch-bound
@@ -1476,7 +1483,10 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
       const cudaError_t em = cudaMemsetAsync(a.active, 0, 4, st);
       if (em != cudaSuccess) return em;
     }
-    WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
+    if (small_ct)
+      WCK((w_decide<128, RankT><<<a.B, 128, 0, st>>>(a)));
+    else
+      WCK((w_decide<512, RankT><<<a.B, 512, 0, st>>>(a)));
     return cudaSuccess;
   };
   auto level_part2 = [&](WideArgs& a) -> cudaError_t {  // route .. list pass
@@ -1484,7 +1494,10 @@ cudaError_t run_wide_t(WideArgs a, cudaStream_t st, int sms, uint32_t* h_active,
     if (n >= a.coop_min) WCK((w_route_coop<RankT><<<sms * 8, 128, 0, st>>>(a)));
     WCK((w_route<RankT, true><<<wgrid, 256, 0, st>>>(a)));
     WCK((w_route<RankT, false><<<wgrid, 256, 0, st>>>(a)));
-    WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
+    if (small_ct)
+      WCK((w_segtab<128><<<a.B, 128, 0, st>>>(a)));
+    else
+      WCK((w_segtab<512><<<a.B, 512, 0, st>>>(a)));
     WCK((w_pay<<<wgrid * 4, 256, 0, st>>>(a)));
     if (a.g.d.nlisted) {
       if (lw_smem) {
