@@ -83,11 +83,17 @@ __device__ __forceinline__ uint32_t owner(const uint32_t* off, uint32_t B, uint3
 }
 
 // lane-group width of the mid-size chain kernel: the widest power of two that still
-// fits all m sampled columns of a node in one warp (G = 32 / pow2ceil(m), >= 1)
+// fits all m sampled columns of a node in one warp (G = 32 / pow2ceil(m)), but at least
+// kGrpMin lanes per chain -- a node with more columns than 32 / kGrpMin then takes
+// several warps (grp_tpn)
+#ifndef AIWC_GRP_MIN
+#define AIWC_GRP_MIN 1
+#endif
+constexpr uint32_t kGrpMin = AIWC_GRP_MIN;
 __host__ __device__ inline uint32_t grp_width(uint32_t m) {
   uint32_t c = 1;
   while (c < m && c < 32) c <<= 1;
-  return 32u / c;
+  return 32u / c > kGrpMin ? 32u / c : kGrpMin;
 }
 
 // Per-tree parameters: with several forests (GrowArgs::tree_cell) the batch's tree b is
