@@ -200,8 +200,9 @@ int aiwc_evaluate_folds(const double* col, const double* y, uint64_t n, uint32_t
                         double* predicted_seconds);
 
 /* Hands the device's recycled fit memory (the grower's slot arena, idle per-fit blocks,
- * the stream-ordered pool's reserve) back to the driver, e.g. before other libraries
- * allocate large buffers.  The next large fit re-allocates what it needs. */
+ * the stream-ordered pool's reserve) and the process's idle pinned host buffers back to
+ * the driver, e.g. before other libraries allocate large buffers.  The next large fit
+ * re-allocates what it needs. */
 int aiwc_release_cached(int device);
 
 /* ---- measurement (not part of the reference API) ----------------------------------

@@ -292,7 +292,22 @@ struct PinnedPool {
   static void give(std::pair<char*, size_t> b) {
     if (!b.first) return;
     std::lock_guard<std::mutex> g(mu());
-    free_list().push_back(b);
+    auto& v = free_list();
+    v.push_back(b);
+    // at most 48 GB of idle pinned host memory (forest mirrors are ~14 GB at C4): the
+    // oldest blocks are unpinned first
+    size_t idle = 0;
+    for (auto& x : v) idle += x.second;
+    while (idle > (size_t{48} << 30) && v.size() > 1) {
+      idle -= v.front().second;
+      cudaFreeHost(v.front().first);
+      v.erase(v.begin());
+    }
+  }
+  static void release_all() {
+    std::lock_guard<std::mutex> g(mu());
+    for (auto& x : free_list()) cudaFreeHost(x.first);
+    free_list().clear();
   }
 };
 
@@ -825,6 +840,7 @@ int aiwc_release_cached(int device) {
       if (!ar.busy) ar.buf.release();
     }
     cache_flush(device);
+    PinnedPool::release_all();  // idle pinned host buffers (forest mirrors, staging)
     CK(cudaDeviceSynchronize());
     cudaMemPool_t mp;
     if (cudaDeviceGetDefaultMemPool(&mp, device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
