@@ -400,7 +400,8 @@ def main():
     barrier()
     for it in range(1 + max(1, args.e2e_steps)):
         s = time.perf_counter()
-        p2 = pkg.PreparedDataset(table.col, table.y, table.n, table.p, device=local)
+        p2 = pkg.PreparedDataset(table.col, table.y, table.n, table.p, device=local,
+                                 host_mirror=True)
         s1 = time.perf_counter()
         if world == 1:
             f2 = pkg.fit(p2, params)
@@ -497,8 +498,9 @@ def main():
                 "d2h_bytes_per_step": d2h, "steps": len(e2e_times), "warmup": 1,
                 "step_s": [round(x, 4) for x in e2e_times],
                 "step_parts_s": {"ctx_create,fit,export,inbag": e2e_parts},
-                "path": "aiwc_ctx_create(host col,y)+aiwc_fit+aiwc_forest_host_view(nodes,inbag "
-                        "DMA'd into the forest's pinned host mirror)"},
+                "path": "aiwc_ctx_create(host col,y; host mirror on)+aiwc_fit (in-bag draws "
+                        "DMA'd to pinned host memory as tree batches finish)+"
+                        "aiwc_forest_host_view (nodes DMA'd into the forest's pinned mirror)"},
         "gpu_launches": launches,
         "clocks": clk_summary,
         "setup_s": setup_s,

@@ -73,6 +73,9 @@ int aiwc_ctx_create(const double* col, const double* y, uint64_t n, uint32_t p,
                     int device, aiwc_ctx** out);
 int aiwc_ctx_free(aiwc_ctx* ctx);
 int aiwc_ctx_info(const aiwc_ctx* ctx, uint64_t* n, uint32_t* p, int* device);
+/* on != 0: fits on this dataset also copy their in-bag draws into a pinned host mirror
+ * while later tree batches grow, so aiwc_forest_host_view only has to move the nodes. */
+int aiwc_ctx_set_host_mirror(aiwc_ctx* ctx, int on);
 
 /* ---- fit -------------------------------------------------------------------
  * Grows trees [tree_begin, tree_end) of the forest keyed by (seed, tree index)

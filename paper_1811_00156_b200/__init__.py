@@ -212,7 +212,8 @@ synthesize = Table
 class PreparedDataset:
     """Device-resident column store + presort (forest.hpp:458-475)."""
 
-    def __init__(self, col: np.ndarray, y: np.ndarray, n: int, p: int, device: int = 0):
+    def __init__(self, col: np.ndarray, y: np.ndarray, n: int, p: int, device: int = 0,
+                 host_mirror: bool = False):
         self.col = np.ascontiguousarray(col, np.float64).reshape(-1)
         self.y = np.ascontiguousarray(y, np.float64)
         if self.col.size != n * p or self.y.size != n:
@@ -222,6 +223,8 @@ class PreparedDataset:
                                      C.byref(h)))
         self._h = h
         self.n, self.p, self.device = n, p, device
+        if host_mirror:  # fits stream their in-bag draws to pinned host memory as they grow
+            _check(lib().aiwc_ctx_set_host_mirror(h, 1))
 
     @classmethod
     def from_table(cls, t: Table, device: int = 0) -> "PreparedDataset":

@@ -584,6 +584,9 @@ struct aiwc_ctx {
     bool leader = false;
     size_t returning = 0;  // callers of the last batch that have not queued again yet
   } q;
+  // fits also stream their in-bag draws into a pinned host mirror while later batches
+  // grow (aiwc_ctx_set_host_mirror): the forest's host view then only moves its nodes
+  bool host_mirror = false;
   // grow scratch + launch stream, reused across fits on this dataset (serialised by `mu`)
   std::mutex mu;
   cudaStream_t stream = nullptr;
@@ -671,11 +674,13 @@ struct aiwc_forest {
   // first aiwc_forest_host_view: [thr N][value N][feature N][left N][right N][inbag T*n]
   std::mutex view_mu;
   std::pair<char*, size_t> view_pin{nullptr, 0};  // from PinnedPool
+  std::pair<char*, size_t> inbag_pin{nullptr, 0};  // in-bag mirror filled during the fit
   ~aiwc_forest() {
     if (sm_stream) cudaStreamDestroy(sm_stream);
     PinnedPool::give(sm_pin);
     PinnedPool::give(pinned);
     PinnedPool::give(view_pin);
+    PinnedPool::give(inbag_pin);
   }
 };
 
@@ -829,6 +834,14 @@ int aiwc_ctx_free(aiwc_ctx* ctx) {
   delete ctx;
   cudaSetDevice(prev);
   return AIWC_OK;
+}
+
+int aiwc_ctx_set_host_mirror(aiwc_ctx* ctx, int on) {
+  return guard([&] {
+    if (!ctx) throw Status(AIWC_EARG, "ctx is NULL");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->host_mirror = on != 0;
+  });
 }
 
 int aiwc_release_cached(int device) {
@@ -1068,6 +1081,22 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
     f->inbag.alloc_cached(size_t{T} * n, dev);
     f->oobleaf.alloc_cached(size_t{T} * n, dev);
   }
+  // in-bag host mirror: each batch's draws go to pinned memory on a copy stream while the
+  // next batches grow (the wide grower writes a batch's draws in its first kernel)
+  cudaStream_t cstream = nullptr;
+  struct CsGuard {
+    cudaStream_t& s;
+    ~CsGuard() {
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    }
+  } csg{cstream};
+  if (ctx->host_mirror && !folds && !cells && f->inbag.p) {
+    f->inbag_pin = PinnedPool::take(size_t{T} * n * 4);
+    CK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+  }
   f->oob_ctx = ctx->uid;
   tmark("inbag+oobleaf");
   a.inbag = f->inbag.p;
@@ -1258,6 +1287,10 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
             cudaError_t e = run_wide(ctx->rank_bytes, w, ls, sms, h_active.get() + k, &nl);
             g_launches += nl;
             if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
+            if (e == cudaSuccess && cstream)  // this batch's draws to the host mirror
+              e = cudaMemcpyAsync(f->inbag_pin.first + size_t{t0} * n * 4,
+                                  f->inbag.p + size_t{t0} * n, size_t{w.B} * n * 4,
+                                  cudaMemcpyDeviceToHost, cstream);
             if (e != cudaSuccess) {
               lane_err[k] = e;
               return;
@@ -1271,6 +1304,11 @@ void fit_body(aiwc_ctx* ctx, uint32_t num_trees, uint32_t mtry, uint32_t min_nod
     } else {
       CK(launch_grow(nt, ctx->rank_bytes, a, slots, dyn, st.s, nullptr));
       g_launches += 1;
+      if (cstream) {
+        CK(cudaStreamSynchronize(st.s));
+        CK(cudaMemcpyAsync(f->inbag_pin.first, f->inbag.p, size_t{T} * n * 4,
+                           cudaMemcpyDeviceToHost, cstream));
+      }
     }
     CK(cudaEventRecord(ev1, st.s));
     f->grow_launches += 1;
@@ -1708,7 +1746,8 @@ int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double*
     std::lock_guard<std::mutex> lock(f->view_mu);
     const uint64_t N = f->off.back();
     const bool has_inbag = f->inbag.p != nullptr || (f->host_cached && f->h_inbag);
-    const size_t ib = has_inbag ? size_t{f->trees} * f->n * 4 : 0;
+    const bool fit_mirror = f->inbag_pin.first != nullptr;  // filled during the fit
+    const size_t ib = has_inbag && !fit_mirror ? size_t{f->trees} * f->n * 4 : 0;
     auto parts = [&](char* b) {
       double* t = reinterpret_cast<double*>(b);
       double* v = t + N;
@@ -1770,7 +1809,9 @@ int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double*
     if (feature) *feature = fe;
     if (left) *left = le;
     if (right) *right = ri;
-    if (inbag) *inbag = ib ? in : nullptr;
+    if (inbag)
+      *inbag = fit_mirror ? reinterpret_cast<const uint32_t*>(f->inbag_pin.first)
+                          : (ib ? in : nullptr);
   });
 }
 

@@ -496,3 +496,18 @@ def test_host_view_equals_export(c1, seed):
     ib = f.inbag(view=True)
     del f  # the views keep the forest (and its mirror) alive
     assert ib.shape == (64, t.n) and int(ib.sum()) > 0
+
+
+@pytest.mark.parametrize("trees", [16, 200])
+def test_fit_time_inbag_mirror(c1, seed, trees):
+    """host_mirror datasets stream each batch's in-bag draws to pinned memory during the fit
+    (both growers: 16 trees take the CTA-per-tree one, 200 the batched one); the host view
+    equals the copying export, and the forest equals the same fit without the mirror."""
+    t, prep = c1
+    pm = pkg.PreparedDataset(t.col, t.y, t.n, t.p, host_mirror=True)
+    params = pkg.ForestParams(trees, 6, 5, seed)
+    f = pkg.fit(pm, params)
+    g = pkg.fit(prep, params)
+    assert np.array_equal(f.inbag(view=True), g.inbag())
+    for x, y in zip(f.export(view=True), g.export()):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
