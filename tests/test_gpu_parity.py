@@ -511,3 +511,16 @@ def test_fit_time_inbag_mirror(c1, seed, trees):
     assert np.array_equal(f.inbag(view=True), g.inbag())
     for x, y in zip(f.export(view=True), g.export()):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
+def test_release_cached_between_fits(c1, seed):
+    """aiwc_release_cached returns the recycled device / pinned memory while forests and
+    their host views stay valid; the next fit re-allocates and grows the same forest."""
+    t, prep = c1
+    params = pkg.ForestParams(100, 6, 5, seed)
+    f = pkg.fit(prep, params)
+    view = f.export(view=True)
+    pkg.release_cached(0)
+    g = pkg.fit(prep, params)
+    for x, y in zip(view, g.export()):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
