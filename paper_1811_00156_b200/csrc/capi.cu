@@ -1786,10 +1786,12 @@ int aiwc_forest_host_view(aiwc_forest* f, const int32_t** feature, const double*
           Stream st;
           // right children written by the device straight into the mapped pinned mirror
           // (no 1.5 GB device temporary); the other arrays by DMA
-          right_child_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 1u << 20)),
-                               256, 0, st.s>>>(f->left.p, N, ri);
-          CK(cudaGetLastError());
-          g_launches += 1;
+          if (N) {
+            right_child_kernel<<<static_cast<unsigned>(std::min<uint64_t>((N + 255) / 256, 1u << 20)),
+                                 256, 0, st.s>>>(f->left.p, N, ri);
+            CK(cudaGetLastError());
+            g_launches += 1;
+          }
           CK(cudaMemcpyAsync(t, f->thr.p, N * 8, cudaMemcpyDeviceToHost, st.s));
           CK(cudaMemcpyAsync(v, f->value.p, N * 8, cudaMemcpyDeviceToHost, st.s));
           CK(cudaMemcpyAsync(fe, f->feature.p, N * 4, cudaMemcpyDeviceToHost, st.s));
